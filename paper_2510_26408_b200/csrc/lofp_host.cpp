@@ -1,0 +1,584 @@
+// lofp_host.cpp — host side of liblofp: the C ABI of include/lofp.h, circuit
+// canonicalisation, light-cone topology maps, DFS level / factor planning, per-call
+// Appendix-A table layout and kernel launches.  See DESIGN.md for the derivations
+// (readings R1-R9) and the paper passages each step follows.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/lofp.h"
+#include "lofp_internal.h"
+
+namespace {
+
+constexpr double kPi = 3.14159265358979323846;
+
+struct DevBuf {
+  void *p = nullptr;
+  size_t n = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= n) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&p, bytes ? bytes : 16);
+    if (e == cudaSuccess) n = bytes;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+struct HostPinned {
+  void *p = nullptr;
+  size_t n = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= n) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMallocHost(&p, bytes ? bytes : 16);
+    if (e == cudaSuccess) n = bytes;
+    return e;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+// A beam splitter after canonicalisation: port 1 = mode k-1, port 2 = mode k.
+struct CanonBS {
+  int layer;  // 1-based
+  int cut;    // k = max(mode_a, mode_b)
+  double theta, phi;
+};
+
+}  // namespace
+
+struct lofp_ctx {
+  int M = 0, D = 0, nbs = 0;
+  std::vector<CanonBS> bs;                  // layer-major
+  std::vector<std::vector<uint8_t>> act;    // [D+1][M+1]
+  std::vector<std::vector<int>> rho, sigma; // [D+1][M+1]
+  std::vector<std::vector<int>> varlevel;   // [D+1][M+1]: DFS level of free output (l,k) or -1
+  std::vector<LevelDesc> levels;            // [L]
+  std::vector<FactorDesc> factors;          // root factors first, then by level
+  int L = 0, nroot = 0;
+  // static device data
+  DevBuf d_levels, d_factors, d_rho0, d_sigma0, d_bs_cs;
+  // per-call device data
+  DevBuf d_flags, d_G, d_root, d_feas, d_ctr, d_ring, d_edesc, d_offsets, d_entries, d_cumS;
+  DevBuf d_hostT, d_hostA;
+  HostPinned h_stage, h_ctr;
+  unsigned ring_cap = 0;
+  cudaEvent_t ev_start = nullptr, ev_enum0 = nullptr, ev_enum1 = nullptr, ev_end = nullptr,
+              ev_upload = nullptr;
+  cudaStream_t own_stream = nullptr;
+  bool have_call = false;
+  lofp_run_stats stats{};
+  std::string err;
+  int device = 0;
+};
+
+namespace {
+
+lofp_status fail(lofp_ctx *c, lofp_status s, const std::string &msg) {
+  if (c) c->err = msg;
+  return s;
+}
+
+lofp_status cuda_fail(lofp_ctx *c, cudaError_t e, const char *where) {
+  std::string m = std::string(where) + ": " + cudaGetErrorString(e);
+  return fail(c, e == cudaErrorMemoryAllocation ? LOFP_E_OOM : LOFP_E_CUDA, m);
+}
+
+#define CK(expr, where)                              \
+  do {                                               \
+    cudaError_t _e = (expr);                         \
+    if (_e != cudaSuccess) return cuda_fail(ctx, _e, where); \
+  } while (0)
+
+// Value references into the per-lane array [levels | G(0..M) | cumS(0..M)].
+inline uint16_t refG(const lofp_ctx *c, int k) { return (uint16_t)(c->L + k); }
+inline uint16_t refS(const lofp_ctx *c, int k) { return (uint16_t)(c->L + c->M + 1 + k); }
+
+// Reference of F_t(k): the latest BS output at cut k in layers <= t, else cum(S)(k).
+// Forced outputs (rho == sigma) equal G(k) (reading R5); cuts 0 and M are G(0) = 0 and
+// G(M) = N.
+uint16_t ref_of(const lofp_ctx *c, int t, int k) {
+  if (k <= 0) return refG(c, 0);
+  if (k >= c->M) return refG(c, c->M);
+  for (int l = t; l >= 1; --l) {
+    if (c->act[l][k]) {
+      int v = c->varlevel[l][k];
+      return v >= 0 ? (uint16_t)v : refG(c, k);
+    }
+  }
+  return refS(c, k);
+}
+
+lofp_status plan_circuit(lofp_ctx *c) {
+  const int M = c->M, D = c->D;
+  c->act.assign(D + 1, std::vector<uint8_t>(M + 1, 0));
+  for (const CanonBS &b : c->bs) c->act[b.layer][b.cut] = 1;
+  // Box index maps (reading R5): rho_D(k) = sigma_D(k) = k; going back through layer l,
+  // an active cut k takes rho_{l-1}(k) = rho_l(k-1), sigma_{l-1}(k) = sigma_l(k+1).
+  c->rho.assign(D + 1, std::vector<int>(M + 1));
+  c->sigma.assign(D + 1, std::vector<int>(M + 1));
+  for (int k = 0; k <= M; ++k) c->rho[D][k] = c->sigma[D][k] = k;
+  for (int l = D; l >= 1; --l)
+    for (int k = 0; k <= M; ++k) {
+      c->rho[l - 1][k] = c->act[l][k] ? c->rho[l][k - 1] : c->rho[l][k];
+      c->sigma[l - 1][k] = c->act[l][k] ? c->sigma[l][k + 1] : c->sigma[l][k];
+    }
+  // DFS levels: free BS outputs in layer-major order (the green waveguides)
+  c->varlevel.assign(D + 1, std::vector<int>(M + 1, -1));
+  int L = 0;
+  std::vector<std::pair<int, int>> lv;  // (l, k)
+  for (int l = 1; l <= D; ++l)
+    for (int k = 1; k < M; ++k)
+      if (c->act[l][k] && c->rho[l][k] != c->sigma[l][k]) {
+        c->varlevel[l][k] = L++;
+        lv.push_back({l, k});
+      }
+  if (L > LOFP_MAX_LEVELS) return fail(c, LOFP_E_UNSUPPORTED, "too many free BS outputs (DFS levels)");
+  c->L = L;
+  // factors: every BS element, attached to the deepest DFS level among its inputs
+  struct F {
+    int level;
+    FactorDesc d;
+  };
+  std::vector<F> fs;
+  for (int i = 0; i < c->nbs; ++i) {
+    const CanonBS &b = c->bs[i];
+    FactorDesc d{};
+    d.xl = ref_of(c, b.layer - 1, b.cut - 1);
+    d.xm = ref_of(c, b.layer - 1, b.cut);
+    d.xr = ref_of(c, b.layer - 1, b.cut + 1);
+    d.y = ref_of(c, b.layer, b.cut);
+    d.bs = (uint16_t)i;
+    int at = -1;
+    for (uint16_t r : {d.xl, d.xm, d.xr, d.y})
+      if (r < L) at = std::max(at, (int)r);
+    fs.push_back({at, d});
+  }
+  std::stable_sort(fs.begin(), fs.end(), [](const F &a, const F &b) { return a.level < b.level; });
+  c->factors.clear();
+  c->nroot = 0;
+  for (const F &f : fs) {
+    if (f.level < 0) ++c->nroot;
+    c->factors.push_back(f.d);
+  }
+  c->levels.assign(L, LevelDesc{});
+  size_t fi = c->nroot;
+  for (int j = 0; j < L; ++j) {
+    int l = lv[j].first, k = lv[j].second;
+    LevelDesc &d = c->levels[j];
+    d.refL = ref_of(c, l - 1, k - 1);
+    d.refR = ref_of(c, l - 1, k + 1);
+    d.gLo = refG(c, c->rho[l][k]);
+    d.gHi = refG(c, c->sigma[l][k]);
+    d.fbeg = (uint16_t)fi;
+    while (fi < fs.size() && fs[fi].level == j) ++fi;
+    d.fend = (uint16_t)fi;
+  }
+  return LOFP_OK;
+}
+
+// Per-segment occupation caps: min(photons of S in the past light cone, photons of
+// max-over-batch T in the future light cone).  cap[j][m] for the segment of
+// mode m after layer j.
+std::vector<std::vector<int>> segment_caps(const lofp_ctx *c, const std::vector<int> &S,
+                                           const int32_t *tmax) {
+  const int M = c->M, D = c->D;
+  std::vector<std::vector<int>> cap(D + 1, std::vector<int>(M, 0));
+  std::vector<std::vector<const CanonBS *>> byl(D + 1);
+  for (const CanonBS &b : c->bs) byl[b.layer].push_back(&b);
+  std::vector<uint8_t> in(M);
+  for (int j = 0; j <= D; ++j)
+    for (int m = 0; m < M; ++m) {
+      std::fill(in.begin(), in.end(), 0);
+      in[m] = 1;
+      for (int l = j; l >= 1; --l)
+        for (const CanonBS *b : byl[l])
+          if (in[b->cut - 1] || in[b->cut]) in[b->cut - 1] = in[b->cut] = 1;
+      int past = 0;
+      for (int i = 0; i < M; ++i) if (in[i]) past += S[i];
+      std::fill(in.begin(), in.end(), 0);
+      in[m] = 1;
+      for (int l = j + 1; l <= D; ++l)
+        for (const CanonBS *b : byl[l])
+          if (in[b->cut - 1] || in[b->cut]) in[b->cut - 1] = in[b->cut] = 1;
+      int fut = 0;
+      for (int i = 0; i < M; ++i) if (in[i]) fut += tmax[i];
+      cap[j][m] = std::min(past, fut);
+    }
+  return cap;
+}
+
+lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const int32_t *output_occ,
+                double *amps, unsigned long long *counts, cudaStream_t stream) {
+  if (!ctx) return LOFP_E_INVALID_ARG;
+  ctx->err.clear();
+  if (!input_occ || batch < 0) return fail(ctx, LOFP_E_INVALID_ARG, "null input_occ or negative batch");
+  if (batch > 0 && (!output_occ || !amps)) return fail(ctx, LOFP_E_INVALID_ARG, "null output_occ or amps");
+  if (batch > (int64_t)0xffffffff) return fail(ctx, LOFP_E_UNSUPPORTED, "batch too large");
+  const int M = ctx->M;
+  std::vector<int> S(M);
+  int N = 0;
+  for (int m = 0; m < M; ++m) {
+    if (input_occ[m] < 0) return fail(ctx, LOFP_E_INVALID_ARG, "negative input occupation");
+    S[m] = input_occ[m];
+    N += S[m];
+    if (N > LOFP_MAX_PHOTONS) return fail(ctx, LOFP_E_UNSUPPORTED, "too many photons");
+  }
+  CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+  ctx->stats = lofp_run_stats{};
+  ctx->stats.batch = batch;
+  ctx->stats.levels = ctx->L;
+  ctx->have_call = false;
+  if (batch == 0) return LOFP_OK;
+  // serialise with this context's previous call (its buffers are reused)
+  CK(cudaStreamWaitEvent(stream, ctx->ev_end, 0), "cudaStreamWaitEvent");
+  CK(cudaEventSynchronize(ctx->ev_upload), "cudaEventSynchronize");
+
+  const int64_t B = batch;
+  CallArgs a{};
+  a.M = M;
+  a.D = ctx->D;
+  a.N = N;
+  a.L = ctx->L;
+  a.B = B;
+  a.grow = ((M + 1) + 15) & ~15;
+  a.T = output_occ;
+  a.amps = amps;
+  a.counts = counts;
+  CK(ctx->d_flags.ensure((size_t)B), "alloc flags");
+  CK(ctx->d_G.ensure((size_t)B * a.grow), "alloc G");
+  CK(ctx->d_root.ensure((size_t)B * 16), "alloc root");
+  CK(ctx->d_feas.ensure((size_t)B * 4), "alloc feas");
+  CK(ctx->d_ctr.ensure(sizeof(Counters)), "alloc counters");
+  CK(ctx->d_cumS.ensure(256), "alloc cumS");
+  a.flags = (uint8_t *)ctx->d_flags.p;
+  a.G = (uint8_t *)ctx->d_G.p;
+  a.root = (double *)ctx->d_root.p;
+  a.feas = (uint32_t *)ctx->d_feas.p;
+  a.ctr = (Counters *)ctx->d_ctr.p;
+  a.rho0 = (const uint8_t *)ctx->d_rho0.p;
+  a.sigma0 = (const uint8_t *)ctx->d_sigma0.p;
+  a.cumS = (const uint8_t *)ctx->d_cumS.p;
+  a.levels = (const LevelDesc *)ctx->d_levels.p;
+  a.bs_cs = (const double *)ctx->d_bs_cs.p;
+
+  CK(cudaEventRecord(ctx->ev_start, stream), "cudaEventRecord");
+  // cum(S) to the device (pinned staging; the previous upload has completed)
+  CK(ctx->h_stage.ensure(4096), "alloc staging");
+  uint8_t *cs = (uint8_t *)ctx->h_stage.p;
+  {
+    int f = 0;
+    for (int k = 0; k <= M; ++k) {
+      cs[k] = (uint8_t)f;
+      if (k < M) f += S[k];
+    }
+  }
+  CK(cudaMemcpyAsync(ctx->d_cumS.p, cs, M + 1, cudaMemcpyHostToDevice, stream), "upload cumS");
+  CK(cudaMemsetAsync(a.ctr, 0, sizeof(Counters), stream), "reset counters");
+  CK(lofp_launch_prep(a, stream), "prep kernel");
+  // the batch's per-mode maximum sizes the tables (one synchronisation per call)
+  CK(ctx->h_ctr.ensure(sizeof(Counters)), "alloc pinned counters");
+  CK(cudaMemcpyAsync(ctx->h_ctr.p, a.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, stream), "read tmax");
+  CK(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+  const Counters *hc = (const Counters *)ctx->h_ctr.p;
+  int32_t tmax[LOFP_MAX_MODES];
+  for (int m = 0; m < M; ++m) tmax[m] = hc->tmax[m];
+
+  // Appendix-A table layout inside the light-cone caps
+  std::vector<std::vector<int>> cap = segment_caps(ctx, S, tmax);
+  std::vector<int32_t> offsets;
+  std::vector<EntryDesc> edesc;
+  std::vector<int32_t> offbase(ctx->nbs), stride(ctx->nbs);
+  for (int i = 0; i < ctx->nbs; ++i) {
+    const CanonBS &b = ctx->bs[i];
+    int X1 = cap[b.layer - 1][b.cut - 1], X2 = cap[b.layer - 1][b.cut];
+    int Y1 = cap[b.layer][b.cut - 1], Y2 = cap[b.layer][b.cut];
+    offbase[i] = (int32_t)offsets.size();
+    stride[i] = X2 + 1;
+    for (int x1 = 0; x1 <= X1; ++x1)
+      for (int x2 = 0; x2 <= X2; ++x2) {
+        int n = x1 + x2;
+        int ylo = std::max(0, n - Y2), yhi = std::min(Y1, n);
+        offsets.push_back((int32_t)edesc.size() - ylo);
+        for (int y1 = ylo; y1 <= yhi; ++y1) {
+          EntryDesc e{};
+          e.bs = (uint16_t)i;
+          e.x1 = (uint8_t)x1;
+          e.x2 = (uint8_t)x2;
+          e.y1 = (uint8_t)y1;
+          edesc.push_back(e);
+        }
+      }
+  }
+  if (edesc.empty()) {  // keep one dummy entry so that pointers are valid
+    EntryDesc e{};
+    edesc.push_back(e);
+  }
+  std::vector<FactorDesc> facs = ctx->factors;
+  for (FactorDesc &f : facs) {
+    f.offbase = offbase[f.bs];
+    f.stride = (uint16_t)stride[f.bs];
+  }
+  a.nfactors = (int)facs.size();
+  a.nroot = ctx->nroot;
+  a.nentries = (int)edesc.size();
+  a.noffsets = (int)offsets.size();
+  CK(ctx->d_edesc.ensure(edesc.size() * sizeof(EntryDesc)), "alloc edesc");
+  CK(ctx->d_offsets.ensure(std::max<size_t>(offsets.size(), 1) * 4), "alloc offsets");
+  CK(ctx->d_entries.ensure(edesc.size() * 16), "alloc entries");
+  CK(ctx->d_factors.ensure(std::max<size_t>(facs.size(), 1) * sizeof(FactorDesc)), "alloc factors");
+  size_t need = edesc.size() * sizeof(EntryDesc) + offsets.size() * 4 + facs.size() * sizeof(FactorDesc) + 64;
+  CK(ctx->h_stage.ensure(need), "alloc staging");
+  {
+    uint8_t *st = (uint8_t *)ctx->h_stage.p;
+    size_t o = 0;
+    memcpy(st + o, edesc.data(), edesc.size() * sizeof(EntryDesc));
+    CK(cudaMemcpyAsync(ctx->d_edesc.p, st + o, edesc.size() * sizeof(EntryDesc), cudaMemcpyHostToDevice, stream),
+       "upload edesc");
+    o += edesc.size() * sizeof(EntryDesc);
+    if (!offsets.empty()) {
+      memcpy(st + o, offsets.data(), offsets.size() * 4);
+      CK(cudaMemcpyAsync(ctx->d_offsets.p, st + o, offsets.size() * 4, cudaMemcpyHostToDevice, stream),
+         "upload offsets");
+      o += offsets.size() * 4;
+    }
+    if (!facs.empty()) {
+      memcpy(st + o, facs.data(), facs.size() * sizeof(FactorDesc));
+      CK(cudaMemcpyAsync(ctx->d_factors.p, st + o, facs.size() * sizeof(FactorDesc), cudaMemcpyHostToDevice,
+                         stream),
+         "upload factors");
+    }
+    CK(cudaEventRecord(ctx->ev_upload, stream), "cudaEventRecord");
+  }
+  a.edesc = (const EntryDesc *)ctx->d_edesc.p;
+  a.offsets = (const int32_t *)ctx->d_offsets.p;
+  a.entries = (double *)ctx->d_entries.p;
+  a.factors = (const FactorDesc *)ctx->d_factors.p;
+  ctx->stats.table_entries = a.nentries;
+
+  CK(lofp_launch_tables(a, stream), "table kernel");
+  CK(lofp_launch_feasible(a, stream), "feasibility kernel");
+  CK(cudaEventRecord(ctx->ev_enum0, stream), "cudaEventRecord");
+  if (a.L > 0) {
+    int grid = 0, block = 0;
+    size_t smem = 0;
+    cudaError_t e = lofp_enum_config(a, counts != nullptr, &grid, &block, &smem);
+    if (e == cudaErrorInvalidConfiguration || smem > 227 * 1024)
+      return fail(ctx, LOFP_E_UNSUPPORTED, "BS tables do not fit in shared memory");
+    CK(e, "enumeration config");
+    unsigned lanes = (unsigned)grid * (unsigned)block;
+    unsigned cap = 1024;
+    while (cap < 4u * lanes + 4096u) cap <<= 1;
+    if (cap > ctx->ring_cap) {
+      CK(ctx->d_ring.ensure((size_t)cap * sizeof(Item)), "alloc work queue");
+      CK(cudaMemsetAsync(ctx->d_ring.p, 0, (size_t)cap * sizeof(Item), stream), "clear work queue");
+      ctx->ring_cap = cap;
+    }
+    a.ring = (Item *)ctx->d_ring.p;
+    a.ring_mask = ctx->ring_cap - 1;
+    ctx->stats.smem_bytes = (int32_t)smem;
+    ctx->stats.grid_blocks = grid;
+    ctx->stats.block_threads = block;
+    CK(lofp_launch_enum(a, counts != nullptr, grid, block, smem, stream), "enumeration kernel");
+  }
+  CK(cudaEventRecord(ctx->ev_enum1, stream), "cudaEventRecord");
+  CK(cudaMemcpyAsync(ctx->h_ctr.p, a.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, stream), "read counters");
+  CK(cudaEventRecord(ctx->ev_end, stream), "cudaEventRecord");
+  ctx->have_call = true;
+  return LOFP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *lofp_status_string(lofp_status s) {
+  switch (s) {
+    case LOFP_OK: return "ok";
+    case LOFP_E_INVALID_ARG: return "invalid argument";
+    case LOFP_E_UNSUPPORTED: return "unsupported";
+    case LOFP_E_CUDA: return "CUDA error";
+    case LOFP_E_OOM: return "out of device memory";
+    case LOFP_E_BAD_OUTPUT: return "bad output row";
+  }
+  return "unknown status";
+}
+
+const char *lofp_last_error(const lofp_ctx *ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+lofp_status lofp_create(int32_t modes, int32_t n_layers, const int32_t *bs_per_layer, const lofp_bs *bs,
+                        lofp_ctx **out) {
+  if (!out) return LOFP_E_INVALID_ARG;
+  *out = nullptr;
+  if (modes < 1 || n_layers < 0) return LOFP_E_INVALID_ARG;
+  if (modes > LOFP_MAX_MODES || n_layers > LOFP_MAX_LAYERS) return LOFP_E_UNSUPPORTED;
+  if (n_layers > 0 && !bs_per_layer) return LOFP_E_INVALID_ARG;
+  int64_t total = 0;
+  for (int l = 0; l < n_layers; ++l) {
+    if (bs_per_layer[l] < 0) return LOFP_E_INVALID_ARG;
+    total += bs_per_layer[l];
+  }
+  if (total > 0 && !bs) return LOFP_E_INVALID_ARG;
+  if (total > 65535) return LOFP_E_UNSUPPORTED;
+  lofp_ctx *ctx = new (std::nothrow) lofp_ctx();
+  if (!ctx) return LOFP_E_OOM;
+  ctx->M = modes;
+  ctx->D = n_layers;
+  ctx->nbs = (int)total;
+  lofp_status st = LOFP_OK;
+  int idx = 0;
+  for (int l = 0; l < n_layers && st == LOFP_OK; ++l) {
+    std::vector<uint8_t> used(modes, 0);
+    for (int i = 0; i < bs_per_layer[l]; ++i, ++idx) {
+      const lofp_bs &b = bs[idx];
+      if (b.mode_a < 0 || b.mode_b < 0 || b.mode_a >= modes || b.mode_b >= modes || b.mode_a == b.mode_b ||
+          !std::isfinite(b.theta) || !std::isfinite(b.phi)) {
+        st = LOFP_E_INVALID_ARG;
+        break;
+      }
+      if (used[b.mode_a] || used[b.mode_b]) {
+        st = LOFP_E_INVALID_ARG;
+        break;
+      }
+      used[b.mode_a] = used[b.mode_b] = 1;
+      if (std::abs(b.mode_a - b.mode_b) != 1) {
+        st = LOFP_E_UNSUPPORTED;
+        break;
+      }
+      CanonBS c;
+      c.layer = l + 1;
+      c.cut = std::max(b.mode_a, b.mode_b);
+      c.theta = b.theta;
+      // port swap: (b, a, theta, phi) == (a, b, theta, pi - phi) (reading R4)
+      c.phi = b.mode_a < b.mode_b ? b.phi : kPi - b.phi;
+      ctx->bs.push_back(c);
+    }
+  }
+  if (st == LOFP_OK) st = plan_circuit(ctx);
+  if (st != LOFP_OK) {
+    delete ctx;
+    return st;
+  }
+  cudaError_t e = cudaGetDevice(&ctx->device);
+  const int M = modes, D = n_layers;
+  std::vector<uint8_t> r0(M + 1), s0(M + 1);
+  for (int k = 0; k <= M; ++k) {
+    r0[k] = (uint8_t)ctx->rho[0][k];
+    s0[k] = (uint8_t)ctx->sigma[0][k];
+  }
+  std::vector<double> csv(4 * std::max(ctx->nbs, 1));
+  for (int i = 0; i < ctx->nbs; ++i) {
+    csv[4 * i] = std::cos(ctx->bs[i].theta);
+    csv[4 * i + 1] = std::sin(ctx->bs[i].theta);
+    csv[4 * i + 2] = std::cos(ctx->bs[i].phi);
+    csv[4 * i + 3] = std::sin(ctx->bs[i].phi);
+  }
+  (void)D;
+  if (e == cudaSuccess) e = ctx->d_levels.ensure(std::max<size_t>(ctx->levels.size(), 1) * sizeof(LevelDesc));
+  if (e == cudaSuccess && !ctx->levels.empty())
+    e = cudaMemcpy(ctx->d_levels.p, ctx->levels.data(), ctx->levels.size() * sizeof(LevelDesc),
+                   cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = ctx->d_rho0.ensure(M + 1);
+  if (e == cudaSuccess) e = ctx->d_sigma0.ensure(M + 1);
+  if (e == cudaSuccess) e = cudaMemcpy(ctx->d_rho0.p, r0.data(), M + 1, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(ctx->d_sigma0.p, s0.data(), M + 1, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = ctx->d_bs_cs.ensure(csv.size() * 8);
+  if (e == cudaSuccess) e = cudaMemcpy(ctx->d_bs_cs.p, csv.data(), csv.size() * 8, cudaMemcpyHostToDevice);
+  for (cudaEvent_t *ev : {&ctx->ev_start, &ctx->ev_enum0, &ctx->ev_enum1, &ctx->ev_end, &ctx->ev_upload})
+    if (e == cudaSuccess) e = cudaEventCreate(ev);
+  if (e != cudaSuccess) {
+    lofp_status s = e == cudaErrorMemoryAllocation ? LOFP_E_OOM : LOFP_E_CUDA;
+    lofp_destroy(ctx);
+    return s;
+  }
+  *out = ctx;
+  return LOFP_OK;
+}
+
+lofp_status lofp_amplitudes(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const int32_t *output_occ,
+                            double *amps, void *cuda_stream) {
+  return run(ctx, input_occ, batch, output_occ, amps, nullptr, (cudaStream_t)cuda_stream);
+}
+
+lofp_status lofp_amplitudes_counted(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch,
+                                    const int32_t *output_occ, double *amps, uint64_t *path_counts,
+                                    void *cuda_stream) {
+  if (batch > 0 && !path_counts) return fail(ctx, LOFP_E_INVALID_ARG, "null path_counts");
+  return run(ctx, input_occ, batch, output_occ, amps, (unsigned long long *)path_counts,
+             (cudaStream_t)cuda_stream);
+}
+
+lofp_status lofp_amplitudes_host(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch,
+                                 const int32_t *output_occ, double *amps) {
+  if (!ctx) return LOFP_E_INVALID_ARG;
+  if (batch < 0 || !input_occ) return fail(ctx, LOFP_E_INVALID_ARG, "bad arguments");
+  if (batch == 0) return LOFP_OK;
+  if (!output_occ || !amps) return fail(ctx, LOFP_E_INVALID_ARG, "null output_occ or amps");
+  CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+  if (!ctx->own_stream) CK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking), "stream");
+  size_t tb = (size_t)batch * ctx->M * 4, ab = (size_t)batch * 16;
+  CK(ctx->d_hostT.ensure(tb), "alloc T");
+  CK(ctx->d_hostA.ensure(ab), "alloc amps");
+  CK(cudaMemcpyAsync(ctx->d_hostT.p, output_occ, tb, cudaMemcpyHostToDevice, ctx->own_stream), "copy T");
+  lofp_status s = run(ctx, input_occ, batch, (const int32_t *)ctx->d_hostT.p, (double *)ctx->d_hostA.p, nullptr,
+                      ctx->own_stream);
+  if (s != LOFP_OK) return s;
+  CK(cudaMemcpyAsync(amps, ctx->d_hostA.p, ab, cudaMemcpyDeviceToHost, ctx->own_stream), "copy amps");
+  CK(cudaStreamSynchronize(ctx->own_stream), "cudaStreamSynchronize");
+  return LOFP_OK;
+}
+
+lofp_status lofp_stats(lofp_ctx *ctx, lofp_run_stats *out) {
+  if (!ctx || !out) return LOFP_E_INVALID_ARG;
+  if (ctx->have_call) {
+    CK(cudaEventSynchronize(ctx->ev_end), "cudaEventSynchronize");
+    const Counters *hc = (const Counters *)ctx->h_ctr.p;
+    ctx->stats.feasible = (int64_t)hc->nfeas;
+    ctx->stats.items = (int64_t)hc->items;
+    ctx->stats.donations = (int64_t)hc->donations;
+    ctx->stats.bad_rows = (int32_t)hc->bad_rows;
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ctx->ev_enum0, ctx->ev_enum1) == cudaSuccess) ctx->stats.enum_ms = ms;
+    if (cudaEventElapsedTime(&ms, ctx->ev_start, ctx->ev_end) == cudaSuccess) ctx->stats.total_ms = ms;
+    ctx->have_call = false;
+  }
+  *out = ctx->stats;
+  return ctx->stats.bad_rows ? LOFP_E_BAD_OUTPUT : LOFP_OK;
+}
+
+void lofp_destroy(lofp_ctx *ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->ev_end) cudaEventSynchronize(ctx->ev_end);
+  for (DevBuf *b : {&ctx->d_levels, &ctx->d_factors, &ctx->d_rho0, &ctx->d_sigma0, &ctx->d_bs_cs, &ctx->d_flags,
+                    &ctx->d_G, &ctx->d_root, &ctx->d_feas, &ctx->d_ctr, &ctx->d_ring, &ctx->d_edesc,
+                    &ctx->d_offsets, &ctx->d_entries, &ctx->d_cumS, &ctx->d_hostT, &ctx->d_hostA})
+    b->release();
+  ctx->h_stage.release();
+  ctx->h_ctr.release();
+  for (cudaEvent_t ev : {ctx->ev_start, ctx->ev_enum0, ctx->ev_enum1, ctx->ev_end, ctx->ev_upload})
+    if (ev) cudaEventDestroy(ev);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+}
+
+}  // extern "C"

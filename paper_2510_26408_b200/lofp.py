@@ -1,0 +1,157 @@
+"""Python binding of liblofp (include/lofp.h): argument marshalling only.
+
+Every step of the path sum runs in the CUDA library; PyTorch is used here only for
+device memory (the output buffer) and the current CUDA stream.  There is no CPU
+fallback: if liblofp.so is missing this module raises on import.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblofp.so")
+
+LOFP_OK, LOFP_E_INVALID_ARG, LOFP_E_UNSUPPORTED, LOFP_E_CUDA, LOFP_E_OOM, LOFP_E_BAD_OUTPUT = range(6)
+
+
+class lofp_bs(ctypes.Structure):
+    _fields_ = [("mode_a", ctypes.c_int32), ("mode_b", ctypes.c_int32),
+                ("theta", ctypes.c_double), ("phi", ctypes.c_double)]
+
+
+class lofp_run_stats(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int64), ("feasible", ctypes.c_int64), ("items", ctypes.c_int64),
+                ("donations", ctypes.c_int64), ("levels", ctypes.c_int32), ("table_entries", ctypes.c_int32),
+                ("smem_bytes", ctypes.c_int32), ("grid_blocks", ctypes.c_int32),
+                ("block_threads", ctypes.c_int32), ("bad_rows", ctypes.c_int32),
+                ("enum_ms", ctypes.c_float), ("total_ms", ctypes.c_float)]
+
+
+EXPORTS = ["lofp_create", "lofp_amplitudes", "lofp_amplitudes_counted", "lofp_amplitudes_host",
+           "lofp_destroy", "lofp_status_string", "lofp_last_error", "lofp_stats"]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(LIB_PATH)
+    P = ctypes.c_void_p
+    lib.lofp_create.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
+                                ctypes.POINTER(lofp_bs), ctypes.POINTER(P)]
+    lib.lofp_create.restype = ctypes.c_int
+    lib.lofp_amplitudes.argtypes = [P, ctypes.POINTER(ctypes.c_int32), ctypes.c_int64, P, P, P]
+    lib.lofp_amplitudes.restype = ctypes.c_int
+    lib.lofp_amplitudes_counted.argtypes = [P, ctypes.POINTER(ctypes.c_int32), ctypes.c_int64, P, P, P, P]
+    lib.lofp_amplitudes_counted.restype = ctypes.c_int
+    lib.lofp_amplitudes_host.argtypes = [P, ctypes.POINTER(ctypes.c_int32), ctypes.c_int64, P, P]
+    lib.lofp_amplitudes_host.restype = ctypes.c_int
+    lib.lofp_destroy.argtypes = [P]
+    lib.lofp_destroy.restype = None
+    lib.lofp_status_string.argtypes = [ctypes.c_int]
+    lib.lofp_status_string.restype = ctypes.c_char_p
+    lib.lofp_last_error.argtypes = [P]
+    lib.lofp_last_error.restype = ctypes.c_char_p
+    lib.lofp_stats.argtypes = [P, ctypes.POINTER(lofp_run_stats)]
+    lib.lofp_stats.restype = ctypes.c_int
+    return lib
+
+
+_lib = _load()
+
+
+class LofpError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        self.status = status
+        super().__init__(f"{_lib.lofp_status_string(status).decode()}: {msg}")
+
+
+def _occ(S, M):
+    s = np.ascontiguousarray(np.asarray(S, dtype=np.int32))
+    if s.shape != (M,):
+        raise ValueError(f"input occupation must have {M} entries")
+    return s
+
+
+class Circuit:
+    """A mesh of beam splitters: ``layers`` is a list of layers, each a list of
+    ``(mode_a, mode_b, theta, phi)`` (mode_a = BS port 1)."""
+
+    def __init__(self, modes: int, layers):
+        self.modes = int(modes)
+        self.layers = [list(l) for l in layers]
+        flat = [bs for l in self.layers for bs in l]
+        bpl = (ctypes.c_int32 * max(len(self.layers), 1))(*[len(l) for l in self.layers])
+        arr = (lofp_bs * max(len(flat), 1))(*[lofp_bs(int(a), int(b), float(t), float(p)) for a, b, t, p in flat])
+        h = ctypes.c_void_p()
+        st = _lib.lofp_create(self.modes, len(self.layers), bpl, arr, ctypes.byref(h))
+        if st != LOFP_OK:
+            raise LofpError(st, "lofp_create failed")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.lofp_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st):
+        if st != LOFP_OK:
+            raise LofpError(st, _lib.lofp_last_error(self._h).decode())
+
+    def amplitudes(self, S, T, out=None, counts=None, stream=None):
+        """<T_b|U_P|S> for every row of the int32 CUDA tensor T [B, M] -> complex128 CUDA [B].
+
+        ``counts``: optional uint64-compatible int64 CUDA tensor [B] receiving the exact
+        number of valid paths summed per output.  Runs on ``stream`` (default: torch's
+        current stream); the result is ready when that stream is.
+        """
+        import torch
+        if T.dtype != torch.int32 or not T.is_cuda or T.dim() != 2 or T.shape[1] != self.modes:
+            raise ValueError("T must be an int32 CUDA tensor of shape [B, modes]")
+        T = T.contiguous()
+        B = T.shape[0]
+        if out is None:
+            out = torch.empty((B, 2), dtype=torch.float64, device=T.device)
+        s = _occ(S, self.modes)
+        strm = (stream or torch.cuda.current_stream(T.device)).cuda_stream
+        sp = s.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+        if counts is None:
+            st = _lib.lofp_amplitudes(self._h, sp, B, ctypes.c_void_p(T.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                      ctypes.c_void_p(strm))
+        else:
+            if counts.dtype != torch.int64 or counts.numel() != B or not counts.is_cuda:
+                raise ValueError("counts must be an int64 CUDA tensor [B]")
+            st = _lib.lofp_amplitudes_counted(self._h, sp, B, ctypes.c_void_p(T.data_ptr()),
+                                              ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(counts.data_ptr()),
+                                              ctypes.c_void_p(strm))
+        self._check(st)
+        return torch.view_as_complex(out)
+
+    def amplitudes_host(self, S, T) -> np.ndarray:
+        """End-to-end call with host buffers (numpy in, numpy out)."""
+        s = _occ(S, self.modes)
+        t = np.ascontiguousarray(np.asarray(T, dtype=np.int32))
+        if t.ndim != 2 or t.shape[1] != self.modes:
+            raise ValueError("T must have shape [B, modes]")
+        out = np.empty((t.shape[0], 2), dtype=np.float64)
+        st = _lib.lofp_amplitudes_host(self._h, s.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), t.shape[0],
+                                       ctypes.c_void_p(t.ctypes.data), ctypes.c_void_p(out.ctypes.data))
+        self._check(st)
+        return out.view(np.complex128)[:, 0]
+
+    def stats(self) -> dict:
+        st = lofp_run_stats()
+        rc = _lib.lofp_stats(self._h, ctypes.byref(st))
+        if rc not in (LOFP_OK, LOFP_E_BAD_OUTPUT):
+            self._check(rc)
+        d = {k: getattr(st, k) for k, _ in lofp_run_stats._fields_}
+        d["status"] = rc
+        return d

@@ -1,0 +1,220 @@
+"""GPU parity: liblofp (CUDA, through the C ABI) against the CPU oracle.
+
+Tolerance (BASELINE.json north_star): |a - a_ref| <= 1e-12 + 1e-9 |a_ref| in fp64.
+Path counts (integers) must match the oracle exactly: every path of eq. (1) is summed
+exactly once.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import lofp_inputs as li
+import oracle
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def lofp():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    import paper_2510_26408_b200 as pkg
+    return pkg
+
+
+def tol_ok(got, ref):
+    err = np.abs(np.asarray(got) - np.asarray(ref))
+    return (err <= 1e-12 + 1e-9 * np.abs(ref)).all(), float(err.max()) if err.size else 0.0
+
+
+def run(lofp, M, layers, S, T, counted=True):
+    circ = lofp.Circuit(M, layers)
+    Td = torch.from_numpy(np.ascontiguousarray(T, dtype=np.int32)).cuda()
+    counts = torch.zeros(len(T), dtype=torch.int64, device="cuda") if counted else None
+    a = circ.amplitudes(S, Td, counts=counts)
+    torch.cuda.synchronize()
+    st = circ.stats()
+    return a.cpu().numpy(), (counts.cpu().numpy().astype(np.uint64) if counted else None), st, circ
+
+
+def load(idx):
+    return np.load(os.path.join(ROOT, "data", f"cfg{idx}.npz"))
+
+
+def test_config0_all_outputs(lofp):
+    c = li.config(0)
+    T = c.draw_outputs()
+    got, cnt, st, _ = run(lofp, c.M, c.layers, c.S, T)
+    ref, leaves = oracle.path_sum(c.M, c.layers, c.S, T, return_leaves=True)
+    ok, err = tol_ok(got, ref)
+    assert ok, err
+    assert np.array_equal(cnt, leaves)
+    assert abs(np.sum(np.abs(got) ** 2) - 1) < 1e-12
+    # HOM-free sanity: amplitudes agree with Ryser too
+    assert tol_ok(got, oracle.amplitudes_permanent(c.M, c.layers, c.S, T))[0]
+
+
+def test_config1_literal_batch(lofp):
+    c = li.config(1)
+    d = load(1)
+    T = d["T_literal"].astype(np.int32)
+    got, cnt, st, _ = run(lofp, c.M, c.layers, c.S, T)
+    assert np.array_equal(cnt, d["P_literal"])
+    ref = oracle.path_sum(c.M, c.layers, c.S, T)
+    ok, err = tol_ok(got, ref)
+    assert ok, err
+    assert st["feasible"] == int((d["P_literal"] > 0).sum())
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_circuits(lofp, seed):
+    """Partial layers, reversed pairs, every depth 0..7, all outputs."""
+    rng = np.random.default_rng(9000 + seed)
+    M = int(rng.integers(1, 10))
+    D = int(rng.integers(0, 8))
+    N = int(rng.integers(0, 6))
+    layers = li.random_nn_circuit(M, D, rng, fill=float(rng.uniform(0.4, 1.0)), reverse_prob=0.4)
+    S = np.zeros(M, dtype=np.int32)
+    for m in rng.integers(0, M, size=N):
+        S[m] += 1
+    T = li.all_outputs(M, N)
+    if len(T) > 300:
+        T = T[rng.choice(len(T), 300, replace=False)]
+    # add rows with the wrong photon number
+    T = np.concatenate([T, np.clip(T[:3] + 1, 0, None)])
+    got, cnt, st, _ = run(lofp, M, layers, S, T)
+    ref, leaves = oracle.path_sum(M, layers, S, T, return_leaves=True)
+    ok, err = tol_ok(got, ref)
+    assert ok, err
+    assert np.array_equal(cnt, leaves)
+
+
+def test_bunched_and_special_angles(lofp):
+    rng = np.random.default_rng(5)
+    M, D = 8, 6
+    layers = li.clements_mesh(M, D, seed=11)
+    # theta exactly 0 and pi/2 on some BS (0^0 cases)
+    layers = [[(a, b, (0.0 if (i + l) % 3 == 0 else (math.pi / 2 if (i + l) % 3 == 1 else th)), ph)
+               for i, (a, b, th, ph) in enumerate(layer)] for l, layer in enumerate(layers)]
+    S = np.array([3, 0, 0, 2, 0, 0, 1, 0], dtype=np.int32)
+    T = li.all_outputs(M, 6)
+    T = T[rng.choice(len(T), 400, replace=False)]
+    got, cnt, _, _ = run(lofp, M, layers, S, T)
+    ref, leaves = oracle.path_sum(M, layers, S, T, return_leaves=True)
+    assert tol_ok(got, ref)[0]
+    assert np.array_equal(cnt, leaves)
+
+
+@pytest.mark.parametrize("idx", [2, 3, 4])
+def test_conditioned_batch_counts_full_size(lofp, idx):
+    """Full conditioned batch, bench launch configuration: exact path count per output."""
+    c = li.config(idx)
+    d = load(idx)
+    T = d["T_cond"].astype(np.int32)
+    got, cnt, st, _ = run(lofp, c.M, c.layers, c.S, T)
+    assert np.array_equal(cnt, d["P_cond"])
+    assert np.isfinite(got).all()
+    assert st["feasible"] == len(T)
+
+
+@pytest.mark.parametrize("idx", [2, 3, 4])
+def test_conditioned_batch_sampled_values(lofp, idx):
+    """Full conditioned batch through the normal (uncounted) path; sampled outputs checked
+    one by one against the oracle path sum (small P) and Ryser (any P)."""
+    c = li.config(idx)
+    d = load(idx)
+    T = d["T_cond"].astype(np.int32)
+    P = d["P_cond"]
+    got, _, _, _ = run(lofp, c.M, c.layers, c.S, T, counted=False)
+    order = np.argsort(P, kind="stable")
+    small = order[:12]
+    ref = oracle.path_sum(c.M, c.layers, c.S, T[small])
+    ok, err = tol_ok(got[small], ref)
+    assert ok, err
+    rng = np.random.default_rng(idx)
+    pick = rng.choice(len(T), 6 if idx == 4 else 24, replace=False)
+    refr = oracle.amplitudes_permanent(c.M, c.layers, c.S, T[pick])
+    ok, err = tol_ok(got[pick], refr)
+    assert ok, err
+
+
+def test_config2_literal_structural_zeros(lofp):
+    c = li.config(2)
+    d = load(2)
+    T = d["T_literal"].astype(np.int32)
+    got, cnt, st, _ = run(lofp, c.M, c.layers, c.S, T)
+    reach = oracle.reachable(c.M, c.layers, c.S, T)
+    assert np.array_equal(cnt, d["P_literal"])
+    assert (got[~reach] == 0).all()
+    assert st["feasible"] == int(reach.sum())
+
+
+def test_config3_literal_small_outputs(lofp):
+    """Literal configs[3] draws whose tree is small enough to enumerate."""
+    c = li.config(3)
+    d = load(3)
+    sel = np.nonzero(d["P_literal"] <= 2 * 10 ** 8)[0]
+    T = d["T_literal"][sel].astype(np.int32)
+    got, cnt, _, _ = run(lofp, c.M, c.layers, c.S, T)
+    assert np.array_equal(cnt, d["P_literal"][sel])
+    pick = sel[np.argsort(d["P_literal"][sel])[:8]]
+    ref = oracle.path_sum(c.M, c.layers, c.S, d["T_literal"][pick].astype(np.int32))
+    idx = [int(np.nonzero(sel == p)[0][0]) for p in pick]
+    assert tol_ok(got[idx], ref)[0]
+
+
+def test_host_api_matches_device_api(lofp):
+    c = li.config(1)
+    T = load(1)["T_literal"].astype(np.int32)[:200]
+    circ = lofp.Circuit(c.M, c.layers)
+    a_host = circ.amplitudes_host(c.S, T)
+    a_dev = circ.amplitudes(c.S, torch.from_numpy(T).cuda()).cpu().numpy()
+    torch.cuda.synchronize()
+    assert tol_ok(a_host, a_dev)[0]
+
+
+def test_edge_cases(lofp):
+    # vacuum, identity, D = 0, M = 1, empty batch
+    c = li.config(1)
+    got, cnt, _, _ = run(lofp, c.M, c.layers, np.zeros(c.M, dtype=np.int32), np.zeros((2, c.M), dtype=np.int32))
+    assert np.all(got == 1) and np.all(cnt == 1)
+    got, _, _, _ = run(lofp, 4, [], [1, 0, 2, 0], np.array([[1, 0, 2, 0], [0, 1, 2, 0]]))
+    assert got.tolist() == [1, 0]
+    got, _, _, _ = run(lofp, 1, [[], []], [3], np.array([[3], [2]]))
+    assert got.tolist() == [1, 0]
+    circ = lofp.Circuit(c.M, c.layers)
+    out = circ.amplitudes(c.S, torch.zeros((0, c.M), dtype=torch.int32, device="cuda"))
+    assert out.shape == (0,)
+    # a negative entry: NaN for that row, LOFP_E_BAD_OUTPUT from stats
+    T = load(1)["T_literal"].astype(np.int32)[:4].copy()
+    T[2, 3] = -1
+    a = circ.amplitudes(c.S, torch.from_numpy(T).cuda())
+    torch.cuda.synchronize()
+    a = a.cpu().numpy()
+    st = circ.stats()
+    assert np.isnan(a[2]) and np.isfinite(a[[0, 1, 3]]).all()
+    assert st["status"] == 5 and st["bad_rows"] == 1
+    # argument errors
+    with pytest.raises(lofp.LofpError):
+        lofp.Circuit(4, [[(0, 1, 0.1, 0.2), (1, 2, 0.3, 0.4)]])  # overlapping pairs
+    with pytest.raises(lofp.LofpError):
+        lofp.Circuit(4, [[(0, 1, float("nan"), 0.2)]])
+    with pytest.raises(lofp.LofpError):
+        circ.amplitudes(-np.ones(c.M, dtype=np.int32), torch.zeros((1, c.M), dtype=torch.int32, device="cuda"))
+
+
+def test_reversed_pairs_equal_swapped_phase(lofp):
+    rng = np.random.default_rng(77)
+    M = 7
+    layers = li.random_nn_circuit(M, 5, rng)
+    rev = [[(b, a, th, ph) for (a, b, th, ph) in l] for l in layers]
+    S = np.array([1, 1, 0, 2, 0, 0, 1], dtype=np.int32)
+    T = li.all_outputs(M, 5)[:200]
+    g1, _, _, _ = run(lofp, M, rev, S, T, counted=False)
+    ref = oracle.path_sum(M, rev, S, T)
+    assert tol_ok(g1, ref)[0]
