@@ -1,0 +1,31 @@
+"""Quick GPU throughput probe (development aid, not the bench): times lofp_amplitudes on a
+prefix of each config's batch sized to a path budget."""
+import os, sys, time, json
+import numpy as np
+import torch
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import lofp_inputs as li
+from paper_2510_26408_b200 import Circuit
+
+budget = float(sys.argv[1]) if len(sys.argv) > 1 else 2e10
+for idx in (1, 2, 3, 4):
+    c = li.config(idx)
+    d = np.load(os.path.join(ROOT, "data", f"cfg{idx}.npz"))
+    T = (d["T_cond"] if "T_cond" in d.files else d["T_literal"]).astype(np.int32)
+    P = (d["P_cond"] if "P_cond" in d.files else d["P_literal"]).astype(np.float64)
+    n = int(np.searchsorted(np.cumsum(P), budget)) if P.sum() > budget else len(P)
+    n = max(n, 1)
+    T, P = T[:n], P[:n]
+    circ = Circuit(c.M, c.layers)
+    Td = torch.from_numpy(T).cuda()
+    circ.amplitudes(c.S, Td[: min(n, 64)]); torch.cuda.synchronize()
+    res = []
+    for rep in range(2):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(); a = circ.amplitudes(c.S, Td); e1.record(); torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1); st = circ.stats()
+        res.append(ms)
+    print(json.dumps(dict(cfg=idx, outputs=n, paths=P.sum(), ms=min(res), paths_per_s=P.sum() / (min(res) * 1e-3),
+                          enum_ms=st["enum_ms"], total_ms=st["total_ms"], items=st["items"], donations=st["donations"],
+                          levels=st["levels"], entries=st["table_entries"], smem=st["smem_bytes"], grid=st["grid_blocks"])), flush=True)
