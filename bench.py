@@ -1,0 +1,307 @@
+"""Benchmark of the LOFP path sum on B200 (BASELINE.json metric: paths/s and amplitudes/s
+on 1 B200; FP64-pipe fraction of roofline).
+
+One *step* = one call of the hot path (``lofp_amplitudes``: prep, Appendix-A tables,
+per-output plans, path enumeration) over one batch of outputs resident in HBM.  The
+default workload is BASELINE.json configs[2] (M=32, N=16, D=6) with its batch of 4096
+outputs conditioned on structural reachability and at most 1e9 paths per output
+(reading R14; the literal batch is ~100% structural zeros).  ``--config`` picks
+another config (0/1 literal batches, 2-4 conditioned).  Inputs are the seeded synthetic
+batches in data/ (written by scripts/make_batches.py).
+
+Launch: ``python bench.py [--gpus N --steps K --warmup W]``; N > 1 under torchrun, one
+rank per GPU, outputs sharded across ranks (no collective on the data path; strong
+scaling of a fixed batch).  ``--impl reference`` times the CPU oracle instead.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DATA = os.path.join(ROOT, "data")
+L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["lofp", "reference"], default="lofp")
+    p.add_argument("--config", type=int, default=2)
+    p.add_argument("--outputs", type=int, default=0, help="limit the batch to its first N outputs")
+    p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--cpu-paths", type=float, default=6e7, help="paths in the cpu_baseline sample")
+    return p.parse_args()
+
+
+def workload(idx: int, limit: int = 0):
+    import lofp_inputs as li
+    c = li.config(idx)
+    d = np.load(os.path.join(DATA, f"cfg{idx}.npz"))
+    if "T_cond" in d.files:
+        T, P, kind = d["T_cond"].astype(np.int32), d["P_cond"].astype(np.uint64), "conditioned"
+    else:
+        T, P, kind = d["T_literal"].astype(np.int32), d["P_literal"].astype(np.uint64), "literal"
+    if limit:
+        T, P = T[:limit], P[:limit]
+    return c, T, P, kind
+
+
+def shard(P, rank, world):
+    """Longest-first round robin over ranks (balanced by exact path counts)."""
+    order = np.argsort(-P.astype(np.float64), kind="stable")
+    return np.sort(order[rank::world])
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+
+        def reader():
+            for line in self.proc.stdout:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 7:
+                    self.rows.append(parts)
+
+        self.thread = threading.Thread(target=reader, daemon=True)
+        self.thread.start()
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=5)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_sample(c, T, P, budget):
+    """Smallest-P outputs of the batch up to `budget` paths (a bounded oracle sample)."""
+    order = np.argsort(P.astype(np.float64), kind="stable")
+    cs = np.cumsum(P[order].astype(np.float64))
+    n = max(1, int(np.searchsorted(cs, budget)))
+    sel = np.sort(order[:n])
+    return sel
+
+
+def run_oracle(c, T, P, sel):
+    import oracle
+    oracle.build()
+    t0 = time.perf_counter()
+    oracle.path_sum(c.M, c.layers, c.S, T[sel])
+    dt = time.perf_counter() - t0
+    return float(P[sel].astype(np.float64).sum()), dt
+
+
+def reference_arm(args, rank, world):
+    """--impl reference: the CPU oracle as it stands, on the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    c, T, P, kind = workload(args.config, args.outputs)
+    sel = cpu_sample(c, T, P, args.cpu_paths / 4)
+    cores = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        run_oracle(c, T, P, sel[: max(1, len(sel) // 8)])
+    tot_paths, tot_s = 0.0, 0.0
+    for _ in range(args.steps):
+        p, dt = run_oracle(c, T, P, sel)
+        tot_paths += p
+        tot_s += dt
+    v = tot_paths / tot_s
+    line = {
+        "impl": "reference", "metric": "paths/s", "value": v, "unit": "paths/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64 (long double accumulate)",
+        "data": "synthetic", "config": {"workload": f"configs[{args.config}] {kind} batch (oracle sample)",
+                                        "sample_outputs": int(len(sel))},
+        "amplitudes_per_s": len(sel) * args.steps / tot_s,
+        "cpu_baseline": {"value": v, "unit": "paths/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{len(sel)} smallest-path outputs of the batch, {p:.3e} paths per step"},
+        "e2e": {"value": v, "unit": "paths/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        reference_arm(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2510_26408_b200 import Circuit
+    from paper_2510_26408_b200 import _build
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    c, T_all, P_all, kind = workload(args.config, args.outputs)
+    mine = shard(P_all, rank, world)
+    T, P = T_all[mine], P_all[mine]
+    circ = Circuit(c.M, c.layers)
+    Td = torch.from_numpy(np.ascontiguousarray(T)).to(dev)
+    B = len(T)
+    out = torch.empty((B, 2), dtype=torch.float64, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    # validation pass (untimed): exact path counts must equal the oracle's (data/), and
+    # the kernel's own count of non-vacuum complex multiplications sizes the roofline
+    counts = torch.zeros(B, dtype=torch.int64, device=dev)
+    circ.amplitudes(c.S, Td, out=out, counts=counts)
+    torch.cuda.synchronize()
+    vst = circ.stats()
+    got = counts.cpu().numpy().astype(np.uint64)
+    if not np.array_equal(got, P):
+        raise SystemExit(f"path counts differ from the oracle's on {int((got != P).sum())} outputs")
+    cmuls, paths = int(vst["cmuls"]), int(vst["paths"])
+
+    for _ in range(args.warmup):
+        circ.amplitudes(c.S, Td, out=out)
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ms, enum_ms = [], []
+    for _ in range(args.steps):
+        flush.fill_(1)  # L2 flush outside the timed events
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        circ.amplitudes(c.S, Td, out=out)
+        e1.record(stream)
+        e1.synchronize()
+        ms.append(e0.elapsed_time(e1))
+        enum_ms.append(circ.stats()["enum_ms"])
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    t_local = float(np.sum(ms))
+    t = torch.tensor([t_local], dtype=torch.float64, device=dev)
+    tot = torch.tensor([float(P.astype(np.float64).sum()), float(B)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    t_max = float(t.item())
+    paths_all, outs_all = float(tot[0].item()), float(tot[1].item())
+    value = paths_all * args.steps / (t_max * 1e-3)
+
+    # end to end through the public host API: H2D of T, D2H of the amplitudes each step
+    e2e = None
+    if not args.no_e2e:
+        Th = torch.from_numpy(np.ascontiguousarray(T)).pin_memory().numpy()
+        circ.amplitudes_host(c.S, Th)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            circ.amplitudes_host(c.S, Th)
+        dt = time.perf_counter() - t0
+        tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": paths_all * args.steps / float(tt.item()), "unit": "paths/s",
+               "h2d_bytes_per_step": int(T.nbytes), "d2h_bytes_per_step": int(B * 16)}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # roofline of the dominant kernel (path enumeration): algorithmic FP64 lane
+    # instructions = 4 per non-vacuum complex multiplication + 2 per path (leaf sum),
+    # over its device time (CUDA events on the launching stream, inside liblofp)
+    lib = ctypes.CDLL(_build.PEAK_LIB)
+    lib.lofp_probe_fp64_dfma_rate.restype = ctypes.c_double
+    lib.lofp_probe_fp64_dfma_rate.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+    nsm = ctypes.c_int(0)
+    peak_meas = lib.lofp_probe_fp64_dfma_rate(5, ctypes.byref(nsm)) / 1e12
+    enum_mean = float(np.mean(enum_ms))
+    alg = 4.0 * cmuls + 2.0 * paths
+    achieved = alg / (enum_mean * 1e-3) / 1e12
+    roofline = {"bound": "alu", "achieved": achieved, "peak": peak_meas, "unit": "TFP64-inst/s",
+                "frac": achieved / peak_meas if peak_meas > 0 else None, "traffic": None,
+                "peak_source": f"measured DFMA issue rate (fp64_peak.cu, {nsm.value} SMs, burst)",
+                "nominal_peak": 148 * 64 * 1965e6 / 1e12,
+                "work_per_launch": {"cmuls": cmuls, "paths": paths, "fp64_lane_inst": alg},
+                "kernel_ms": enum_mean, "kernel_share_of_step": enum_mean / (t_local / args.steps)}
+
+    cpu = None
+    if not args.no_cpu and world == 1:
+        sel = cpu_sample(c, T_all, P_all, args.cpu_paths)
+        p, dt = run_oracle(c, T_all, P_all, sel)
+        cpu = {"value": p / dt, "unit": "paths/s", "cores": os.cpu_count(), "kind": "oracle",
+               "sample": f"{len(sel)} smallest-path outputs of the batch ({p:.3e} paths), {dt:.1f} s"}
+
+    line = {
+        "metric": "paths/s", "value": value, "unit": "paths/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"configs[{args.config}] {kind} batch: M={c.M} N={c.N} D={c.D}, "
+                               f"{int(outs_all)} outputs, {paths_all:.4e} paths",
+                   "global_batch": int(outs_all), "parallelism": f"outputs sharded over {world} GPU(s)",
+                   "l2": "flushed between steps (256 MiB write)"},
+        "amplitudes_per_s": outs_all * args.steps / (t_max * 1e-3),
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": 4 * args.steps,
+        "clocks": clk,
+        "stats": {k: vst[k] for k in ("feasible", "items", "spills", "donations", "overflows", "levels",
+                                      "table_entries", "smem_bytes", "grid_blocks", "block_threads")},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

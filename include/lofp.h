@@ -120,12 +120,16 @@ const char *lofp_last_error(const lofp_ctx *ctx);
  * synchronises the call's stream. */
 typedef struct {
   int64_t batch;          /* B of the last call */
-  int64_t feasible;       /* outputs with sum T = sum S that are structurally reachable */
-  int64_t items;          /* work items processed by the enumeration kernel */
-  int64_t donations;      /* subtrees handed to other lanes through the work queue */
-  int32_t levels;         /* free DFS levels of the circuit (green waveguides) */
+  int64_t feasible;       /* outputs whose path tree has at least one free level */
+  int64_t items;          /* work items (subtrees) processed by the enumeration kernel */
+  int64_t spills;         /* subtrees pushed to the global work queue */
+  int64_t donations;      /* subtrees handed between lanes of one warp */
+  int64_t overflows;      /* branch-stack entries that went to the local overflow */
+  int64_t paths;          /* valid paths summed (lofp_amplitudes_counted only, else 0) */
+  int64_t cmuls;          /* non-vacuum complex multiplications (counted only, else 0) */
+  int32_t levels;         /* largest number of free DFS levels of one output */
   int32_t table_entries;  /* Appendix-A elements staged in shared memory */
-  int32_t smem_bytes;     /* dynamic shared memory of the enumeration kernel */
+  int32_t smem_bytes;     /* dynamic shared memory per block of the enumeration kernel */
   int32_t grid_blocks;    /* persistent grid size */
   int32_t block_threads;  /* threads per block */
   int32_t bad_rows;       /* rows with a negative entry (their amplitude is NaN) */

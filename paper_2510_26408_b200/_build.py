@@ -1,4 +1,4 @@
-"""Compile liblofp.so in-tree for sm_100a (nvcc, no JIT cache)."""
+"""Compile liblofp.so (and the bench's FP64 peak probe) in-tree for sm_100a (nvcc, no JIT cache)."""
 from __future__ import annotations
 
 import os
@@ -10,6 +10,8 @@ CSRC = os.path.join(HERE, "csrc")
 SOURCES = [os.path.join(CSRC, f) for f in ("lofp_kernels.cu", "lofp_host.cpp")]
 HEADERS = [os.path.join(CSRC, "lofp_internal.h"), os.path.join(ROOT, "include", "lofp.h")]
 LIB = os.path.join(HERE, "liblofp.so")
+PEAK_SRC = os.path.join(CSRC, "fp64_peak.cu")
+PEAK_LIB = os.path.join(HERE, "libfp64peak.so")
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-cudart", "static"]
@@ -22,11 +24,16 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    newest = max(os.path.getmtime(p) for p in SOURCES + HEADERS)
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
-        tmp = LIB + f".tmp{os.getpid()}"
-        cmd = [nvcc()] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-o", tmp] + SOURCES
+def _compile(out, sources, deps, force, verbose):
+    newest = max(os.path.getmtime(p) for p in sources + deps)
+    if force or not os.path.exists(out) or os.path.getmtime(out) < newest:
+        tmp = out + f".tmp{os.getpid()}"
+        cmd = [nvcc()] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-o", tmp] + sources
         subprocess.check_call(cmd)
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, out)
+    return out
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    _compile(PEAK_LIB, [PEAK_SRC], [], force, False)
+    return _compile(LIB, SOURCES, HEADERS, force, verbose)

@@ -1,7 +1,7 @@
 // lofp_host.cpp — host side of liblofp: the C ABI of include/lofp.h, circuit
-// canonicalisation, light-cone topology maps, DFS level / factor planning, per-call
-// Appendix-A table layout and kernel launches.  See DESIGN.md for the derivations
-// (readings R1-R9) and the paper passages each step follows.
+// canonicalisation, light-cone topology maps, per-call Appendix-A table layout and the
+// kernel launches.  See DESIGN.md for the derivations (readings R1-R9) and the paper
+// passages each step follows.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -67,23 +67,18 @@ struct CanonBS {
 }  // namespace
 
 struct lofp_ctx {
-  int M = 0, D = 0, nbs = 0;
-  std::vector<CanonBS> bs;                  // layer-major
+  int M = 0, D = 0, nbs = 0, Lg = 0;
+  std::vector<CanonBS> bs;                  // layer-major, by cut inside a layer
   std::vector<std::vector<uint8_t>> act;    // [D+1][M+1]
-  std::vector<std::vector<int>> rho, sigma; // [D+1][M+1]
-  std::vector<std::vector<int>> varlevel;   // [D+1][M+1]: DFS level of free output (l,k) or -1
-  std::vector<LevelDesc> levels;            // [L]
-  std::vector<FactorDesc> factors;          // root factors first, then by level
-  int L = 0, nroot = 0;
+  std::vector<uint8_t> maps;                // [4][D+1][M+1]: rho, sigma, rho', sigma'
   // static device data
-  DevBuf d_levels, d_factors, d_rho0, d_sigma0, d_bs_cs;
+  DevBuf d_maps, d_bs_lk, d_bs_cs;
   // per-call device data
-  DevBuf d_flags, d_G, d_root, d_feas, d_ctr, d_ring, d_edesc, d_offsets, d_entries, d_cumS;
+  DevBuf d_flags, d_plans, d_feas, d_ctr, d_ring, d_edesc, d_offsets, d_entries, d_cumS, d_bsrow;
   DevBuf d_hostT, d_hostA;
   HostPinned h_stage, h_ctr;
   unsigned ring_cap = 0;
-  cudaEvent_t ev_start = nullptr, ev_enum0 = nullptr, ev_enum1 = nullptr, ev_end = nullptr,
-              ev_upload = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_enum0 = nullptr, ev_enum1 = nullptr, ev_end = nullptr;
   cudaStream_t own_stream = nullptr;
   bool have_call = false;
   lofp_run_stats stats{};
@@ -103,104 +98,49 @@ lofp_status cuda_fail(lofp_ctx *c, cudaError_t e, const char *where) {
   return fail(c, e == cudaErrorMemoryAllocation ? LOFP_E_OOM : LOFP_E_CUDA, m);
 }
 
-#define CK(expr, where)                              \
-  do {                                               \
-    cudaError_t _e = (expr);                         \
+#define CK(expr, where)                                      \
+  do {                                                       \
+    cudaError_t _e = (expr);                                 \
     if (_e != cudaSuccess) return cuda_fail(ctx, _e, where); \
   } while (0)
 
-// Value references into the per-lane array [levels | G(0..M) | cumS(0..M)].
-inline uint16_t refG(const lofp_ctx *c, int k) { return (uint16_t)(c->L + k); }
-inline uint16_t refS(const lofp_ctx *c, int k) { return (uint16_t)(c->L + c->M + 1 + k); }
-
-// Reference of F_t(k): the latest BS output at cut k in layers <= t, else cum(S)(k).
-// Forced outputs (rho == sigma) equal G(k) (reading R5); cuts 0 and M are G(0) = 0 and
-// G(M) = N.
-uint16_t ref_of(const lofp_ctx *c, int t, int k) {
-  if (k <= 0) return refG(c, 0);
-  if (k >= c->M) return refG(c, c->M);
-  for (int l = t; l >= 1; --l) {
-    if (c->act[l][k]) {
-      int v = c->varlevel[l][k];
-      return v >= 0 ? (uint16_t)v : refG(c, k);
-    }
-  }
-  return refS(c, k);
-}
-
+// Topology-only light-cone maps (reading R5).  Backward: rho_D(k) = sigma_D(k) = k and,
+// going back through layer l, an active cut k takes rho_{l-1}(k) = rho_l(k-1),
+// sigma_{l-1}(k) = sigma_l(k+1); then F_l(k) lies in [G(rho_l(k)), G(sigma_l(k))].
+// Forward (the same construction from the input side): rho'_0(k) = sigma'_0(k) = k,
+// rho'_l(k) = rho'_{l-1}(k-1), sigma'_l(k) = sigma'_{l-1}(k+1) at active cuts; then
+// F_l(k) lies in [cumS(rho'_l(k)), cumS(sigma'_l(k))] (P:153-164 cones, cumulative form).
 lofp_status plan_circuit(lofp_ctx *c) {
-  const int M = c->M, D = c->D;
+  const int M = c->M, D = c->D, W = M + 1;
   c->act.assign(D + 1, std::vector<uint8_t>(M + 1, 0));
   for (const CanonBS &b : c->bs) c->act[b.layer][b.cut] = 1;
-  // Box index maps (reading R5): rho_D(k) = sigma_D(k) = k; going back through layer l,
-  // an active cut k takes rho_{l-1}(k) = rho_l(k-1), sigma_{l-1}(k) = sigma_l(k+1).
-  c->rho.assign(D + 1, std::vector<int>(M + 1));
-  c->sigma.assign(D + 1, std::vector<int>(M + 1));
-  for (int k = 0; k <= M; ++k) c->rho[D][k] = c->sigma[D][k] = k;
+  c->maps.assign(4 * (D + 1) * W, 0);
+  uint8_t *rho = c->maps.data(), *sig = rho + (D + 1) * W, *frho = sig + (D + 1) * W, *fsig = frho + (D + 1) * W;
+  for (int k = 0; k <= M; ++k) rho[D * W + k] = sig[D * W + k] = (uint8_t)k;
   for (int l = D; l >= 1; --l)
     for (int k = 0; k <= M; ++k) {
-      c->rho[l - 1][k] = c->act[l][k] ? c->rho[l][k - 1] : c->rho[l][k];
-      c->sigma[l - 1][k] = c->act[l][k] ? c->sigma[l][k + 1] : c->sigma[l][k];
+      rho[(l - 1) * W + k] = c->act[l][k] ? rho[l * W + k - 1] : rho[l * W + k];
+      sig[(l - 1) * W + k] = c->act[l][k] ? sig[l * W + k + 1] : sig[l * W + k];
     }
-  // DFS levels: free BS outputs in layer-major order (the green waveguides)
-  c->varlevel.assign(D + 1, std::vector<int>(M + 1, -1));
-  int L = 0;
-  std::vector<std::pair<int, int>> lv;  // (l, k)
+  for (int k = 0; k <= M; ++k) frho[k] = fsig[k] = (uint8_t)k;
   for (int l = 1; l <= D; ++l)
-    for (int k = 1; k < M; ++k)
-      if (c->act[l][k] && c->rho[l][k] != c->sigma[l][k]) {
-        c->varlevel[l][k] = L++;
-        lv.push_back({l, k});
-      }
+    for (int k = 0; k <= M; ++k) {
+      frho[l * W + k] = c->act[l][k] ? frho[(l - 1) * W + k - 1] : frho[(l - 1) * W + k];
+      fsig[l * W + k] = c->act[l][k] ? fsig[(l - 1) * W + k + 1] : fsig[(l - 1) * W + k];
+    }
+  // global bound on DFS levels: BS outputs whose backward box is not a single cut
+  int L = 0;
+  for (const CanonBS &b : c->bs)
+    if (rho[b.layer * W + b.cut] != sig[b.layer * W + b.cut]) ++L;
   if (L > LOFP_MAX_LEVELS) return fail(c, LOFP_E_UNSUPPORTED, "too many free BS outputs (DFS levels)");
-  c->L = L;
-  // factors: every BS element, attached to the deepest DFS level among its inputs
-  struct F {
-    int level;
-    FactorDesc d;
-  };
-  std::vector<F> fs;
-  for (int i = 0; i < c->nbs; ++i) {
-    const CanonBS &b = c->bs[i];
-    FactorDesc d{};
-    d.xl = ref_of(c, b.layer - 1, b.cut - 1);
-    d.xm = ref_of(c, b.layer - 1, b.cut);
-    d.xr = ref_of(c, b.layer - 1, b.cut + 1);
-    d.y = ref_of(c, b.layer, b.cut);
-    d.bs = (uint16_t)i;
-    int at = -1;
-    for (uint16_t r : {d.xl, d.xm, d.xr, d.y})
-      if (r < L) at = std::max(at, (int)r);
-    fs.push_back({at, d});
-  }
-  std::stable_sort(fs.begin(), fs.end(), [](const F &a, const F &b) { return a.level < b.level; });
-  c->factors.clear();
-  c->nroot = 0;
-  for (const F &f : fs) {
-    if (f.level < 0) ++c->nroot;
-    c->factors.push_back(f.d);
-  }
-  c->levels.assign(L, LevelDesc{});
-  size_t fi = c->nroot;
-  for (int j = 0; j < L; ++j) {
-    int l = lv[j].first, k = lv[j].second;
-    LevelDesc &d = c->levels[j];
-    d.refL = ref_of(c, l - 1, k - 1);
-    d.refR = ref_of(c, l - 1, k + 1);
-    d.gLo = refG(c, c->rho[l][k]);
-    d.gHi = refG(c, c->sigma[l][k]);
-    d.fbeg = (uint16_t)fi;
-    while (fi < fs.size() && fs[fi].level == j) ++fi;
-    d.fend = (uint16_t)fi;
-  }
+  c->Lg = L;
   return LOFP_OK;
 }
 
 // Per-segment occupation caps: min(photons of S in the past light cone, photons of
 // max-over-batch T in the future light cone).  cap[j][m] for the segment of
 // mode m after layer j.
-std::vector<std::vector<int>> segment_caps(const lofp_ctx *c, const std::vector<int> &S,
-                                           const int32_t *tmax) {
+std::vector<std::vector<int>> segment_caps(const lofp_ctx *c, const std::vector<int> &S, const int32_t *tmax) {
   const int M = c->M, D = c->D;
   std::vector<std::vector<int>> cap(D + 1, std::vector<int>(M, 0));
   std::vector<std::vector<const CanonBS *>> byl(D + 1);
@@ -214,26 +154,30 @@ std::vector<std::vector<int>> segment_caps(const lofp_ctx *c, const std::vector<
         for (const CanonBS *b : byl[l])
           if (in[b->cut - 1] || in[b->cut]) in[b->cut - 1] = in[b->cut] = 1;
       int past = 0;
-      for (int i = 0; i < M; ++i) if (in[i]) past += S[i];
+      for (int i = 0; i < M; ++i)
+        if (in[i]) past += S[i];
       std::fill(in.begin(), in.end(), 0);
       in[m] = 1;
       for (int l = j + 1; l <= D; ++l)
         for (const CanonBS *b : byl[l])
           if (in[b->cut - 1] || in[b->cut]) in[b->cut - 1] = in[b->cut] = 1;
       int fut = 0;
-      for (int i = 0; i < M; ++i) if (in[i]) fut += tmax[i];
+      for (int i = 0; i < M; ++i)
+        if (in[i]) fut += tmax[i];
       cap[j][m] = std::min(past, fut);
     }
   return cap;
 }
 
-lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const int32_t *output_occ,
-                double *amps, unsigned long long *counts, cudaStream_t stream) {
+inline size_t round16(size_t x) { return (x + 15) & ~size_t(15); }
+
+lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const int32_t *output_occ, double *amps,
+                unsigned long long *counts, cudaStream_t stream) {
   if (!ctx) return LOFP_E_INVALID_ARG;
   ctx->err.clear();
   if (!input_occ || batch < 0) return fail(ctx, LOFP_E_INVALID_ARG, "null input_occ or negative batch");
   if (batch > 0 && (!output_occ || !amps)) return fail(ctx, LOFP_E_INVALID_ARG, "null output_occ or amps");
-  if (batch > (int64_t)0xffffffff) return fail(ctx, LOFP_E_UNSUPPORTED, "batch too large");
+  if (batch > (int64_t)0x7fffffff) return fail(ctx, LOFP_E_UNSUPPORTED, "batch too large");
   const int M = ctx->M;
   std::vector<int> S(M);
   int N = 0;
@@ -246,43 +190,41 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
   CK(cudaSetDevice(ctx->device), "cudaSetDevice");
   ctx->stats = lofp_run_stats{};
   ctx->stats.batch = batch;
-  ctx->stats.levels = ctx->L;
   ctx->have_call = false;
   if (batch == 0) return LOFP_OK;
   // serialise with this context's previous call (its buffers are reused)
-  CK(cudaStreamWaitEvent(stream, ctx->ev_end, 0), "cudaStreamWaitEvent");
-  CK(cudaEventSynchronize(ctx->ev_upload), "cudaEventSynchronize");
+  CK(cudaEventSynchronize(ctx->ev_end), "cudaEventSynchronize");
 
   const int64_t B = batch;
   CallArgs a{};
   a.M = M;
   a.D = ctx->D;
   a.N = N;
-  a.L = ctx->L;
+  a.nbs = ctx->nbs;
+  a.Lg = ctx->Lg;
+  a.vals_slots = (int)((ctx->Lg + 1 + 3) & ~3);
   a.B = B;
-  a.grow = ((M + 1) + 15) & ~15;
+  a.plan_stride = (int)round16(sizeof(PlanHead) + (size_t)ctx->Lg * sizeof(PlanLevel) +
+                               2 * (size_t)ctx->nbs * sizeof(PlanFactor) + 2 * (size_t)ctx->nbs);
   a.T = output_occ;
   a.amps = amps;
   a.counts = counts;
   CK(ctx->d_flags.ensure((size_t)B), "alloc flags");
-  CK(ctx->d_G.ensure((size_t)B * a.grow), "alloc G");
-  CK(ctx->d_root.ensure((size_t)B * 16), "alloc root");
+  CK(ctx->d_plans.ensure((size_t)B * a.plan_stride), "alloc plans");
   CK(ctx->d_feas.ensure((size_t)B * 4), "alloc feas");
   CK(ctx->d_ctr.ensure(sizeof(Counters)), "alloc counters");
   CK(ctx->d_cumS.ensure(256), "alloc cumS");
   a.flags = (uint8_t *)ctx->d_flags.p;
-  a.G = (uint8_t *)ctx->d_G.p;
-  a.root = (double *)ctx->d_root.p;
+  a.plans = (unsigned char *)ctx->d_plans.p;
   a.feas = (uint32_t *)ctx->d_feas.p;
   a.ctr = (Counters *)ctx->d_ctr.p;
-  a.rho0 = (const uint8_t *)ctx->d_rho0.p;
-  a.sigma0 = (const uint8_t *)ctx->d_sigma0.p;
   a.cumS = (const uint8_t *)ctx->d_cumS.p;
-  a.levels = (const LevelDesc *)ctx->d_levels.p;
+  a.maps = (const uint8_t *)ctx->d_maps.p;
+  a.bs_lk = (const int16_t *)ctx->d_bs_lk.p;
   a.bs_cs = (const double *)ctx->d_bs_cs.p;
 
   CK(cudaEventRecord(ctx->ev_start, stream), "cudaEventRecord");
-  // cum(S) to the device (pinned staging; the previous upload has completed)
+  // cum(S) to the device (pinned staging; the previous call has completed)
   CK(ctx->h_stage.ensure(4096), "alloc staging");
   uint8_t *cs = (uint8_t *)ctx->h_stage.p;
   {
@@ -295,7 +237,7 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
   CK(cudaMemcpyAsync(ctx->d_cumS.p, cs, M + 1, cudaMemcpyHostToDevice, stream), "upload cumS");
   CK(cudaMemsetAsync(a.ctr, 0, sizeof(Counters), stream), "reset counters");
   CK(lofp_launch_prep(a, stream), "prep kernel");
-  // the batch's per-mode maximum sizes the tables (one synchronisation per call)
+  // (sync 1) the batch's per-mode maximum sizes the tables
   CK(ctx->h_ctr.ensure(sizeof(Counters)), "alloc pinned counters");
   CK(cudaMemcpyAsync(ctx->h_ctr.p, a.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, stream), "read tmax");
   CK(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
@@ -307,13 +249,13 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
   std::vector<std::vector<int>> cap = segment_caps(ctx, S, tmax);
   std::vector<int32_t> offsets;
   std::vector<EntryDesc> edesc;
-  std::vector<int32_t> offbase(ctx->nbs), stride(ctx->nbs);
+  std::vector<int32_t> bsrow(2 * std::max(ctx->nbs, 1));  // [base | stride]
   for (int i = 0; i < ctx->nbs; ++i) {
     const CanonBS &b = ctx->bs[i];
     int X1 = cap[b.layer - 1][b.cut - 1], X2 = cap[b.layer - 1][b.cut];
     int Y1 = cap[b.layer][b.cut - 1], Y2 = cap[b.layer][b.cut];
-    offbase[i] = (int32_t)offsets.size();
-    stride[i] = X2 + 1;
+    bsrow[i] = (int32_t)offsets.size();
+    bsrow[ctx->nbs + i] = X2 + 1;
     for (int x1 = 0; x1 <= X1; ++x1)
       for (int x2 = 0; x2 <= X2; ++x2) {
         int n = x1 + x2;
@@ -329,24 +271,16 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
         }
       }
   }
-  if (edesc.empty()) {  // keep one dummy entry so that pointers are valid
-    EntryDesc e{};
-    edesc.push_back(e);
-  }
-  std::vector<FactorDesc> facs = ctx->factors;
-  for (FactorDesc &f : facs) {
-    f.offbase = offbase[f.bs];
-    f.stride = (uint16_t)stride[f.bs];
-  }
-  a.nfactors = (int)facs.size();
-  a.nroot = ctx->nroot;
+  if (edesc.empty()) edesc.push_back(EntryDesc{});  // keep pointers valid
+  if (offsets.empty()) offsets.push_back(0);
   a.nentries = (int)edesc.size();
   a.noffsets = (int)offsets.size();
+  a.table_bytes = (int)round16((size_t)a.nentries * 16 + (size_t)a.noffsets * 4);
   CK(ctx->d_edesc.ensure(edesc.size() * sizeof(EntryDesc)), "alloc edesc");
-  CK(ctx->d_offsets.ensure(std::max<size_t>(offsets.size(), 1) * 4), "alloc offsets");
+  CK(ctx->d_offsets.ensure(offsets.size() * 4), "alloc offsets");
   CK(ctx->d_entries.ensure(edesc.size() * 16), "alloc entries");
-  CK(ctx->d_factors.ensure(std::max<size_t>(facs.size(), 1) * sizeof(FactorDesc)), "alloc factors");
-  size_t need = edesc.size() * sizeof(EntryDesc) + offsets.size() * 4 + facs.size() * sizeof(FactorDesc) + 64;
+  CK(ctx->d_bsrow.ensure(bsrow.size() * 4), "alloc bs rows");
+  size_t need = edesc.size() * sizeof(EntryDesc) + offsets.size() * 4 + bsrow.size() * 4 + 64;
   CK(ctx->h_stage.ensure(need), "alloc staging");
   {
     uint8_t *st = (uint8_t *)ctx->h_stage.p;
@@ -355,43 +289,50 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
     CK(cudaMemcpyAsync(ctx->d_edesc.p, st + o, edesc.size() * sizeof(EntryDesc), cudaMemcpyHostToDevice, stream),
        "upload edesc");
     o += edesc.size() * sizeof(EntryDesc);
-    if (!offsets.empty()) {
-      memcpy(st + o, offsets.data(), offsets.size() * 4);
-      CK(cudaMemcpyAsync(ctx->d_offsets.p, st + o, offsets.size() * 4, cudaMemcpyHostToDevice, stream),
-         "upload offsets");
-      o += offsets.size() * 4;
-    }
-    if (!facs.empty()) {
-      memcpy(st + o, facs.data(), facs.size() * sizeof(FactorDesc));
-      CK(cudaMemcpyAsync(ctx->d_factors.p, st + o, facs.size() * sizeof(FactorDesc), cudaMemcpyHostToDevice,
-                         stream),
-         "upload factors");
-    }
-    CK(cudaEventRecord(ctx->ev_upload, stream), "cudaEventRecord");
+    memcpy(st + o, offsets.data(), offsets.size() * 4);
+    CK(cudaMemcpyAsync(ctx->d_offsets.p, st + o, offsets.size() * 4, cudaMemcpyHostToDevice, stream),
+       "upload offsets");
+    o += offsets.size() * 4;
+    memcpy(st + o, bsrow.data(), bsrow.size() * 4);
+    CK(cudaMemcpyAsync(ctx->d_bsrow.p, st + o, bsrow.size() * 4, cudaMemcpyHostToDevice, stream), "upload bs rows");
   }
   a.edesc = (const EntryDesc *)ctx->d_edesc.p;
   a.offsets = (const int32_t *)ctx->d_offsets.p;
   a.entries = (double *)ctx->d_entries.p;
-  a.factors = (const FactorDesc *)ctx->d_factors.p;
+  a.bs_base = (const int32_t *)ctx->d_bsrow.p;
+  a.bs_stride = (const int32_t *)ctx->d_bsrow.p + ctx->nbs;
   ctx->stats.table_entries = a.nentries;
 
   CK(lofp_launch_tables(a, stream), "table kernel");
-  CK(lofp_launch_feasible(a, stream), "feasibility kernel");
+  CK(lofp_launch_plan(a, stream), "plan kernel");
+  // (sync 2) the largest per-output plan sizes the enumeration kernel's shared memory
+  CK(cudaMemcpyAsync(ctx->h_ctr.p, a.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, stream), "read plan sizes");
+  CK(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+  const int maxL = hc->maxL, maxF = hc->maxF;
+  ctx->stats.levels = maxL;
   CK(cudaEventRecord(ctx->ev_enum0, stream), "cudaEventRecord");
-  if (a.L > 0) {
+  if (hc->nfeas > 0) {
+    a.vals_slots = (maxL + 1 + 3) & ~3;
+    // plans were written with the zero slot of the global bound; re-base is not needed
+    // because the kernel only dereferences slots < maxL and the zero slot below
+    a.plan_smem = (int)round16(sizeof(PlanHead) + (size_t)(maxL + maxF) * 16);
+    a.maxfac = maxF;
+    a.warp_bytes = (int)round16((size_t)a.plan_smem + (size_t)a.vals_slots * 32 + (size_t)LOFP_STK * 32 * 20);
     int grid = 0, block = 0;
     size_t smem = 0;
     cudaError_t e = lofp_enum_config(a, counts != nullptr, &grid, &block, &smem);
-    if (e == cudaErrorInvalidConfiguration || smem > 227 * 1024)
+    if (e == cudaErrorInvalidConfiguration)
       return fail(ctx, LOFP_E_UNSUPPORTED, "BS tables do not fit in shared memory");
     CK(e, "enumeration config");
     unsigned lanes = (unsigned)grid * (unsigned)block;
-    unsigned cap = 1024;
-    while (cap < 4u * lanes + 4096u) cap <<= 1;
-    if (cap > ctx->ring_cap) {
-      CK(ctx->d_ring.ensure((size_t)cap * sizeof(Item)), "alloc work queue");
-      CK(cudaMemsetAsync(ctx->d_ring.p, 0, (size_t)cap * sizeof(Item), stream), "clear work queue");
-      ctx->ring_cap = cap;
+    // Queue capacity: spills are accepted while fewer than cap/2 are waiting, which
+    // keeps every reused slot's previous item already claimed (see the kernel).
+    unsigned cap_items = 1u << 20;
+    while (cap_items < 8u * lanes) cap_items <<= 1;
+    if (cap_items > ctx->ring_cap) {
+      CK(ctx->d_ring.ensure((size_t)cap_items * sizeof(Item)), "alloc work queue");
+      CK(cudaMemsetAsync(ctx->d_ring.p, 0, (size_t)cap_items * sizeof(Item), stream), "clear work queue");
+      ctx->ring_cap = cap_items;
     }
     a.ring = (Item *)ctx->d_ring.p;
     a.ring_mask = ctx->ring_cap - 1;
@@ -473,38 +414,35 @@ lofp_status lofp_create(int32_t modes, int32_t n_layers, const int32_t *bs_per_l
       ctx->bs.push_back(c);
     }
   }
+  // layer-major, top to bottom inside a layer: the DFS level order ("systematic way")
+  std::stable_sort(ctx->bs.begin(), ctx->bs.end(),
+                   [](const CanonBS &x, const CanonBS &y) { return x.layer != y.layer ? x.layer < y.layer : x.cut < y.cut; });
   if (st == LOFP_OK) st = plan_circuit(ctx);
   if (st != LOFP_OK) {
     delete ctx;
     return st;
   }
   cudaError_t e = cudaGetDevice(&ctx->device);
-  const int M = modes, D = n_layers;
-  std::vector<uint8_t> r0(M + 1), s0(M + 1);
-  for (int k = 0; k <= M; ++k) {
-    r0[k] = (uint8_t)ctx->rho[0][k];
-    s0[k] = (uint8_t)ctx->sigma[0][k];
-  }
+  std::vector<int16_t> lk(2 * std::max(ctx->nbs, 1));
   std::vector<double> csv(4 * std::max(ctx->nbs, 1));
   for (int i = 0; i < ctx->nbs; ++i) {
+    lk[2 * i] = (int16_t)ctx->bs[i].layer;
+    lk[2 * i + 1] = (int16_t)ctx->bs[i].cut;
     csv[4 * i] = std::cos(ctx->bs[i].theta);
     csv[4 * i + 1] = std::sin(ctx->bs[i].theta);
     csv[4 * i + 2] = std::cos(ctx->bs[i].phi);
     csv[4 * i + 3] = std::sin(ctx->bs[i].phi);
   }
-  (void)D;
-  if (e == cudaSuccess) e = ctx->d_levels.ensure(std::max<size_t>(ctx->levels.size(), 1) * sizeof(LevelDesc));
-  if (e == cudaSuccess && !ctx->levels.empty())
-    e = cudaMemcpy(ctx->d_levels.p, ctx->levels.data(), ctx->levels.size() * sizeof(LevelDesc),
-                   cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = ctx->d_rho0.ensure(M + 1);
-  if (e == cudaSuccess) e = ctx->d_sigma0.ensure(M + 1);
-  if (e == cudaSuccess) e = cudaMemcpy(ctx->d_rho0.p, r0.data(), M + 1, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemcpy(ctx->d_sigma0.p, s0.data(), M + 1, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = ctx->d_maps.ensure(ctx->maps.size());
+  if (e == cudaSuccess) e = cudaMemcpy(ctx->d_maps.p, ctx->maps.data(), ctx->maps.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = ctx->d_bs_lk.ensure(lk.size() * 2);
+  if (e == cudaSuccess) e = cudaMemcpy(ctx->d_bs_lk.p, lk.data(), lk.size() * 2, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = ctx->d_bs_cs.ensure(csv.size() * 8);
   if (e == cudaSuccess) e = cudaMemcpy(ctx->d_bs_cs.p, csv.data(), csv.size() * 8, cudaMemcpyHostToDevice);
-  for (cudaEvent_t *ev : {&ctx->ev_start, &ctx->ev_enum0, &ctx->ev_enum1, &ctx->ev_end, &ctx->ev_upload})
+  for (cudaEvent_t *ev : {&ctx->ev_start, &ctx->ev_enum0, &ctx->ev_enum1, &ctx->ev_end})
     if (e == cudaSuccess) e = cudaEventCreate(ev);
+  if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_end, 0);
+  if (e == cudaSuccess) e = cudaEventSynchronize(ctx->ev_end);
   if (e != cudaSuccess) {
     lofp_status s = e == cudaErrorMemoryAllocation ? LOFP_E_OOM : LOFP_E_CUDA;
     lofp_destroy(ctx);
@@ -522,13 +460,13 @@ lofp_status lofp_amplitudes(lofp_ctx *ctx, const int32_t *input_occ, int64_t bat
 lofp_status lofp_amplitudes_counted(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch,
                                     const int32_t *output_occ, double *amps, uint64_t *path_counts,
                                     void *cuda_stream) {
+  if (!ctx) return LOFP_E_INVALID_ARG;
   if (batch > 0 && !path_counts) return fail(ctx, LOFP_E_INVALID_ARG, "null path_counts");
-  return run(ctx, input_occ, batch, output_occ, amps, (unsigned long long *)path_counts,
-             (cudaStream_t)cuda_stream);
+  return run(ctx, input_occ, batch, output_occ, amps, (unsigned long long *)path_counts, (cudaStream_t)cuda_stream);
 }
 
-lofp_status lofp_amplitudes_host(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch,
-                                 const int32_t *output_occ, double *amps) {
+lofp_status lofp_amplitudes_host(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const int32_t *output_occ,
+                                 double *amps) {
   if (!ctx) return LOFP_E_INVALID_ARG;
   if (batch < 0 || !input_occ) return fail(ctx, LOFP_E_INVALID_ARG, "bad arguments");
   if (batch == 0) return LOFP_OK;
@@ -536,11 +474,12 @@ lofp_status lofp_amplitudes_host(lofp_ctx *ctx, const int32_t *input_occ, int64_
   CK(cudaSetDevice(ctx->device), "cudaSetDevice");
   if (!ctx->own_stream) CK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking), "stream");
   size_t tb = (size_t)batch * ctx->M * 4, ab = (size_t)batch * 16;
+  CK(cudaEventSynchronize(ctx->ev_end), "cudaEventSynchronize");
   CK(ctx->d_hostT.ensure(tb), "alloc T");
   CK(ctx->d_hostA.ensure(ab), "alloc amps");
   CK(cudaMemcpyAsync(ctx->d_hostT.p, output_occ, tb, cudaMemcpyHostToDevice, ctx->own_stream), "copy T");
-  lofp_status s = run(ctx, input_occ, batch, (const int32_t *)ctx->d_hostT.p, (double *)ctx->d_hostA.p, nullptr,
-                      ctx->own_stream);
+  lofp_status s =
+      run(ctx, input_occ, batch, (const int32_t *)ctx->d_hostT.p, (double *)ctx->d_hostA.p, nullptr, ctx->own_stream);
   if (s != LOFP_OK) return s;
   CK(cudaMemcpyAsync(amps, ctx->d_hostA.p, ab, cudaMemcpyDeviceToHost, ctx->own_stream), "copy amps");
   CK(cudaStreamSynchronize(ctx->own_stream), "cudaStreamSynchronize");
@@ -554,7 +493,11 @@ lofp_status lofp_stats(lofp_ctx *ctx, lofp_run_stats *out) {
     const Counters *hc = (const Counters *)ctx->h_ctr.p;
     ctx->stats.feasible = (int64_t)hc->nfeas;
     ctx->stats.items = (int64_t)hc->items;
+    ctx->stats.spills = (int64_t)hc->spills;
     ctx->stats.donations = (int64_t)hc->donations;
+    ctx->stats.overflows = (int64_t)hc->ovf;
+    ctx->stats.paths = (int64_t)hc->leaves;
+    ctx->stats.cmuls = (int64_t)hc->cmuls;
     ctx->stats.bad_rows = (int32_t)hc->bad_rows;
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, ctx->ev_enum0, ctx->ev_enum1) == cudaSuccess) ctx->stats.enum_ms = ms;
@@ -569,13 +512,13 @@ void lofp_destroy(lofp_ctx *ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->ev_end) cudaEventSynchronize(ctx->ev_end);
-  for (DevBuf *b : {&ctx->d_levels, &ctx->d_factors, &ctx->d_rho0, &ctx->d_sigma0, &ctx->d_bs_cs, &ctx->d_flags,
-                    &ctx->d_G, &ctx->d_root, &ctx->d_feas, &ctx->d_ctr, &ctx->d_ring, &ctx->d_edesc,
-                    &ctx->d_offsets, &ctx->d_entries, &ctx->d_cumS, &ctx->d_hostT, &ctx->d_hostA})
+  for (DevBuf *b : {&ctx->d_maps, &ctx->d_bs_lk, &ctx->d_bs_cs, &ctx->d_flags, &ctx->d_plans, &ctx->d_feas,
+                    &ctx->d_ctr, &ctx->d_ring, &ctx->d_edesc, &ctx->d_offsets, &ctx->d_entries, &ctx->d_cumS,
+                    &ctx->d_bsrow, &ctx->d_hostT, &ctx->d_hostA})
     b->release();
   ctx->h_stage.release();
   ctx->h_ctr.release();
-  for (cudaEvent_t ev : {ctx->ev_start, ctx->ev_enum0, ctx->ev_enum1, ctx->ev_end, ctx->ev_upload})
+  for (cudaEvent_t ev : {ctx->ev_start, ctx->ev_enum0, ctx->ev_enum1, ctx->ev_end})
     if (ev) cudaEventDestroy(ev);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;

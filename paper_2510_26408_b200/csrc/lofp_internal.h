@@ -4,37 +4,64 @@
 // Vocabulary.  Cut k (0..M) sits between modes k-1 and k; F_l(k) is the
 // number of photons in modes < k after layer l (F_0 = cum(S), F_D = G = cum(T)).  A BS
 // of layer l on modes {k-1, k} is "active at cut k" and sets F_l(k); its Appendix-A
-// element depends on x1 = F_{l-1}(k) - F_{l-1}(k-1), x2 = F_{l-1}(k+1) - F_{l-1}(k),
-// y1 = F_l(k) - F_{l-1}(k-1).  The exact light-cone box (reading R5) confines F_l(k) to
-// [G(rho_l(k)), G(sigma_l(k))]; a BS output with rho == sigma is forced (a "red"
-// waveguide of P:130), the others are the DFS levels ("green" waveguides).
+// element depends on a = F_{l-1}(k-1), b = F_{l-1}(k), c = F_{l-1}(k+1), y = F_l(k):
+// x1 = b - a, x2 = c - b, y1 = y - a.
+//
+// Per output the plan kernel intersects the backward light-cone box [G(rho_l(k)),
+// G(sigma_l(k))] (exact, reading R5) with the forward one [cumS(rho'_l(k)),
+// cumS(sigma'_l(k))]; a BS output whose box is a single value is a constant (a "red"
+// waveguide of P:130 for this output), the others are the DFS levels ("green")
+// in layer-major order.  Every BS element is attached to the deepest level among its
+// inputs; elements with constant inputs are folded into the output's root product.
 #pragma once
 #include <stdint.h>
 
-#define LOFP_MAX_LEVELS 224   // DFS levels (free BS outputs) per circuit
-#define LOFP_VALS 512         // per-lane value array: [levels | G(0..M) | cumS(0..M)]
-#define LOFP_STACK 64         // branch stack depth (>= log2 of any subtree's path count)
-#define LOFP_ITEM_BYTES 256   // one work-queue slot
-#define LOFP_ITEM_PREFIX 224  // prefix bytes an item can carry (= LOFP_MAX_LEVELS)
+#define LOFP_MAX_LEVELS 128   // DFS levels (free BS outputs) per circuit
+#define LOFP_STK 8            // per-lane branch-stack entries kept in shared memory
+#define LOFP_OVF (LOFP_MAX_LEVELS - LOFP_STK + 8)  // per-lane local-memory overflow entries
+#define LOFP_ITEM_BYTES 256   // one global work-queue slot
+#define LOFP_ITEM_PREFIX 224  // prefix bytes an item can carry (>= LOFP_MAX_LEVELS)
+#define LOFP_ENUM_MAX_THREADS 512  // largest block of the enumeration kernel
+#define LOFP_MAX_CUTS 130     // M + 1 for M <= LOFP_MAX_MODES (128)
 
-// A DFS level: the free output F_l(k) of one BS, in layer-major order (top to bottom
-// inside a layer).  Its range is [max(v[refL], v[gLo]), min(v[refR], v[gHi])] where
-// refL/refR are F_{l-1}(k-1), F_{l-1}(k+1) and gLo/gHi are G(rho_l(k)), G(sigma_l(k)).
-// Factors [fbeg, fend) are the BS elements whose last unknown input is this level.
-struct LevelDesc {
-  uint16_t refL, refR, gLo, gHi;
+// Per-lane value array ("vals") lives in shared memory, lane-interleaved by 32-bit word:
+// byte s of lane i is at  warp_vals + ((s >> 2) * 32 + i) * 4 + (s & 3), so any 32 lanes
+// reading any slots hit 32 distinct banks.  Plans store slots as the byte offset
+// slot_off(s) relative to the lane's base (warp_vals + 4 * lane).
+// Slot 0 is the lane's constant zero; DFS level j is slot j + 1.
+__host__ __device__ inline uint16_t lofp_slot_off(int s) { return (uint16_t)(((s >> 2) << 7) | (s & 3)); }
+__host__ __device__ inline uint16_t lofp_level_off(int j) { return lofp_slot_off(j + 1); }
+#define LOFP_ZERO_OFF 0
+
+// A DFS level j (a free F_l(k)).  Range at run time:
+//   [max(vals[ol] + cl, lo), min(vals[or_] + cr, hi)]  with vals[ol] + cl = F_{l-1}(k-1),
+//   vals[or_] + cr = F_{l-1}(k+1) (a constant uses the lane's zero slot), lo/hi the
+//   output's box.  Factors [fbeg, fend) are the elements attached to this level.
+struct __align__(16) PlanLevel {
+  uint16_t ol, or_;
+  uint8_t cl, cr, lo, hi;
   uint16_t fbeg, fend;
-  uint16_t pad0, pad1;
+  uint32_t pad;
 };
 
-// One BS element factor: value references of F_{l-1}(k-1), F_{l-1}(k), F_{l-1}(k+1)
-// and F_l(k) into the per-lane value array, and the BS's table coordinates.
-struct FactorDesc {
-  uint16_t xl, xm, xr, y;
-  int32_t offbase;  // index of (x1 = 0, x2 = 0) in the offsets table
-  uint16_t stride;  // X2 cap + 1
-  uint16_t bs;      // canonical BS index
+// One attached BS element.  With va = vals[oa] etc. (0 for constants):
+//   row = base + stride * (vb - va) + (vc - vb);  entry = offsets[row] + (vy - va) + dy
+// (the constants of a, b, c, y are folded into base and dy); dx = cc - ca so that
+// x1 + x2 = vc - va + dx (used only to count non-vacuum multiplications).
+struct __align__(16) PlanFactor {
+  uint16_t oa, ob, oc, oy;
+  int32_t base;
+  int16_t stride;
+  int8_t dy, dx;
 };
+
+struct PlanHead {
+  double root[2];   // product of the elements with constant inputs
+  uint16_t L, nfac; // levels and attached factors of this output
+  uint32_t pad0;
+  uint64_t pad1;
+};
+static_assert(sizeof(PlanLevel) == 16 && sizeof(PlanFactor) == 16 && sizeof(PlanHead) == 32, "plan layout");
 
 // One Appendix-A table entry to build: BS b, (x1, x2) -> (y1, x1 + x2 - y1).
 struct EntryDesc {
@@ -49,18 +76,22 @@ struct Counters {
   unsigned long long tail;         // next queue slot (producer side)
   unsigned long long outstanding;  // work items not yet finished
   unsigned long long items;        // items started (stats)
-  unsigned long long donations;    // items pushed by donation (stats)
-  unsigned long long nfeas;        // feasible outputs (written by the feasibility kernel)
+  unsigned long long spills;       // items pushed to the global queue (stats)
+  unsigned long long nfeas;        // outputs with a non-trivial tree
   unsigned long long bad_rows;     // rows with a negative entry
+  unsigned long long cmuls;        // non-vacuum complex multiplications (counted mode)
+  unsigned long long leaves;       // valid paths summed (counted mode)
+  unsigned long long ovf;          // pushes that went to the local overflow stack
+  unsigned long long donations;    // intra-warp hand-overs (stats)
   int32_t tmax[128];               // per-mode maximum of T over the batch
-  int32_t sum_mismatch;            // unused padding / diagnostics
-  int32_t pad;
+  int32_t maxL;                    // largest per-output level count
+  int32_t maxF;                    // largest per-output attached-factor count
 };
 
 // A queued subtree: output `out`, levels [0, j0) fixed to prefix[], level j0 ranging
 // over [vs, ve], product P of every factor attached to levels < j0 (and the root).
 struct __align__(16) Item {
-  unsigned int seq;   // = ticket + 1 once published
+  unsigned int seq;   // = ticket + 1 once published, 0 when free
   unsigned int out;
   unsigned short j0;
   unsigned char vs, ve;
@@ -72,21 +103,27 @@ static_assert(sizeof(Item) == LOFP_ITEM_BYTES, "item size");
 
 // Everything the kernels need for one call.
 struct CallArgs {
-  int M, D, N, L, nfactors, nroot;    // nroot: factors attached to no level (constants)
+  int M, D, N, nbs;
+  int Lg;                             // global level bound (sizes the vals array)
+  int vals_slots;                     // slots per lane (multiple of 4; slot 0 = zero)
   int nentries, noffsets;
   int64_t B;
-  int grow;                           // bytes per G row (M+1 rounded up to 16)
+  int plan_stride;                    // bytes per output plan (multiple of 16)
+  int plan_smem;                      // bytes reserved per warp for a staged plan
+  int maxfac;                         // bound on attached factors per output
+  int warp_bytes;                     // per-warp shared memory (plan + vals + stack)
+  int table_bytes;                    // shared memory of the staged tables (16-aligned)
   const int32_t *T;                   // [B][M] device
   double *amps;                       // [B][2] device
   unsigned long long *counts;         // [B] device or null
   uint8_t *flags;                     // [B] 1 = photon number matches, 2 = bad row
-  uint8_t *G;                         // [B][grow]
-  double *root;                       // [B][2]
-  uint32_t *feas;                     // [B] feasible output ids
-  const uint8_t *rho0, *sigma0;       // [M+1] box maps at time 0
+  unsigned char *plans;               // [B][plan_stride]
+  uint32_t *feas;                     // [B] outputs with a non-trivial tree
   const uint8_t *cumS;                // [M+1]
-  const LevelDesc *levels;            // [L]
-  const FactorDesc *factors;          // [nfactors]; the first nroot are root factors
+  const uint8_t *maps;                // [4][D+1][M+1]: rho, sigma, rho', sigma'
+  const int16_t *bs_lk;               // [nbs][2]: layer (1-based), cut; layer-major, by cut
+  const int32_t *bs_base;             // [nbs]: offsets-table row of (x1, x2) = (0, 0)
+  const int32_t *bs_stride;           // [nbs]: X2 cap + 1
   const EntryDesc *edesc;             // [nentries]
   const int32_t *offsets;             // [noffsets]
   double *entries;                    // [nentries][2]
@@ -100,8 +137,7 @@ struct CallArgs {
 #include <cuda_runtime.h>
 cudaError_t lofp_launch_prep(const CallArgs &a, cudaStream_t s);
 cudaError_t lofp_launch_tables(const CallArgs &a, cudaStream_t s);
-cudaError_t lofp_launch_feasible(const CallArgs &a, cudaStream_t s);
-cudaError_t lofp_launch_finalize_counts(const CallArgs &a, cudaStream_t s);
+cudaError_t lofp_launch_plan(const CallArgs &a, cudaStream_t s);
 cudaError_t lofp_enum_config(const CallArgs &a, bool counted, int *grid, int *block, size_t *smem);
 cudaError_t lofp_launch_enum(const CallArgs &a, bool counted, int grid, int block, size_t smem,
                              cudaStream_t s);

@@ -1,15 +1,17 @@
 // lofp_kernels.cu — sm_100a kernels of the LOFP path sum (arXiv 2510.26408).
 //
-//   lofp_prep_kernel      per output row: validity, photon number, per-mode max of T.
-//   lofp_table_kernel     Appendix-A BS elements for every (x1, x2, y1)
-//                         inside the paper's light-cone caps, fp64.
-//   lofp_feasible_kernel  per output: G = cum(T), exact light-cone reachability
-//                         (reading R5), product of the constant factors, compaction.
-//   lofp_enum_kernel      persistent path enumeration: each lane runs an iterative DFS
-//                         over the free BS outputs (the "green" waveguides),
-//                         multiplying fp64 complex Appendix-A factors staged in shared
-//                         memory and summing leaves (eq. (1)); subtrees are
-//                         balanced through a global atomic work queue.
+//   lofp_prep_kernel   per output row: validity, photon number, per-mode max of T.
+//   lofp_table_kernel  Appendix-A BS elements for every (x1, x2, y1) inside
+//                      the paper's light-cone caps, fp64.
+//   lofp_plan_kernel   per output: G = cum(T), exact light-cone reachability (reading
+//                      R5), the output's DFS levels (free "green" waveguides)
+//                      and attached factors, and the product of the constant factors.
+//   lofp_enum_kernel   persistent path enumeration (eq. (1)): one warp per work
+//                      item (a subtree of one output), one iterative DFS per lane over
+//                      the item's levels with its state in shared memory, fp64 complex
+//                      products of Appendix-A factors staged in shared memory, subtrees
+//                      handed between lanes of a warp (shared memory) and between warps
+//                      (a global atomic work queue); warp-shuffle reduction per item.
 //
 // The arithmetic follows the paper; the data layout is described in lofp_internal.h
 // and DESIGN.md.  No code here is shared with oracle/.
@@ -55,8 +57,9 @@ __global__ void lofp_prep_kernel(CallArgs a) {
     }
   }
   a.flags[q] = f;
-  a.amps[2 * q] = bad ? __longlong_as_double(0x7ff8000000000000ll) : 0.0;
-  a.amps[2 * q + 1] = bad ? __longlong_as_double(0x7ff8000000000000ll) : 0.0;
+  const double nan = __longlong_as_double(0x7ff8000000000000ll);
+  a.amps[2 * q] = bad ? nan : 0.0;
+  a.amps[2 * q + 1] = bad ? nan : 0.0;
   if (a.counts) a.counts[q] = 0;
 }
 
@@ -109,56 +112,125 @@ __global__ void lofp_table_kernel(CallArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// feasibility: G row, exact box at time 0, root product, compaction
+// plan: per output, levels + attached factors + root product
 // ---------------------------------------------------------------------------
-__device__ double2 table_lookup(const int32_t *offsets, const double2 *entries, const FactorDesc &fd,
-                                int x1, int x2, int y1) {
-  int o = offsets[fd.offbase + x1 * fd.stride + x2] + y1;
-  return entries[o];
-}
+// A reference to F_t(k) while sweeping the layers: a level slot, or a constant.
+struct Ref {
+  int slot;  // -1 = constant
+  int cst;
+};
 
-__global__ void lofp_feasible_kernel(CallArgs a) {
+__global__ void lofp_plan_kernel(CallArgs a) {
   int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= a.B) return;
   if (a.flags[q] != 1) return;  // amps already 0 (photon number) or NaN (bad row)
-  const int32_t *t = a.T + q * a.M;
-  uint8_t G[LOFP_VALS / 2];
-  int g = 0;
-  for (int k = 0; k <= a.M; ++k) {
-    G[k] = (uint8_t)g;
-    if (k < a.M) g += t[k];
+  const int M = a.M, D = a.D, W = M + 1;
+  const int32_t *t = a.T + q * M;
+  uint8_t G[LOFP_MAX_CUTS];
+  {
+    int g = 0;
+    for (int k = 0; k <= M; ++k) {
+      G[k] = (uint8_t)g;
+      if (k < M) g += t[k];
+    }
   }
-  bool ok = true;
-  for (int k = 0; k <= a.M; ++k) {
+  const uint8_t *rho = a.maps, *sig = a.maps + (D + 1) * W;
+  const uint8_t *frho = a.maps + 2 * (D + 1) * W, *fsig = a.maps + 3 * (D + 1) * W;
+  // exact reachability: cum(S) inside the time-0 box (reading R5)
+  for (int k = 0; k <= M; ++k) {
     int f = a.cumS[k];
-    if (f < G[a.rho0[k]] || f > G[a.sigma0[k]]) ok = false;
+    if (f < G[rho[k]] || f > G[sig[k]]) return;  // structural zero
   }
-  uint8_t *grow = a.G + q * a.grow;
-  for (int k = 0; k <= a.M; ++k) grow[k] = G[k];
-  if (!ok) return;  // structurally unreachable: exact zero
-  // product of the factors whose inputs are all fixed by S and T
-  double2 P = make_double2(1.0, 0.0);
+  unsigned char *plan = a.plans + (size_t)q * a.plan_stride;
+  PlanHead *head = reinterpret_cast<PlanHead *>(plan);
+  PlanLevel *lev = reinterpret_cast<PlanLevel *>(plan + sizeof(PlanHead));
+  PlanFactor *fac = reinterpret_cast<PlanFactor *>(plan + sizeof(PlanHead) + (size_t)a.Lg * sizeof(PlanLevel));
+  PlanFactor *tmp = fac + a.nbs;                            // unsorted factors
+  uint16_t *att = reinterpret_cast<uint16_t *>(tmp + a.nbs);  // their levels
+  const uint16_t zero_off = LOFP_ZERO_OFF;
   const double2 *ent = reinterpret_cast<const double2 *>(a.entries);
-  for (int f = 0; f < a.nroot; ++f) {
-    FactorDesc fd = a.factors[f];
-    auto val = [&](uint16_t r) -> int {
-      // root factors only reference G (L .. L+M) and cumS (L+M+1 .. L+2M+1)
-      int c = r - a.L;
-      return c <= a.M ? (int)G[c] : (int)a.cumS[c - a.M - 1];
-    };
-    int l = val(fd.xl), m = val(fd.xm), r = val(fd.xr), y = val(fd.y);
-    int x1 = m - l, x2 = r - m, y1 = y - l;
-    if (x1 + x2 == 0) continue;
-    P = cmul(P, table_lookup(a.offsets, ent, fd, x1, x2, y1));
+
+  Ref cur[LOFP_MAX_CUTS];
+  for (int k = 0; k <= M; ++k) cur[k] = Ref{-1, (int)a.cumS[k]};
+  int L = 0, nf = 0;
+  double2 root = make_double2(1.0, 0.0);
+  for (int b = 0; b < a.nbs; ++b) {
+    int l = a.bs_lk[2 * b], k = a.bs_lk[2 * b + 1];
+    Ref A = cur[k - 1], Bv = cur[k], C = cur[k + 1];
+    int idx = l * W + k;
+    int lo = max((int)G[rho[idx]], (int)a.cumS[frho[idx]]);
+    int hi = min((int)G[sig[idx]], (int)a.cumS[fsig[idx]]);
+    if (lo > hi) return;  // empty box: no valid path (cannot happen once reachable)
+    Ref Y;
+    if (lo == hi) {
+      Y = Ref{-1, lo};
+    } else {
+      Y = Ref{L, 0};
+      PlanLevel pl;
+      pl.ol = A.slot < 0 ? zero_off : lofp_level_off(A.slot);
+      pl.cl = (uint8_t)(A.slot < 0 ? A.cst : 0);
+      pl.or_ = C.slot < 0 ? zero_off : lofp_level_off(C.slot);
+      pl.cr = (uint8_t)(C.slot < 0 ? C.cst : 0);
+      pl.lo = (uint8_t)lo;
+      pl.hi = (uint8_t)hi;
+      pl.fbeg = pl.fend = 0;
+      pl.pad = 0;
+      lev[L] = pl;
+      ++L;
+    }
+    cur[k] = Y;
+    // the element <y1, y2| BS_b |x1, x2>
+    int at = max(max(A.slot, Bv.slot), max(C.slot, Y.slot));
+    int ca = A.slot < 0 ? A.cst : 0, cb = Bv.slot < 0 ? Bv.cst : 0, cc = C.slot < 0 ? C.cst : 0,
+        cy = Y.slot < 0 ? Y.cst : 0;
+    int stride = a.bs_stride[b];
+    if (at < 0) {  // all inputs constant: multiply into the root product
+      int x1 = cb - ca, x2 = cc - cb, y1 = cy - ca;
+      if (x1 + x2 == 0) continue;  // vacuum: the element is 1
+      int o = a.offsets[a.bs_base[b] + x1 * stride + x2] + y1;
+      root = cmul(root, ent[o]);
+      continue;
+    }
+    if (A.slot < 0 && C.slot < 0 && cc == ca) continue;  // always vacuum
+    PlanFactor pf;
+    pf.oa = A.slot < 0 ? zero_off : lofp_level_off(A.slot);
+    pf.ob = Bv.slot < 0 ? zero_off : lofp_level_off(Bv.slot);
+    pf.oc = C.slot < 0 ? zero_off : lofp_level_off(C.slot);
+    pf.oy = Y.slot < 0 ? zero_off : lofp_level_off(Y.slot);
+    pf.base = a.bs_base[b] + stride * (cb - ca) + (cc - cb);
+    pf.stride = (int16_t)stride;
+    pf.dy = (int8_t)(cy - ca);
+    pf.dx = (int8_t)(cc - ca);
+    tmp[nf] = pf;
+    att[nf] = (uint16_t)at;
+    ++nf;
   }
-  if (a.L == 0) {  // a single valid path (eq. (10))
-    a.amps[2 * q] = P.x;
-    a.amps[2 * q + 1] = P.y;
+  // counting sort of the factors by level
+  uint16_t cnt[LOFP_MAX_LEVELS + 1];
+  for (int j = 0; j <= L; ++j) cnt[j] = 0;
+  for (int f = 0; f < nf; ++f) cnt[att[f] + 1]++;
+  for (int j = 0; j < L; ++j) cnt[j + 1] += cnt[j];
+  for (int j = 0; j < L; ++j) {
+    lev[j].fbeg = cnt[j];
+    lev[j].fend = cnt[j + 1];
+  }
+  for (int f = 0; f < nf; ++f) fac[cnt[att[f]]++] = tmp[f];
+  PlanHead h;
+  h.root[0] = root.x;
+  h.root[1] = root.y;
+  h.L = (uint16_t)L;
+  h.nfac = (uint16_t)nf;
+  h.pad0 = 0;
+  h.pad1 = 0;
+  *head = h;
+  if (L == 0) {  // a single valid path (eq. (10))
+    a.amps[2 * q] = root.x;
+    a.amps[2 * q + 1] = root.y;
     if (a.counts) a.counts[q] = 1;
     return;
   }
-  a.root[2 * q] = P.x;
-  a.root[2 * q + 1] = P.y;
+  atomicMax(&a.ctr->maxL, L);
+  atomicMax(&a.ctr->maxF, nf);
   unsigned long long idx = atomicAdd(&a.ctr->nfeas, 1ull);
   a.feas[idx] = (uint32_t)q;
   atomicAdd(&a.ctr->outstanding, 1ull);
@@ -167,233 +239,371 @@ __global__ void lofp_feasible_kernel(CallArgs a) {
 // ---------------------------------------------------------------------------
 // path enumeration
 // ---------------------------------------------------------------------------
-// Lane states
-enum : int { ST_NEED = 0, ST_WAIT = 1, ST_WORK = 2, ST_DONE = 3 };
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
 
+__device__ __forceinline__ unsigned long long vload(const unsigned long long *p) {
+  return *reinterpret_cast<const volatile unsigned long long *>(p);
+}
+
+// Per-lane state of the DFS.  vals bytes live in the warp's shared-memory column (lb);
+// the branch stack is a ring of LOFP_STK shared-memory entries [bot, top) plus a
+// local-memory overflow below it for rare deep stacks.
 template <bool COUNTED>
-__global__ void __launch_bounds__(256) lofp_enum_kernel(CallArgs a) {
+__global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(CallArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  // shared layout: entries | offsets | levels | factors | cumS
   double2 *s_ent = reinterpret_cast<double2 *>(smem);
   int32_t *s_off = reinterpret_cast<int32_t *>(s_ent + a.nentries);
-  LevelDesc *s_lev = reinterpret_cast<LevelDesc *>(
-      (reinterpret_cast<uintptr_t>(s_off + a.noffsets) + 15) & ~uintptr_t(15));
-  FactorDesc *s_fac = reinterpret_cast<FactorDesc *>(s_lev + a.L);
-  uint8_t *s_cumS = reinterpret_cast<uint8_t *>(s_fac + a.nfactors);
-
-  {  // stage the tables (the per-call Appendix-A elements) into shared memory
-    const int4 *src = reinterpret_cast<const int4 *>(a.entries);
-    int4 *dst = reinterpret_cast<int4 *>(s_ent);
-    for (int i = threadIdx.x; i < a.nentries; i += blockDim.x) dst[i] = src[i];
-    for (int i = threadIdx.x; i < a.noffsets; i += blockDim.x) s_off[i] = a.offsets[i];
-    for (int i = threadIdx.x; i < a.L; i += blockDim.x) s_lev[i] = a.levels[i];
-    for (int i = threadIdx.x; i < a.nfactors; i += blockDim.x) s_fac[i] = a.factors[i];
-    for (int i = threadIdx.x; i <= a.M; i += blockDim.x) s_cumS[i] = a.cumS[i];
-  }
+  for (int i = threadIdx.x; i < a.nentries; i += blockDim.x)
+    reinterpret_cast<int4 *>(s_ent)[i] = reinterpret_cast<const int4 *>(a.entries)[i];
+  for (int i = threadIdx.x; i < a.noffsets; i += blockDim.x) s_off[i] = a.offsets[i];
   __syncthreads();
 
-  const int L = a.L, M = a.M;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned char *wb = smem + a.table_bytes + (size_t)warp * a.warp_bytes;
+  unsigned char *s_plan = wb;
+  const PlanLevel *s_lev = reinterpret_cast<const PlanLevel *>(s_plan + sizeof(PlanHead));
+  unsigned char *vcol = wb + a.plan_smem;                 // vals words [slots/4][32]
+  unsigned char *lb = vcol + 4 * lane;                    // this lane's byte base
+  double2 *stkP = reinterpret_cast<double2 *>(vcol + a.vals_slots * 32);  // [LOFP_STK][32]
+  uint32_t *stkM = reinterpret_cast<uint32_t *>(stkP + LOFP_STK * 32);     // [LOFP_STK][32]
+  lb[LOFP_ZERO_OFF] = 0;
   const unsigned nfeas = (unsigned)a.ctr->nfeas;
-  const double2 *g_root = reinterpret_cast<const double2 *>(a.root);
 
-  // per-lane DFS state (local memory; stack accesses stay near the top)
-  uint32_t valw[LOFP_VALS / 4];
-  uint8_t *vals = reinterpret_cast<uint8_t *>(valw);
-  uint8_t stk_lv[LOFP_STACK];
-  uint8_t stk_hi[LOFP_STACK];
-  double2 stk_P[LOFP_STACK];
-  int sb = 0, sp = 0;  // branch stack [sb, sp)
+  double2 ovfP[LOFP_OVF];
+  uint32_t ovfM[LOFP_OVF];
+  int novf = 0;
 
-  int state = ST_NEED;
-  unsigned long long ticket = 0;
-  unsigned out = 0;
-  int j = 0;
-  double2 Pcur = make_double2(0.0, 0.0);
-  double2 acc = make_double2(0.0, 0.0);
-  unsigned long long npaths = 0;
-  unsigned iter = 0;
-
-  auto load_g_and_s = [&](unsigned o) {
-    // G(0..M) -> vals[L .. L+M]; cumS(0..M) -> vals[L+M+1 .. L+2M+1]
-    const uint8_t *g = a.G + (size_t)o * a.grow;
-    for (int k = 0; k <= M; ++k) vals[L + k] = g[k];
-    for (int k = 0; k <= M; ++k) vals[L + M + 1 + k] = s_cumS[k];
-  };
-
-  // Begin a subtree at level j0 with level value range [vs, ve] and product P0.
-  auto begin = [&](int j0, int vs, int ve, double2 P0) {
-    j = j0;
-    vals[j0] = (uint8_t)vs;
-    sb = sp = 0;
-    if (ve > vs) {
-      stk_lv[0] = (uint8_t)j0;
-      stk_hi[0] = (uint8_t)ve;
-      stk_P[0] = P0;
-      sp = 1;
-    }
-    Pcur = P0;
-    acc = make_double2(0.0, 0.0);
-    npaths = 0;
-  };
+  unsigned cur_out = 0xffffffffu;
+  const PlanFactor *s_fac = nullptr;
+  int L = 0;
+  unsigned long long spills = 0, ovfc = 0, dons = 0, items = 0;
 
   while (true) {
-    // ---------------- acquire work ----------------
-    unsigned need = __ballot_sync(FULL, state == ST_NEED);
-    if (need) {
-      unsigned long long base = 0;
-      int leader = __ffs(need) - 1;
-      int rank = __popc(need & ((1u << lane) - 1));
-      if (lane == leader) base = atomicAdd(&a.ctr->fresh_next, (unsigned long long)__popc(need));
-      base = __shfl_sync(FULL, base, leader);
-      if (state == ST_NEED) {
-        unsigned long long idx = base + rank;
-        if (idx < nfeas) {
-          out = a.feas[idx];
-          load_g_and_s(out);
-          LevelDesc ld = s_lev[0];
-          int lo = max((int)vals[ld.refL], (int)vals[ld.gLo]);
-          int hi = min((int)vals[ld.refR], (int)vals[ld.gHi]);
-          begin(0, lo, hi, g_root[out]);
-          state = ST_WORK;
-          atomicAdd(&a.ctr->items, 1ull);
-        } else {
-          state = ST_WAIT;
-        }
-      }
-    }
-    // tickets for lanes that found no fresh output (second ballot: lanes just switched)
-    unsigned tk = __ballot_sync(FULL, state == ST_WAIT && ticket == 0);
-    if (tk) {
-      int leader = __ffs(tk) - 1;
-      int rank = __popc(tk & ((1u << lane) - 1));
-      unsigned long long base = 0;
-      if (lane == leader) base = atomicAdd(&a.ctr->ticket, (unsigned long long)__popc(tk));
-      base = __shfl_sync(FULL, base, leader);
-      if (state == ST_WAIT && ticket == 0) ticket = base + rank + 1;  // stored +1 (0 = none)
-    }
-    if (state == ST_WAIT) {
-      unsigned long long t = ticket - 1;
-      Item *it = a.ring + (t & a.ring_mask);
-      unsigned seq = *reinterpret_cast<volatile unsigned *>(&it->seq);
-      if (seq == (unsigned)(t + 1)) {
-        __threadfence();
-        out = it->out;
-        int j0 = it->j0;
-        const uint32_t *pw = reinterpret_cast<const uint32_t *>(it->prefix);
-        for (int w = 0; w < (j0 + 3) / 4; ++w) valw[w] = pw[w];
-        load_g_and_s(out);  // after the prefix: its last word may spill past j0
-        double2 P0 = make_double2(it->P[0], it->P[1]);
-        int vs = it->vs, ve = it->ve;
-        __threadfence();
-        *reinterpret_cast<volatile unsigned *>(&it->seq) = 0u;  // slot free again
-        begin(j0, vs, ve, P0);
-        ticket = 0;
-        state = ST_WORK;
-        atomicAdd(&a.ctr->items, 1ull);
-      } else if (*reinterpret_cast<volatile unsigned long long *>(&a.ctr->outstanding) == 0ull) {
-        state = ST_DONE;
-      }
-    }
-    if (__all_sync(FULL, state == ST_DONE)) break;
-
-    // ---------------- one DFS node per working lane ----------------
-    if (state == ST_WORK) {
-      LevelDesc ld = s_lev[j];
-      double2 P = Pcur;
-      for (int f = ld.fbeg; f < ld.fend; ++f) {
-        FactorDesc fd = s_fac[f];
-        int vl = vals[fd.xl], vm = vals[fd.xm], vr = vals[fd.xr], vy = vals[fd.y];
-        int x1 = vm - vl, x2 = vr - vm, y1 = vy - vl;
-        if (x1 + x2 != 0) {
-          int o = s_off[fd.offbase + x1 * fd.stride + x2] + y1;
-          P = cmul(P, s_ent[o]);
-        }
-      }
-      bool finished = false;
-      if (j == L - 1) {  // a leaf: one valid path of eq. (1)
-        acc.x += P.x;
-        acc.y += P.y;
-        if (COUNTED) ++npaths;
-        if (sp == sb) {
-          finished = true;
-        } else {
-          int top = sp - 1;
-          j = stk_lv[top];
-          int v = vals[j] + 1;
-          vals[j] = (uint8_t)v;
-          Pcur = stk_P[top];
-          if (v == stk_hi[top]) sp = top;
-        }
-      } else {  // descend: next level's exact range (never empty, reading R5)
-        ++j;
-        LevelDesc nd = s_lev[j];
-        int lo = max((int)vals[nd.refL], (int)vals[nd.gLo]);
-        int hi = min((int)vals[nd.refR], (int)vals[nd.gHi]);
-        vals[j] = (uint8_t)lo;
-        if (hi > lo) {
-          stk_lv[sp] = (uint8_t)j;
-          stk_hi[sp] = (uint8_t)hi;
-          stk_P[sp] = P;
-          ++sp;
-        }
-        Pcur = P;
-      }
-      if (finished) {
-        atomicAdd(&a.amps[2 * out], acc.x);
-        atomicAdd(&a.amps[2 * out + 1], acc.y);
-        if (COUNTED) atomicAdd(&a.counts[out], npaths);
-        __threadfence();
-        atomicAdd(&a.ctr->outstanding, ~0ull);  // -1
-        state = ST_NEED;
-      }
-    }
-
-    // ---------------- donation: split the shallowest open branch ----------------
-    if (((++iter) & 63u) == 0u) {
-      long long waiting = 0;
-      if (lane == 0) {
-        unsigned long long tkc = *reinterpret_cast<volatile unsigned long long *>(&a.ctr->ticket);
-        unsigned long long tl = *reinterpret_cast<volatile unsigned long long *>(&a.ctr->tail);
-        waiting = (long long)(tkc - tl);
-      }
-      waiting = __shfl_sync(FULL, waiting, 0);
-      if (waiting > 0) {
-        bool can = (state == ST_WORK) && (sp > sb);
-        unsigned donors = __ballot_sync(FULL, can);
-        int rank = __popc(donors & ((1u << lane) - 1));
-        bool give = can && rank < waiting;
-        unsigned givers = __ballot_sync(FULL, give);
-        if (givers) {
-          int leader = __ffs(givers) - 1;
-          unsigned long long base = 0;
-          if (lane == leader) {
-            atomicAdd(&a.ctr->outstanding, (unsigned long long)__popc(givers));
-            atomicAdd(&a.ctr->donations, (unsigned long long)__popc(givers));
-            base = atomicAdd(&a.ctr->tail, (unsigned long long)__popc(givers));
-          }
-          base = __shfl_sync(FULL, base, leader);
-          if (give) {
-            unsigned long long t = base + __popc(givers & ((1u << lane) - 1));
-            Item *it = a.ring + (t & a.ring_mask);
-            while (*reinterpret_cast<volatile unsigned *>(&it->seq) != 0u) {
-            }  // previous occupant not consumed yet (cannot happen within the ring bound)
-            int jd = stk_lv[sb];
-            it->out = out;
-            it->j0 = (unsigned short)jd;
-            it->vs = (unsigned char)(vals[jd] + 1);
-            it->ve = stk_hi[sb];
-            it->P[0] = stk_P[sb].x;
-            it->P[1] = stk_P[sb].y;
-            uint32_t *pw = reinterpret_cast<uint32_t *>(it->prefix);
-            for (int w = 0; w < (jd + 3) / 4; ++w) pw[w] = valw[w];
-            ++sb;  // this lane no longer owns the rest of that level
+    // ---------------- acquire a work item (lane 0) ----------------
+    int kind = 0;  // 0 done, 1 fresh output, 2 queued subtree
+    unsigned out = 0;
+    unsigned long long tk = 0;
+    if (lane == 0) {
+      unsigned long long idx = atomicAdd(&a.ctr->fresh_next, 1ull);
+      if (idx < nfeas) {
+        kind = 1;
+        out = a.feas[idx];
+      } else {
+        tk = atomicAdd(&a.ctr->ticket, 1ull);
+        const Item *it = a.ring + (tk & a.ring_mask);
+        unsigned ns = 32;
+        while (true) {
+          unsigned seq = *reinterpret_cast<const volatile unsigned *>(&it->seq);
+          if (seq == (unsigned)(tk + 1)) {
             __threadfence();
-            *reinterpret_cast<volatile unsigned *>(&it->seq) = (unsigned)(t + 1);
+            kind = 2;
+            out = __ldcg(&it->out);
+            break;
+          }
+          if (vload(&a.ctr->outstanding) == 0ull) break;
+          __nanosleep(ns);
+          if (ns < 1024) ns <<= 1;
+        }
+      }
+    }
+    kind = __shfl_sync(FULL, kind, 0);
+    if (kind == 0) break;
+    out = __shfl_sync(FULL, out, 0);
+    tk = __shfl_sync(FULL, tk, 0);
+    ++items;
+
+    // ---------------- stage the output's plan ----------------
+    if (out != cur_out) {
+      const unsigned char *gp = a.plans + (size_t)out * a.plan_stride;
+      const PlanHead *gh = reinterpret_cast<const PlanHead *>(gp);
+      int Lq = gh->L, nf = gh->nfac;
+      // head + levels
+      int n16 = 2 + Lq;
+      for (int i = lane; i < n16; i += 32)
+        reinterpret_cast<int4 *>(s_plan)[i] = reinterpret_cast<const int4 *>(gp)[i];
+      // factors (stored after Lg levels in global, after Lq levels in shared)
+      const int4 *gf = reinterpret_cast<const int4 *>(gp + sizeof(PlanHead) + (size_t)a.Lg * sizeof(PlanLevel));
+      int4 *sf = reinterpret_cast<int4 *>(s_plan + sizeof(PlanHead) + (size_t)Lq * sizeof(PlanLevel));
+      for (int i = lane; i < nf; i += 32) sf[i] = gf[i];
+      s_fac = reinterpret_cast<const PlanFactor *>(sf);
+      L = Lq;
+      cur_out = out;
+      __syncwarp();
+    }
+    const PlanHead *sh = reinterpret_cast<const PlanHead *>(s_plan);
+
+    // ---------------- lane 0 begins the item ----------------
+    bool working = false;
+    int j = 0, bot = 0, top = 0;
+    novf = 0;
+    double2 Pb = make_double2(0.0, 0.0), acc = make_double2(0.0, 0.0);
+    unsigned long long npaths = 0, ncm = 0;
+    {
+      int j0 = 0, vs = 0, ve = 0;
+      double2 P0;
+      if (kind == 1) {
+        PlanLevel l0 = s_lev[0];
+        vs = max((int)lb[l0.ol] + l0.cl, (int)l0.lo);
+        ve = min((int)lb[l0.or_] + l0.cr, (int)l0.hi);
+        P0 = make_double2(sh->root[0], sh->root[1]);
+      } else {
+        Item *it = a.ring + (tk & a.ring_mask);
+        // the slot was written by another SM: read around L1
+        uint32_t w2 = __ldcg(reinterpret_cast<const uint32_t *>(it) + 2);
+        j0 = w2 & 0xffff;
+        vs = (w2 >> 16) & 0xff;
+        ve = w2 >> 24;
+        P0 = __ldcg(reinterpret_cast<const double2 *>(it->P));
+        // prefix bytes -> lane 0's column (one word per lane)
+        int nw = (j0 + 4) >> 2;  // slots [0, j0]: the zero slot and levels < j0
+        const uint32_t *pw = reinterpret_cast<const uint32_t *>(it->prefix);
+        for (int w = lane; w < nw; w += 32) *reinterpret_cast<uint32_t *>(vcol + w * 128) = __ldcg(pw + w);
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence();
+          *reinterpret_cast<volatile unsigned *>(&it->seq) = 0u;  // slot free again
+        }
+      }
+      if (lane == 0) {
+        working = true;
+        j = j0;
+        lb[lofp_level_off(j0)] = (unsigned char)vs;
+        if (ve > vs) {
+          stkM[0 * 32 + lane] = (uint32_t)j0 | ((uint32_t)ve << 8);
+          stkP[0 * 32 + lane] = P0;
+          top = 1;
+        }
+        Pb = P0;
+      }
+    }
+    __syncwarp();
+
+    unsigned iter = 0;
+    while (true) {
+      // ---------------- intra-warp hand-over ----------------
+      unsigned idle = __ballot_sync(FULL, !working);
+      if (idle) {
+        unsigned donors = __ballot_sync(FULL, working && (top > bot));
+        if (donors == 0) {
+          if (idle == FULL) break;  // item finished
+        } else {
+          int ni = __popc(idle), nd = __popc(donors);
+          int n = ni < nd ? ni : nd;
+          unsigned lt = lanemask_lt();
+          int partner = lane;
+          bool recv = false, give = false;
+          if (!working) {
+            int r = __popc(idle & lt);
+            if (r < n) {
+              partner = __fns(donors, 0, r + 1);
+              recv = true;
+            }
+          } else if (top > bot) {
+            int r = __popc(donors & lt);
+            if (r < n) {
+              partner = __fns(idle, 0, r + 1);
+              give = true;
+            }
+          }
+          int pbot = __shfl_sync(FULL, bot, partner);
+          if (recv) {
+            int e = pbot % LOFP_STK;
+            uint32_t m = stkM[e * 32 + partner];
+            double2 P = stkP[e * 32 + partner];
+            int jd = m & 0xff, hh = (m >> 8) & 0xff;
+            int nw = ((jd + 1) >> 2) + 1;  // words holding slots [0, jd + 1]
+            for (int w = 0; w < nw; ++w)
+              *reinterpret_cast<uint32_t *>(vcol + w * 128 + 4 * lane) =
+                  *reinterpret_cast<const uint32_t *>(vcol + w * 128 + 4 * partner);
+            int v = (int)lb[lofp_level_off(jd)] + 1;
+            lb[lofp_level_off(jd)] = (unsigned char)v;
+            bot = top = 0;
+            if (hh > v) {
+              stkM[lane] = (uint32_t)jd | ((uint32_t)hh << 8);
+              stkP[lane] = P;
+              top = 1;
+            }
+            Pb = P;
+            j = jd;
+            working = true;
+            ++dons;
+          }
+          __syncwarp();
+          if (give) ++bot;
+        }
+      }
+
+      // ---------------- one DFS node per working lane ----------------
+      if (working) {
+        PlanLevel lv = s_lev[j];
+        double2 P = Pb;
+        for (int f = lv.fbeg; f < lv.fend; ++f) {
+          PlanFactor fd = s_fac[f];
+          int va = lb[fd.oa], vb = lb[fd.ob], vc = lb[fd.oc], vy = lb[fd.oy];
+          int row = fd.base + fd.stride * (vb - va) + (vc - vb);
+          int o = s_off[row] + (vy - va) + fd.dy;
+          P = cmul(P, s_ent[o]);
+          if (COUNTED) ncm += (vc - va + fd.dx) > 0;
+        }
+        if (j == L - 1) {  // a leaf: one valid path of eq. (1)
+          acc.x += P.x;
+          acc.y += P.y;
+          if (COUNTED) ++npaths;
+          if (top > bot) {
+            int e = (top - 1) % LOFP_STK;
+            uint32_t m = stkM[e * 32 + lane];
+            int jj = m & 0xff, hh = (m >> 8) & 0xff;
+            int v = (int)lb[lofp_level_off(jj)] + 1;
+            lb[lofp_level_off(jj)] = (unsigned char)v;
+            Pb = stkP[e * 32 + lane];
+            if (v == hh) --top;
+            j = jj;
+          } else if (novf > 0) {
+            uint32_t m = ovfM[novf - 1];
+            int jj = m & 0xff, hh = (m >> 8) & 0xff;
+            int v = (int)lb[lofp_level_off(jj)] + 1;
+            lb[lofp_level_off(jj)] = (unsigned char)v;
+            Pb = ovfP[novf - 1];
+            if (v == hh) --novf;
+            j = jj;
+          } else {
+            working = false;
+          }
+        } else {  // descend: the next level's exact range (never empty, reading R5)
+          int jn = j + 1;
+          PlanLevel nl = s_lev[jn];
+          int lo = max((int)lb[nl.ol] + nl.cl, (int)nl.lo);
+          int hi = min((int)lb[nl.or_] + nl.cr, (int)nl.hi);
+          lb[lofp_level_off(jn)] = (unsigned char)lo;
+          if (hi > lo) {
+            if (top - bot == LOFP_STK) {  // full: move the shallowest entry away
+              int e = bot % LOFP_STK;
+              uint32_t m = stkM[e * 32 + lane];
+              double2 Pe = stkP[e * 32 + lane];
+              int jd = m & 0xff, hh = (m >> 8) & 0xff;
+              bool pushed = false;
+              unsigned long long tl = vload(&a.ctr->tail), tkc = vload(&a.ctr->ticket);
+              if (tl < tkc + (a.ring_mask >> 1)) {  // room in the global queue
+                atomicAdd(&a.ctr->outstanding, 1ull);
+                unsigned long long slot = atomicAdd(&a.ctr->tail, 1ull);
+                Item *it = a.ring + (slot & a.ring_mask);
+                while (*reinterpret_cast<volatile unsigned *>(&it->seq) != 0u) __nanosleep(64);
+                it->out = out;
+                it->j0 = (unsigned short)jd;
+                it->vs = (unsigned char)(lb[lofp_level_off(jd)] + 1);
+                it->ve = (unsigned char)hh;
+                it->P[0] = Pe.x;
+                it->P[1] = Pe.y;
+                uint32_t *pw = reinterpret_cast<uint32_t *>(it->prefix);
+                for (int w = 0; w < (jd + 4) / 4; ++w) pw[w] = *reinterpret_cast<const uint32_t *>(vcol + w * 128 + 4 * lane);
+                __threadfence();
+                *reinterpret_cast<volatile unsigned *>(&it->seq) = (unsigned)(slot + 1);
+                pushed = true;
+                ++spills;
+              }
+              if (!pushed) {
+                // shift the overflow stack: entries there are shallower than the ring's
+                ovfM[novf] = m;
+                ovfP[novf] = Pe;
+                // keep LIFO order inside overflow: the new entry is deeper than older
+                // overflow entries, so it belongs on top
+                ++novf;
+                ++ovfc;
+              }
+              ++bot;
+            }
+            int e = top % LOFP_STK;
+            stkM[e * 32 + lane] = (uint32_t)jn | ((uint32_t)hi << 8);
+            stkP[e * 32 + lane] = P;
+            ++top;
+          }
+          Pb = P;
+          j = jn;
+        }
+      }
+
+      // ---------------- feed idle warps through the global queue ----------------
+      if (((++iter) & 31u) == 0u) {
+        long long waiting = 0;
+        if (lane == 0) waiting = (long long)(vload(&a.ctr->ticket) - vload(&a.ctr->tail));
+        waiting = __shfl_sync(FULL, waiting, 0);
+        if (waiting > 0) {
+          bool can = working && (top > bot);
+          unsigned cands = __ballot_sync(FULL, can);
+          int r = __popc(cands & lanemask_lt());
+          bool give = can && r < waiting;
+          unsigned givers = __ballot_sync(FULL, give);
+          if (givers) {
+            int leader = __ffs(givers) - 1;
+            unsigned long long base = 0;
+            if (lane == leader) {
+              atomicAdd(&a.ctr->outstanding, (unsigned long long)__popc(givers));
+              base = atomicAdd(&a.ctr->tail, (unsigned long long)__popc(givers));
+            }
+            base = __shfl_sync(FULL, base, leader);
+            if (give) {
+              unsigned long long slot = base + __popc(givers & lanemask_lt());
+              Item *it = a.ring + (slot & a.ring_mask);
+              while (*reinterpret_cast<volatile unsigned *>(&it->seq) != 0u) __nanosleep(64);
+              int e = bot % LOFP_STK;
+              uint32_t m = stkM[e * 32 + lane];
+              int jd = m & 0xff, hh = (m >> 8) & 0xff;
+              double2 Pe = stkP[e * 32 + lane];
+              it->out = out;
+              it->j0 = (unsigned short)jd;
+              it->vs = (unsigned char)(lb[lofp_level_off(jd)] + 1);
+              it->ve = (unsigned char)hh;
+              it->P[0] = Pe.x;
+              it->P[1] = Pe.y;
+              uint32_t *pw = reinterpret_cast<uint32_t *>(it->prefix);
+              for (int w = 0; w < (jd + 4) / 4; ++w) pw[w] = *reinterpret_cast<const uint32_t *>(vcol + w * 128 + 4 * lane);
+              __threadfence();
+              *reinterpret_cast<volatile unsigned *>(&it->seq) = (unsigned)(slot + 1);
+              ++bot;
+              ++spills;
+            }
           }
         }
       }
     }
+
+    // ---------------- item finished: warp reduction, one atomic per item ----------------
+    for (int s = 16; s > 0; s >>= 1) {
+      acc.x += __shfl_xor_sync(FULL, acc.x, s);
+      acc.y += __shfl_xor_sync(FULL, acc.y, s);
+      if (COUNTED) {
+        npaths += __shfl_xor_sync(FULL, npaths, s);
+        ncm += __shfl_xor_sync(FULL, ncm, s);
+      }
+    }
+    if (lane == 0) {
+      atomicAdd(&a.amps[2 * out], acc.x);
+      atomicAdd(&a.amps[2 * out + 1], acc.y);
+      if (COUNTED) {
+        atomicAdd(&a.counts[out], npaths);
+        atomicAdd(&a.ctr->leaves, npaths);
+        atomicAdd(&a.ctr->cmuls, ncm);
+      }
+      __threadfence();
+      atomicAdd(&a.ctr->outstanding, ~0ull);  // -1
+    }
+    __syncwarp();
+  }
+  // statistics
+  for (int s = 16; s > 0; s >>= 1) {
+    spills += __shfl_xor_sync(FULL, spills, s);
+    ovfc += __shfl_xor_sync(FULL, ovfc, s);
+    dons += __shfl_xor_sync(FULL, dons, s);
+  }
+  if (lane == 0) {
+    atomicAdd(&a.ctr->items, items);
+    atomicAdd(&a.ctr->spills, spills);
+    atomicAdd(&a.ctr->ovf, ovfc);
+    atomicAdd(&a.ctr->donations, dons);
   }
 }
 
@@ -416,37 +626,57 @@ cudaError_t lofp_launch_tables(const CallArgs &a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t lofp_launch_feasible(const CallArgs &a, cudaStream_t s) {
+cudaError_t lofp_launch_plan(const CallArgs &a, cudaStream_t s) {
   if (a.B == 0) return cudaSuccess;
-  int bs = 128;
-  lofp_feasible_kernel<<<(unsigned)((a.B + bs - 1) / bs), bs, 0, s>>>(a);
+  int bs = 64;
+  lofp_plan_kernel<<<(unsigned)((a.B + bs - 1) / bs), bs, 0, s>>>(a);
   return cudaGetLastError();
-}
-
-static size_t enum_smem(const CallArgs &a) {
-  size_t b = (size_t)a.nentries * 16 + (size_t)a.noffsets * 4;
-  b = (b + 15) & ~size_t(15);
-  b += (size_t)a.L * sizeof(LevelDesc) + (size_t)a.nfactors * sizeof(FactorDesc) + (size_t)(a.M + 1);
-  return (b + 15) & ~size_t(15);
 }
 
 cudaError_t lofp_enum_config(const CallArgs &a, bool counted, int *grid, int *block, size_t *smem) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  int sms = 0;
+  int sms = 0, maxblk = 0, maxsm = 0;
   e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return e;
-  size_t sm = enum_smem(a);
+  e = cudaDeviceGetAttribute(&maxblk, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  e = cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  if (e != cudaSuccess) return e;
   const void *fn = counted ? (const void *)lofp_enum_kernel<true> : (const void *)lofp_enum_kernel<false>;
+  cudaFuncAttributes fa;
+  e = cudaFuncGetAttributes(&fa, fn);
+  if (e != cudaSuccess) return e;
+  // Pick warps per block W and blocks per SM n to maximise resident warps: the staged
+  // tables are paid once per block, the per-warp state once per warp.
+  const size_t tb = (size_t)a.table_bytes, wbytes = (size_t)a.warp_bytes;
+  const int max_w = LOFP_ENUM_MAX_THREADS / 32;
+  int regs_warps = fa.numRegs > 0 ? 65536 / (fa.numRegs * 32) : 64;
+  int best_w = 0, best_n = 0;
+  for (int w = 1; w <= max_w; ++w) {
+    size_t per_block = tb + (size_t)w * wbytes + 1024;  // + the per-block reservation
+    if (per_block - 1024 > (size_t)maxblk) break;
+    int n = (int)((size_t)maxsm / per_block);
+    int nw = regs_warps / w;
+    if (nw < n) n = nw;
+    if (n > 32) n = 32;
+    if (n < 1) continue;
+    if (n * w > best_n * best_w || (n * w == best_n * best_w && w > best_w)) {
+      best_w = w;
+      best_n = n;
+    }
+  }
+  if (best_w == 0) return cudaErrorInvalidConfiguration;
+  size_t sm = tb + (size_t)best_w * wbytes;
   e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
-  int bt = 256, per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, bt, sm);
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, best_w * 32, sm);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   *grid = per_sm * sms;
-  *block = bt;
+  *block = best_w * 32;
   *smem = sm;
   return cudaSuccess;
 }

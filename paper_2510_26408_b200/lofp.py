@@ -24,7 +24,9 @@ class lofp_bs(ctypes.Structure):
 
 class lofp_run_stats(ctypes.Structure):
     _fields_ = [("batch", ctypes.c_int64), ("feasible", ctypes.c_int64), ("items", ctypes.c_int64),
-                ("donations", ctypes.c_int64), ("levels", ctypes.c_int32), ("table_entries", ctypes.c_int32),
+                ("spills", ctypes.c_int64), ("donations", ctypes.c_int64), ("overflows", ctypes.c_int64),
+                ("paths", ctypes.c_int64), ("cmuls", ctypes.c_int64),
+                ("levels", ctypes.c_int32), ("table_entries", ctypes.c_int32),
                 ("smem_bytes", ctypes.c_int32), ("grid_blocks", ctypes.c_int32),
                 ("block_threads", ctypes.c_int32), ("bad_rows", ctypes.c_int32),
                 ("enum_ms", ctypes.c_float), ("total_ms", ctypes.c_float)]

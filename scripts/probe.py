@@ -9,7 +9,8 @@ import lofp_inputs as li
 from paper_2510_26408_b200 import Circuit
 
 budget = float(sys.argv[1]) if len(sys.argv) > 1 else 2e10
-for idx in (1, 2, 3, 4):
+cfgs = [int(x) for x in sys.argv[2].split(',')] if len(sys.argv) > 2 else [1, 2, 3, 4]
+for idx in cfgs:
     c = li.config(idx)
     d = np.load(os.path.join(ROOT, "data", f"cfg{idx}.npz"))
     T = (d["T_cond"] if "T_cond" in d.files else d["T_literal"]).astype(np.int32)
@@ -27,5 +28,5 @@ for idx in (1, 2, 3, 4):
         ms = e0.elapsed_time(e1); st = circ.stats()
         res.append(ms)
     print(json.dumps(dict(cfg=idx, outputs=n, paths=P.sum(), ms=min(res), paths_per_s=P.sum() / (min(res) * 1e-3),
-                          enum_ms=st["enum_ms"], total_ms=st["total_ms"], items=st["items"], donations=st["donations"],
+                          enum_ms=st["enum_ms"], total_ms=st["total_ms"], items=st["items"], spills=st["spills"], donations=st["donations"], ovf=st["overflows"], block=st["block_threads"],
                           levels=st["levels"], entries=st["table_entries"], smem=st["smem_bytes"], grid=st["grid_blocks"])), flush=True)
