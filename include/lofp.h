@@ -139,6 +139,12 @@ typedef struct {
 
 lofp_status lofp_stats(lofp_ctx *ctx, lofp_run_stats *out);
 
+/* Work-distribution histograms of the last lofp_amplitudes_counted call (zeros after an
+ * uncounted call): subtrees handed between lanes of a warp (handover) and pushed to the
+ * global queue (spill), indexed by (deepest level - level of the handed-over branch),
+ * clamped to 63.  handover and spill are host uint64 [64].  Synchronises the call. */
+lofp_status lofp_work_histograms(lofp_ctx *ctx, uint64_t *handover, uint64_t *spill);
+
 #ifdef __cplusplus
 }
 #endif

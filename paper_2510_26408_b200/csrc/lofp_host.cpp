@@ -204,8 +204,11 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
   a.Lg = ctx->Lg;
   a.vals_slots = (int)((ctx->Lg + 1 + 3) & ~3);
   a.B = B;
+  // head | levels [Lg] | factors [nbs] | scatter u16 [4 nbs] | pad | scratch factors [nbs] |
+  // scratch scatter u32 [4 nbs]  (see lofp_plan_kernel)
   a.plan_stride = (int)round16(sizeof(PlanHead) + (size_t)ctx->Lg * sizeof(PlanLevel) +
-                               2 * (size_t)ctx->nbs * sizeof(PlanFactor) + 2 * (size_t)ctx->nbs);
+                               2 * (size_t)ctx->nbs * sizeof(PlanFactor) + 8 * (size_t)ctx->nbs + 16 +
+                               16 * (size_t)ctx->nbs);
   a.T = output_occ;
   a.amps = amps;
   a.counts = counts;
@@ -308,16 +311,17 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
   // (sync 2) the largest per-output plan sizes the enumeration kernel's shared memory
   CK(cudaMemcpyAsync(ctx->h_ctr.p, a.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, stream), "read plan sizes");
   CK(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
-  const int maxL = hc->maxL, maxF = hc->maxF;
+  const int maxL = hc->maxL, maxF = hc->maxF, maxS = hc->maxS;
   ctx->stats.levels = maxL;
   CK(cudaEventRecord(ctx->ev_enum0, stream), "cudaEventRecord");
   if (hc->nfeas > 0) {
     a.vals_slots = (maxL + 1 + 3) & ~3;
     // plans were written with the zero slot of the global bound; re-base is not needed
     // because the kernel only dereferences slots < maxL and the zero slot below
-    a.plan_smem = (int)round16(sizeof(PlanHead) + (size_t)(maxL + maxF) * 16);
+    a.plan_smem = (int)round16(sizeof(PlanHead) + (size_t)(maxL + maxF) * 16 + 2 * (size_t)maxS);
     a.maxfac = maxF;
-    a.warp_bytes = (int)round16((size_t)a.plan_smem + (size_t)a.vals_slots * 32 + (size_t)LOFP_STK * 32 * 20);
+    a.warp_bytes = (int)round16((size_t)a.plan_smem + (size_t)a.vals_slots * 32 + (size_t)maxF * 128 +
+                                (size_t)LOFP_STK * 32 * 20 + 32);
     int grid = 0, block = 0;
     size_t smem = 0;
     cudaError_t e = lofp_enum_config(a, counts != nullptr, &grid, &block, &smem);
@@ -506,6 +510,21 @@ lofp_status lofp_stats(lofp_ctx *ctx, lofp_run_stats *out) {
   }
   *out = ctx->stats;
   return ctx->stats.bad_rows ? LOFP_E_BAD_OUTPUT : LOFP_OK;
+}
+
+lofp_status lofp_work_histograms(lofp_ctx *ctx, uint64_t *handover, uint64_t *spill) {
+  if (!ctx || !handover || !spill) return LOFP_E_INVALID_ARG;
+  if (ctx->h_ctr.p == nullptr) {
+    for (int i = 0; i < 64; ++i) handover[i] = spill[i] = 0;
+    return LOFP_OK;
+  }
+  CK(cudaEventSynchronize(ctx->ev_end), "cudaEventSynchronize");
+  const Counters *hc = (const Counters *)ctx->h_ctr.p;
+  for (int i = 0; i < 64; ++i) {
+    handover[i] = hc->don_hist[i];
+    spill[i] = hc->spill_hist[i];
+  }
+  return LOFP_OK;
 }
 
 void lofp_destroy(lofp_ctx *ctx) {

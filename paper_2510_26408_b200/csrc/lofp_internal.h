@@ -18,9 +18,10 @@
 
 #define LOFP_MAX_LEVELS 128   // DFS levels (free BS outputs) per circuit
 #define LOFP_STK 8            // per-lane branch-stack entries kept in shared memory
-#define LOFP_OVF (LOFP_MAX_LEVELS - LOFP_STK + 8)  // per-lane local-memory overflow entries
+#define LOFP_OVF 128           // per-lane local-memory overflow entries (>= LOFP_MAX_LEVELS)
 #define LOFP_ITEM_BYTES 256   // one global work-queue slot
 #define LOFP_ITEM_PREFIX 224  // prefix bytes an item can carry (>= LOFP_MAX_LEVELS)
+#define LOFP_SPILL_MIN_DIST 6  // global-queue spills only for branches >= this many levels above the leaf level
 #define LOFP_ENUM_MAX_THREADS 512  // largest block of the enumeration kernel
 #define LOFP_MAX_CUTS 130     // M + 1 for M <= LOFP_MAX_MODES (128)
 
@@ -36,29 +37,36 @@ __host__ __device__ inline uint16_t lofp_level_off(int j) { return lofp_slot_off
 // A DFS level j (a free F_l(k)).  Range at run time:
 //   [max(vals[ol] + cl, lo), min(vals[or_] + cr, hi)]  with vals[ol] + cl = F_{l-1}(k-1),
 //   vals[or_] + cr = F_{l-1}(k+1) (a constant uses the lane's zero slot), lo/hi the
-//   output's box.  Factors [fbeg, fend) are the elements attached to this level.
+//   output's box.  Factors [fbeg, fend) are the elements attached to this level;
+//   scatter entries [sbeg, send) are the key bytes that hold this level's value.
 struct __align__(16) PlanLevel {
   uint16_t ol, or_;
   uint8_t cl, cr, lo, hi;
   uint16_t fbeg, fend;
-  uint32_t pad;
+  uint16_t sbeg, send;
 };
 
-// One attached BS element.  With va = vals[oa] etc. (0 for constants):
-//   row = base + stride * (vb - va) + (vc - vb);  entry = offsets[row] + (vy - va) + dy
-// (the constants of a, b, c, y are folded into base and dy); dx = cc - ca so that
-// x1 + x2 = vc - va + dx (used only to count non-vacuum multiplications).
+// One attached BS element.  Its per-lane key word holds the variable parts of its four
+// inputs as bytes (a, b, c, y) = (F_{l-1}(k-1), F_{l-1}(k), F_{l-1}(k+1), F_l(k)); a
+// constant input contributes 0 and is folded into base / dy / dx.  Then
+//   row   = dp4a(key, crow, base)      = off_b + stride (x1) + x2
+//   entry = offsets[row] + dp4a(key, (-1, 0, 0, 1), dy)   (+ y1)
+//   x1 + x2 = dp4a(key, (-1, 0, 1, 0), dx)                 (counted mode only)
+// with crow = (-stride, stride - 1, 1, 0) as signed bytes.
 struct __align__(16) PlanFactor {
-  uint16_t oa, ob, oc, oy;
+  int32_t crow;
   int32_t base;
-  int16_t stride;
-  int8_t dy, dx;
+  int16_t dy;
+  int8_t dx;
+  uint8_t pad0;
+  uint32_t pad1;
 };
 
 struct PlanHead {
   double root[2];   // product of the elements with constant inputs
   uint16_t L, nfac; // levels and attached factors of this output
-  uint32_t pad0;
+  uint16_t nscat;   // scatter entries (u16 key-byte offsets, after the factors)
+  uint16_t pad0;
   uint64_t pad1;
 };
 static_assert(sizeof(PlanLevel) == 16 && sizeof(PlanFactor) == 16 && sizeof(PlanHead) == 32, "plan layout");
@@ -83,9 +91,13 @@ struct Counters {
   unsigned long long leaves;       // valid paths summed (counted mode)
   unsigned long long ovf;          // pushes that went to the local overflow stack
   unsigned long long donations;    // intra-warp hand-overs (stats)
+  unsigned long long don_hist[64]; // counted mode: hand-overs by (leaf level - level)
+  unsigned long long spill_hist[64];  // counted mode: queue spills by (leaf level - level)
   int32_t tmax[128];               // per-mode maximum of T over the batch
   int32_t maxL;                    // largest per-output level count
   int32_t maxF;                    // largest per-output attached-factor count
+  int32_t maxS;                    // largest per-output scatter-list length
+  int32_t pad;
 };
 
 // A queued subtree: output `out`, levels [0, j0) fixed to prefix[], level j0 ranging
@@ -110,7 +122,7 @@ struct CallArgs {
   int64_t B;
   int plan_stride;                    // bytes per output plan (multiple of 16)
   int plan_smem;                      // bytes reserved per warp for a staged plan
-  int maxfac;                         // bound on attached factors per output
+  int maxfac;                         // attached factors per output (max; key words per lane)
   int warp_bytes;                     // per-warp shared memory (plan + vals + stack)
   int table_bytes;                    // shared memory of the staged tables (16-aligned)
   const int32_t *T;                   // [B][M] device

@@ -120,6 +120,16 @@ struct Ref {
   int cst;
 };
 
+// A factor before sorting: input slots (-1 = constant), attachment level, folded table
+// coordinates.
+struct __align__(16) FacTmp {
+  int8_t s[4];
+  int16_t at, stride;
+  int32_t base;
+  int16_t dy, dx;
+};
+static_assert(sizeof(FacTmp) == 16, "FacTmp layout");
+
 __global__ void lofp_plan_kernel(CallArgs a) {
   int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= a.B) return;
@@ -144,9 +154,12 @@ __global__ void lofp_plan_kernel(CallArgs a) {
   unsigned char *plan = a.plans + (size_t)q * a.plan_stride;
   PlanHead *head = reinterpret_cast<PlanHead *>(plan);
   PlanLevel *lev = reinterpret_cast<PlanLevel *>(plan + sizeof(PlanHead));
+  // plan layout: head | levels [Lg] | factors [nbs] | scatter u16 [4 nbs] | scratch
   PlanFactor *fac = reinterpret_cast<PlanFactor *>(plan + sizeof(PlanHead) + (size_t)a.Lg * sizeof(PlanLevel));
-  PlanFactor *tmp = fac + a.nbs;                            // unsorted factors
-  uint16_t *att = reinterpret_cast<uint16_t *>(tmp + a.nbs);  // their levels
+  uint16_t *scat = reinterpret_cast<uint16_t *>(fac + a.nbs);
+  FacTmp *tmp = reinterpret_cast<FacTmp *>((reinterpret_cast<uintptr_t>(scat + 4 * (size_t)a.nbs) + 15) &
+                                           ~uintptr_t(15));  // unsorted factors
+  uint32_t *stmp = reinterpret_cast<uint32_t *>(tmp + a.nbs);         // unsorted scatter
   const uint16_t zero_off = LOFP_ZERO_OFF;
   const double2 *ent = reinterpret_cast<const double2 *>(a.entries);
 
@@ -174,7 +187,7 @@ __global__ void lofp_plan_kernel(CallArgs a) {
       pl.lo = (uint8_t)lo;
       pl.hi = (uint8_t)hi;
       pl.fbeg = pl.fend = 0;
-      pl.pad = 0;
+      pl.sbeg = pl.send = 0;
       lev[L] = pl;
       ++L;
     }
@@ -192,34 +205,59 @@ __global__ void lofp_plan_kernel(CallArgs a) {
       continue;
     }
     if (A.slot < 0 && C.slot < 0 && cc == ca) continue;  // always vacuum
-    PlanFactor pf;
-    pf.oa = A.slot < 0 ? zero_off : lofp_level_off(A.slot);
-    pf.ob = Bv.slot < 0 ? zero_off : lofp_level_off(Bv.slot);
-    pf.oc = C.slot < 0 ? zero_off : lofp_level_off(C.slot);
-    pf.oy = Y.slot < 0 ? zero_off : lofp_level_off(Y.slot);
-    pf.base = a.bs_base[b] + stride * (cb - ca) + (cc - cb);
-    pf.stride = (int16_t)stride;
-    pf.dy = (int8_t)(cy - ca);
-    pf.dx = (int8_t)(cc - ca);
-    tmp[nf] = pf;
-    att[nf] = (uint16_t)at;
+    FacTmp ft;
+    ft.s[0] = (int8_t)A.slot;
+    ft.s[1] = (int8_t)Bv.slot;
+    ft.s[2] = (int8_t)C.slot;
+    ft.s[3] = (int8_t)Y.slot;
+    ft.at = (int16_t)at;
+    ft.stride = (int16_t)stride;
+    ft.base = a.bs_base[b] + stride * (cb - ca) + (cc - cb);
+    ft.dy = (int16_t)(cy - ca);
+    ft.dx = (int16_t)(cc - ca);
+    tmp[nf] = ft;
     ++nf;
   }
-  // counting sort of the factors by level
+  // counting sort of the factors by level; factor f (sorted) owns key word f
   uint16_t cnt[LOFP_MAX_LEVELS + 1];
   for (int j = 0; j <= L; ++j) cnt[j] = 0;
-  for (int f = 0; f < nf; ++f) cnt[att[f] + 1]++;
+  for (int f = 0; f < nf; ++f) cnt[tmp[f].at + 1]++;
   for (int j = 0; j < L; ++j) cnt[j + 1] += cnt[j];
   for (int j = 0; j < L; ++j) {
     lev[j].fbeg = cnt[j];
     lev[j].fend = cnt[j + 1];
   }
-  for (int f = 0; f < nf; ++f) fac[cnt[att[f]]++] = tmp[f];
+  int ns = 0;
+  for (int f = 0; f < nf; ++f) {
+    const FacTmp ft = tmp[f];
+    int w = cnt[ft.at]++;
+    PlanFactor pf;
+    pf.crow = (int32_t)(((uint32_t)(uint8_t)(int8_t)(-ft.stride)) | ((uint32_t)(uint8_t)(int8_t)(ft.stride - 1) << 8) |
+                        (1u << 16));
+    pf.base = ft.base;
+    pf.dy = ft.dy;
+    pf.dx = (int8_t)ft.dx;
+    pf.pad0 = 0;
+    pf.pad1 = 0;
+    fac[w] = pf;
+    for (int p = 0; p < 4; ++p)
+      if (ft.s[p] >= 0) stmp[ns++] = ((uint32_t)ft.s[p] << 16) | (uint32_t)(w * 128 + p);
+  }
+  // counting sort of the scatter entries by the level whose value they hold
+  for (int j = 0; j <= L; ++j) cnt[j] = 0;
+  for (int i = 0; i < ns; ++i) cnt[(stmp[i] >> 16) + 1]++;
+  for (int j = 0; j < L; ++j) cnt[j + 1] += cnt[j];
+  for (int j = 0; j < L; ++j) {
+    lev[j].sbeg = cnt[j];
+    lev[j].send = cnt[j + 1];
+  }
+  for (int i = 0; i < ns; ++i) scat[cnt[stmp[i] >> 16]++] = (uint16_t)(stmp[i] & 0xffff);
   PlanHead h;
   h.root[0] = root.x;
   h.root[1] = root.y;
   h.L = (uint16_t)L;
   h.nfac = (uint16_t)nf;
+  h.nscat = (uint16_t)ns;
   h.pad0 = 0;
   h.pad1 = 0;
   *head = h;
@@ -231,6 +269,7 @@ __global__ void lofp_plan_kernel(CallArgs a) {
   }
   atomicMax(&a.ctr->maxL, L);
   atomicMax(&a.ctr->maxF, nf);
+  atomicMax(&a.ctr->maxS, ns);
   unsigned long long idx = atomicAdd(&a.ctr->nfeas, 1ull);
   a.feas[idx] = (uint32_t)q;
   atomicAdd(&a.ctr->outstanding, 1ull);
@@ -249,9 +288,48 @@ __device__ __forceinline__ unsigned long long vload(const unsigned long long *p)
   return *reinterpret_cast<const volatile unsigned long long *>(p);
 }
 
-// Per-lane state of the DFS.  vals bytes live in the warp's shared-memory column (lb);
-// the branch stack is a ring of LOFP_STK shared-memory entries [bot, top) plus a
-// local-memory overflow below it for rare deep stacks.
+// Per-lane state of the DFS, all in the warp's shared memory:
+//   vals  value bytes of the levels (slot 0 = constant zero, level j = slot j + 1),
+//         lane-interleaved by word (lofp_slot_off): the prefix handed to other lanes/warps;
+//   keys  one word per attached factor: the variable bytes (a, b, c, y) of its inputs,
+//         written when a level's value is set (scatter list of the plan), read with one
+//         32-bit load per factor and turned into the table index with two dp4a;
+//   stack ring of LOFP_STK branch entries [bot, top) (product before the level, level,
+//         last value), a local-memory overflow below it for rare deep stacks.
+struct WarpSmem {
+  unsigned char *plan;  // staged plan of the current output
+  unsigned char *vcol;  // vals words [slots/4][32]
+  unsigned char *kcol;  // key words [nfac][32]
+  double2 *stkP;        // [LOFP_STK][32]
+  uint32_t *stkM;       // [LOFP_STK][32]
+};
+
+// Write value v of level j: the vals byte and every key byte that holds it.
+__device__ __forceinline__ void set_level(unsigned char *lb, unsigned char *kb, const PlanLevel &lvref,
+                                          const uint16_t *scat, int j, int v) {
+  const uint32_t se = *reinterpret_cast<const uint32_t *>(&lvref.sbeg);  // sbeg | send << 16
+  const int sbeg = se & 0xffff, send = se >> 16;
+  lb[lofp_level_off(j)] = (unsigned char)v;
+#pragma unroll 2
+  for (int s = sbeg; s < send; ++s) kb[scat[s]] = (unsigned char)v;
+}
+
+// Product of the factors attached to level lv, times P.
+template <bool COUNTED>
+__device__ __forceinline__ double2 level_product(double2 P, const PlanLevel &lv, const PlanFactor *fac,
+                                                 const unsigned char *kb, const int32_t *s_off,
+                                                 const double2 *s_ent, unsigned long long &ncm) {
+  for (int f = lv.fbeg; f < lv.fend; ++f) {
+    const PlanFactor fd = fac[f];
+    const int key = *reinterpret_cast<const int *>(kb + f * 128);
+    const int row = __dp4a(key, fd.crow, fd.base);
+    const int o = s_off[row] + __dp4a(key, 0x010000ff, (int)fd.dy);  // + y - a
+    P = cmul(P, s_ent[o]);
+    if (COUNTED) ncm += __dp4a(key, 0x000100ff, (int)fd.dx) > 0;  // x1 + x2 = c - a
+  }
+  return P;
+}
+
 template <bool COUNTED>
 __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(CallArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -266,21 +344,46 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
   unsigned char *wb = smem + a.table_bytes + (size_t)warp * a.warp_bytes;
   unsigned char *s_plan = wb;
   const PlanLevel *s_lev = reinterpret_cast<const PlanLevel *>(s_plan + sizeof(PlanHead));
-  unsigned char *vcol = wb + a.plan_smem;                 // vals words [slots/4][32]
-  unsigned char *lb = vcol + 4 * lane;                    // this lane's byte base
-  double2 *stkP = reinterpret_cast<double2 *>(vcol + a.vals_slots * 32);  // [LOFP_STK][32]
-  uint32_t *stkM = reinterpret_cast<uint32_t *>(stkP + LOFP_STK * 32);     // [LOFP_STK][32]
+  unsigned char *vcol = wb + a.plan_smem;                                   // [slots/4][32] words
+  unsigned char *kcol = vcol + a.vals_slots * 32;                           // [maxfac][32] words
+  double2 *stkP = reinterpret_cast<double2 *>(kcol + (size_t)a.maxfac * 128);  // [LOFP_STK][32]
+  uint32_t *stkM = reinterpret_cast<uint32_t *>(stkP + LOFP_STK * 32);         // [LOFP_STK][32]
+  double2 *mbP = reinterpret_cast<double2 *>(stkM + LOFP_STK * 32);             // hand-over mailbox
+  uint32_t *mbM = reinterpret_cast<uint32_t *>(mbP + 1);
+  unsigned char *lb = vcol + 4 * lane;  // this lane's vals byte base
+  unsigned char *kb = kcol + 4 * lane;  // this lane's key byte base
   lb[LOFP_ZERO_OFF] = 0;
   const unsigned nfeas = (unsigned)a.ctr->nfeas;
 
+  // local-memory overflow below the shared ring: entries [obot, otop) (ring indices mod
+  // LOFP_OVF), all shallower than the shared-memory entries
   double2 ovfP[LOFP_OVF];
   uint32_t ovfM[LOFP_OVF];
-  int novf = 0;
+  int obot = 0, otop = 0;
 
   unsigned cur_out = 0xffffffffu;
   const PlanFactor *s_fac = nullptr;
-  int L = 0;
+  const uint16_t *s_scat = nullptr;
+  int L = 0, NF = 0;
   unsigned long long spills = 0, ovfc = 0, dons = 0, items = 0;
+
+  // spill the stack entry e (level jd, last value hh) of this lane to the global queue
+  auto spill = [&](unsigned long long slot, unsigned out, uint32_t m, double2 Pe) {
+    Item *it = a.ring + (slot & a.ring_mask);
+    while (*reinterpret_cast<volatile unsigned *>(&it->seq) != 0u) __nanosleep(64);
+    int jd = m & 0xff, hh = (m >> 8) & 0xff;
+    if (COUNTED) atomicAdd(&a.ctr->spill_hist[min(L - 1 - jd, 63)], 1ull);
+    it->out = out;
+    it->j0 = (unsigned short)jd;
+    it->vs = (unsigned char)(lb[lofp_level_off(jd)] + 1);
+    it->ve = (unsigned char)hh;
+    it->P[0] = Pe.x;
+    it->P[1] = Pe.y;
+    uint32_t *pw = reinterpret_cast<uint32_t *>(it->prefix);
+    for (int w = 0; w < (jd + 4) / 4; ++w) pw[w] = *reinterpret_cast<const uint32_t *>(vcol + w * 128 + 4 * lane);
+    __threadfence();
+    *reinterpret_cast<volatile unsigned *>(&it->seq) = (unsigned)(slot + 1);
+  };
 
   while (true) {
     // ---------------- acquire a work item (lane 0) ----------------
@@ -320,17 +423,19 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
     if (out != cur_out) {
       const unsigned char *gp = a.plans + (size_t)out * a.plan_stride;
       const PlanHead *gh = reinterpret_cast<const PlanHead *>(gp);
-      int Lq = gh->L, nf = gh->nfac;
-      // head + levels
-      int n16 = 2 + Lq;
-      for (int i = lane; i < n16; i += 32)
+      int Lq = gh->L, nf = gh->nfac, ns = gh->nscat;
+      for (int i = lane; i < 2 + Lq; i += 32)
         reinterpret_cast<int4 *>(s_plan)[i] = reinterpret_cast<const int4 *>(gp)[i];
-      // factors (stored after Lg levels in global, after Lq levels in shared)
-      const int4 *gf = reinterpret_cast<const int4 *>(gp + sizeof(PlanHead) + (size_t)a.Lg * sizeof(PlanLevel));
-      int4 *sf = reinterpret_cast<int4 *>(s_plan + sizeof(PlanHead) + (size_t)Lq * sizeof(PlanLevel));
-      for (int i = lane; i < nf; i += 32) sf[i] = gf[i];
+      const unsigned char *gf = gp + sizeof(PlanHead) + (size_t)a.Lg * sizeof(PlanLevel);
+      unsigned char *sf = s_plan + sizeof(PlanHead) + (size_t)Lq * sizeof(PlanLevel);
+      for (int i = lane; i < nf; i += 32) reinterpret_cast<int4 *>(sf)[i] = reinterpret_cast<const int4 *>(gf)[i];
+      const uint16_t *gs = reinterpret_cast<const uint16_t *>(gf + (size_t)a.nbs * sizeof(PlanFactor));
+      uint16_t *ss = reinterpret_cast<uint16_t *>(sf + (size_t)nf * sizeof(PlanFactor));
+      for (int i = lane; i < ns; i += 32) ss[i] = gs[i];
       s_fac = reinterpret_cast<const PlanFactor *>(sf);
+      s_scat = ss;
       L = Lq;
+      NF = nf;
       cur_out = out;
       __syncwarp();
     }
@@ -338,11 +443,13 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
 
     // ---------------- lane 0 begins the item ----------------
     bool working = false;
-    int j = 0, bot = 0, top = 0;
-    novf = 0;
+    int j = 0, bot = 0, top = 0, leafhi = 0;
+    obot = otop = 0;
     double2 Pb = make_double2(0.0, 0.0), acc = make_double2(0.0, 0.0);
     unsigned long long npaths = 0, ncm = 0;
     {
+      // all key words of this warp start at zero (constant inputs contribute 0)
+      for (int f = 0; f < NF; ++f) *reinterpret_cast<uint32_t *>(kb + f * 128) = 0u;
       int j0 = 0, vs = 0, ve = 0;
       double2 P0;
       if (kind == 1) {
@@ -358,7 +465,6 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
         vs = (w2 >> 16) & 0xff;
         ve = w2 >> 24;
         P0 = __ldcg(reinterpret_cast<const double2 *>(it->P));
-        // prefix bytes -> lane 0's column (one word per lane)
         int nw = (j0 + 4) >> 2;  // slots [0, j0]: the zero slot and levels < j0
         const uint32_t *pw = reinterpret_cast<const uint32_t *>(it->prefix);
         for (int w = lane; w < nw; w += 32) *reinterpret_cast<uint32_t *>(vcol + w * 128) = __ldcg(pw + w);
@@ -366,13 +472,20 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
         if (lane == 0) {
           __threadfence();
           *reinterpret_cast<volatile unsigned *>(&it->seq) = 0u;  // slot free again
+          for (int jj = 0; jj < j0; ++jj) {  // rebuild the keys of the prefix levels
+            PlanLevel lj = s_lev[jj];
+            int v = lb[lofp_level_off(jj)];
+            for (int q = lj.sbeg; q < lj.send; ++q) kb[s_scat[q]] = (unsigned char)v;
+          }
         }
       }
       if (lane == 0) {
         working = true;
         j = j0;
-        lb[lofp_level_off(j0)] = (unsigned char)vs;
-        if (ve > vs) {
+        set_level(lb, kb, s_lev[j0], s_scat, j0, vs);
+        if (j0 == L - 1) {
+          leafhi = ve;
+        } else if (ve > vs) {
           stkM[0 * 32 + lane] = (uint32_t)j0 | ((uint32_t)ve << 8);
           stkP[0 * 32 + lane] = P0;
           top = 1;
@@ -385,44 +498,59 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
     unsigned iter = 0;
     while (true) {
       // ---------------- intra-warp hand-over ----------------
+      // One per step: the lane holding the shallowest open branch of the warp gives it
+      // (all its remaining siblings) to the lowest idle lane.
       unsigned idle = __ballot_sync(FULL, !working);
       if (idle) {
-        unsigned donors = __ballot_sync(FULL, working && (top > bot));
-        if (donors == 0) {
+        int myshal = 0x7fffffff;
+        if (working) {
+          if (otop > obot)
+            myshal = (int)(ovfM[obot % LOFP_OVF] & 0xff);
+          else if (top > bot)
+            myshal = (int)(stkM[(bot % LOFP_STK) * 32 + lane] & 0xff);
+        }
+        int shal = __reduce_min_sync(FULL, myshal);
+        if (shal == 0x7fffffff) {
           if (idle == FULL) break;  // item finished
         } else {
-          int ni = __popc(idle), nd = __popc(donors);
-          int n = ni < nd ? ni : nd;
-          unsigned lt = lanemask_lt();
-          int partner = lane;
-          bool recv = false, give = false;
-          if (!working) {
-            int r = __popc(idle & lt);
-            if (r < n) {
-              partner = __fns(donors, 0, r + 1);
-              recv = true;
+          int donor = __ffs(__ballot_sync(FULL, myshal == shal)) - 1;
+          int recv = __ffs(idle) - 1;
+          if (lane == donor) {  // publish the shallowest open branch
+            uint32_t m;
+            double2 P;
+            if (otop > obot) {
+              m = ovfM[obot % LOFP_OVF];
+              P = ovfP[obot % LOFP_OVF];
+              ++obot;
+            } else {
+              int e = bot % LOFP_STK;
+              m = stkM[e * 32 + lane];
+              P = stkP[e * 32 + lane];
+              ++bot;
             }
-          } else if (top > bot) {
-            int r = __popc(donors & lt);
-            if (r < n) {
-              partner = __fns(idle, 0, r + 1);
-              give = true;
-            }
+            mbM[0] = m;
+            mbP[0] = P;
           }
-          int pbot = __shfl_sync(FULL, bot, partner);
-          if (recv) {
-            int e = pbot % LOFP_STK;
-            uint32_t m = stkM[e * 32 + partner];
-            double2 P = stkP[e * 32 + partner];
+          __syncwarp();
+          if (lane == recv) {
+            uint32_t m = mbM[0];
+            double2 P = mbP[0];
             int jd = m & 0xff, hh = (m >> 8) & 0xff;
             int nw = ((jd + 1) >> 2) + 1;  // words holding slots [0, jd + 1]
             for (int w = 0; w < nw; ++w)
               *reinterpret_cast<uint32_t *>(vcol + w * 128 + 4 * lane) =
-                  *reinterpret_cast<const uint32_t *>(vcol + w * 128 + 4 * partner);
+                  *reinterpret_cast<const uint32_t *>(vcol + w * 128 + 4 * donor);
+            // the donor's keys hold the prefix values (deeper bytes are rewritten on descent)
+            for (int f = 0; f < NF; ++f)
+              *reinterpret_cast<uint32_t *>(kcol + f * 128 + 4 * lane) =
+                  *reinterpret_cast<const uint32_t *>(kcol + f * 128 + 4 * donor);
             int v = (int)lb[lofp_level_off(jd)] + 1;
-            lb[lofp_level_off(jd)] = (unsigned char)v;
+            set_level(lb, kb, s_lev[jd], s_scat, jd, v);
             bot = top = 0;
-            if (hh > v) {
+            leafhi = 0;
+            if (jd == L - 1) {
+              leafhi = hh;
+            } else if (hh > v) {
               stkM[lane] = (uint32_t)jd | ((uint32_t)hh << 8);
               stkP[lane] = P;
               top = 1;
@@ -431,139 +559,104 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             j = jd;
             working = true;
             ++dons;
+            if (COUNTED) atomicAdd(&a.ctr->don_hist[min(L - 1 - jd, 63)], 1ull);
           }
           __syncwarp();
-          if (give) ++bot;
         }
       }
 
       // ---------------- one DFS node per working lane ----------------
+      // Every working lane does the same work per step: the product of its current
+      // level's factors, then one move (next leaf sibling / descend / pop) and one write
+      // of the new level value into the vals byte and the key bytes.
       if (working) {
-        PlanLevel lv = s_lev[j];
-        double2 P = Pb;
-        for (int f = lv.fbeg; f < lv.fend; ++f) {
-          PlanFactor fd = s_fac[f];
-          int va = lb[fd.oa], vb = lb[fd.ob], vc = lb[fd.oc], vy = lb[fd.oy];
-          int row = fd.base + fd.stride * (vb - va) + (vc - vb);
-          int o = s_off[row] + (vy - va) + fd.dy;
-          P = cmul(P, s_ent[o]);
-          if (COUNTED) ncm += (vc - va + fd.dx) > 0;
-        }
+        const PlanLevel lv = s_lev[j];
+        double2 P = level_product<COUNTED>(Pb, lv, s_fac, kb, s_off, s_ent, ncm);
+        int nj = j, nv = 0;
         if (j == L - 1) {  // a leaf: one valid path of eq. (1)
           acc.x += P.x;
           acc.y += P.y;
           if (COUNTED) ++npaths;
-          if (top > bot) {
+          int v = lb[lofp_level_off(j)];
+          if (v < leafhi) {
+            nv = v + 1;  // next sibling, same product prefix Pb
+          } else if (top > bot) {  // pop the deepest open branch
             int e = (top - 1) % LOFP_STK;
             uint32_t m = stkM[e * 32 + lane];
-            int jj = m & 0xff, hh = (m >> 8) & 0xff;
-            int v = (int)lb[lofp_level_off(jj)] + 1;
-            lb[lofp_level_off(jj)] = (unsigned char)v;
+            nj = m & 0xff;
+            nv = (int)lb[lofp_level_off(nj)] + 1;
             Pb = stkP[e * 32 + lane];
-            if (v == hh) --top;
-            j = jj;
-          } else if (novf > 0) {
-            uint32_t m = ovfM[novf - 1];
-            int jj = m & 0xff, hh = (m >> 8) & 0xff;
-            int v = (int)lb[lofp_level_off(jj)] + 1;
-            lb[lofp_level_off(jj)] = (unsigned char)v;
-            Pb = ovfP[novf - 1];
-            if (v == hh) --novf;
-            j = jj;
+            if (nv == (int)((m >> 8) & 0xff)) --top;
+          } else if (otop > obot) {
+            int e = (otop - 1) % LOFP_OVF;
+            uint32_t m = ovfM[e];
+            nj = m & 0xff;
+            nv = (int)lb[lofp_level_off(nj)] + 1;
+            Pb = ovfP[e];
+            if (nv == (int)((m >> 8) & 0xff)) --otop;
           } else {
             working = false;
           }
         } else {  // descend: the next level's exact range (never empty, reading R5)
-          int jn = j + 1;
-          PlanLevel nl = s_lev[jn];
-          int lo = max((int)lb[nl.ol] + nl.cl, (int)nl.lo);
+          nj = j + 1;
+          const PlanLevel nl = s_lev[nj];
+          nv = max((int)lb[nl.ol] + nl.cl, (int)nl.lo);
           int hi = min((int)lb[nl.or_] + nl.cr, (int)nl.hi);
-          lb[lofp_level_off(jn)] = (unsigned char)lo;
-          if (hi > lo) {
-            if (top - bot == LOFP_STK) {  // full: move the shallowest entry away
+          if (nj == L - 1) {
+            leafhi = hi;  // the leaf siblings are walked by the leaf branch above
+          } else if (hi > nv) {
+            if (top - bot == LOFP_STK) {  // full: the shallowest entry goes to the overflow
               int e = bot % LOFP_STK;
-              uint32_t m = stkM[e * 32 + lane];
-              double2 Pe = stkP[e * 32 + lane];
-              int jd = m & 0xff, hh = (m >> 8) & 0xff;
-              bool pushed = false;
-              unsigned long long tl = vload(&a.ctr->tail), tkc = vload(&a.ctr->ticket);
-              if (tl < tkc + (a.ring_mask >> 1)) {  // room in the global queue
-                atomicAdd(&a.ctr->outstanding, 1ull);
-                unsigned long long slot = atomicAdd(&a.ctr->tail, 1ull);
-                Item *it = a.ring + (slot & a.ring_mask);
-                while (*reinterpret_cast<volatile unsigned *>(&it->seq) != 0u) __nanosleep(64);
-                it->out = out;
-                it->j0 = (unsigned short)jd;
-                it->vs = (unsigned char)(lb[lofp_level_off(jd)] + 1);
-                it->ve = (unsigned char)hh;
-                it->P[0] = Pe.x;
-                it->P[1] = Pe.y;
-                uint32_t *pw = reinterpret_cast<uint32_t *>(it->prefix);
-                for (int w = 0; w < (jd + 4) / 4; ++w) pw[w] = *reinterpret_cast<const uint32_t *>(vcol + w * 128 + 4 * lane);
-                __threadfence();
-                *reinterpret_cast<volatile unsigned *>(&it->seq) = (unsigned)(slot + 1);
-                pushed = true;
-                ++spills;
-              }
-              if (!pushed) {
-                // shift the overflow stack: entries there are shallower than the ring's
-                ovfM[novf] = m;
-                ovfP[novf] = Pe;
-                // keep LIFO order inside overflow: the new entry is deeper than older
-                // overflow entries, so it belongs on top
-                ++novf;
-                ++ovfc;
-              }
+              int o = otop % LOFP_OVF;
+              ovfM[o] = stkM[e * 32 + lane];
+              ovfP[o] = stkP[e * 32 + lane];
+              ++otop;
               ++bot;
+              ++ovfc;
             }
             int e = top % LOFP_STK;
-            stkM[e * 32 + lane] = (uint32_t)jn | ((uint32_t)hi << 8);
+            stkM[e * 32 + lane] = (uint32_t)nj | ((uint32_t)hi << 8);
             stkP[e * 32 + lane] = P;
             ++top;
           }
           Pb = P;
-          j = jn;
+        }
+        if (working) {
+          j = nj;
+          set_level(lb, kb, s_lev[nj], s_scat, nj, nv);
         }
       }
 
       // ---------------- feed idle warps through the global queue ----------------
+      // At most one subtree per warp per check: the warp's shallowest open branch, and
+      // only when it is far from the leaves (a large subtree) and some warp is waiting.
       if (((++iter) & 31u) == 0u) {
         long long waiting = 0;
         if (lane == 0) waiting = (long long)(vload(&a.ctr->ticket) - vload(&a.ctr->tail));
         waiting = __shfl_sync(FULL, waiting, 0);
         if (waiting > 0) {
-          bool can = working && (top > bot);
-          unsigned cands = __ballot_sync(FULL, can);
-          int r = __popc(cands & lanemask_lt());
-          bool give = can && r < waiting;
-          unsigned givers = __ballot_sync(FULL, give);
-          if (givers) {
-            int leader = __ffs(givers) - 1;
-            unsigned long long base = 0;
-            if (lane == leader) {
-              atomicAdd(&a.ctr->outstanding, (unsigned long long)__popc(givers));
-              base = atomicAdd(&a.ctr->tail, (unsigned long long)__popc(givers));
-            }
-            base = __shfl_sync(FULL, base, leader);
-            if (give) {
-              unsigned long long slot = base + __popc(givers & lanemask_lt());
-              Item *it = a.ring + (slot & a.ring_mask);
-              while (*reinterpret_cast<volatile unsigned *>(&it->seq) != 0u) __nanosleep(64);
-              int e = bot % LOFP_STK;
-              uint32_t m = stkM[e * 32 + lane];
-              int jd = m & 0xff, hh = (m >> 8) & 0xff;
-              double2 Pe = stkP[e * 32 + lane];
-              it->out = out;
-              it->j0 = (unsigned short)jd;
-              it->vs = (unsigned char)(lb[lofp_level_off(jd)] + 1);
-              it->ve = (unsigned char)hh;
-              it->P[0] = Pe.x;
-              it->P[1] = Pe.y;
-              uint32_t *pw = reinterpret_cast<uint32_t *>(it->prefix);
-              for (int w = 0; w < (jd + 4) / 4; ++w) pw[w] = *reinterpret_cast<const uint32_t *>(vcol + w * 128 + 4 * lane);
-              __threadfence();
-              *reinterpret_cast<volatile unsigned *>(&it->seq) = (unsigned)(slot + 1);
-              ++bot;
+          int myshal = 0x7fffffff;
+          if (working) {
+            if (otop > obot)
+              myshal = (int)(ovfM[obot % LOFP_OVF] & 0xff);
+            else if (top > bot)
+              myshal = (int)(stkM[(bot % LOFP_STK) * 32 + lane] & 0xff);
+          }
+          int shal = __reduce_min_sync(FULL, myshal);
+          if (shal != 0x7fffffff && L - 1 - shal >= LOFP_SPILL_MIN_DIST) {
+            int giver = __ffs(__ballot_sync(FULL, myshal == shal)) - 1;
+            if (lane == giver) {
+              atomicAdd(&a.ctr->outstanding, 1ull);
+              unsigned long long slot = atomicAdd(&a.ctr->tail, 1ull);
+              if (otop > obot) {
+                int e = obot % LOFP_OVF;
+                spill(slot, out, ovfM[e], ovfP[e]);
+                ++obot;
+              } else {
+                int e = bot % LOFP_STK;
+                spill(slot, out, stkM[e * 32 + lane], stkP[e * 32 + lane]);
+                ++bot;
+              }
               ++spills;
             }
           }

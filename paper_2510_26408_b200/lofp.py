@@ -33,7 +33,7 @@ class lofp_run_stats(ctypes.Structure):
 
 
 EXPORTS = ["lofp_create", "lofp_amplitudes", "lofp_amplitudes_counted", "lofp_amplitudes_host",
-           "lofp_destroy", "lofp_status_string", "lofp_last_error", "lofp_stats"]
+           "lofp_destroy", "lofp_status_string", "lofp_last_error", "lofp_stats", "lofp_work_histograms"]
 
 
 def _load():
@@ -58,6 +58,8 @@ def _load():
     lib.lofp_last_error.restype = ctypes.c_char_p
     lib.lofp_stats.argtypes = [P, ctypes.POINTER(lofp_run_stats)]
     lib.lofp_stats.restype = ctypes.c_int
+    lib.lofp_work_histograms.argtypes = [P, P, P]
+    lib.lofp_work_histograms.restype = ctypes.c_int
     return lib
 
 
@@ -148,6 +150,13 @@ class Circuit:
                                        ctypes.c_void_p(t.ctypes.data), ctypes.c_void_p(out.ctypes.data))
         self._check(st)
         return out.view(np.complex128)[:, 0]
+
+    def work_histograms(self):
+        """(handover, spill) histograms of the last counted call, by distance from the leaf level."""
+        h = np.zeros(64, dtype=np.uint64)
+        sp = np.zeros(64, dtype=np.uint64)
+        self._check(_lib.lofp_work_histograms(self._h, ctypes.c_void_p(h.ctypes.data), ctypes.c_void_p(sp.ctypes.data)))
+        return h, sp
 
     def stats(self) -> dict:
         st = lofp_run_stats()

@@ -15,6 +15,9 @@ for idx in cfgs:
     d = np.load(os.path.join(ROOT, "data", f"cfg{idx}.npz"))
     T = (d["T_cond"] if "T_cond" in d.files else d["T_literal"]).astype(np.int32)
     P = (d["P_cond"] if "P_cond" in d.files else d["P_literal"]).astype(np.float64)
+    if os.environ.get("PROBE_SMALLEST"):  # the smallest trees first: many outputs, short run
+        o = np.argsort(P, kind="stable")
+        T, P = T[o], P[o]
     n = int(np.searchsorted(np.cumsum(P), budget)) if P.sum() > budget else len(P)
     n = max(n, 1)
     T, P = T[:n], P[:n]
@@ -27,6 +30,12 @@ for idx in cfgs:
         e0.record(); a = circ.amplitudes(c.S, Td); e1.record(); torch.cuda.synchronize()
         ms = e0.elapsed_time(e1); st = circ.stats()
         res.append(ms)
+    if os.environ.get("PROBE_HIST"):
+        cnt = torch.zeros(n, dtype=torch.int64, device="cuda")
+        circ.amplitudes(c.S, Td, counts=cnt); torch.cuda.synchronize()
+        h, sp = circ.work_histograms()
+        print("handover by leaf-distance:", h[:40].tolist())
+        print("spill by leaf-distance:", sp[:40].tolist())
     print(json.dumps(dict(cfg=idx, outputs=n, paths=P.sum(), ms=min(res), paths_per_s=P.sum() / (min(res) * 1e-3),
                           enum_ms=st["enum_ms"], total_ms=st["total_ms"], items=st["items"], spills=st["spills"], donations=st["donations"], ovf=st["overflows"], block=st["block_threads"],
                           levels=st["levels"], entries=st["table_entries"], smem=st["smem_bytes"], grid=st["grid_blocks"])), flush=True)
