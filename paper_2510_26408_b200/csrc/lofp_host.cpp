@@ -315,9 +315,12 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
   ctx->stats.levels = maxL;
   CK(cudaEventRecord(ctx->ev_enum0, stream), "cudaEventRecord");
   if (hc->nfeas > 0) {
-    a.vals_slots = (maxL + 1 + 3) & ~3;
+    a.vals_slots = (maxL + 2 + 3) & ~3;  // zero slot, levels, a scratch slot
     // plans were written with the zero slot of the global bound; re-base is not needed
     // because the kernel only dereferences slots < maxL and the zero slot below
+    // (the step's uniform loops read up to maxF descriptors / key words and maxS + 3
+    // scatter entries past a level's own list: vals, keys and stack follow inside the
+    // warp's region, so those reads never leave it)
     a.plan_smem = (int)round16(sizeof(PlanHead) + (size_t)(maxL + maxF) * 16 + 2 * (size_t)maxS);
     a.maxfac = maxF;
     a.warp_bytes = (int)round16((size_t)a.plan_smem + (size_t)a.vals_slots * 32 + (size_t)maxF * 128 +
@@ -341,6 +344,8 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
     a.ring = (Item *)ctx->d_ring.p;
     a.ring_mask = ctx->ring_cap - 1;
     ctx->stats.smem_bytes = (int32_t)smem;
+    ctx->stats.max_factors = maxF;
+    ctx->stats.max_scatter = maxS;
     ctx->stats.grid_blocks = grid;
     ctx->stats.block_threads = block;
     CK(lofp_launch_enum(a, counts != nullptr, grid, block, smem, stream), "enumeration kernel");

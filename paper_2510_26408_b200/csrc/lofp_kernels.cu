@@ -304,29 +304,52 @@ struct WarpSmem {
   uint32_t *stkM;       // [LOFP_STK][32]
 };
 
-// Write value v of level j: the vals byte and every key byte that holds it.
+// Write value v of level j: the vals byte and every key byte that holds it.  (Used off
+// the hot step; the step writes with a warp-uniform trip count, see below.)
 __device__ __forceinline__ void set_level(unsigned char *lb, unsigned char *kb, const PlanLevel &lvref,
                                           const uint16_t *scat, int j, int v) {
   const uint32_t se = *reinterpret_cast<const uint32_t *>(&lvref.sbeg);  // sbeg | send << 16
   const int sbeg = se & 0xffff, send = se >> 16;
   lb[lofp_level_off(j)] = (unsigned char)v;
-#pragma unroll 2
   for (int s = sbeg; s < send; ++s) kb[scat[s]] = (unsigned char)v;
 }
 
-// Product of the factors attached to level lv, times P.
+// Product of the factors attached to level lv, times P.  The trip count is the warp's
+// largest factor count (nmax, warp-uniform) so that every lane runs the same instruction
+// stream; a lane past its own count multiplies by table entry 0, which is exactly 1 (the
+// vacuum element of BS 0, R16).
 template <bool COUNTED>
-__device__ __forceinline__ double2 level_product(double2 P, const PlanLevel &lv, const PlanFactor *fac,
+__device__ __forceinline__ int factor_entry(const PlanFactor *fp, const unsigned char *kp, int i, int fcnt,
+                                            const int32_t *s_off, unsigned long long &ncm) {
+  const int2 fd = *reinterpret_cast<const int2 *>(fp + i);  // crow, base
+  const int key = *reinterpret_cast<const int *>(kp + i * 128);
+  const int row = __dp4a(key, fd.x, fd.y);
+  const int o = s_off[row] + __dp4a(key, 0x010000ff, (int)fp[i].dy);  // + y - a
+  const bool on = i < fcnt;
+  if (COUNTED) ncm += (on && __dp4a(key, 0x000100ff, (int)fp[i].dx) > 0);  // x1 + x2 = c - a
+  return on ? o : 0;
+}
+
+// Product of the factors attached to a level, times P.  The trip count is the warp's
+// largest factor count (nmax, warp-uniform) so that every lane runs the same instruction
+// stream; a lane past its own count reads the following descriptors/keys (inside the
+// warp's shared memory) and multiplies by table entry 0, which is exactly 1 (the vacuum
+// element of BS 0, R16).  Factors are taken in pairs: e_i e_{i+1} does not depend on P,
+// so the dependent fp64 chain is one complex multiplication per pair.
+template <bool COUNTED>
+__device__ __forceinline__ double2 level_product(double2 P, int fbeg, int fcnt, int nmax, const PlanFactor *fac,
                                                  const unsigned char *kb, const int32_t *s_off,
                                                  const double2 *s_ent, unsigned long long &ncm) {
-  for (int f = lv.fbeg; f < lv.fend; ++f) {
-    const PlanFactor fd = fac[f];
-    const int key = *reinterpret_cast<const int *>(kb + f * 128);
-    const int row = __dp4a(key, fd.crow, fd.base);
-    const int o = s_off[row] + __dp4a(key, 0x010000ff, (int)fd.dy);  // + y - a
-    P = cmul(P, s_ent[o]);
-    if (COUNTED) ncm += __dp4a(key, 0x000100ff, (int)fd.dx) > 0;  // x1 + x2 = c - a
+  const PlanFactor *fp = fac + fbeg;
+  const unsigned char *kp = kb + fbeg * 128;
+  int i = 0;
+#pragma unroll 1
+  for (; i + 1 < nmax; i += 2) {
+    const int o0 = factor_entry<COUNTED>(fp, kp, i, fcnt, s_off, ncm);
+    const int o1 = factor_entry<COUNTED>(fp, kp, i + 1, fcnt, s_off, ncm);
+    P = cmul(P, cmul(s_ent[o0], s_ent[o1]));
   }
+  if (i < nmax) P = cmul(P, s_ent[factor_entry<COUNTED>(fp, kp, i, fcnt, s_off, ncm)]);
   return P;
 }
 
@@ -353,21 +376,24 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
   unsigned char *lb = vcol + 4 * lane;  // this lane's vals byte base
   unsigned char *kb = kcol + 4 * lane;  // this lane's key byte base
   lb[LOFP_ZERO_OFF] = 0;
+  const uint16_t dummy_off = lofp_slot_off(a.vals_slots - 1);  // scratch byte for idle lanes
   const unsigned nfeas = (unsigned)a.ctr->nfeas;
 
   // local-memory overflow below the shared ring: entries [obot, otop) (ring indices mod
   // LOFP_OVF), all shallower than the shared-memory entries
   double2 ovfP[LOFP_OVF];
   uint32_t ovfM[LOFP_OVF];
-  int obot = 0, otop = 0;
 
   unsigned cur_out = 0xffffffffu;
   const PlanFactor *s_fac = nullptr;
   const uint16_t *s_scat = nullptr;
   int L = 0, NF = 0;
   unsigned long long spills = 0, ovfc = 0, dons = 0, items = 0;
+  uint32_t *const mySM = stkM + lane;    // this lane's stack metas, entry e at [e * 32]
+  double2 *const mySP = stkP + lane;     // this lane's stack products
+  const int dummy_rel = (int)dummy_off - a.vals_slots * 32;  // kb + dummy_rel = scratch byte
 
-  // spill the stack entry e (level jd, last value hh) of this lane to the global queue
+  // spill a branch (level jd = m & 0xff, last value m >> 8) of this lane to the global queue
   auto spill = [&](unsigned long long slot, unsigned out, uint32_t m, double2 Pe) {
     Item *it = a.ring + (slot & a.ring_mask);
     while (*reinterpret_cast<volatile unsigned *>(&it->seq) != 0u) __nanosleep(64);
@@ -440,11 +466,16 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
       __syncwarp();
     }
     const PlanHead *sh = reinterpret_cast<const PlanHead *>(s_plan);
+    const int Lm1 = L - 1;
 
     // ---------------- lane 0 begins the item ----------------
+    // Lane state: j = current level, v = its value, Pb = product before level j's
+    // factors, leafhi = last sibling when j is the leaf level, stack [bot, top) of open
+    // branches (meta = level | last value << 8, product before that level), overflow
+    // [obot, otop) below it.
     bool working = false;
-    int j = 0, bot = 0, top = 0, leafhi = 0;
-    obot = otop = 0;
+    int j = 0, v = 0, leafhi = 0;
+    unsigned bot = 0, top = 0, obot = 0, otop = 0;
     double2 Pb = make_double2(0.0, 0.0), acc = make_double2(0.0, 0.0);
     unsigned long long npaths = 0, ncm = 0;
     {
@@ -472,22 +503,20 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
         if (lane == 0) {
           __threadfence();
           *reinterpret_cast<volatile unsigned *>(&it->seq) = 0u;  // slot free again
-          for (int jj = 0; jj < j0; ++jj) {  // rebuild the keys of the prefix levels
-            PlanLevel lj = s_lev[jj];
-            int v = lb[lofp_level_off(jj)];
-            for (int q = lj.sbeg; q < lj.send; ++q) kb[s_scat[q]] = (unsigned char)v;
-          }
+          for (int jj = 0; jj < j0; ++jj)  // rebuild the keys of the prefix levels
+            set_level(lb, kb, s_lev[jj], s_scat, jj, lb[lofp_level_off(jj)]);
         }
       }
       if (lane == 0) {
         working = true;
         j = j0;
+        v = vs;
         set_level(lb, kb, s_lev[j0], s_scat, j0, vs);
-        if (j0 == L - 1) {
+        if (j0 == Lm1) {
           leafhi = ve;
         } else if (ve > vs) {
-          stkM[0 * 32 + lane] = (uint32_t)j0 | ((uint32_t)ve << 8);
-          stkP[0 * 32 + lane] = P0;
+          mySM[0] = (uint32_t)j0 | ((uint32_t)ve << 8);
+          mySP[0] = P0;
           top = 1;
         }
         Pb = P0;
@@ -500,32 +529,32 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
       // ---------------- intra-warp hand-over ----------------
       // One per step: the lane holding the shallowest open branch of the warp gives it
       // (all its remaining siblings) to the lowest idle lane.
-      unsigned idle = __ballot_sync(FULL, !working);
+      const unsigned idle = __ballot_sync(FULL, !working);
       if (idle) {
         int myshal = 0x7fffffff;
         if (working) {
-          if (otop > obot)
-            myshal = (int)(ovfM[obot % LOFP_OVF] & 0xff);
-          else if (top > bot)
-            myshal = (int)(stkM[(bot % LOFP_STK) * 32 + lane] & 0xff);
+          if (otop != obot)
+            myshal = (int)(ovfM[obot & (LOFP_OVF - 1)] & 0xff);
+          else if (top != bot)
+            myshal = (int)(mySM[(bot & (LOFP_STK - 1)) * 32] & 0xff);
         }
-        int shal = __reduce_min_sync(FULL, myshal);
+        const int shal = __reduce_min_sync(FULL, myshal);
         if (shal == 0x7fffffff) {
           if (idle == FULL) break;  // item finished
         } else {
-          int donor = __ffs(__ballot_sync(FULL, myshal == shal)) - 1;
-          int recv = __ffs(idle) - 1;
+          const int donor = __ffs(__ballot_sync(FULL, myshal == shal)) - 1;
+          const int recv = __ffs(idle) - 1;
           if (lane == donor) {  // publish the shallowest open branch
             uint32_t m;
             double2 P;
-            if (otop > obot) {
-              m = ovfM[obot % LOFP_OVF];
-              P = ovfP[obot % LOFP_OVF];
+            if (otop != obot) {
+              m = ovfM[obot & (LOFP_OVF - 1)];
+              P = ovfP[obot & (LOFP_OVF - 1)];
               ++obot;
             } else {
-              int e = bot % LOFP_STK;
-              m = stkM[e * 32 + lane];
-              P = stkP[e * 32 + lane];
+              const unsigned e = (bot & (LOFP_STK - 1)) * 32;
+              m = mySM[e];
+              P = mySP[e];
               ++bot;
             }
             mbM[0] = m;
@@ -533,10 +562,10 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
           }
           __syncwarp();
           if (lane == recv) {
-            uint32_t m = mbM[0];
-            double2 P = mbP[0];
-            int jd = m & 0xff, hh = (m >> 8) & 0xff;
-            int nw = ((jd + 1) >> 2) + 1;  // words holding slots [0, jd + 1]
+            const uint32_t m = mbM[0];
+            const double2 P = mbP[0];
+            const int jd = m & 0xff, hh = (m >> 8) & 0xff;
+            const int nw = ((jd + 1) >> 2) + 1;  // words holding slots [0, jd + 1]
             for (int w = 0; w < nw; ++w)
               *reinterpret_cast<uint32_t *>(vcol + w * 128 + 4 * lane) =
                   *reinterpret_cast<const uint32_t *>(vcol + w * 128 + 4 * donor);
@@ -544,86 +573,109 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             for (int f = 0; f < NF; ++f)
               *reinterpret_cast<uint32_t *>(kcol + f * 128 + 4 * lane) =
                   *reinterpret_cast<const uint32_t *>(kcol + f * 128 + 4 * donor);
-            int v = (int)lb[lofp_level_off(jd)] + 1;
-            set_level(lb, kb, s_lev[jd], s_scat, jd, v);
-            bot = top = 0;
+            const int nv = (int)lb[lofp_level_off(jd)] + 1;
+            set_level(lb, kb, s_lev[jd], s_scat, jd, nv);
+            bot = top = obot = otop = 0;
             leafhi = 0;
-            if (jd == L - 1) {
+            if (jd == Lm1) {
               leafhi = hh;
-            } else if (hh > v) {
-              stkM[lane] = (uint32_t)jd | ((uint32_t)hh << 8);
-              stkP[lane] = P;
+            } else if (hh > nv) {
+              mySM[0] = (uint32_t)jd | ((uint32_t)hh << 8);
+              mySP[0] = P;
               top = 1;
             }
             Pb = P;
             j = jd;
+            v = nv;
             working = true;
             ++dons;
-            if (COUNTED) atomicAdd(&a.ctr->don_hist[min(L - 1 - jd, 63)], 1ull);
+            if (COUNTED) atomicAdd(&a.ctr->don_hist[min(Lm1 - jd, 63)], 1ull);
           }
           __syncwarp();
         }
       }
 
-      // ---------------- one DFS node per working lane ----------------
-      // Every working lane does the same work per step: the product of its current
-      // level's factors, then one move (next leaf sibling / descend / pop) and one write
-      // of the new level value into the vals byte and the key bytes.
-      if (working) {
-        const PlanLevel lv = s_lev[j];
-        double2 P = level_product<COUNTED>(Pb, lv, s_fac, kb, s_off, s_ent, ncm);
-        int nj = j, nv = 0;
-        if (j == L - 1) {  // a leaf: one valid path of eq. (1)
+      // ---------------- one DFS node per lane ----------------
+      // Every lane runs the same instruction stream: the product of its current level's
+      // factors (warp-uniform trip count), one move -- next leaf sibling, pop of the
+      // deepest open branch, or descent -- chosen by predicates, and one write of the new
+      // value into the vals byte and the key bytes (warp-uniform trip count; a lane with
+      // nothing to write writes a scratch byte).
+      {
+        const PlanLevel lv = s_lev[working ? j : 0];
+        const int fcnt = working ? (int)lv.fend - (int)lv.fbeg : 0;
+        const int nmax = __reduce_max_sync(FULL, fcnt);
+        const double2 P = level_product<COUNTED>(Pb, lv.fbeg, fcnt, nmax, s_fac, kb, s_off, s_ent, ncm);
+        const bool isleaf = working && j == Lm1;
+        if (isleaf) {
           acc.x += P.x;
           acc.y += P.y;
           if (COUNTED) ++npaths;
-          int v = lb[lofp_level_off(j)];
-          if (v < leafhi) {
-            nv = v + 1;  // next sibling, same product prefix Pb
-          } else if (top > bot) {  // pop the deepest open branch
-            int e = (top - 1) % LOFP_STK;
-            uint32_t m = stkM[e * 32 + lane];
-            nj = m & 0xff;
-            nv = (int)lb[lofp_level_off(nj)] + 1;
-            Pb = stkP[e * 32 + lane];
-            if (nv == (int)((m >> 8) & 0xff)) --top;
-          } else if (otop > obot) {
-            int e = (otop - 1) % LOFP_OVF;
-            uint32_t m = ovfM[e];
-            nj = m & 0xff;
-            nv = (int)lb[lofp_level_off(nj)] + 1;
-            Pb = ovfP[e];
-            if (nv == (int)((m >> 8) & 0xff)) --otop;
-          } else {
-            working = false;
+        }
+        const bool sib = isleaf && v < leafhi;
+        const bool desc = working && !isleaf;
+        const bool popsm = isleaf && !sib && top != bot;
+        const unsigned te = ((top - 1u) & (LOFP_STK - 1)) * 32;
+        uint32_t m = mySM[te];
+        double2 Ps = mySP[te];
+        bool popov = false;
+        if (isleaf && !sib && !popsm && otop != obot) {  // rare: the local overflow
+          popov = true;
+          const unsigned e = (otop - 1u) & (LOFP_OVF - 1);
+          m = ovfM[e];
+          Ps = ovfP[e];
+        }
+        const bool pop = popsm || popov;
+        const bool moves = desc || sib || pop;
+        const int nj = desc ? j + 1 : (sib ? j : (pop ? (int)(m & 0xff) : 0));
+        const PlanLevel nl = s_lev[nj];
+        const uint16_t noff = lofp_level_off(nj);
+        const int dlo = max((int)lb[nl.ol] + nl.cl, (int)nl.lo);
+        const int dhi = min((int)lb[nl.or_] + nl.cr, (int)nl.hi);
+        const int pv = (int)lb[noff] + 1;
+        const int nv = desc ? dlo : (sib ? v + 1 : pv);
+        if (pop) {
+          Pb = Ps;
+          if (pv == (int)((m >> 8) & 0xff)) {
+            if (popsm) --top; else --otop;
           }
-        } else {  // descend: the next level's exact range (never empty, reading R5)
-          nj = j + 1;
-          const PlanLevel nl = s_lev[nj];
-          nv = max((int)lb[nl.ol] + nl.cl, (int)nl.lo);
-          int hi = min((int)lb[nl.or_] + nl.cr, (int)nl.hi);
-          if (nj == L - 1) {
-            leafhi = hi;  // the leaf siblings are walked by the leaf branch above
-          } else if (hi > nv) {
+        }
+        if (desc) {
+          Pb = P;
+          if (nj == Lm1) {
+            leafhi = dhi;  // leaf siblings are walked one per step
+          } else if (dhi > dlo) {
             if (top - bot == LOFP_STK) {  // full: the shallowest entry goes to the overflow
-              int e = bot % LOFP_STK;
-              int o = otop % LOFP_OVF;
-              ovfM[o] = stkM[e * 32 + lane];
-              ovfP[o] = stkP[e * 32 + lane];
+              const unsigned e = (bot & (LOFP_STK - 1)) * 32, o = otop & (LOFP_OVF - 1);
+              ovfM[o] = mySM[e];
+              ovfP[o] = mySP[e];
               ++otop;
               ++bot;
               ++ovfc;
             }
-            int e = top % LOFP_STK;
-            stkM[e * 32 + lane] = (uint32_t)nj | ((uint32_t)hi << 8);
-            stkP[e * 32 + lane] = P;
+            const unsigned e = (top & (LOFP_STK - 1)) * 32;
+            mySM[e] = (uint32_t)nj | ((uint32_t)dhi << 8);
+            mySP[e] = P;
             ++top;
           }
-          Pb = P;
         }
-        if (working) {
+        working = moves;
+        if (moves) {
           j = nj;
-          set_level(lb, kb, s_lev[nj], s_scat, nj, nv);
+          v = nv;
+        }
+        // the new value: vals byte and key bytes
+        lb[moves ? (int)noff : (int)dummy_off] = (unsigned char)nv;
+        const int scnt = moves ? (int)nl.send - (int)nl.sbeg : 0;
+        const int smax = __reduce_max_sync(FULL, scnt);
+        const uint16_t *sp = s_scat + nl.sbeg;  // reads past the list stay in the warp's smem
+#pragma unroll 1
+        for (int i = 0; i < smax; i += 4) {  // four loads in flight, then four stores
+          const uint2 w = make_uint2(sp[i] | ((uint32_t)sp[i + 1] << 16), sp[i + 2] | ((uint32_t)sp[i + 3] << 16));
+          kb[i < scnt ? (int)(w.x & 0xffff) : dummy_rel] = (unsigned char)nv;
+          kb[i + 1 < scnt ? (int)(w.x >> 16) : dummy_rel] = (unsigned char)nv;
+          kb[i + 2 < scnt ? (int)(w.y & 0xffff) : dummy_rel] = (unsigned char)nv;
+          kb[i + 3 < scnt ? (int)(w.y >> 16) : dummy_rel] = (unsigned char)nv;
         }
       }
 
@@ -637,24 +689,24 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
         if (waiting > 0) {
           int myshal = 0x7fffffff;
           if (working) {
-            if (otop > obot)
-              myshal = (int)(ovfM[obot % LOFP_OVF] & 0xff);
-            else if (top > bot)
-              myshal = (int)(stkM[(bot % LOFP_STK) * 32 + lane] & 0xff);
+            if (otop != obot)
+              myshal = (int)(ovfM[obot & (LOFP_OVF - 1)] & 0xff);
+            else if (top != bot)
+              myshal = (int)(mySM[(bot & (LOFP_STK - 1)) * 32] & 0xff);
           }
-          int shal = __reduce_min_sync(FULL, myshal);
-          if (shal != 0x7fffffff && L - 1 - shal >= LOFP_SPILL_MIN_DIST) {
-            int giver = __ffs(__ballot_sync(FULL, myshal == shal)) - 1;
+          const int shal = __reduce_min_sync(FULL, myshal);
+          if (shal != 0x7fffffff && Lm1 - shal >= LOFP_SPILL_MIN_DIST) {
+            const int giver = __ffs(__ballot_sync(FULL, myshal == shal)) - 1;
             if (lane == giver) {
               atomicAdd(&a.ctr->outstanding, 1ull);
-              unsigned long long slot = atomicAdd(&a.ctr->tail, 1ull);
-              if (otop > obot) {
-                int e = obot % LOFP_OVF;
+              const unsigned long long slot = atomicAdd(&a.ctr->tail, 1ull);
+              if (otop != obot) {
+                const unsigned e = obot & (LOFP_OVF - 1);
                 spill(slot, out, ovfM[e], ovfP[e]);
                 ++obot;
               } else {
-                int e = bot % LOFP_STK;
-                spill(slot, out, stkM[e * 32 + lane], stkP[e * 32 + lane]);
+                const unsigned e = (bot & (LOFP_STK - 1)) * 32;
+                spill(slot, out, mySM[e], mySP[e]);
                 ++bot;
               }
               ++spills;
