@@ -126,7 +126,10 @@ typedef struct {
   int64_t donations;      /* subtrees handed between lanes of one warp */
   int64_t overflows;      /* branch-stack entries that went to the local overflow */
   int64_t paths;          /* valid paths summed (lofp_amplitudes_counted only, else 0) */
-  int64_t cmuls;          /* non-vacuum complex multiplications (counted only, else 0) */
+  int64_t cmuls;          /* complex multiplications executed (counted only, else 0): DFS
+                             factors with x1 + x2 > 0, chain pair-table factors, chain products */
+  int64_t chains;         /* chain subtrees enumerated by the lockstep chain engine */
+  int64_t chain_fallbacks;/* chains walked depth-first instead (pair table over capacity) */
   int32_t levels;         /* largest number of free DFS levels of one output */
   int32_t table_entries;  /* Appendix-A elements staged in shared memory */
   int32_t smem_bytes;     /* dynamic shared memory per block of the enumeration kernel */

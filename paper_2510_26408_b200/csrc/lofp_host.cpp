@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -323,8 +324,10 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
     // warp's region, so those reads never leave it)
     a.plan_smem = (int)round16(sizeof(PlanHead) + (size_t)(maxL + maxF) * 16 + 2 * (size_t)maxS);
     a.maxfac = maxF;
+    a.chain_on = hc->nchain > 0 && !std::getenv("LOFP_NO_CHAIN");  // env: debugging knob
     a.warp_bytes = (int)round16((size_t)a.plan_smem + (size_t)a.vals_slots * 32 + (size_t)maxF * 128 +
-                                (size_t)LOFP_STK * 32 * 20 + 32);
+                                (size_t)LOFP_STK * 32 * 20 + 32 +
+                                (a.chain_on ? (size_t)LOFP_W_MAX * 16 + (size_t)LOFP_SUF_MAX * 32 * 16 + 161 * 4 : 0));
     int grid = 0, block = 0;
     size_t smem = 0;
     cudaError_t e = lofp_enum_config(a, counts != nullptr, &grid, &block, &smem);
@@ -507,6 +510,8 @@ lofp_status lofp_stats(lofp_ctx *ctx, lofp_run_stats *out) {
     ctx->stats.overflows = (int64_t)hc->ovf;
     ctx->stats.paths = (int64_t)hc->leaves;
     ctx->stats.cmuls = (int64_t)hc->cmuls;
+    ctx->stats.chains = (int64_t)hc->chains;
+    ctx->stats.chain_fallbacks = (int64_t)hc->chain_fb;
     ctx->stats.bad_rows = (int32_t)hc->bad_rows;
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, ctx->ev_enum0, ctx->ev_enum1) == cudaSuccess) ctx->stats.enum_ms = ms;

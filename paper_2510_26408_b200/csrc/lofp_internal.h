@@ -22,6 +22,9 @@
 #define LOFP_ITEM_BYTES 256   // one global work-queue slot
 #define LOFP_ITEM_PREFIX 224  // prefix bytes an item can carry (>= LOFP_MAX_LEVELS)
 #define LOFP_SPILL_MIN_DIST 6  // global-queue spills only for branches >= this many levels above the leaf level
+#define LOFP_CHAIN_MIN 8       // shortest chain handed to the lockstep chain engine
+#define LOFP_W_MAX 256         // chain pair-table entries per warp (else: plain DFS)
+#define LOFP_SUF_MAX 6         // suffix product slots of the chain odometer
 #define LOFP_ENUM_MAX_THREADS 512  // largest block of the enumeration kernel
 #define LOFP_MAX_CUTS 130     // M + 1 for M <= LOFP_MAX_MODES (128)
 
@@ -59,14 +62,19 @@ struct __align__(16) PlanFactor {
   int16_t dy;
   int8_t dx;
   uint8_t pad0;
-  uint32_t pad1;
+  uint32_t chain;  // factors of chain levels: bits 0-3 key bytes from chain levels,
+                   // bits 4-7 of those from its own level, bits 8-11 from the previous one
 };
 
+// The chain of an output (R17): the suffix of levels [jb, L) (the last
+// free layer) whose ranges depend only on levels < jb and whose factors depend, among
+// chain levels, only on their own level and the previous one.  Given levels < jb its
+// subtree is a Cartesian product of fixed ranges, enumerated by a whole warp in lockstep.
 struct PlanHead {
   double root[2];   // product of the elements with constant inputs
   uint16_t L, nfac; // levels and attached factors of this output
   uint16_t nscat;   // scatter entries (u16 key-byte offsets, after the factors)
-  uint16_t pad0;
+  uint16_t jb;      // first chain level (L = no chain)
   uint64_t pad1;
 };
 static_assert(sizeof(PlanLevel) == 16 && sizeof(PlanFactor) == 16 && sizeof(PlanHead) == 32, "plan layout");
@@ -91,13 +99,15 @@ struct Counters {
   unsigned long long leaves;       // valid paths summed (counted mode)
   unsigned long long ovf;          // pushes that went to the local overflow stack
   unsigned long long donations;    // intra-warp hand-overs (stats)
+  unsigned long long chains;       // chain subtrees enumerated by the chain engine
+  unsigned long long chain_fb;     // chains handed back to the plain walk (pair table too big)
   unsigned long long don_hist[64]; // counted mode: hand-overs by (leaf level - level)
   unsigned long long spill_hist[64];  // counted mode: queue spills by (leaf level - level)
   int32_t tmax[128];               // per-mode maximum of T over the batch
   int32_t maxL;                    // largest per-output level count
   int32_t maxF;                    // largest per-output attached-factor count
   int32_t maxS;                    // largest per-output scatter-list length
-  int32_t pad;
+  int32_t nchain;                  // outputs whose plan has a chain
 };
 
 // A queued subtree: output `out`, levels [0, j0) fixed to prefix[], level j0 ranging
@@ -124,6 +134,7 @@ struct CallArgs {
   int plan_smem;                      // bytes reserved per warp for a staged plan
   int maxfac;                         // attached factors per output (max; key words per lane)
   int warp_bytes;                     // per-warp shared memory (plan + vals + stack)
+  int chain_on;                       // some output has a chain: engine scratch present
   int table_bytes;                    // shared memory of the staged tables (16-aligned)
   const int32_t *T;                   // [B][M] device
   double *amps;                       // [B][2] device

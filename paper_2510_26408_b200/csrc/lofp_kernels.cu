@@ -165,6 +165,8 @@ __global__ void lofp_plan_kernel(CallArgs a) {
 
   Ref cur[LOFP_MAX_CUTS];
   for (int k = 0; k <= M; ++k) cur[k] = Ref{-1, (int)a.cumS[k]};
+  uint8_t lev_layer[LOFP_MAX_LEVELS];
+  int8_t lev_rl[LOFP_MAX_LEVELS], lev_rr[LOFP_MAX_LEVELS];
   int L = 0, nf = 0;
   double2 root = make_double2(1.0, 0.0);
   for (int b = 0; b < a.nbs; ++b) {
@@ -189,6 +191,9 @@ __global__ void lofp_plan_kernel(CallArgs a) {
       pl.fbeg = pl.fend = 0;
       pl.sbeg = pl.send = 0;
       lev[L] = pl;
+      lev_layer[L] = (uint8_t)l;
+      lev_rl[L] = (int8_t)A.slot;
+      lev_rr[L] = (int8_t)C.slot;
       ++L;
     }
     cur[k] = Y;
@@ -227,10 +232,36 @@ __global__ void lofp_plan_kernel(CallArgs a) {
     lev[j].fbeg = cnt[j];
     lev[j].fend = cnt[j + 1];
   }
+  // the chain: the last free layer's levels, if their ranges and factors qualify (R17)
+  int jb = L;
+  if (L >= LOFP_CHAIN_MIN) {
+    int cand = L - 1;
+    while (cand > 0 && lev_layer[cand - 1] == lev_layer[L - 1]) --cand;
+    if (cand < L - 32) cand = L - 32;  // one lane per chain level in the engine
+    bool ok = true;
+    for (int m = cand; m < L; ++m)
+      if (lev_rl[m] >= cand || lev_rr[m] >= cand) ok = false;
+    for (int f = 0; f < nf && ok; ++f) {
+      const int at = tmp[f].at;
+      if (at < cand) continue;
+      for (int p = 0; p < 4; ++p) {
+        const int sl = tmp[f].s[p];
+        if (sl >= cand && sl != at && sl != at - 1) ok = false;
+      }
+    }
+    if (ok && L - cand >= LOFP_CHAIN_MIN) jb = cand;
+  }
   int ns = 0;
   for (int f = 0; f < nf; ++f) {
     const FacTmp ft = tmp[f];
     int w = cnt[ft.at]++;
+    uint32_t chain = 0;
+    if (ft.at >= jb)
+      for (int p = 0; p < 4; ++p) {
+        if (ft.s[p] >= jb) chain |= 1u << p;
+        if (ft.s[p] >= jb && ft.s[p] == ft.at) chain |= 16u << p;
+        if (ft.s[p] >= jb && ft.s[p] == ft.at - 1) chain |= 256u << p;
+      }
     PlanFactor pf;
     pf.crow = (int32_t)(((uint32_t)(uint8_t)(int8_t)(-ft.stride)) | ((uint32_t)(uint8_t)(int8_t)(ft.stride - 1) << 8) |
                         (1u << 16));
@@ -238,7 +269,7 @@ __global__ void lofp_plan_kernel(CallArgs a) {
     pf.dy = ft.dy;
     pf.dx = (int8_t)ft.dx;
     pf.pad0 = 0;
-    pf.pad1 = 0;
+    pf.chain = chain;
     fac[w] = pf;
     for (int p = 0; p < 4; ++p)
       if (ft.s[p] >= 0) stmp[ns++] = ((uint32_t)ft.s[p] << 16) | (uint32_t)(w * 128 + p);
@@ -258,7 +289,7 @@ __global__ void lofp_plan_kernel(CallArgs a) {
   h.L = (uint16_t)L;
   h.nfac = (uint16_t)nf;
   h.nscat = (uint16_t)ns;
-  h.pad0 = 0;
+  h.jb = (uint16_t)jb;
   h.pad1 = 0;
   *head = h;
   if (L == 0) {  // a single valid path (eq. (10))
@@ -270,6 +301,7 @@ __global__ void lofp_plan_kernel(CallArgs a) {
   atomicMax(&a.ctr->maxL, L);
   atomicMax(&a.ctr->maxF, nf);
   atomicMax(&a.ctr->maxS, ns);
+  if (jb < L) atomicAdd(&a.ctr->nchain, 1);
   unsigned long long idx = atomicAdd(&a.ctr->nfeas, 1ull);
   a.feas[idx] = (uint32_t)q;
   atomicAdd(&a.ctr->outstanding, 1ull);
@@ -321,20 +353,22 @@ __device__ __forceinline__ void set_level(unsigned char *lb, unsigned char *kb, 
 template <bool COUNTED>
 __device__ __forceinline__ int factor_entry(const PlanFactor *fp, const unsigned char *kp, int i, int fcnt,
                                             const int32_t *s_off, unsigned long long &ncm) {
-  const int2 fd = *reinterpret_cast<const int2 *>(fp + i);  // crow, base
-  const int key = *reinterpret_cast<const int *>(kp + i * 128);
-  const int row = __dp4a(key, fd.x, fd.y);
-  const int o = s_off[row] + __dp4a(key, 0x010000ff, (int)fp[i].dy);  // + y - a
+  // past the lane's own count: re-read its last factor (always a valid descriptor, key
+  // and table row) and use entry 0 (= 1)
   const bool on = i < fcnt;
-  if (COUNTED) ncm += (on && __dp4a(key, 0x000100ff, (int)fp[i].dx) > 0);  // x1 + x2 = c - a
+  const int fi = on ? i : max(fcnt - 1, 0);
+  const int2 fd = *reinterpret_cast<const int2 *>(fp + fi);  // crow, base
+  const int key = *reinterpret_cast<const int *>(kp + fi * 128);
+  const int row = __dp4a(key, fd.x, fd.y);
+  const int o = s_off[on ? row : 0] + __dp4a(key, 0x010000ff, (int)fp[fi].dy);  // + y - a
+  if (COUNTED) ncm += (on && __dp4a(key, 0x000100ff, (int)fp[fi].dx) > 0);  // x1 + x2 = c - a
   return on ? o : 0;
 }
 
 // Product of the factors attached to a level, times P.  The trip count is the warp's
 // largest factor count (nmax, warp-uniform) so that every lane runs the same instruction
-// stream; a lane past its own count reads the following descriptors/keys (inside the
-// warp's shared memory) and multiplies by table entry 0, which is exactly 1 (the vacuum
-// element of BS 0, R16).  Factors are taken in pairs: e_i e_{i+1} does not depend on P,
+// stream; a lane past its own count multiplies by table entry 0, which is exactly 1 (the
+// vacuum element of BS 0, R16).  Factors are taken in pairs: e_i e_{i+1} does not depend on P,
 // so the dependent fp64 chain is one complex multiplication per pair.
 template <bool COUNTED>
 __device__ __forceinline__ double2 level_product(double2 P, int fbeg, int fcnt, int nmax, const PlanFactor *fac,
@@ -373,6 +407,14 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
   uint32_t *stkM = reinterpret_cast<uint32_t *>(stkP + LOFP_STK * 32);         // [LOFP_STK][32]
   double2 *mbP = reinterpret_cast<double2 *>(stkM + LOFP_STK * 32);             // hand-over mailbox
   uint32_t *mbM = reinterpret_cast<uint32_t *>(mbP + 1);
+  // chain engine scratch: pair table W, per-lane suffix products, per-digit arrays
+  double2 *cW = mbP + 2;                                     // [LOFP_W_MAX]
+  double2 *cPs = cW + LOFP_W_MAX;                            // [LOFP_SUF_MAX][32]
+  int *c_lo = reinterpret_cast<int *>(cPs + LOFP_SUF_MAX * 32);  // [32]
+  int *c_r = c_lo + 32;                                      // [32]
+  int *c_wb = c_r + 32;                                      // [33]
+  int *c_pv = c_wb + 33;                                     // [32] prefix place values
+  int *c_u = c_pv + 32;                                      // [32] suffix digits (uniform)
   unsigned char *lb = vcol + 4 * lane;  // this lane's vals byte base
   unsigned char *kb = kcol + 4 * lane;  // this lane's key byte base
   lb[LOFP_ZERO_OFF] = 0;
@@ -388,7 +430,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
   const PlanFactor *s_fac = nullptr;
   const uint16_t *s_scat = nullptr;
   int L = 0, NF = 0;
-  unsigned long long spills = 0, ovfc = 0, dons = 0, items = 0;
+  unsigned long long spills = 0, ovfc = 0, dons = 0, items = 0, nchains = 0, nchainfb = 0;
   uint32_t *const mySM = stkM + lane;    // this lane's stack metas, entry e at [e * 32]
   double2 *const mySP = stkP + lane;     // this lane's stack products
   const int dummy_rel = (int)dummy_off - a.vals_slots * 32;  // kb + dummy_rel = scratch byte
@@ -435,7 +477,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
           }
           if (vload(&a.ctr->outstanding) == 0ull) break;
           __nanosleep(ns);
-          if (ns < 1024) ns <<= 1;
+          if (ns < 8192) ns <<= 1;
         }
       }
     }
@@ -467,6 +509,8 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
     }
     const PlanHead *sh = reinterpret_cast<const PlanHead *>(s_plan);
     const int Lm1 = L - 1;
+    const int jbq = a.chain_on ? (int)sh->jb : L;  // first chain level (== L: no chain)
+    bool chain_pending = false;
 
     // ---------------- lane 0 begins the item ----------------
     // Lane state: j = current level, v = its value, Pb = product before level j's
@@ -507,7 +551,11 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             set_level(lb, kb, s_lev[jj], s_scat, jj, lb[lofp_level_off(jj)]);
         }
       }
-      if (lane == 0) {
+      if (lane == 0 && kind == 1 && jbq == 0) {  // the whole tree is one chain
+        working = true;
+        chain_pending = true;
+        Pb = P0;
+      } else if (lane == 0) {
         working = true;
         j = j0;
         v = vs;
@@ -602,18 +650,19 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
       // value into the vals byte and the key bytes (warp-uniform trip count; a lane with
       // nothing to write writes a scratch byte).
       {
-        const PlanLevel lv = s_lev[working ? j : 0];
-        const int fcnt = working ? (int)lv.fend - (int)lv.fbeg : 0;
+        const bool stepping = working && !chain_pending;  // a pending lane waits for the engine
+        const PlanLevel lv = s_lev[stepping ? j : 0];
+        const int fcnt = stepping ? (int)lv.fend - (int)lv.fbeg : 0;
         const int nmax = __reduce_max_sync(FULL, fcnt);
         const double2 P = level_product<COUNTED>(Pb, lv.fbeg, fcnt, nmax, s_fac, kb, s_off, s_ent, ncm);
-        const bool isleaf = working && j == Lm1;
+        const bool isleaf = stepping && j == Lm1;
         if (isleaf) {
           acc.x += P.x;
           acc.y += P.y;
           if (COUNTED) ++npaths;
         }
         const bool sib = isleaf && v < leafhi;
-        const bool desc = working && !isleaf;
+        const bool desc = stepping && !isleaf;
         const bool popsm = isleaf && !sib && top != bot;
         const unsigned te = ((top - 1u) & (LOFP_STK - 1)) * 32;
         uint32_t m = mySM[te];
@@ -640,7 +689,11 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             if (popsm) --top; else --otop;
           }
         }
-        if (desc) {
+        const bool tochain = desc && nj == jbq;
+        if (tochain) {
+          Pb = P;  // product through level jb - 1: the chain's root product
+          chain_pending = true;
+        } else if (desc) {
           Pb = P;
           if (nj == Lm1) {
             leafhi = dhi;  // leaf siblings are walked one per step
@@ -659,14 +712,15 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             ++top;
           }
         }
-        working = moves;
-        if (moves) {
+        const bool wr = moves && !tochain;
+        if (stepping) working = moves;
+        if (wr) {
           j = nj;
           v = nv;
         }
         // the new value: vals byte and key bytes
-        lb[moves ? (int)noff : (int)dummy_off] = (unsigned char)nv;
-        const int scnt = moves ? (int)nl.send - (int)nl.sbeg : 0;
+        lb[wr ? (int)noff : (int)dummy_off] = (unsigned char)nv;
+        const int scnt = wr ? (int)nl.send - (int)nl.sbeg : 0;
         const int smax = __reduce_max_sync(FULL, scnt);
         const uint16_t *sp = s_scat + nl.sbeg;  // reads past the list stay in the warp's smem
 #pragma unroll 1
@@ -676,6 +730,239 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
           kb[i + 1 < scnt ? (int)(w.x >> 16) : dummy_rel] = (unsigned char)nv;
           kb[i + 2 < scnt ? (int)(w.y & 0xffff) : dummy_rel] = (unsigned char)nv;
           kb[i + 3 < scnt ? (int)(w.y >> 16) : dummy_rel] = (unsigned char)nv;
+        }
+      }
+
+      // ---------------- chain engine (lockstep, whole warp) ----------------
+      // Each lane that reached the first chain level hands its chain -- the Cartesian
+      // product of the chain levels' ranges, fixed by its levels < jb -- to the whole warp:
+      // (1) lane m computes chain level m's range; (2) the pair table
+      // W_m(v_{m-1}, v_m) = product of level m's factors is built (one entry per lane per
+      // round); (3) every path of the chain is enumerated: the leading digits are split
+      // over the lanes, the remaining digits run one odometer shared by all lanes (warp-
+      // uniform control), each path's product = root * prod_m W_m formed with prefix
+      // sharing and added to the lane's accumulator.  Then the emitting lane pops its
+      // stack as after a finished subtree.
+      {
+        unsigned pend = __ballot_sync(FULL, chain_pending);
+        while (pend) {
+          const int em = __ffs(pend) - 1;
+          pend &= pend - 1;
+          const unsigned char *lbe = vcol + 4 * em, *kbe = kcol + 4 * em;
+          const double2 Proot = make_double2(__shfl_sync(FULL, Pb.x, em), __shfl_sync(FULL, Pb.y, em));
+          const int Mb = L - jbq;
+          int clo = 0, crr = 1;
+          if (lane < Mb) {
+            const PlanLevel cl = s_lev[jbq + lane];
+            clo = max((int)lbe[cl.ol] + cl.cl, (int)cl.lo);
+            crr = min((int)lbe[cl.or_] + cl.cr, (int)cl.hi) - clo + 1;
+          }
+          int rprev = __shfl_up_sync(FULL, crr, 1);
+          if (lane == 0) rprev = 1;
+          const int sz = lane < Mb ? rprev * crr : 0;
+          int inc = sz;
+          for (int o = 1; o < 32; o <<= 1) {
+            const int tv = __shfl_up_sync(FULL, inc, o);
+            if (lane >= o) inc += tv;
+          }
+          const int E = __shfl_sync(FULL, inc, 31);
+          double Rd = (double)crr;  // leaves of the chain (product of the ranges)
+          for (int o = 1; o < 32; o <<= 1) Rd *= __shfl_xor_sync(FULL, Rd, o);
+          const bool fb = E > LOFP_W_MAX || Rd > 2.0e9;
+          if (lane == 0) {
+            if (fb) ++nchainfb; else ++nchains;
+          }
+          if (fb) {  // too many pairs or paths: the emitting lane walks the chain itself
+            if (lane == em) {
+              chain_pending = false;
+              j = jbq;
+              v = clo;  // lane em's own range of level jb (it is lane 0's value: broadcast)
+            }
+            const int lo0 = __shfl_sync(FULL, clo, 0), r0 = __shfl_sync(FULL, crr, 0);
+            if (lane == em) {
+              v = lo0;
+              set_level(lb, kb, s_lev[jbq], s_scat, jbq, lo0);
+              if (jbq == Lm1) {
+                leafhi = lo0 + r0 - 1;
+              } else if (r0 > 1) {
+                if (top - bot == LOFP_STK) {
+                  const unsigned e2 = (bot & (LOFP_STK - 1)) * 32, o2 = otop & (LOFP_OVF - 1);
+                  ovfM[o2] = mySM[e2];
+                  ovfP[o2] = mySP[e2];
+                  ++otop;
+                  ++bot;
+                  ++ovfc;
+                }
+                const unsigned e2 = (top & (LOFP_STK - 1)) * 32;
+                mySM[e2] = (uint32_t)jbq | ((uint32_t)(lo0 + r0 - 1) << 8);
+                mySP[e2] = Pb;
+                ++top;
+              }
+            }
+            continue;
+          }
+          c_lo[lane] = clo;
+          c_r[lane] = crr;
+          c_wb[lane] = inc - sz;
+          if (lane == 0) c_wb[32] = E;
+          __syncwarp();
+          // (2) pair table
+          for (int w = lane; w < E; w += 32) {
+            int m = 0;
+            for (int st = 16; st > 0; st >>= 1)
+              if (m + st < Mb && c_wb[m + st] <= w) m += st;
+            const int rm = c_r[m], rel = w - c_wb[m];
+            const int ii = rel / rm, kk = rel - ii * rm;
+            const int vm = c_lo[m] + kk, vp = m > 0 ? c_lo[m - 1] + ii : 0;
+            const PlanLevel lv = s_lev[jbq + m];
+            double2 Q = make_double2(1.0, 0.0);
+            for (int f = lv.fbeg; f < lv.fend; ++f) {
+              const PlanFactor fd = s_fac[f];
+              int key = *reinterpret_cast<const int *>(kbe + f * 128);
+              const uint32_t cm = fd.chain & 15u, sm = (fd.chain >> 4) & 15u, pm = (fd.chain >> 8) & 15u;
+              const uint32_t cmask = (cm & 1u ? 0xffu : 0u) | (cm & 2u ? 0xff00u : 0u) | (cm & 4u ? 0xff0000u : 0u) |
+                                     (cm & 8u ? 0xff000000u : 0u);
+              const uint32_t s01 = (sm & 1u) | ((sm & 2u) << 7) | ((sm & 4u) << 14) | ((sm & 8u) << 21);
+              const uint32_t p01 = (pm & 1u) | ((pm & 2u) << 7) | ((pm & 4u) << 14) | ((pm & 8u) << 21);
+              key = (int)(((uint32_t)key & ~cmask) + (uint32_t)vm * s01 + (uint32_t)vp * p01);
+              const int row = __dp4a(key, fd.crow, fd.base);
+              const int o = s_off[row] + __dp4a(key, 0x010000ff, (int)fd.dy);
+              Q = cmul(Q, s_ent[o]);
+              if (COUNTED) ncm += __dp4a(key, 0x000100ff, (int)fd.dx) > 0;
+            }
+            cW[w] = Q;
+          }
+          // (3) enumeration.  Digits [0, t) (prefix) are split over the lanes, digits
+          // [t, Mb) (suffix) form a table Suf[s] = prod_{m > t} W_m shared by all lanes
+          // (one lane per entry).  Every path of the chain is then formed as
+          //   (root * prod_{m < t} W_m * W_t) * Suf[s]
+          // -- one complex multiplication per path in a warp-uniform inner loop -- and
+          // added to the lane's accumulator.  t maximises lane use with |Suf| <= 64.
+          __syncwarp();
+          int t = Mb, best_t = Mb;
+          long long Rs = 1, best_rs = 1;
+          long long R = 1;
+          for (int m = 0; m < Mb; ++m) R *= c_r[m];
+          float best_u = -1.f;
+          while (true) {
+            const long long Ct = R / Rs;
+            const long long rounds = (Ct + 31) / 32;
+            const float u = (float)Ct / (float)(32 * rounds);
+            if (u > best_u + 1e-6f) {
+              best_u = u;
+              best_t = t;
+              best_rs = Rs;
+            }
+            if (t == 0 || Rs * c_r[t - 1] > 64) break;
+            --t;
+            Rs *= c_r[t];
+          }
+          t = best_t;
+          const int Rsi = (int)best_rs;
+          const long long Ct = R / best_rs;
+          {  // place values of the prefix digits (digit t-1 least significant)
+            long long pv = 1;
+            for (int m = t - 1; m >= 0; --m) {
+              if (lane == 0) c_pv[m] = (int)pv;
+              pv *= c_r[m];
+            }
+          }
+          // suffix table: entry s (digit t most significant) = prod_{m = t+1}^{Mb-1} W_m
+          for (int sidx = lane; sidx < Rsi; sidx += 32) {
+            int rem = sidx, cur = 0, nxt = 0;
+            double2 Q = make_double2(1.0, 0.0);
+            // decode from the last digit; walk W_m for m = Mb-1 down to t+1
+            for (int m = Mb - 1; m > t; --m) {
+              const int rm = c_r[m];
+              cur = rem % rm;
+              rem /= rm;
+              nxt = rem % c_r[m - 1];  // digit m-1
+              const int idx = c_wb[m] + nxt * rm + cur;
+              Q = cmul(Q, cW[idx]);
+              if (COUNTED) ++ncm;
+            }
+            cPs[sidx] = Q;
+          }
+          __syncwarp();
+          const int rt = t < Mb ? c_r[t] : 1;
+          const int blk = Rsi / rt;  // suffix entries per value of digit t
+          for (long long c0 = 0; c0 < Ct; c0 += 32) {
+            const long long cc = c0 + lane;
+            const bool act = cc < Ct;
+            const int ci = act ? (int)cc : 0;
+            double2 P = Proot;
+            int vprev = 0;
+            for (int m = 0; m < t; ++m) {
+              const int d = (int)(((unsigned)ci / (unsigned)c_pv[m]) % (unsigned)c_r[m]);
+              const int idx = c_wb[m] + (m > 0 ? vprev * c_r[m] : 0) + d;
+              P = cmul(P, cW[idx]);
+              if (COUNTED) ncm += act;
+              vprev = d;  // digit (offset from the level's low end)
+            }
+            if (t == Mb) {  // no suffix: the prefix is the whole path
+              if (act) {
+                acc.x += P.x;
+                acc.y += P.y;
+                if (COUNTED) ++npaths;
+              }
+              continue;
+            }
+            for (int dt = 0; dt < rt; ++dt) {
+              const double2 Q = cmul(P, cW[c_wb[t] + (t > 0 ? vprev * rt : 0) + dt]);
+              if (COUNTED) ncm += act;
+              const double2 *sf = cPs + dt * blk;
+              double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+              int k = 0;
+              for (; k + 1 < blk; k += 2) {
+                const double2 l0 = cmul(Q, sf[k]), l1 = cmul(Q, sf[k + 1]);
+                a0.x += l0.x;
+                a0.y += l0.y;
+                a1.x += l1.x;
+                a1.y += l1.y;
+              }
+              if (k < blk) {
+                const double2 l0 = cmul(Q, sf[k]);
+                a0.x += l0.x;
+                a0.y += l0.y;
+              }
+              if (act) {
+                acc.x += a0.x + a1.x;
+                acc.y += a0.y + a1.y;
+                if (COUNTED) {
+                  npaths += blk;
+                  ncm += blk;
+                }
+              }
+            }
+          }
+          __syncwarp();
+          // the emitting lane continues its depth-first walk after the chain's subtree
+          if (lane == em) {
+            chain_pending = false;
+            if (top != bot) {
+              const unsigned e2 = ((top - 1u) & (LOFP_STK - 1)) * 32;
+              const uint32_t m2 = mySM[e2];
+              const int jj = m2 & 0xff;
+              const int nv2 = (int)lb[lofp_level_off(jj)] + 1;
+              Pb = mySP[e2];
+              if (nv2 == (int)((m2 >> 8) & 0xff)) --top;
+              j = jj;
+              v = nv2;
+              set_level(lb, kb, s_lev[jj], s_scat, jj, nv2);
+            } else if (otop != obot) {
+              const unsigned e2 = (otop - 1u) & (LOFP_OVF - 1);
+              const uint32_t m2 = ovfM[e2];
+              const int jj = m2 & 0xff;
+              const int nv2 = (int)lb[lofp_level_off(jj)] + 1;
+              Pb = ovfP[e2];
+              if (nv2 == (int)((m2 >> 8) & 0xff)) --otop;
+              j = jj;
+              v = nv2;
+              set_level(lb, kb, s_lev[jj], s_scat, jj, nv2);
+            } else {
+              working = false;
+            }
+          }
         }
       }
 
@@ -745,6 +1032,8 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
     dons += __shfl_xor_sync(FULL, dons, s);
   }
   if (lane == 0) {
+    atomicAdd(&a.ctr->chains, nchains);
+    atomicAdd(&a.ctr->chain_fb, nchainfb);
     atomicAdd(&a.ctr->items, items);
     atomicAdd(&a.ctr->spills, spills);
     atomicAdd(&a.ctr->ovf, ovfc);

@@ -26,6 +26,7 @@ class lofp_run_stats(ctypes.Structure):
     _fields_ = [("batch", ctypes.c_int64), ("feasible", ctypes.c_int64), ("items", ctypes.c_int64),
                 ("spills", ctypes.c_int64), ("donations", ctypes.c_int64), ("overflows", ctypes.c_int64),
                 ("paths", ctypes.c_int64), ("cmuls", ctypes.c_int64),
+                ("chains", ctypes.c_int64), ("chain_fallbacks", ctypes.c_int64),
                 ("levels", ctypes.c_int32), ("table_entries", ctypes.c_int32),
                 ("smem_bytes", ctypes.c_int32), ("grid_blocks", ctypes.c_int32),
                 ("block_threads", ctypes.c_int32), ("bad_rows", ctypes.c_int32),

@@ -37,5 +37,5 @@ for idx in cfgs:
         print("handover by leaf-distance:", h[:40].tolist())
         print("spill by leaf-distance:", sp[:40].tolist())
     print(json.dumps(dict(cfg=idx, outputs=n, paths=P.sum(), ms=min(res), paths_per_s=P.sum() / (min(res) * 1e-3),
-                          enum_ms=st["enum_ms"], total_ms=st["total_ms"], items=st["items"], spills=st["spills"], donations=st["donations"], ovf=st["overflows"], block=st["block_threads"], maxF=st["max_factors"], maxS=st["max_scatter"],
+                          enum_ms=st["enum_ms"], total_ms=st["total_ms"], items=st["items"], spills=st["spills"], donations=st["donations"], ovf=st["overflows"], block=st["block_threads"], maxF=st["max_factors"], maxS=st["max_scatter"], chains=st["chains"], chain_fb=st["chain_fallbacks"],
                           levels=st["levels"], entries=st["table_entries"], smem=st["smem_bytes"], grid=st["grid_blocks"])), flush=True)

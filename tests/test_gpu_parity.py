@@ -234,3 +234,48 @@ def test_reversed_pairs_equal_swapped_phase(lofp):
     g1, _, _, _ = run(lofp, M, rev, S, T, counted=False)
     ref = oracle.path_sum(M, rev, S, T)
     assert tol_ok(g1, ref)[0]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_wide_circuits_chain_engine(lofp, seed):
+    """Wide meshes (M = 18..24, D = 3..5): the last free layer has >= 8 levels for many
+    outputs, so their subtrees go through the lockstep chain engine (R17).
+    Values and exact path counts against the oracle."""
+    rng = np.random.default_rng(4200 + seed)
+    M = int(rng.integers(18, 23))
+    D = int(rng.integers(3, 5))
+    layers = li.clements_mesh(M, D, seed=100 + seed)
+    N = int(rng.integers(M // 2 + 2, M - 3))
+    S = np.zeros(M, dtype=np.int32)
+    S[np.sort(rng.choice(M, N, replace=False))] = 1
+    T = li.uniform_subsets(M, N, 4000, rng)
+    reach = oracle.reachable(M, layers, S, T)
+    T = T[reach]
+    P = np.array(oracle.count_paths(M, layers, S, T), dtype=object)
+    T = T[(P > 0) & (P <= 3 * 10 ** 5)][:150]
+    assert len(T) > 20
+    got, cnt, st, _ = run(lofp, M, layers, S, T)
+    assert st["chains"] > 0  # the lockstep chain engine ran
+    ref, leaves = oracle.path_sum(M, layers, S, T, return_leaves=True)
+    ok, err = tol_ok(got, ref)
+    assert ok, err
+    assert np.array_equal(cnt, leaves)
+
+
+def test_bunched_wide_chain_fallback(lofp):
+    """Dense bunched input on a wide mesh: chain pair tables can exceed the per-warp
+    capacity, exercising the fallback to the plain depth-first walk."""
+    M, D = 20, 3
+    layers = li.clements_mesh(M, D, seed=77)
+    S = np.zeros(M, dtype=np.int32)
+    S[[1, 4, 7, 10, 13, 16]] = 3
+    rng = np.random.default_rng(3)
+    T = li.bounded_patterns(M, int(S.sum()), 4, 3000, rng)[0]
+    T = T[oracle.reachable(M, layers, S, T)]
+    P = np.array(oracle.count_paths(M, layers, S, T), dtype=object)
+    T = T[(P > 0) & (P <= 3 * 10 ** 6)][:60]
+    assert len(T) > 5
+    got, cnt, _, _ = run(lofp, M, layers, S, T)
+    ref, leaves = oracle.path_sum(M, layers, S, T, return_leaves=True)
+    assert tol_ok(got, ref)[0]
+    assert np.array_equal(cnt, leaves)
