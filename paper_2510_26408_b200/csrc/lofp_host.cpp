@@ -324,10 +324,14 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
     // warp's region, so those reads never leave it)
     a.plan_smem = (int)round16(sizeof(PlanHead) + (size_t)(maxL + maxF) * 16 + 2 * (size_t)maxS);
     a.maxfac = maxF;
-    a.chain_on = hc->nchain > 0 && !std::getenv("LOFP_NO_CHAIN");  // env: debugging knob
+    // The chain engine costs every warp its scratch (fewer resident warps): use it when
+    // most outputs of the batch have a chain worth a warp (env LOFP_NO_CHAIN: off, for
+    // debugging; LOFP_FORCE_CHAIN: on whenever any output has one, for testing).
+    a.chain_on = hc->nchain > 0 && !std::getenv("LOFP_NO_CHAIN") &&
+                 (2ull * (unsigned long long)hc->nchain >= hc->nfeas || std::getenv("LOFP_FORCE_CHAIN"));
     a.warp_bytes = (int)round16((size_t)a.plan_smem + (size_t)a.vals_slots * 32 + (size_t)maxF * 128 +
                                 (size_t)LOFP_STK * 32 * 20 + 32 +
-                                (a.chain_on ? (size_t)LOFP_W_MAX * 16 + (size_t)LOFP_SUF_MAX * 32 * 16 + 161 * 4 : 0));
+                                (a.chain_on ? (size_t)LOFP_W_MAX * 16 + (size_t)LOFP_SUF_MAX * 32 * 16 + 161 * 4 + 1024 : 0));
     int grid = 0, block = 0;
     size_t smem = 0;
     cudaError_t e = lofp_enum_config(a, counts != nullptr, &grid, &block, &smem);

@@ -22,8 +22,12 @@
 #define LOFP_ITEM_BYTES 256   // one global work-queue slot
 #define LOFP_ITEM_PREFIX 224  // prefix bytes an item can carry (>= LOFP_MAX_LEVELS)
 #define LOFP_SPILL_MIN_DIST 6  // global-queue spills only for branches >= this many levels above the leaf level
-#define LOFP_CHAIN_MIN 8       // shortest chain handed to the lockstep chain engine
+#define LOFP_CHAIN_MIN 4       // shortest chain handed to the lockstep chain engine
+#define LOFP_CHAIN_RBOX 1024   // smallest box product (paths bound) of an output's chain
 #define LOFP_W_MAX 256         // chain pair-table entries per warp (else: plain DFS)
+#ifndef LOFP_CHAIN_RMIN
+#define LOFP_CHAIN_RMIN 32     // fewest paths of a chain enumerated by the engine (else: plain DFS)
+#endif
 #define LOFP_SUF_MAX 6         // suffix product slots of the chain odometer
 #define LOFP_ENUM_MAX_THREADS 512  // largest block of the enumeration kernel
 #define LOFP_MAX_CUTS 130     // M + 1 for M <= LOFP_MAX_MODES (128)

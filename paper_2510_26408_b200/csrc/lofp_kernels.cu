@@ -249,7 +249,11 @@ __global__ void lofp_plan_kernel(CallArgs a) {
         if (sl >= cand && sl != at && sl != at - 1) ok = false;
       }
     }
-    if (ok && L - cand >= LOFP_CHAIN_MIN) jb = cand;
+    // worth a warp only when the chain's box admits many paths (the box product bounds
+    // the paths of every chain subtree of this output)
+    double rbox = 1.0;
+    for (int m = cand; m < L; ++m) rbox *= (double)((int)lev[m].hi - (int)lev[m].lo + 1);
+    if (ok && L - cand >= LOFP_CHAIN_MIN && rbox >= (double)LOFP_CHAIN_RBOX) jb = cand;
   }
   int ns = 0;
   for (int f = 0; f < nf; ++f) {
@@ -414,7 +418,8 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
   int *c_r = c_lo + 32;                                      // [32]
   int *c_wb = c_r + 32;                                      // [33]
   int *c_pv = c_wb + 33;                                     // [32] prefix place values
-  int *c_u = c_pv + 32;                                      // [32] suffix digits (uniform)
+  int *c_u = c_pv + 32;                                      // [32] (spare)
+  unsigned char *c_dig = reinterpret_cast<unsigned char *>(c_u + 32);  // [32 digits][32 lanes]
   unsigned char *lb = vcol + 4 * lane;  // this lane's vals byte base
   unsigned char *kb = kcol + 4 * lane;  // this lane's key byte base
   lb[LOFP_ZERO_OFF] = 0;
@@ -768,11 +773,11 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
           const int E = __shfl_sync(FULL, inc, 31);
           double Rd = (double)crr;  // leaves of the chain (product of the ranges)
           for (int o = 1; o < 32; o <<= 1) Rd *= __shfl_xor_sync(FULL, Rd, o);
-          const bool fb = E > LOFP_W_MAX || Rd > 2.0e9;
+          const bool fb = E > LOFP_W_MAX || Rd > 2.0e9 || Rd < (double)LOFP_CHAIN_RMIN;
           if (lane == 0) {
             if (fb) ++nchainfb; else ++nchains;
           }
-          if (fb) {  // too many pairs or paths: the emitting lane walks the chain itself
+          if (fb) {  // too few paths (or too many pairs/paths): the emitting lane walks the chain itself
             if (lane == em) {
               chain_pending = false;
               j = jbq;
@@ -839,32 +844,27 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
           // -- one complex multiplication per path in a warp-uniform inner loop -- and
           // added to the lane's accumulator.  t maximises lane use with |Suf| <= 64.
           __syncwarp();
-          int t = Mb, best_t = Mb;
-          long long Rs = 1, best_rs = 1;
+          // split: the shortest prefix with >= 32 combinations (every lane busy), then
+          // lengthened until the suffix table has <= 64 entries
           long long R = 1;
           for (int m = 0; m < Mb; ++m) R *= c_r[m];
-          float best_u = -1.f;
-          while (true) {
-            const long long Ct = R / Rs;
-            const long long rounds = (Ct + 31) / 32;
-            const float u = (float)Ct / (float)(32 * rounds);
-            if (u > best_u + 1e-6f) {
-              best_u = u;
-              best_t = t;
-              best_rs = Rs;
-            }
-            if (t == 0 || Rs * c_r[t - 1] > 64) break;
-            --t;
-            Rs *= c_r[t];
-          }
-          t = best_t;
-          const int Rsi = (int)best_rs;
-          const long long Ct = R / best_rs;
-          {  // place values of the prefix digits (digit t-1 least significant)
-            long long pv = 1;
+          int t = 0;
+          long long Ct = 1;
+          while (t < Mb && Ct < 32) Ct *= c_r[t++];
+          while (t < Mb && R / Ct > 64) Ct *= c_r[t++];
+          const int Rsi = (int)(R / Ct);
+          // per-lane prefix digits (digit t-1 least significant) of the lane's first prefix
+          // index (= lane), and the digits of the stride 32, for an incremental add per round
+          {
+            int rem = lane, r32 = 32;
             for (int m = t - 1; m >= 0; --m) {
-              if (lane == 0) c_pv[m] = (int)pv;
-              pv *= c_r[m];
+              const int rm = c_r[m];
+              const float inv = 1.0f / (float)rm;
+              const int q = (int)(((float)rem + 0.5f) * inv), q32 = (int)(((float)r32 + 0.5f) * inv);
+              c_dig[m * 32 + lane] = (unsigned char)(rem - q * rm);
+              if (lane == 0) c_pv[m] = r32 - q32 * rm;  // digit m of 32
+              rem = q;
+              r32 = q32;
             }
           }
           // suffix table: entry s (digit t most significant) = prod_{m = t+1}^{Mb-1} W_m
@@ -872,11 +872,13 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             int rem = sidx, cur = 0, nxt = 0;
             double2 Q = make_double2(1.0, 0.0);
             // decode from the last digit; walk W_m for m = Mb-1 down to t+1
-            for (int m = Mb - 1; m > t; --m) {
+            for (int m = Mb - 1; m > t; --m) {  // small integers: exact float divmod
               const int rm = c_r[m];
-              cur = rem % rm;
-              rem /= rm;
-              nxt = rem % c_r[m - 1];  // digit m-1
+              const int q = (int)(((float)rem + 0.5f) / (float)rm);
+              cur = rem - q * rm;
+              rem = q;
+              const int rp = c_r[m - 1];
+              nxt = rem - (int)(((float)rem + 0.5f) / (float)rp) * rp;  // digit m-1
               const int idx = c_wb[m] + nxt * rm + cur;
               Q = cmul(Q, cW[idx]);
               if (COUNTED) ++ncm;
@@ -889,11 +891,19 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
           for (long long c0 = 0; c0 < Ct; c0 += 32) {
             const long long cc = c0 + lane;
             const bool act = cc < Ct;
-            const int ci = act ? (int)cc : 0;
+            if (c0 > 0) {  // advance this lane's prefix index by 32 (mixed-radix add)
+              int carry = 0;
+              for (int m = t - 1; m >= 0; --m) {
+                int d = c_dig[m * 32 + lane] + c_pv[m] + carry;
+                carry = d >= c_r[m];
+                d -= carry ? c_r[m] : 0;
+                c_dig[m * 32 + lane] = (unsigned char)d;
+              }
+            }
             double2 P = Proot;
             int vprev = 0;
             for (int m = 0; m < t; ++m) {
-              const int d = (int)(((unsigned)ci / (unsigned)c_pv[m]) % (unsigned)c_r[m]);
+              const int d = c_dig[m * 32 + lane];
               const int idx = c_wb[m] + (m > 0 ? vprev * c_r[m] : 0) + d;
               P = cmul(P, cW[idx]);
               if (COUNTED) ncm += act;

@@ -236,8 +236,13 @@ def test_reversed_pairs_equal_swapped_phase(lofp):
     assert tol_ok(g1, ref)[0]
 
 
+@pytest.fixture
+def force_chain(monkeypatch):
+    monkeypatch.setenv("LOFP_FORCE_CHAIN", "1")
+
+
 @pytest.mark.parametrize("seed", range(6))
-def test_wide_circuits_chain_engine(lofp, seed):
+def test_wide_circuits_chain_engine(lofp, seed, force_chain):
     """Wide meshes (M = 18..24, D = 3..5): the last free layer has >= 8 levels for many
     outputs, so their subtrees go through the lockstep chain engine (R17).
     Values and exact path counts against the oracle."""
@@ -262,7 +267,7 @@ def test_wide_circuits_chain_engine(lofp, seed):
     assert np.array_equal(cnt, leaves)
 
 
-def test_bunched_wide_chain_fallback(lofp):
+def test_bunched_wide_chain_fallback(lofp, force_chain):
     """Dense bunched input on a wide mesh: chain pair tables can exceed the per-warp
     capacity, exercising the fallback to the plain depth-first walk."""
     M, D = 20, 3
