@@ -3,7 +3,7 @@ on 1 B200; FP64-pipe fraction of roofline).
 
 One *step* = one call of the hot path (``lofp_amplitudes``: prep, Appendix-A tables,
 per-output plans, path enumeration) over one batch of outputs resident in HBM.  The
-default workload is BASELINE.json configs[2] (M=32, N=16, D=6) with its batch of 4096
+default workload is BASELINE.json configs[4] (M=64, N=24, D=4) with its batch of 16384
 outputs conditioned on structural reachability and at most 1e9 paths per output
 (reading R14; the literal batch is ~100% structural zeros).  ``--config`` picks
 another config (0/1 literal batches, 2-4 conditioned).  Inputs are the seeded synthetic
@@ -39,7 +39,7 @@ def parse():
     p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["lofp", "reference"], default="lofp")
-    p.add_argument("--config", type=int, default=2)
+    p.add_argument("--config", type=int, default=4)
     p.add_argument("--outputs", type=int, default=0, help="limit the batch to its first N outputs")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     p.add_argument("--no-e2e", action="store_true")

@@ -210,6 +210,12 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
   a.plan_stride = (int)round16(sizeof(PlanHead) + (size_t)ctx->Lg * sizeof(PlanLevel) +
                                2 * (size_t)ctx->nbs * sizeof(PlanFactor) + 8 * (size_t)ctx->nbs + 16 +
                                16 * (size_t)ctx->nbs);
+  // chain-engine thresholds (env overrides exist for the tests, which exercise the
+  // engine on small circuits)
+  a.chain_rbox = LOFP_CHAIN_RBOX;
+  a.chain_rmin = LOFP_CHAIN_RMIN;
+  if (const char *e = std::getenv("LOFP_CHAIN_RBOX")) a.chain_rbox = std::atof(e);
+  if (const char *e = std::getenv("LOFP_CHAIN_RMIN")) a.chain_rmin = std::atoi(e);
   a.T = output_occ;
   a.amps = amps;
   a.counts = counts;

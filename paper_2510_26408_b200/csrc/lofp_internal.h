@@ -139,6 +139,8 @@ struct CallArgs {
   int maxfac;                         // attached factors per output (max; key words per lane)
   int warp_bytes;                     // per-warp shared memory (plan + vals + stack)
   int chain_on;                       // some output has a chain: engine scratch present
+  int chain_rmin;                     // fewest paths of a chain run by the engine
+  double chain_rbox;                  // smallest box product of an output's chain
   int table_bytes;                    // shared memory of the staged tables (16-aligned)
   const int32_t *T;                   // [B][M] device
   double *amps;                       // [B][2] device

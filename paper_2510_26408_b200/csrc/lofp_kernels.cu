@@ -253,7 +253,7 @@ __global__ void lofp_plan_kernel(CallArgs a) {
     // the paths of every chain subtree of this output)
     double rbox = 1.0;
     for (int m = cand; m < L; ++m) rbox *= (double)((int)lev[m].hi - (int)lev[m].lo + 1);
-    if (ok && L - cand >= LOFP_CHAIN_MIN && rbox >= (double)LOFP_CHAIN_RBOX) jb = cand;
+    if (ok && L - cand >= LOFP_CHAIN_MIN && rbox >= a.chain_rbox) jb = cand;
   }
   int ns = 0;
   for (int f = 0; f < nf; ++f) {
@@ -773,7 +773,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
           const int E = __shfl_sync(FULL, inc, 31);
           double Rd = (double)crr;  // leaves of the chain (product of the ranges)
           for (int o = 1; o < 32; o <<= 1) Rd *= __shfl_xor_sync(FULL, Rd, o);
-          const bool fb = E > LOFP_W_MAX || Rd > 2.0e9 || Rd < (double)LOFP_CHAIN_RMIN;
+          const bool fb = E > LOFP_W_MAX || Rd > 2.0e9 || Rd < (double)a.chain_rmin;
           if (lane == 0) {
             if (fb) ++nchainfb; else ++nchains;
           }

@@ -238,7 +238,10 @@ def test_reversed_pairs_equal_swapped_phase(lofp):
 
 @pytest.fixture
 def force_chain(monkeypatch):
+    """Route every qualifying chain of these small circuits through the chain engine."""
     monkeypatch.setenv("LOFP_FORCE_CHAIN", "1")
+    monkeypatch.setenv("LOFP_CHAIN_RBOX", "1")
+    monkeypatch.setenv("LOFP_CHAIN_RMIN", "1")
 
 
 @pytest.mark.parametrize("seed", range(6))
