@@ -28,7 +28,7 @@
 #ifndef LOFP_CHAIN_RMIN
 #define LOFP_CHAIN_RMIN 32     // fewest paths of a chain enumerated by the engine (else: plain DFS)
 #endif
-#define LOFP_SUF_MAX 6         // suffix product slots of the chain odometer
+#define LOFP_SUF_ENTRIES 64     // chain suffix-table entries per warp
 #define LOFP_ENUM_MAX_THREADS 512  // largest block of the enumeration kernel
 #define LOFP_MAX_CUTS 130     // M + 1 for M <= LOFP_MAX_MODES (128)
 
