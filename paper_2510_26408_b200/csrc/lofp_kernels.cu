@@ -413,8 +413,8 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
   uint32_t *mbM = reinterpret_cast<uint32_t *>(mbP + 1);
   // chain engine scratch: pair table W, per-lane suffix products, per-digit arrays
   double2 *cW = mbP + 2;                                     // [LOFP_W_MAX]
-  double2 *cPs = cW + LOFP_W_MAX;                            // [LOFP_SUF_MAX][32]
-  int *c_lo = reinterpret_cast<int *>(cPs + LOFP_SUF_MAX * 32);  // [32]
+  double2 *cPs = cW + LOFP_W_MAX;                            // [LOFP_SUF_ENTRIES] suffix table
+  int *c_lo = reinterpret_cast<int *>(cPs + LOFP_SUF_ENTRIES);  // [32]
   int *c_r = c_lo + 32;                                      // [32]
   int *c_wb = c_r + 32;                                      // [33]
   int *c_pv = c_wb + 33;                                     // [32] prefix place values
@@ -851,7 +851,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
           int t = 0;
           long long Ct = 1;
           while (t < Mb && Ct < 32) Ct *= c_r[t++];
-          while (t < Mb && R / Ct > 64) Ct *= c_r[t++];
+          while (t < Mb && R / Ct > LOFP_SUF_ENTRIES) Ct *= c_r[t++];
           const int Rsi = (int)(R / Ct);
           // per-lane prefix digits (digit t-1 least significant) of the lane's first prefix
           // index (= lane), and the digits of the stride 32, for an incremental add per round
