@@ -547,6 +547,16 @@ lofp_status lofp_work_histograms(lofp_ctx *ctx, uint64_t *handover, uint64_t *sp
   return LOFP_OK;
 }
 
+lofp_status lofp_phase_cycles(lofp_ctx *ctx, uint64_t *cycles) {
+  if (!ctx || !cycles) return LOFP_E_INVALID_ARG;
+  for (int i = 0; i < 8; ++i) cycles[i] = 0;
+  if (ctx->h_ctr.p == nullptr) return LOFP_OK;
+  CK(cudaEventSynchronize(ctx->ev_end), "cudaEventSynchronize");
+  const Counters *hc = (const Counters *)ctx->h_ctr.p;
+  for (int i = 0; i < 8; ++i) cycles[i] = hc->phase_cyc[i];
+  return LOFP_OK;
+}
+
 void lofp_destroy(lofp_ctx *ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);

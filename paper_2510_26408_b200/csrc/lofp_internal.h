@@ -104,6 +104,7 @@ struct Counters {
   unsigned long long ovf;          // pushes that went to the local overflow stack
   unsigned long long donations;    // intra-warp hand-overs (stats)
   unsigned long long chains;       // chain subtrees enumerated by the chain engine
+  unsigned long long phase_cyc[8]; // counted mode: SM cycles per phase (lane 0 of each warp)
   unsigned long long chain_fb;     // chains handed back to the plain walk (pair table too big)
   unsigned long long don_hist[64]; // counted mode: hand-overs by (leaf level - level)
   unsigned long long spill_hist[64];  // counted mode: queue spills by (leaf level - level)

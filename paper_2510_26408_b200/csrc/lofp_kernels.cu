@@ -418,8 +418,8 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
   int *c_r = c_lo + 32;                                      // [32]
   int *c_wb = c_r + 32;                                      // [33]
   int *c_pv = c_wb + 33;                                     // [32] prefix place values
-  int *c_u = c_pv + 32;                                      // [32] (spare)
-  unsigned char *c_dig = reinterpret_cast<unsigned char *>(c_u + 32);  // [32 digits][32 lanes]
+  float *c_inv = reinterpret_cast<float *>(c_pv + 32);       // [32] 1 / range size
+  unsigned char *c_dig = reinterpret_cast<unsigned char *>(c_inv + 32);  // [32 digits][32 lanes]
   unsigned char *lb = vcol + 4 * lane;  // this lane's vals byte base
   unsigned char *kb = kcol + 4 * lane;  // this lane's key byte base
   lb[LOFP_ZERO_OFF] = 0;
@@ -436,6 +436,16 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
   const uint16_t *s_scat = nullptr;
   int L = 0, NF = 0;
   unsigned long long spills = 0, ovfc = 0, dons = 0, items = 0, nchains = 0, nchainfb = 0;
+  unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tph = COUNTED ? clock64() : 0;
+#define LOFP_PHASE(k)                        \
+  do {                                       \
+    if (COUNTED) {                           \
+      const long long _t = clock64();        \
+      ph[k] += (unsigned long long)(_t - tph); \
+      tph = _t;                              \
+    }                                        \
+  } while (0)
   uint32_t *const mySM = stkM + lane;    // this lane's stack metas, entry e at [e * 32]
   double2 *const mySP = stkP + lane;     // this lane's stack products
   const int dummy_rel = (int)dummy_off - a.vals_slots * 32;  // kb + dummy_rel = scratch byte
@@ -492,6 +502,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
     tk = __shfl_sync(FULL, tk, 0);
     ++items;
 
+    LOFP_PHASE(6);
     // ---------------- stage the output's plan ----------------
     if (out != cur_out) {
       const unsigned char *gp = a.plans + (size_t)out * a.plan_stride;
@@ -738,6 +749,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
         }
       }
 
+      LOFP_PHASE(0);
       // ---------------- chain engine (lockstep, whole warp) ----------------
       // Each lane that reached the first chain level hands its chain -- the Cartesian
       // product of the chain levels' ranges, fixed by its levels < jb -- to the whole warp:
@@ -806,8 +818,10 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             }
             continue;
           }
+          LOFP_PHASE(1);
           c_lo[lane] = clo;
           c_r[lane] = crr;
+          c_inv[lane] = 1.0f / (float)crr;  // exact small-integer division: q = (n + 0.5) * inv
           c_wb[lane] = inc - sz;
           if (lane == 0) c_wb[32] = E;
           __syncwarp();
@@ -817,7 +831,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             for (int st = 16; st > 0; st >>= 1)
               if (m + st < Mb && c_wb[m + st] <= w) m += st;
             const int rm = c_r[m], rel = w - c_wb[m];
-            const int ii = rel / rm, kk = rel - ii * rm;
+            const int ii = (int)(((float)rel + 0.5f) * c_inv[m]), kk = rel - ii * rm;
             const int vm = c_lo[m] + kk, vp = m > 0 ? c_lo[m - 1] + ii : 0;
             const PlanLevel lv = s_lev[jbq + m];
             double2 Q = make_double2(1.0, 0.0);
@@ -837,6 +851,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             }
             cW[w] = Q;
           }
+          LOFP_PHASE(2);
           // (3) enumeration.  Digits [0, t) (prefix) are split over the lanes, digits
           // [t, Mb) (suffix) form a table Suf[s] = prod_{m > t} W_m shared by all lanes
           // (one lane per entry).  Every path of the chain is then formed as
@@ -859,7 +874,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             int rem = lane, r32 = 32;
             for (int m = t - 1; m >= 0; --m) {
               const int rm = c_r[m];
-              const float inv = 1.0f / (float)rm;
+              const float inv = c_inv[m];
               const int q = (int)(((float)rem + 0.5f) * inv), q32 = (int)(((float)r32 + 0.5f) * inv);
               c_dig[m * 32 + lane] = (unsigned char)(rem - q * rm);
               if (lane == 0) c_pv[m] = r32 - q32 * rm;  // digit m of 32
@@ -874,11 +889,11 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             // decode from the last digit; walk W_m for m = Mb-1 down to t+1
             for (int m = Mb - 1; m > t; --m) {  // small integers: exact float divmod
               const int rm = c_r[m];
-              const int q = (int)(((float)rem + 0.5f) / (float)rm);
+              const int q = (int)(((float)rem + 0.5f) * c_inv[m]);
               cur = rem - q * rm;
               rem = q;
               const int rp = c_r[m - 1];
-              nxt = rem - (int)(((float)rem + 0.5f) / (float)rp) * rp;  // digit m-1
+              nxt = rem - (int)(((float)rem + 0.5f) * c_inv[m - 1]) * rp;  // digit m-1
               const int idx = c_wb[m] + nxt * rm + cur;
               Q = cmul(Q, cW[idx]);
               if (COUNTED) ++ncm;
@@ -886,6 +901,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             cPs[sidx] = Q;
           }
           __syncwarp();
+          LOFP_PHASE(3);
           const int rt = t < Mb ? c_r[t] : 1;
           const int blk = Rsi / rt;  // suffix entries per value of digit t
           for (long long c0 = 0; c0 < Ct; c0 += 32) {
@@ -946,6 +962,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             }
           }
           __syncwarp();
+          LOFP_PHASE(4);
           // the emitting lane continues its depth-first walk after the chain's subtree
           if (lane == em) {
             chain_pending = false;
@@ -976,6 +993,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
         }
       }
 
+      LOFP_PHASE(5);
       // ---------------- feed idle warps through the global queue ----------------
       // At most one subtree per warp per check: the warp's shallowest open branch, and
       // only when it is far from the leaves (a large subtree) and some warp is waiting.
@@ -1013,6 +1031,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
       }
     }
 
+    LOFP_PHASE(7);
     // ---------------- item finished: warp reduction, one atomic per item ----------------
     for (int s = 16; s > 0; s >>= 1) {
       acc.x += __shfl_xor_sync(FULL, acc.x, s);
@@ -1041,6 +1060,8 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
     ovfc += __shfl_xor_sync(FULL, ovfc, s);
     dons += __shfl_xor_sync(FULL, dons, s);
   }
+  if (COUNTED && lane == 0)
+    for (int k = 0; k < 8; ++k) atomicAdd(&a.ctr->phase_cyc[k], ph[k]);
   if (lane == 0) {
     atomicAdd(&a.ctr->chains, nchains);
     atomicAdd(&a.ctr->chain_fb, nchainfb);

@@ -35,7 +35,8 @@ class lofp_run_stats(ctypes.Structure):
 
 
 EXPORTS = ["lofp_create", "lofp_amplitudes", "lofp_amplitudes_counted", "lofp_amplitudes_host",
-           "lofp_destroy", "lofp_status_string", "lofp_last_error", "lofp_stats", "lofp_work_histograms"]
+           "lofp_destroy", "lofp_status_string", "lofp_last_error", "lofp_stats", "lofp_work_histograms",
+           "lofp_phase_cycles"]
 
 
 def _load():
@@ -62,6 +63,8 @@ def _load():
     lib.lofp_stats.restype = ctypes.c_int
     lib.lofp_work_histograms.argtypes = [P, P, P]
     lib.lofp_work_histograms.restype = ctypes.c_int
+    lib.lofp_phase_cycles.argtypes = [P, P]
+    lib.lofp_phase_cycles.restype = ctypes.c_int
     return lib
 
 
@@ -159,6 +162,12 @@ class Circuit:
         sp = np.zeros(64, dtype=np.uint64)
         self._check(_lib.lofp_work_histograms(self._h, ctypes.c_void_p(h.ctypes.data), ctypes.c_void_p(sp.ctypes.data)))
         return h, sp
+
+    def phase_cycles(self):
+        """Enumeration-kernel cycle split of the last counted call (see include/lofp.h)."""
+        c = np.zeros(8, dtype=np.uint64)
+        self._check(_lib.lofp_phase_cycles(self._h, ctypes.c_void_p(c.ctypes.data)))
+        return c
 
     def stats(self) -> dict:
         st = lofp_run_stats()

@@ -34,6 +34,9 @@ for idx in cfgs:
         cnt = torch.zeros(n, dtype=torch.int64, device="cuda")
         circ.amplitudes(c.S, Td, counts=cnt); torch.cuda.synchronize()
         h, sp = circ.work_histograms()
+        pc = circ.phase_cycles().astype(float)
+        names = ["dfs", "ranges", "Wbuild", "split+suf", "paths", "return", "acquire", "feed"]
+        print("phase cycles %:", {n: round(100 * x / pc.sum(), 1) for n, x in zip(names, pc)})
         print("handover by leaf-distance:", h[:40].tolist())
         print("spill by leaf-distance:", sp[:40].tolist())
     print(json.dumps(dict(cfg=idx, outputs=n, paths=P.sum(), ms=min(res), paths_per_s=P.sum() / (min(res) * 1e-3),
