@@ -838,11 +838,10 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             for (int f = lv.fbeg; f < lv.fend; ++f) {
               const PlanFactor fd = s_fac[f];
               int key = *reinterpret_cast<const int *>(kbe + f * 128);
-              const uint32_t cm = fd.chain & 15u, sm = (fd.chain >> 4) & 15u, pm = (fd.chain >> 8) & 15u;
-              const uint32_t cmask = (cm & 1u ? 0xffu : 0u) | (cm & 2u ? 0xff00u : 0u) | (cm & 4u ? 0xff0000u : 0u) |
-                                     (cm & 8u ? 0xff000000u : 0u);
-              const uint32_t s01 = (sm & 1u) | ((sm & 2u) << 7) | ((sm & 4u) << 14) | ((sm & 8u) << 21);
-              const uint32_t p01 = (pm & 1u) | ((pm & 2u) << 7) | ((pm & 4u) << 14) | ((pm & 8u) << 21);
+              // 4 flag bits -> one 0x01 per flagged byte (bit i moves to bit 8 i)
+              const uint32_t cmask = (((fd.chain & 15u) * 0x00204081u) & 0x01010101u) * 0xffu;
+              const uint32_t s01 = (((fd.chain >> 4) & 15u) * 0x00204081u) & 0x01010101u;
+              const uint32_t p01 = (((fd.chain >> 8) & 15u) * 0x00204081u) & 0x01010101u;
               key = (int)(((uint32_t)key & ~cmask) + (uint32_t)vm * s01 + (uint32_t)vp * p01);
               const int row = __dp4a(key, fd.crow, fd.base);
               const int o = s_off[row] + __dp4a(key, 0x010000ff, (int)fd.dy);
