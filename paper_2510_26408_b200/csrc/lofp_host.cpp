@@ -216,6 +216,8 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
   a.chain_rmin = LOFP_CHAIN_RMIN;
   if (const char *e = std::getenv("LOFP_CHAIN_RBOX")) a.chain_rbox = std::atof(e);
   if (const char *e = std::getenv("LOFP_CHAIN_RMIN")) a.chain_rmin = std::atoi(e);
+  a.small_paths = LOFP_SMALL_PATHS;
+  if (const char *e = std::getenv("LOFP_SMALL_PATHS")) a.small_paths = std::min(std::atoi(e), 256);
   a.T = output_occ;
   a.amps = amps;
   a.counts = counts;
@@ -337,7 +339,7 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
                  (2ull * (unsigned long long)hc->nchain >= hc->nfeas || std::getenv("LOFP_FORCE_CHAIN"));
     a.warp_bytes = (int)round16((size_t)a.plan_smem + (size_t)a.vals_slots * 32 + (size_t)maxF * 128 +
                                 (size_t)LOFP_STK * 32 * 20 + 32 +
-                                (a.chain_on ? (size_t)LOFP_W_MAX * 16 + (size_t)LOFP_SUF_ENTRIES * 16 + 161 * 4 + 1024 : 0));
+                                (a.chain_on ? (size_t)LOFP_W_MAX * 16 + (size_t)LOFP_SUF_ENTRIES * 16 + 161 * 4 + 1024 + 512 + 264 + 4 * 32 * LOFP_SMALL_LEVELS + 16 : 0));
     int grid = 0, block = 0;
     size_t smem = 0;
     cudaError_t e = lofp_enum_config(a, counts != nullptr, &grid, &block, &smem);

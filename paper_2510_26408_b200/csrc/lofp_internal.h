@@ -22,8 +22,11 @@
 #define LOFP_ITEM_BYTES 256   // one global work-queue slot
 #define LOFP_ITEM_PREFIX 224  // prefix bytes an item can carry (>= LOFP_MAX_LEVELS)
 #define LOFP_SPILL_MIN_DIST 6  // global-queue spills only for branches >= this many levels above the leaf level
-#define LOFP_CHAIN_MIN 4       // shortest chain handed to the lockstep chain engine
+#define LOFP_CHAIN_MIN 4       // shortest chain handed to the chain engine
 #define LOFP_CHAIN_RBOX 1024   // smallest box product (paths bound) of an output's chain
+#define LOFP_SMALL_LEVELS 16   // chains with <= this many levels and
+#define LOFP_SMALL_PATHS 0     // < this many paths are enumerated in batches (0: off; the
+                               // batched mode is slower than the walk on the configs measured)
 #define LOFP_W_MAX 256         // chain pair-table entries per warp (else: plain DFS)
 #ifndef LOFP_CHAIN_RMIN
 #define LOFP_CHAIN_RMIN 32     // fewest paths of a chain enumerated by the engine (else: plain DFS)
@@ -141,6 +144,7 @@ struct CallArgs {
   int warp_bytes;                     // per-warp shared memory (plan + vals + stack)
   int chain_on;                       // some output has a chain: engine scratch present
   int chain_rmin;                     // fewest paths of a chain run by the engine
+  int small_paths;                    // chains with fewer paths are batched (0: off)
   double chain_rbox;                  // smallest box product of an output's chain
   int table_bytes;                    // shared memory of the staged tables (16-aligned)
   const int32_t *T;                   // [B][M] device

@@ -420,6 +420,14 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
   int *c_pv = c_wb + 33;                                     // [32] prefix place values
   float *c_inv = reinterpret_cast<float *>(c_pv + 32);       // [32] 1 / range size
   unsigned char *c_dig = reinterpret_cast<unsigned char *>(c_inv + 32);  // [32 digits][32 lanes]
+  // small-chain batch: per emitting lane (column) its chain's ranges and table offsets
+  double2 *sc_proot = reinterpret_cast<double2 *>(
+      (reinterpret_cast<uintptr_t>(c_dig + 32 * 32) + 15) & ~uintptr_t(15));  // [32] root products
+  int *sc_wbase = reinterpret_cast<int *>(sc_proot + 32);                // [33] pair-table bases
+  int *sc_pbase = sc_wbase + 33;                                         // [33] path bases
+  uint16_t *sc_wb = reinterpret_cast<uint16_t *>(sc_pbase + 33);        // [16 levels][32]
+  unsigned char *sc_lo = reinterpret_cast<unsigned char *>(sc_wb + LOFP_SMALL_LEVELS * 32);  // [16][32]
+  unsigned char *sc_r = sc_lo + LOFP_SMALL_LEVELS * 32;                  // [16][32]
   unsigned char *lb = vcol + 4 * lane;  // this lane's vals byte base
   unsigned char *kb = kcol + 4 * lane;  // this lane's key byte base
   lb[LOFP_ZERO_OFF] = 0;
@@ -587,6 +595,33 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
       }
     }
     __syncwarp();
+
+    // after a chain's subtree is done: pop the deepest open branch (or become idle)
+    auto resume_walk = [&]() {
+      if (top != bot) {
+        const unsigned e2 = ((top - 1u) & (LOFP_STK - 1)) * 32;
+        const uint32_t m2 = mySM[e2];
+        const int jj = m2 & 0xff;
+        const int nv2 = (int)lb[lofp_level_off(jj)] + 1;
+        Pb = mySP[e2];
+        if (nv2 == (int)((m2 >> 8) & 0xff)) --top;
+        j = jj;
+        v = nv2;
+        set_level(lb, kb, s_lev[jj], s_scat, jj, nv2);
+      } else if (otop != obot) {
+        const unsigned e2 = (otop - 1u) & (LOFP_OVF - 1);
+        const uint32_t m2 = ovfM[e2];
+        const int jj = m2 & 0xff;
+        const int nv2 = (int)lb[lofp_level_off(jj)] + 1;
+        Pb = ovfP[e2];
+        if (nv2 == (int)((m2 >> 8) & 0xff)) --otop;
+        j = jj;
+        v = nv2;
+        set_level(lb, kb, s_lev[jj], s_scat, jj, nv2);
+      } else {
+        working = false;
+      }
+    };
 
     unsigned iter = 0;
     while (true) {
@@ -762,6 +797,127 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
       // stack as after a finished subtree.
       {
         unsigned pend = __ballot_sync(FULL, chain_pending);
+        if (pend) {
+          // Every pending lane sizes its own chain; short chains (few paths) are
+          // enumerated together below, the others get a warp pass each.
+          const int Mb = L - jbq;
+          bool small = false;
+          int myE = 0, myR = 0;
+          if (chain_pending && a.small_paths > 0 && Mb <= LOFP_SMALL_LEVELS) {
+            int rprev = 1, E = 0;
+            float R = 1.f;
+            for (int m = 0; m < Mb; ++m) {
+              const PlanLevel cl = s_lev[jbq + m];
+              const int lo = max((int)lb[cl.ol] + cl.cl, (int)cl.lo);
+              const int r = min((int)lb[cl.or_] + cl.cr, (int)cl.hi) - lo + 1;
+              sc_lo[m * 32 + lane] = (unsigned char)lo;
+              sc_r[m * 32 + lane] = (unsigned char)r;
+              sc_wb[m * 32 + lane] = (uint16_t)min(E, 65535);
+              E += rprev * r;
+              rprev = r;
+              R *= (float)r;
+            }
+            small = R < (float)a.small_paths && E <= LOFP_W_MAX;
+            myE = E;
+            myR = (int)R;
+          }
+          unsigned smask = __ballot_sync(FULL, small);
+          pend &= ~smask;
+          // ---- short chains, batched: all their pair tables, then all their paths ----
+          while (smask) {
+            const bool cand = (smask >> lane) & 1u;
+            int incE = cand ? myE : 0;
+            for (int o = 1; o < 32; o <<= 1) {
+              const int tv = __shfl_up_sync(FULL, incE, o);
+              if (lane >= o) incE += tv;
+            }
+            const bool ing = cand && incE <= LOFP_W_MAX;  // a prefix of the candidates
+            const unsigned gmask = __ballot_sync(FULL, ing);
+            smask &= ~gmask;
+            const int eg = ing ? myE : 0, rg = ing ? myR : 0;
+            int ie = eg, ir = rg;
+            for (int o = 1; o < 32; o <<= 1) {
+              const int te = __shfl_up_sync(FULL, ie, o), tr = __shfl_up_sync(FULL, ir, o);
+              if (lane >= o) {
+                ie += te;
+                ir += tr;
+              }
+            }
+            const int Eg = __shfl_sync(FULL, ie, 31), Rg = __shfl_sync(FULL, ir, 31);
+            sc_wbase[lane] = ie - eg;
+            sc_pbase[lane] = ir - rg;
+            if (lane == 0) {
+              sc_wbase[32] = Eg;
+              sc_pbase[32] = Rg;
+            }
+            sc_proot[lane] = Pb;
+            __syncwarp();
+            if (lane == 0) nchains += __popc(gmask);
+            for (int w = lane; w < Eg; w += 32) {  // pair tables W of every chain of the group
+              int c = 0;
+              for (int st = 16; st > 0; st >>= 1)
+                if (sc_wbase[c + st] <= w) c += st;
+              const int loc = w - sc_wbase[c];
+              int m = 0;
+              for (int st = LOFP_SMALL_LEVELS / 2; st > 0; st >>= 1)
+                if (m + st < Mb && sc_wb[(m + st) * 32 + c] <= loc) m += st;
+              const int rm = sc_r[m * 32 + c], rel = loc - sc_wb[m * 32 + c];
+              const int ii = (int)(((float)rel + 0.5f) * __frcp_rn((float)rm)), kk = rel - ii * rm;
+              const int vm = sc_lo[m * 32 + c] + kk, vp = m > 0 ? sc_lo[(m - 1) * 32 + c] + ii : 0;
+              const unsigned char *kbc = kcol + 4 * c;
+              const PlanLevel lv = s_lev[jbq + m];
+              double2 Q = make_double2(1.0, 0.0);
+              for (int f = lv.fbeg; f < lv.fend; ++f) {
+                const PlanFactor fd = s_fac[f];
+                int key = *reinterpret_cast<const int *>(kbc + f * 128);
+                const uint32_t cmask = (((fd.chain & 15u) * 0x00204081u) & 0x01010101u) * 0xffu;
+                const uint32_t s01 = (((fd.chain >> 4) & 15u) * 0x00204081u) & 0x01010101u;
+                const uint32_t p01 = (((fd.chain >> 8) & 15u) * 0x00204081u) & 0x01010101u;
+                key = (int)(((uint32_t)key & ~cmask) + (uint32_t)vm * s01 + (uint32_t)vp * p01);
+                const int row = __dp4a(key, fd.crow, fd.base);
+                const int o = s_off[row] + __dp4a(key, 0x010000ff, (int)fd.dy);
+                Q = cmul(Q, s_ent[o]);
+                if (COUNTED) ncm += __dp4a(key, 0x000100ff, (int)fd.dx) > 0;
+              }
+              cW[w] = Q;
+            }
+            __syncwarp();
+            for (int p = lane; p < Rg; p += 32) {  // every path: root * prod_m W_m
+              int c = 0;
+              for (int st = 16; st > 0; st >>= 1)
+                if (sc_pbase[c + st] <= p) c += st;
+              int rem = p - sc_pbase[c];
+              const double2 *wc = cW + sc_wbase[c];
+              double2 P = sc_proot[c];
+              int m = Mb - 1, rm = sc_r[m * 32 + c];
+              int q = (int)(((float)rem + 0.5f) * __frcp_rn((float)rm));
+              int cur = rem - q * rm;
+              rem = q;
+              for (; m > 0; --m) {  // digits from the last level; W_m(v_{m-1}, v_m)
+                const int rp = sc_r[(m - 1) * 32 + c];
+                const int q2 = (int)(((float)rem + 0.5f) * __frcp_rn((float)rp));
+                const int nxt = rem - q2 * rp;
+                rem = q2;
+                P = cmul(P, wc[sc_wb[m * 32 + c] + nxt * rm + cur]);
+                cur = nxt;
+                rm = rp;
+              }
+              P = cmul(P, wc[cur]);  // W_0(v_0)
+              acc.x += P.x;
+              acc.y += P.y;
+              if (COUNTED) {
+                ++npaths;
+                ncm += Mb;
+              }
+            }
+            __syncwarp();
+            if (ing) {
+              chain_pending = false;
+              resume_walk();
+            }
+          }
+        }
+        LOFP_PHASE(1);
         while (pend) {
           const int em = __ffs(pend) - 1;
           pend &= pend - 1;
@@ -881,23 +1037,30 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
               r32 = q32;
             }
           }
-          // suffix table: entry s (digit t most significant) = prod_{m = t+1}^{Mb-1} W_m
-          for (int sidx = lane; sidx < Rsi; sidx += 32) {
-            int rem = sidx, cur = 0, nxt = 0;
-            double2 Q = make_double2(1.0, 0.0);
-            // decode from the last digit; walk W_m for m = Mb-1 down to t+1
-            for (int m = Mb - 1; m > t; --m) {  // small integers: exact float divmod
-              const int rm = c_r[m];
-              const int q = (int)(((float)rem + 0.5f) * c_inv[m]);
-              cur = rem - q * rm;
-              rem = q;
-              const int rp = c_r[m - 1];
-              nxt = rem - (int)(((float)rem + 0.5f) * c_inv[m - 1]) * rp;  // digit m-1
-              const int idx = c_wb[m] + nxt * rm + cur;
-              Q = cmul(Q, cW[idx]);
-              if (COUNTED) ++ncm;
+          // suffix table: entry s (digit t most significant) = prod_{m = t+1}^{Mb-1} W_m;
+          // entries lane and lane + 32 are built together (two independent chains)
+          {
+            const int s0 = lane, s1 = lane + 32;
+            int rem0 = s0, rem1 = s1;
+            double2 Q0 = make_double2(1.0, 0.0), Q1 = Q0;
+            for (int m = Mb - 1; m > t; --m) {  // decode from the last digit
+              const int rm = c_r[m], rp = c_r[m - 1];
+              const float im = c_inv[m], ip = c_inv[m - 1];
+              const int q0 = (int)(((float)rem0 + 0.5f) * im), q1 = (int)(((float)rem1 + 0.5f) * im);
+              const int cur0 = rem0 - q0 * rm, cur1 = rem1 - q1 * rm;
+              rem0 = q0;
+              rem1 = q1;
+              const int nx0 = rem0 - (int)(((float)rem0 + 0.5f) * ip) * rp;  // digit m-1
+              const int nx1 = rem1 - (int)(((float)rem1 + 0.5f) * ip) * rp;
+              const int blk_m = c_wb[m + 1] - c_wb[m];  // (lane 31's c_wb = E past the chain)
+              const double2 w0 = cW[c_wb[m] + min(nx0 * rm + cur0, blk_m - 1)];
+              const double2 w1 = cW[c_wb[m] + min(nx1 * rm + cur1, blk_m - 1)];
+              Q0 = cmul(Q0, w0);
+              Q1 = cmul(Q1, w1);
+              if (COUNTED) ncm += (s0 < Rsi) + (s1 < Rsi);
             }
-            cPs[sidx] = Q;
+            if (s0 < Rsi) cPs[s0] = Q0;
+            if (s1 < Rsi) cPs[s1] = Q1;
           }
           __syncwarp();
           LOFP_PHASE(3);
@@ -965,29 +1128,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
           // the emitting lane continues its depth-first walk after the chain's subtree
           if (lane == em) {
             chain_pending = false;
-            if (top != bot) {
-              const unsigned e2 = ((top - 1u) & (LOFP_STK - 1)) * 32;
-              const uint32_t m2 = mySM[e2];
-              const int jj = m2 & 0xff;
-              const int nv2 = (int)lb[lofp_level_off(jj)] + 1;
-              Pb = mySP[e2];
-              if (nv2 == (int)((m2 >> 8) & 0xff)) --top;
-              j = jj;
-              v = nv2;
-              set_level(lb, kb, s_lev[jj], s_scat, jj, nv2);
-            } else if (otop != obot) {
-              const unsigned e2 = (otop - 1u) & (LOFP_OVF - 1);
-              const uint32_t m2 = ovfM[e2];
-              const int jj = m2 & 0xff;
-              const int nv2 = (int)lb[lofp_level_off(jj)] + 1;
-              Pb = ovfP[e2];
-              if (nv2 == (int)((m2 >> 8) & 0xff)) --otop;
-              j = jj;
-              v = nv2;
-              set_level(lb, kb, s_lev[jj], s_scat, jj, nv2);
-            } else {
-              working = false;
-            }
+            resume_walk();
           }
         }
       }

@@ -244,6 +244,15 @@ def force_chain(monkeypatch):
     monkeypatch.setenv("LOFP_CHAIN_RMIN", "1")
 
 
+@pytest.fixture
+def small_chains(monkeypatch):
+    """Also batch short chains (the batched mode is off by default)."""
+    monkeypatch.setenv("LOFP_FORCE_CHAIN", "1")
+    monkeypatch.setenv("LOFP_CHAIN_RBOX", "1")
+    monkeypatch.setenv("LOFP_CHAIN_RMIN", "1")
+    monkeypatch.setenv("LOFP_SMALL_PATHS", "256")
+
+
 @pytest.mark.parametrize("seed", range(6))
 def test_wide_circuits_chain_engine(lofp, seed, force_chain):
     """Wide meshes (M = 18..24, D = 3..5): the last free layer has >= 8 levels for many
@@ -286,4 +295,27 @@ def test_bunched_wide_chain_fallback(lofp, force_chain):
     got, cnt, _, _ = run(lofp, M, layers, S, T)
     ref, leaves = oracle.path_sum(M, layers, S, T, return_leaves=True)
     assert tol_ok(got, ref)[0]
+    assert np.array_equal(cnt, leaves)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_wide_circuits_small_chain_batches(lofp, seed, small_chains):
+    """Short chains enumerated in batches (several emitting lanes' chains at once)."""
+    rng = np.random.default_rng(4300 + seed)
+    M = int(rng.integers(16, 21))
+    D = int(rng.integers(3, 6))
+    layers = li.clements_mesh(M, D, seed=200 + seed)
+    N = int(rng.integers(M // 2, M - 3))
+    S = np.zeros(M, dtype=np.int32)
+    S[np.sort(rng.choice(M, N, replace=False))] = 1
+    T = li.uniform_subsets(M, N, 4000, rng)
+    T = T[oracle.reachable(M, layers, S, T)]
+    P = np.array(oracle.count_paths(M, layers, S, T), dtype=object)
+    T = T[(P > 0) & (P <= 3 * 10 ** 5)][:150]
+    assert len(T) > 20
+    got, cnt, st, _ = run(lofp, M, layers, S, T)
+    assert st["chains"] > 0
+    ref, leaves = oracle.path_sum(M, layers, S, T, return_leaves=True)
+    ok, err = tol_ok(got, ref)
+    assert ok, err
     assert np.array_equal(cnt, leaves)
