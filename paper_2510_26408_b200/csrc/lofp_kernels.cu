@@ -391,7 +391,7 @@ __device__ __forceinline__ double2 level_product(double2 P, int fbeg, int fcnt, 
   return P;
 }
 
-template <bool COUNTED>
+template <bool COUNTED, bool CHAIN>
 __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(CallArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   double2 *s_ent = reinterpret_cast<double2 *>(smem);
@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
     }
     const PlanHead *sh = reinterpret_cast<const PlanHead *>(s_plan);
     const int Lm1 = L - 1;
-    const int jbq = a.chain_on ? (int)sh->jb : L;  // first chain level (== L: no chain)
+    const int jbq = CHAIN ? (int)sh->jb : L;  // first chain level (== L: no chain)
     bool chain_pending = false;
 
     // ---------------- lane 0 begins the item ----------------
@@ -796,7 +796,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
       // sharing and added to the lane's accumulator.  Then the emitting lane pops its
       // stack as after a finished subtree.
       {
-        unsigned pend = __ballot_sync(FULL, chain_pending);
+        unsigned pend = CHAIN ? __ballot_sync(FULL, chain_pending) : 0u;
         if (pend) {
           // Every pending lane sizes its own chain; short chains (few paths) are
           // enumerated together below, the others get a warp pass each.
@@ -1249,7 +1249,8 @@ cudaError_t lofp_enum_config(const CallArgs &a, bool counted, int *grid, int *bl
   if (e != cudaSuccess) return e;
   e = cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
   if (e != cudaSuccess) return e;
-  const void *fn = counted ? (const void *)lofp_enum_kernel<true> : (const void *)lofp_enum_kernel<false>;
+  const void *fn = counted ? (a.chain_on ? (const void *)lofp_enum_kernel<true, true> : (const void *)lofp_enum_kernel<true, false>)
+                           : (a.chain_on ? (const void *)lofp_enum_kernel<false, true> : (const void *)lofp_enum_kernel<false, false>);
   cudaFuncAttributes fa;
   e = cudaFuncGetAttributes(&fa, fn);
   if (e != cudaSuccess) return e;
@@ -1288,9 +1289,16 @@ cudaError_t lofp_enum_config(const CallArgs &a, bool counted, int *grid, int *bl
 
 cudaError_t lofp_launch_enum(const CallArgs &a, bool counted, int grid, int block, size_t smem,
                              cudaStream_t s) {
-  if (counted)
-    lofp_enum_kernel<true><<<grid, block, smem, s>>>(a);
-  else
-    lofp_enum_kernel<false><<<grid, block, smem, s>>>(a);
+  if (counted) {
+    if (a.chain_on)
+      lofp_enum_kernel<true, true><<<grid, block, smem, s>>>(a);
+    else
+      lofp_enum_kernel<true, false><<<grid, block, smem, s>>>(a);
+  } else {
+    if (a.chain_on)
+      lofp_enum_kernel<false, true><<<grid, block, smem, s>>>(a);
+    else
+      lofp_enum_kernel<false, false><<<grid, block, smem, s>>>(a);
+  }
   return cudaGetLastError();
 }
