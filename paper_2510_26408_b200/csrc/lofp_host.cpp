@@ -320,7 +320,7 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
   // (sync 2) the largest per-output plan sizes the enumeration kernel's shared memory
   CK(cudaMemcpyAsync(ctx->h_ctr.p, a.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, stream), "read plan sizes");
   CK(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
-  const int maxL = hc->maxL, maxF = hc->maxF, maxS = hc->maxS;
+  const int maxL = hc->maxL, maxF = hc->maxF, maxS = hc->maxS, maxK = hc->maxK;
   ctx->stats.levels = maxL;
   CK(cudaEventRecord(ctx->ev_enum0, stream), "cudaEventRecord");
   if (hc->nfeas > 0) {
@@ -331,13 +331,12 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
     // scatter entries past a level's own list: vals, keys and stack follow inside the
     // warp's region, so those reads never leave it)
     a.plan_smem = (int)round16(sizeof(PlanHead) + (size_t)(maxL + maxF) * 16 + 2 * (size_t)maxS);
-    a.maxfac = maxF;
-    // The chain engine costs every warp its scratch (fewer resident warps): use it when
-    // most outputs of the batch have a chain worth a warp (env LOFP_NO_CHAIN: off, for
-    // debugging; LOFP_FORCE_CHAIN: on whenever any output has one, for testing).
     a.chain_on = hc->nchain > 0 && !std::getenv("LOFP_NO_CHAIN") &&
                  (2ull * (unsigned long long)hc->nchain >= hc->nfeas || std::getenv("LOFP_FORCE_CHAIN"));
-    a.warp_bytes = (int)round16((size_t)a.plan_smem + (size_t)a.vals_slots * 32 + (size_t)maxF * 128 +
+    // key words per lane: every attached factor (none while the engine is on)
+    a.maxfac = a.chain_on ? 0 : maxF;
+    (void)maxK;
+    a.warp_bytes = (int)round16((size_t)a.plan_smem + (size_t)a.vals_slots * 32 + (size_t)a.maxfac * 128 +
                                 (size_t)LOFP_STK * 32 * 20 + 32 +
                                 (a.chain_on ? (size_t)LOFP_W_MAX * 16 + (size_t)LOFP_SUF_ENTRIES * 16 + 161 * 4 + 1024 + 512 + 264 + 4 * 32 * LOFP_SMALL_LEVELS + 16 : 0));
     int grid = 0, block = 0;

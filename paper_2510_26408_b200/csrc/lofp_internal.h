@@ -48,7 +48,8 @@ __host__ __device__ inline uint16_t lofp_level_off(int j) { return lofp_slot_off
 //   [max(vals[ol] + cl, lo), min(vals[or_] + cr, hi)]  with vals[ol] + cl = F_{l-1}(k-1),
 //   vals[or_] + cr = F_{l-1}(k+1) (a constant uses the lane's zero slot), lo/hi the
 //   output's box.  Factors [fbeg, fend) are the elements attached to this level;
-//   scatter entries [sbeg, send) are the key bytes that hold this level's value.
+//   scatter entries [sbeg, send & 0xfff) are the key bytes that hold this level's value;
+//   the last (send >> 12) of them belong to chain factors (skipped while the engine is on).
 struct __align__(16) PlanLevel {
   uint16_t ol, or_;
   uint8_t cl, cr, lo, hi;
@@ -66,11 +67,11 @@ struct __align__(16) PlanLevel {
 struct __align__(16) PlanFactor {
   int32_t crow;
   int32_t base;
-  int16_t dy;
-  int8_t dx;
-  uint8_t pad0;
-  uint32_t chain;  // factors of chain levels: bits 0-3 key bytes from chain levels,
-                   // bits 4-7 of those from its own level, bits 8-11 from the previous one
+  int8_t dy, dx;
+  uint16_t chain;   // factors of chain levels: bits 0-3 key bytes from chain levels,
+                    // bits 4-7 of those from its own level, bits 8-11 from the previous one
+  uint8_t slot[4];  // levels of (a, b, c, y) (0xff: constant), to gather a key from the
+                    // value bytes (chain factors have no key word while the engine is on)
 };
 
 // The chain of an output (R17): the suffix of levels [jb, L) (the last
@@ -115,6 +116,7 @@ struct Counters {
   int32_t maxL;                    // largest per-output level count
   int32_t maxF;                    // largest per-output attached-factor count
   int32_t maxS;                    // largest per-output scatter-list length
+  int32_t maxK;                    // largest per-output count of non-chain factors
   int32_t nchain;                  // outputs whose plan has a chain
 };
 

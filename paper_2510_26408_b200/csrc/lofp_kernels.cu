@@ -255,6 +255,21 @@ __global__ void lofp_plan_kernel(CallArgs a) {
     for (int m = cand; m < L; ++m) rbox *= (double)((int)lev[m].hi - (int)lev[m].lo + 1);
     if (ok && L - cand >= LOFP_CHAIN_MIN && rbox >= a.chain_rbox) jb = cand;
   }
+  // scatter entries per level: those of chain factors go last (<= 15 per level, and the
+  // whole list < 4096 entries, else no chain for this output)
+  if (jb < L) {
+    uint8_t chc[LOFP_MAX_LEVELS];
+    for (int j = 0; j < L; ++j) chc[j] = 0;
+    int tot = 0;
+    bool fits = true;
+    for (int f = 0; f < nf; ++f)
+      for (int p = 0; p < 4; ++p)
+        if (tmp[f].s[p] >= 0) {
+          ++tot;
+          if (tmp[f].at >= jb && ++chc[tmp[f].s[p]] > 15) fits = false;
+        }
+    if (!fits || tot >= 4096) jb = L;
+  }
   int ns = 0;
   for (int f = 0; f < nf; ++f) {
     const FacTmp ft = tmp[f];
@@ -270,23 +285,27 @@ __global__ void lofp_plan_kernel(CallArgs a) {
     pf.crow = (int32_t)(((uint32_t)(uint8_t)(int8_t)(-ft.stride)) | ((uint32_t)(uint8_t)(int8_t)(ft.stride - 1) << 8) |
                         (1u << 16));
     pf.base = ft.base;
-    pf.dy = ft.dy;
+    pf.dy = (int8_t)ft.dy;
     pf.dx = (int8_t)ft.dx;
-    pf.pad0 = 0;
-    pf.chain = chain;
+    pf.chain = (uint16_t)chain;
+    for (int p = 0; p < 4; ++p) pf.slot[p] = (uint8_t)ft.s[p];  // -1 -> 0xff
     fac[w] = pf;
+    const uint32_t isch = ft.at >= jb ? 1u : 0u;
     for (int p = 0; p < 4; ++p)
-      if (ft.s[p] >= 0) stmp[ns++] = ((uint32_t)ft.s[p] << 16) | (uint32_t)(w * 128 + p);
+      if (ft.s[p] >= 0) stmp[ns++] = ((2u * (uint32_t)ft.s[p] + isch) << 16) | (uint32_t)(w * 128 + p);
   }
-  // counting sort of the scatter entries by the level whose value they hold
-  for (int j = 0; j <= L; ++j) cnt[j] = 0;
-  for (int i = 0; i < ns; ++i) cnt[(stmp[i] >> 16) + 1]++;
-  for (int j = 0; j < L; ++j) cnt[j + 1] += cnt[j];
+  // counting sort of the scatter entries by (level, chain factor)
+  uint16_t cnt2[2 * LOFP_MAX_LEVELS + 1];
+  for (int j = 0; j <= 2 * L; ++j) cnt2[j] = 0;
+  for (int i = 0; i < ns; ++i) cnt2[(stmp[i] >> 16) + 1]++;
+  for (int j = 0; j < 2 * L; ++j) cnt2[j + 1] += cnt2[j];
   for (int j = 0; j < L; ++j) {
-    lev[j].sbeg = cnt[j];
-    lev[j].send = cnt[j + 1];
+    const int nch = cnt2[2 * j + 2] - cnt2[2 * j + 1];
+    lev[j].sbeg = cnt2[2 * j];
+    lev[j].send = (uint16_t)((cnt2[2 * j + 2] & 0xfff) | (jb < L ? nch << 12 : 0));
   }
-  for (int i = 0; i < ns; ++i) scat[cnt[stmp[i] >> 16]++] = (uint16_t)(stmp[i] & 0xffff);
+  for (int i = 0; i < ns; ++i) scat[cnt2[stmp[i] >> 16]++] = (uint16_t)(stmp[i] & 0xffff);
+  const int nkeys = jb < L ? (int)lev[jb].fbeg : nf;  // non-chain factors (they come first)
   PlanHead h;
   h.root[0] = root.x;
   h.root[1] = root.y;
@@ -305,6 +324,7 @@ __global__ void lofp_plan_kernel(CallArgs a) {
   atomicMax(&a.ctr->maxL, L);
   atomicMax(&a.ctr->maxF, nf);
   atomicMax(&a.ctr->maxS, ns);
+  atomicMax(&a.ctr->maxK, nkeys);
   if (jb < L) atomicAdd(&a.ctr->nchain, 1);
   unsigned long long idx = atomicAdd(&a.ctr->nfeas, 1ull);
   a.feas[idx] = (uint32_t)q;
@@ -340,29 +360,50 @@ struct WarpSmem {
   uint32_t *stkM;       // [LOFP_STK][32]
 };
 
+// Scatter entries of a level to write: all of them; none while the chain engine is on
+// (then every factor's key is gathered from the value bytes and no key words exist).
+template <bool CHAIN>
+__device__ __forceinline__ int scatter_count(const PlanLevel &lv) {
+  return CHAIN ? 0 : (int)(lv.send & 0xfff) - (int)lv.sbeg;
+}
+
 // Write value v of level j: the vals byte and every key byte that holds it.  (Used off
 // the hot step; the step writes with a warp-uniform trip count, see below.)
+template <bool CHAIN>
 __device__ __forceinline__ void set_level(unsigned char *lb, unsigned char *kb, const PlanLevel &lvref,
                                           const uint16_t *scat, int j, int v) {
-  const uint32_t se = *reinterpret_cast<const uint32_t *>(&lvref.sbeg);  // sbeg | send << 16
-  const int sbeg = se & 0xffff, send = se >> 16;
+  const PlanLevel lv = lvref;
+  const int sbeg = lv.sbeg, n = scatter_count<CHAIN>(lv);
   lb[lofp_level_off(j)] = (unsigned char)v;
-  for (int s = sbeg; s < send; ++s) kb[scat[s]] = (unsigned char)v;
+  for (int s = 0; s < n; ++s) kb[scat[sbeg + s]] = (unsigned char)v;
+}
+
+// A factor's key gathered from value bytes (slot 0xff: constant -> 0).
+__device__ __forceinline__ int gather_key(const PlanFactor &fd, const unsigned char *lb) {
+  uint32_t k = 0;
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int sl = fd.slot[p];
+    const uint32_t b = sl == 0xff ? 0u : (uint32_t)lb[lofp_level_off(sl)];
+    k |= b << (8 * p);
+  }
+  return (int)k;
 }
 
 // Product of the factors attached to level lv, times P.  The trip count is the warp's
 // largest factor count (nmax, warp-uniform) so that every lane runs the same instruction
 // stream; a lane past its own count multiplies by table entry 0, which is exactly 1 (the
 // vacuum element of BS 0, R16).
-template <bool COUNTED>
+template <bool COUNTED, bool CHAIN>
 __device__ __forceinline__ int factor_entry(const PlanFactor *fp, const unsigned char *kp, int i, int fcnt,
-                                            const int32_t *s_off, unsigned long long &ncm) {
+                                            const int32_t *s_off, const unsigned char *lb, unsigned long long &ncm) {
   // past the lane's own count: re-read its last factor (always a valid descriptor, key
   // and table row) and use entry 0 (= 1)
   const bool on = i < fcnt;
   const int fi = on ? i : max(fcnt - 1, 0);
   const int2 fd = *reinterpret_cast<const int2 *>(fp + fi);  // crow, base
-  const int key = *reinterpret_cast<const int *>(kp + fi * 128);
+  // engine on: no key words, the key is gathered from the lane's value bytes
+  const int key = CHAIN ? gather_key(fp[fi], lb) : *reinterpret_cast<const int *>(kp + fi * 128);
   const int row = __dp4a(key, fd.x, fd.y);
   const int o = s_off[on ? row : 0] + __dp4a(key, 0x010000ff, (int)fp[fi].dy);  // + y - a
   if (COUNTED) ncm += (on && __dp4a(key, 0x000100ff, (int)fp[fi].dx) > 0);  // x1 + x2 = c - a
@@ -374,20 +415,21 @@ __device__ __forceinline__ int factor_entry(const PlanFactor *fp, const unsigned
 // stream; a lane past its own count multiplies by table entry 0, which is exactly 1 (the
 // vacuum element of BS 0, R16).  Factors are taken in pairs: e_i e_{i+1} does not depend on P,
 // so the dependent fp64 chain is one complex multiplication per pair.
-template <bool COUNTED>
+template <bool COUNTED, bool CHAIN>
 __device__ __forceinline__ double2 level_product(double2 P, int fbeg, int fcnt, int nmax, const PlanFactor *fac,
                                                  const unsigned char *kb, const int32_t *s_off,
-                                                 const double2 *s_ent, unsigned long long &ncm) {
+                                                 const double2 *s_ent, const unsigned char *lb,
+                                                 unsigned long long &ncm) {
   const PlanFactor *fp = fac + fbeg;
   const unsigned char *kp = kb + fbeg * 128;
   int i = 0;
 #pragma unroll 1
   for (; i + 1 < nmax; i += 2) {
-    const int o0 = factor_entry<COUNTED>(fp, kp, i, fcnt, s_off, ncm);
-    const int o1 = factor_entry<COUNTED>(fp, kp, i + 1, fcnt, s_off, ncm);
+    const int o0 = factor_entry<COUNTED, CHAIN>(fp, kp, i, fcnt, s_off, lb, ncm);
+    const int o1 = factor_entry<COUNTED, CHAIN>(fp, kp, i + 1, fcnt, s_off, lb, ncm);
     P = cmul(P, cmul(s_ent[o0], s_ent[o1]));
   }
-  if (i < nmax) P = cmul(P, s_ent[factor_entry<COUNTED>(fp, kp, i, fcnt, s_off, ncm)]);
+  if (i < nmax) P = cmul(P, s_ent[factor_entry<COUNTED, CHAIN>(fp, kp, i, fcnt, s_off, lb, ncm)]);
   return P;
 }
 
@@ -535,6 +577,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
     const int Lm1 = L - 1;
     const int jbq = CHAIN ? (int)sh->jb : L;  // first chain level (== L: no chain)
     bool chain_pending = false;
+    const int NK = CHAIN ? 0 : NF;  // key words of this output (none while the engine is on)
 
     // ---------------- lane 0 begins the item ----------------
     // Lane state: j = current level, v = its value, Pb = product before level j's
@@ -548,7 +591,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
     unsigned long long npaths = 0, ncm = 0;
     {
       // all key words of this warp start at zero (constant inputs contribute 0)
-      for (int f = 0; f < NF; ++f) *reinterpret_cast<uint32_t *>(kb + f * 128) = 0u;
+      for (int f = 0; f < NK; ++f) *reinterpret_cast<uint32_t *>(kb + f * 128) = 0u;
       int j0 = 0, vs = 0, ve = 0;
       double2 P0;
       if (kind == 1) {
@@ -572,7 +615,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
           __threadfence();
           *reinterpret_cast<volatile unsigned *>(&it->seq) = 0u;  // slot free again
           for (int jj = 0; jj < j0; ++jj)  // rebuild the keys of the prefix levels
-            set_level(lb, kb, s_lev[jj], s_scat, jj, lb[lofp_level_off(jj)]);
+            set_level<CHAIN>(lb, kb, s_lev[jj], s_scat, jj, lb[lofp_level_off(jj)]);
         }
       }
       if (lane == 0 && kind == 1 && jbq == 0) {  // the whole tree is one chain
@@ -583,7 +626,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
         working = true;
         j = j0;
         v = vs;
-        set_level(lb, kb, s_lev[j0], s_scat, j0, vs);
+        set_level<CHAIN>(lb, kb, s_lev[j0], s_scat, j0, vs);
         if (j0 == Lm1) {
           leafhi = ve;
         } else if (ve > vs) {
@@ -607,7 +650,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
         if (nv2 == (int)((m2 >> 8) & 0xff)) --top;
         j = jj;
         v = nv2;
-        set_level(lb, kb, s_lev[jj], s_scat, jj, nv2);
+        set_level<CHAIN>(lb, kb, s_lev[jj], s_scat, jj, nv2);
       } else if (otop != obot) {
         const unsigned e2 = (otop - 1u) & (LOFP_OVF - 1);
         const uint32_t m2 = ovfM[e2];
@@ -617,7 +660,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
         if (nv2 == (int)((m2 >> 8) & 0xff)) --otop;
         j = jj;
         v = nv2;
-        set_level(lb, kb, s_lev[jj], s_scat, jj, nv2);
+        set_level<CHAIN>(lb, kb, s_lev[jj], s_scat, jj, nv2);
       } else {
         working = false;
       }
@@ -669,11 +712,11 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
               *reinterpret_cast<uint32_t *>(vcol + w * 128 + 4 * lane) =
                   *reinterpret_cast<const uint32_t *>(vcol + w * 128 + 4 * donor);
             // the donor's keys hold the prefix values (deeper bytes are rewritten on descent)
-            for (int f = 0; f < NF; ++f)
+            for (int f = 0; f < NK; ++f)
               *reinterpret_cast<uint32_t *>(kcol + f * 128 + 4 * lane) =
                   *reinterpret_cast<const uint32_t *>(kcol + f * 128 + 4 * donor);
             const int nv = (int)lb[lofp_level_off(jd)] + 1;
-            set_level(lb, kb, s_lev[jd], s_scat, jd, nv);
+            set_level<CHAIN>(lb, kb, s_lev[jd], s_scat, jd, nv);
             bot = top = obot = otop = 0;
             leafhi = 0;
             if (jd == Lm1) {
@@ -705,7 +748,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
         const PlanLevel lv = s_lev[stepping ? j : 0];
         const int fcnt = stepping ? (int)lv.fend - (int)lv.fbeg : 0;
         const int nmax = __reduce_max_sync(FULL, fcnt);
-        const double2 P = level_product<COUNTED>(Pb, lv.fbeg, fcnt, nmax, s_fac, kb, s_off, s_ent, ncm);
+        const double2 P = level_product<COUNTED, CHAIN>(Pb, lv.fbeg, fcnt, nmax, s_fac, kb, s_off, s_ent, lb, ncm);
         const bool isleaf = stepping && j == Lm1;
         if (isleaf) {
           acc.x += P.x;
@@ -771,7 +814,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
         }
         // the new value: vals byte and key bytes
         lb[wr ? (int)noff : (int)dummy_off] = (unsigned char)nv;
-        const int scnt = wr ? (int)nl.send - (int)nl.sbeg : 0;
+        const int scnt = wr ? scatter_count<CHAIN>(nl) : 0;
         const int smax = __reduce_max_sync(FULL, scnt);
         const uint16_t *sp = s_scat + nl.sbeg;  // reads past the list stay in the warp's smem
 #pragma unroll 1
@@ -869,7 +912,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
               double2 Q = make_double2(1.0, 0.0);
               for (int f = lv.fbeg; f < lv.fend; ++f) {
                 const PlanFactor fd = s_fac[f];
-                int key = *reinterpret_cast<const int *>(kbc + f * 128);
+                int key = gather_key(fd, vcol + 4 * c);
                 const uint32_t cmask = (((fd.chain & 15u) * 0x00204081u) & 0x01010101u) * 0xffu;
                 const uint32_t s01 = (((fd.chain >> 4) & 15u) * 0x00204081u) & 0x01010101u;
                 const uint32_t p01 = (((fd.chain >> 8) & 15u) * 0x00204081u) & 0x01010101u;
@@ -954,7 +997,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             const int lo0 = __shfl_sync(FULL, clo, 0), r0 = __shfl_sync(FULL, crr, 0);
             if (lane == em) {
               v = lo0;
-              set_level(lb, kb, s_lev[jbq], s_scat, jbq, lo0);
+              set_level<CHAIN>(lb, kb, s_lev[jbq], s_scat, jbq, lo0);
               if (jbq == Lm1) {
                 leafhi = lo0 + r0 - 1;
               } else if (r0 > 1) {
@@ -993,7 +1036,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             double2 Q = make_double2(1.0, 0.0);
             for (int f = lv.fbeg; f < lv.fend; ++f) {
               const PlanFactor fd = s_fac[f];
-              int key = *reinterpret_cast<const int *>(kbe + f * 128);
+              int key = gather_key(fd, lbe);
               // 4 flag bits -> one 0x01 per flagged byte (bit i moves to bit 8 i)
               const uint32_t cmask = (((fd.chain & 15u) * 0x00204081u) & 0x01010101u) * 0xffu;
               const uint32_t s01 = (((fd.chain >> 4) & 15u) * 0x00204081u) & 0x01010101u;
