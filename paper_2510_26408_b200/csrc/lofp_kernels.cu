@@ -1024,7 +1024,20 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
           c_wb[lane] = inc - sz;
           if (lane == 0) c_wb[32] = E;
           __syncwarp();
-          // (2) pair table
+          // (2) pair table.  First the chain factors' keys with their chain bytes cleared
+          // (gathered once per chain from the emitter's value bytes), then one entry per
+          // lane per round: W_m(v_{m-1}, v_m) = product of level m's factors.
+          const int fc0 = s_lev[jbq].fbeg, nfc = NF - fc0;  // chain factors come last
+          uint32_t *ckey = reinterpret_cast<uint32_t *>(cPs);  // (the suffix table comes later)
+          const bool pre = nfc <= 2 * LOFP_SUF_ENTRIES;
+          if (pre) {
+            for (int f = lane; f < nfc; f += 32) {
+              const PlanFactor fd = s_fac[fc0 + f];
+              const uint32_t cmask = (((fd.chain & 15u) * 0x00204081u) & 0x01010101u) * 0xffu;
+              ckey[f] = (uint32_t)gather_key(fd, lbe) & ~cmask;
+            }
+            __syncwarp();
+          }
           for (int w = lane; w < E; w += 32) {
             int m = 0;
             for (int st = 16; st > 0; st >>= 1)
@@ -1036,12 +1049,17 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             double2 Q = make_double2(1.0, 0.0);
             for (int f = lv.fbeg; f < lv.fend; ++f) {
               const PlanFactor fd = s_fac[f];
-              int key = gather_key(fd, lbe);
               // 4 flag bits -> one 0x01 per flagged byte (bit i moves to bit 8 i)
-              const uint32_t cmask = (((fd.chain & 15u) * 0x00204081u) & 0x01010101u) * 0xffu;
               const uint32_t s01 = (((fd.chain >> 4) & 15u) * 0x00204081u) & 0x01010101u;
               const uint32_t p01 = (((fd.chain >> 8) & 15u) * 0x00204081u) & 0x01010101u;
-              key = (int)(((uint32_t)key & ~cmask) + (uint32_t)vm * s01 + (uint32_t)vp * p01);
+              uint32_t base;
+              if (pre) {
+                base = ckey[f - fc0];
+              } else {
+                const uint32_t cmask = (((fd.chain & 15u) * 0x00204081u) & 0x01010101u) * 0xffu;
+                base = (uint32_t)gather_key(fd, lbe) & ~cmask;
+              }
+              const int key = (int)(base + (uint32_t)vm * s01 + (uint32_t)vp * p01);
               const int row = __dp4a(key, fd.crow, fd.base);
               const int o = s_off[row] + __dp4a(key, 0x010000ff, (int)fd.dy);
               Q = cmul(Q, s_ent[o]);
@@ -1049,6 +1067,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             }
             cW[w] = Q;
           }
+          __syncwarp();  // the key scratch is reused by the suffix table below
           LOFP_PHASE(2);
           // (3) enumeration.  Digits [0, t) (prefix) are split over the lanes, digits
           // [t, Mb) (suffix) form a table Suf[s] = prod_{m > t} W_m shared by all lanes
