@@ -1101,8 +1101,8 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
           }
           // suffix table: entry s (digit t most significant) = prod_{m = t+1}^{Mb-1} W_m;
           // entries lane and lane + 32 are built together (two independent chains)
-          {
-            const int s0 = lane, s1 = lane + 32;
+          for (int sbase = 0; sbase < Rsi; sbase += 64) {
+            const int s0 = sbase + lane, s1 = sbase + lane + 32;
             int rem0 = s0, rem1 = s1;
             double2 Q0 = make_double2(1.0, 0.0), Q1 = Q0;
             for (int m = Mb - 1; m > t; --m) {  // decode from the last digit
