@@ -435,6 +435,9 @@ __device__ __forceinline__ double2 level_product(double2 P, int fbeg, int fcnt, 
 
 template <bool COUNTED, bool CHAIN>
 __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(CallArgs a) {
+  // branch-stack entries kept in shared memory: fewer with the chain engine (the walk
+  // above the chains is short; the overflow below the ring catches the rest)
+  constexpr unsigned STK = CHAIN ? LOFP_STK_CHAIN : LOFP_STK;
   extern __shared__ __align__(16) unsigned char smem[];
   double2 *s_ent = reinterpret_cast<double2 *>(smem);
   int32_t *s_off = reinterpret_cast<int32_t *>(s_ent + a.nentries);
@@ -450,8 +453,8 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
   unsigned char *vcol = wb + a.plan_smem;                                   // [slots/4][32] words
   unsigned char *kcol = vcol + a.vals_slots * 32;                           // [maxfac][32] words
   double2 *stkP = reinterpret_cast<double2 *>(kcol + (size_t)a.maxfac * 128);  // [LOFP_STK][32]
-  uint32_t *stkM = reinterpret_cast<uint32_t *>(stkP + LOFP_STK * 32);         // [LOFP_STK][32]
-  double2 *mbP = reinterpret_cast<double2 *>(stkM + LOFP_STK * 32);             // hand-over mailbox
+  uint32_t *stkM = reinterpret_cast<uint32_t *>(stkP + STK * 32);         // [LOFP_STK][32]
+  double2 *mbP = reinterpret_cast<double2 *>(stkM + STK * 32);             // hand-over mailbox
   uint32_t *mbM = reinterpret_cast<uint32_t *>(mbP + 1);
   // chain engine scratch: pair table W, per-lane suffix products, per-digit arrays
   double2 *cW = mbP + 2;                                     // [LOFP_W_MAX]
@@ -642,7 +645,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
     // after a chain's subtree is done: pop the deepest open branch (or become idle)
     auto resume_walk = [&]() {
       if (top != bot) {
-        const unsigned e2 = ((top - 1u) & (LOFP_STK - 1)) * 32;
+        const unsigned e2 = ((top - 1u) & (STK - 1)) * 32;
         const uint32_t m2 = mySM[e2];
         const int jj = m2 & 0xff;
         const int nv2 = (int)lb[lofp_level_off(jj)] + 1;
@@ -678,7 +681,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
           if (otop != obot)
             myshal = (int)(ovfM[obot & (LOFP_OVF - 1)] & 0xff);
           else if (top != bot)
-            myshal = (int)(mySM[(bot & (LOFP_STK - 1)) * 32] & 0xff);
+            myshal = (int)(mySM[(bot & (STK - 1)) * 32] & 0xff);
         }
         const int shal = __reduce_min_sync(FULL, myshal);
         if (shal == 0x7fffffff) {
@@ -694,7 +697,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
               P = ovfP[obot & (LOFP_OVF - 1)];
               ++obot;
             } else {
-              const unsigned e = (bot & (LOFP_STK - 1)) * 32;
+              const unsigned e = (bot & (STK - 1)) * 32;
               m = mySM[e];
               P = mySP[e];
               ++bot;
@@ -758,7 +761,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
         const bool sib = isleaf && v < leafhi;
         const bool desc = stepping && !isleaf;
         const bool popsm = isleaf && !sib && top != bot;
-        const unsigned te = ((top - 1u) & (LOFP_STK - 1)) * 32;
+        const unsigned te = ((top - 1u) & (STK - 1)) * 32;
         uint32_t m = mySM[te];
         double2 Ps = mySP[te];
         bool popov = false;
@@ -792,15 +795,15 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
           if (nj == Lm1) {
             leafhi = dhi;  // leaf siblings are walked one per step
           } else if (dhi > dlo) {
-            if (top - bot == LOFP_STK) {  // full: the shallowest entry goes to the overflow
-              const unsigned e = (bot & (LOFP_STK - 1)) * 32, o = otop & (LOFP_OVF - 1);
+            if (top - bot == STK) {  // full: the shallowest entry goes to the overflow
+              const unsigned e = (bot & (STK - 1)) * 32, o = otop & (LOFP_OVF - 1);
               ovfM[o] = mySM[e];
               ovfP[o] = mySP[e];
               ++otop;
               ++bot;
               ++ovfc;
             }
-            const unsigned e = (top & (LOFP_STK - 1)) * 32;
+            const unsigned e = (top & (STK - 1)) * 32;
             mySM[e] = (uint32_t)nj | ((uint32_t)dhi << 8);
             mySP[e] = P;
             ++top;
@@ -1001,15 +1004,15 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
               if (jbq == Lm1) {
                 leafhi = lo0 + r0 - 1;
               } else if (r0 > 1) {
-                if (top - bot == LOFP_STK) {
-                  const unsigned e2 = (bot & (LOFP_STK - 1)) * 32, o2 = otop & (LOFP_OVF - 1);
+                if (top - bot == STK) {
+                  const unsigned e2 = (bot & (STK - 1)) * 32, o2 = otop & (LOFP_OVF - 1);
                   ovfM[o2] = mySM[e2];
                   ovfP[o2] = mySP[e2];
                   ++otop;
                   ++bot;
                   ++ovfc;
                 }
-                const unsigned e2 = (top & (LOFP_STK - 1)) * 32;
+                const unsigned e2 = (top & (STK - 1)) * 32;
                 mySM[e2] = (uint32_t)jbq | ((uint32_t)(lo0 + r0 - 1) << 8);
                 mySP[e2] = Pb;
                 ++top;
@@ -1209,7 +1212,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             if (otop != obot)
               myshal = (int)(ovfM[obot & (LOFP_OVF - 1)] & 0xff);
             else if (top != bot)
-              myshal = (int)(mySM[(bot & (LOFP_STK - 1)) * 32] & 0xff);
+              myshal = (int)(mySM[(bot & (STK - 1)) * 32] & 0xff);
           }
           const int shal = __reduce_min_sync(FULL, myshal);
           if (shal != 0x7fffffff && Lm1 - shal >= LOFP_SPILL_MIN_DIST) {
@@ -1222,7 +1225,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
                 spill(slot, out, ovfM[e], ovfP[e]);
                 ++obot;
               } else {
-                const unsigned e = (bot & (LOFP_STK - 1)) * 32;
+                const unsigned e = (bot & (STK - 1)) * 32;
                 spill(slot, out, mySM[e], mySP[e]);
                 ++bot;
               }
