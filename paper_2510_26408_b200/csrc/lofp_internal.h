@@ -17,7 +17,7 @@
 #include <stdint.h>
 
 #define LOFP_MAX_LEVELS 128   // DFS levels (free BS outputs) per circuit
-#define LOFP_STK 8            // per-lane branch-stack entries kept in shared memory
+#define LOFP_STK 4            // per-lane branch-stack entries kept in shared memory
 #define LOFP_STK_CHAIN 4      // the same with the chain engine on
 #define LOFP_OVF 128           // per-lane local-memory overflow entries (>= LOFP_MAX_LEVELS)
 #define LOFP_ITEM_BYTES 256   // one global work-queue slot
