@@ -33,7 +33,7 @@
 #define LOFP_CHAIN_RMIN 32     // fewest paths of a chain enumerated by the engine (else: plain DFS)
 #endif
 #define LOFP_SUF_ENTRIES 64     // chain suffix-table entries per warp
-#define LOFP_ENUM_MAX_THREADS 512  // largest block of the enumeration kernel
+#define LOFP_ENUM_MAX_THREADS 640  // largest block of the enumeration kernel
 #define LOFP_MAX_CUTS 130     // M + 1 for M <= LOFP_MAX_MODES (128)
 
 // Per-lane value array ("vals") lives in shared memory, lane-interleaved by 32-bit word:
