@@ -28,7 +28,7 @@
 #define LOFP_SMALL_LEVELS 16   // chains with <= this many levels and
 #define LOFP_SMALL_PATHS 0     // < this many paths are enumerated in batches (0: off; the
                                // batched mode is slower than the walk on the configs measured)
-#define LOFP_W_MAX 256         // chain pair-table entries per warp (else: plain DFS)
+#define LOFP_W_MAX 128         // chain pair-table entries per warp (else: plain DFS)
 #ifndef LOFP_CHAIN_RMIN
 #define LOFP_CHAIN_RMIN 32     // fewest paths of a chain enumerated by the engine (else: plain DFS)
 #endif
