@@ -433,7 +433,7 @@ __device__ __forceinline__ double2 level_product(double2 P, int fbeg, int fcnt, 
   return P;
 }
 
-template <bool COUNTED, bool CHAIN>
+template <bool COUNTED, bool CHAIN, bool SMALL>
 __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(CallArgs a) {
   // branch-stack entries kept in shared memory: fewer with the chain engine (the walk
   // above the chains is short; the overflow below the ring catches the rest)
@@ -849,7 +849,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
           const int Mb = L - jbq;
           bool small = false;
           int myE = 0, myR = 0;
-          if (chain_pending && a.small_paths > 0 && Mb <= LOFP_SMALL_LEVELS) {
+          if (SMALL && chain_pending && Mb <= LOFP_SMALL_LEVELS) {
             int rprev = 1, E = 0;
             float R = 1.f;
             for (int m = 0; m < Mb; ++m) {
@@ -867,7 +867,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             myE = E;
             myR = (int)R;
           }
-          unsigned smask = __ballot_sync(FULL, small);
+          unsigned smask = SMALL ? __ballot_sync(FULL, small) : 0u;
           pend &= ~smask;
           // ---- short chains, batched: all their pair tables, then all their paths ----
           while (smask) {
@@ -1303,6 +1303,17 @@ cudaError_t lofp_launch_plan(const CallArgs &a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// The enumeration kernel variants: validation counters, chain engine, batched short chains
+// (the last only on request; it enlarges the engine's code).
+static const void *pick_enum(bool counted, bool chain, bool small) {
+  if (counted) {
+    if (!chain) return (const void *)lofp_enum_kernel<true, false, false>;
+    return small ? (const void *)lofp_enum_kernel<true, true, true> : (const void *)lofp_enum_kernel<true, true, false>;
+  }
+  if (!chain) return (const void *)lofp_enum_kernel<false, false, false>;
+  return small ? (const void *)lofp_enum_kernel<false, true, true> : (const void *)lofp_enum_kernel<false, true, false>;
+}
+
 cudaError_t lofp_enum_config(const CallArgs &a, bool counted, int *grid, int *block, size_t *smem) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -1314,8 +1325,7 @@ cudaError_t lofp_enum_config(const CallArgs &a, bool counted, int *grid, int *bl
   if (e != cudaSuccess) return e;
   e = cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
   if (e != cudaSuccess) return e;
-  const void *fn = counted ? (a.chain_on ? (const void *)lofp_enum_kernel<true, true> : (const void *)lofp_enum_kernel<true, false>)
-                           : (a.chain_on ? (const void *)lofp_enum_kernel<false, true> : (const void *)lofp_enum_kernel<false, false>);
+  const void *fn = pick_enum(counted, a.chain_on != 0, a.small_paths > 0);
   cudaFuncAttributes fa;
   e = cudaFuncGetAttributes(&fa, fn);
   if (e != cudaSuccess) return e;
@@ -1354,16 +1364,9 @@ cudaError_t lofp_enum_config(const CallArgs &a, bool counted, int *grid, int *bl
 
 cudaError_t lofp_launch_enum(const CallArgs &a, bool counted, int grid, int block, size_t smem,
                              cudaStream_t s) {
-  if (counted) {
-    if (a.chain_on)
-      lofp_enum_kernel<true, true><<<grid, block, smem, s>>>(a);
-    else
-      lofp_enum_kernel<true, false><<<grid, block, smem, s>>>(a);
-  } else {
-    if (a.chain_on)
-      lofp_enum_kernel<false, true><<<grid, block, smem, s>>>(a);
-    else
-      lofp_enum_kernel<false, false><<<grid, block, smem, s>>>(a);
-  }
+  void *args[] = {const_cast<CallArgs *>(&a)};
+  cudaError_t e = cudaLaunchKernel(pick_enum(counted, a.chain_on != 0, a.small_paths > 0), dim3(grid), dim3(block),
+                                   args, smem, s);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
