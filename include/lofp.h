@@ -153,8 +153,8 @@ lofp_status lofp_work_histograms(lofp_ctx *ctx, uint64_t *handover, uint64_t *sp
 /* Enumeration-kernel time split of the last lofp_amplitudes_counted call (zeros after an
  * uncounted call): SM clock cycles summed over warps (lane 0's clock) in 8 phases --
  * 0 depth-first step and hand-over, 1 chain ranges, 2 chain pair table, 3 chain split and
- * suffix table, 4 chain path products, 5 return to the walk, 6 work acquisition and plan
- * staging, 7 global-queue feeding.  cycles is a host uint64 [8].  Synchronises the call. */
+ * prefix digits, 4 chain path products, 5 return to the walk and global-queue feeding,
+ * 6 work acquisition, plan staging and item reduction, 7 chain suffix table.  cycles is a host uint64 [8].  Synchronises the call. */
 lofp_status lofp_phase_cycles(lofp_ctx *ctx, uint64_t *cycles);
 
 #ifdef __cplusplus

@@ -464,7 +464,8 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
   int *c_wb = c_r + 32;                                      // [33]
   int *c_pv = c_wb + 33;                                     // [32] prefix place values
   float *c_inv = reinterpret_cast<float *>(c_pv + 32);       // [32] 1 / range size
-  unsigned char *c_dig = reinterpret_cast<unsigned char *>(c_inv + 32);  // [32 digits][32 lanes]
+  int *c_u32 = reinterpret_cast<int *>(c_inv + 32);              // [32] digits of the stride 32
+  unsigned char *c_dig = reinterpret_cast<unsigned char *>(c_u32 + 32);  // [32 digits][32 lanes]
   // small-chain batch: per emitting lane (column) its chain's ranges and table offsets
   double2 *sc_proot = reinterpret_cast<double2 *>(
       (reinterpret_cast<uintptr_t>(c_dig + 32 * 32) + 15) & ~uintptr_t(15));  // [32] root products
@@ -1080,28 +1081,35 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
           // added to the lane's accumulator.  t maximises lane use with |Suf| <= 64.
           __syncwarp();
           // split: the shortest prefix with >= 32 combinations (every lane busy), then
-          // lengthened until the suffix table has <= 64 entries
-          long long R = 1;
-          for (int m = 0; m < Mb; ++m) R *= c_r[m];
-          int t = 0;
-          long long Ct = 1;
-          while (t < Mb && Ct < 32) Ct *= c_r[t++];
-          while (t < Mb && R / Ct > LOFP_SUF_ENTRIES) Ct *= c_r[t++];
-          const int Rsi = (int)(R / Ct);
-          // per-lane prefix digits (digit t-1 least significant) of the lane's first prefix
-          // index (= lane), and the digits of the stride 32, for an incremental add per round
-          {
-            int rem = lane, r32 = 32;
-            for (int m = t - 1; m >= 0; --m) {
-              const int rm = c_r[m];
-              const float inv = c_inv[m];
-              const int q = (int)(((float)rem + 0.5f) * inv), q32 = (int)(((float)r32 + 0.5f) * inv);
-              c_dig[m * 32 + lane] = (unsigned char)(rem - q * rm);
-              if (lane == 0) c_pv[m] = r32 - q32 * rm;  // digit m of 32
-              rem = q;
-              r32 = q32;
-            }
+          // lengthened until the suffix table has <= 64 entries.  Lane m holds the
+          // inclusive product of the ranges of levels <= m (exact in double).
+          double pinc = (double)crr;
+          for (int o = 1; o < 32; o <<= 1) {
+            const double tv = __shfl_up_sync(FULL, pinc, o);
+            if (lane >= o) pinc *= tv;
           }
+          const double Rdd = __shfl_sync(FULL, pinc, 31);
+          const double thr = fmax(32.0, Rdd / (double)LOFP_SUF_ENTRIES);
+          const unsigned okm = __ballot_sync(FULL, lane < Mb && pinc >= thr);
+          const int t = okm ? __ffs(okm) : Mb;  // prefix digits [0, t)
+          const double Ctd = t > 0 ? __shfl_sync(FULL, pinc, t - 1) : 1.0;
+          const long long Ct = (long long)Ctd;
+          const int Rsi = (int)(Rdd / Ctd + 0.5);
+          // per-lane prefix digits (digit t-1 least significant) of the lane's first prefix
+          // index (= lane), and the digits of the stride 32, for an incremental add per round:
+          // digit m of c = floor(c / pv_m) mod r_m, pv_m = Ct / pinc_m (place value)
+          if (lane < t) c_pv[lane] = __float_as_int(1.0f / (float)(Ctd / pinc));  // 1 / pv_m
+          __syncwarp();
+          for (int m = 0; m < t; ++m) {
+            const float ipv = __int_as_float(c_pv[m]), ir = c_inv[m];
+            const int rm = c_r[m];
+            const int q = (int)(((float)lane + 0.5f) * ipv), q32 = (int)((32.0f + 0.5f) * ipv);
+            const int d = q - (int)(((float)q + 0.5f) * ir) * rm;
+            const int d32 = q32 - (int)(((float)q32 + 0.5f) * ir) * rm;
+            c_dig[m * 32 + lane] = (unsigned char)d;
+            if (lane == 0) c_u32[m] = d32;  // digit m of 32
+          }
+          LOFP_PHASE(3);
           // suffix table: entry s (digit t most significant) = prod_{m = t+1}^{Mb-1} W_m;
           // entries lane and lane + 32 are built together (two independent chains)
           for (int sbase = 0; sbase < Rsi; sbase += 64) {
@@ -1128,7 +1136,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             if (s1 < Rsi) cPs[s1] = Q1;
           }
           __syncwarp();
-          LOFP_PHASE(3);
+          LOFP_PHASE(7);
           const int rt = t < Mb ? c_r[t] : 1;
           const int blk = Rsi / rt;  // suffix entries per value of digit t
           for (long long c0 = 0; c0 < Ct; c0 += 32) {
@@ -1137,7 +1145,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             if (c0 > 0) {  // advance this lane's prefix index by 32 (mixed-radix add)
               int carry = 0;
               for (int m = t - 1; m >= 0; --m) {
-                int d = c_dig[m * 32 + lane] + c_pv[m] + carry;
+                int d = c_dig[m * 32 + lane] + c_u32[m] + carry;
                 carry = d >= c_r[m];
                 d -= carry ? c_r[m] : 0;
                 c_dig[m * 32 + lane] = (unsigned char)d;
@@ -1236,7 +1244,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
       }
     }
 
-    LOFP_PHASE(7);
+    LOFP_PHASE(6);
     // ---------------- item finished: warp reduction, one atomic per item ----------------
     for (int s = 16; s > 0; s >>= 1) {
       acc.x += __shfl_xor_sync(FULL, acc.x, s);

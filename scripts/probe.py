@@ -35,7 +35,7 @@ for idx in cfgs:
         circ.amplitudes(c.S, Td, counts=cnt); torch.cuda.synchronize()
         h, sp = circ.work_histograms()
         pc = circ.phase_cycles().astype(float)
-        names = ["dfs", "ranges", "Wbuild", "split+suf", "paths", "return", "acquire", "feed"]
+        names = ["dfs", "ranges", "Wbuild", "split+digits", "paths", "return+feed", "acquire", "suffix"]
         print("phase cycles %:", {n: round(100 * x / pc.sum(), 1) for n, x in zip(names, pc)})
         print("handover by leaf-distance:", h[:40].tolist())
         print("spill by leaf-distance:", sp[:40].tolist())
