@@ -986,8 +986,13 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             if (lane >= o) inc += tv;
           }
           const int E = __shfl_sync(FULL, inc, 31);
-          double Rd = (double)crr;  // leaves of the chain (product of the ranges)
-          for (int o = 1; o < 32; o <<= 1) Rd *= __shfl_xor_sync(FULL, Rd, o);
+          // lane m: product of the ranges of levels <= m (exact in double); lane 31: paths
+          double pinc = (double)crr;
+          for (int o = 1; o < 32; o <<= 1) {
+            const double tv = __shfl_up_sync(FULL, pinc, o);
+            if (lane >= o) pinc *= tv;
+          }
+          const double Rd = __shfl_sync(FULL, pinc, 31);
           const bool fb = E > LOFP_W_MAX || Rd > 2.0e9 || Rd < (double)a.chain_rmin;
           if (lane == 0) {
             if (fb) ++nchainfb; else ++nchains;
@@ -1081,14 +1086,8 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
           // added to the lane's accumulator.  t maximises lane use with |Suf| <= 64.
           __syncwarp();
           // split: the shortest prefix with >= 32 combinations (every lane busy), then
-          // lengthened until the suffix table has <= 64 entries.  Lane m holds the
-          // inclusive product of the ranges of levels <= m (exact in double).
-          double pinc = (double)crr;
-          for (int o = 1; o < 32; o <<= 1) {
-            const double tv = __shfl_up_sync(FULL, pinc, o);
-            if (lane >= o) pinc *= tv;
-          }
-          const double Rdd = __shfl_sync(FULL, pinc, 31);
+          // lengthened until the suffix table has <= 64 entries (pinc: see the ranges).
+          const double Rdd = Rd;
           const double thr = fmax(32.0, Rdd / (double)LOFP_SUF_ENTRIES);
           const unsigned okm = __ballot_sync(FULL, lane < Mb && pinc >= thr);
           const int t = okm ? __ffs(okm) : Mb;  // prefix digits [0, t)
