@@ -18,7 +18,7 @@
 
 #define LOFP_MAX_LEVELS 128   // DFS levels (free BS outputs) per circuit
 #define LOFP_STK 4            // per-lane branch-stack entries kept in shared memory
-#define LOFP_STK_CHAIN 4      // the same with the chain engine on
+#define LOFP_STK_CHAIN 2      // the same with the chain engine on
 #define LOFP_OVF 128           // per-lane local-memory overflow entries (>= LOFP_MAX_LEVELS)
 #define LOFP_ITEM_BYTES 256   // one global work-queue slot
 #define LOFP_ITEM_PREFIX 224  // prefix bytes an item can carry (>= LOFP_MAX_LEVELS)
