@@ -1209,7 +1209,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
       // ---------------- feed idle warps through the global queue ----------------
       // At most one subtree per warp per check: the warp's shallowest open branch, and
       // only when it is far from the leaves (a large subtree) and some warp is waiting.
-      if (((++iter) & 31u) == 0u) {
+      if (((++iter) & (CHAIN ? 0u : 31u)) == 0u) {  // (a chain step is long: check often)
         long long waiting = 0;
         if (lane == 0) waiting = (long long)(vload(&a.ctr->ticket) - vload(&a.ctr->tail));
         waiting = __shfl_sync(FULL, waiting, 0);
