@@ -1029,7 +1029,8 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
           LOFP_PHASE(1);
           c_lo[lane] = clo;
           c_r[lane] = crr;
-          c_inv[lane] = 1.0f / (float)crr;  // exact small-integer division: q = (n + 0.5) * inv
+          // reciprocal of the range: floor(n / r) = (int)((n + 0.5) * inv) exactly for n < 2^12
+          c_inv[lane] = __fdividef(1.0f, (float)crr);
           c_wb[lane] = inc - sz;
           if (lane == 0) c_wb[32] = E;
           __syncwarp();
@@ -1088,16 +1089,17 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
           // split: the shortest prefix with >= 32 combinations (every lane busy), then
           // lengthened until the suffix table has <= 64 entries (pinc: see the ranges).
           const double Rdd = Rd;
-          const double thr = fmax(32.0, Rdd / (double)LOFP_SUF_ENTRIES);
+          const double thr = fmax(32.0, Rdd * (1.0 / LOFP_SUF_ENTRIES));
           const unsigned okm = __ballot_sync(FULL, lane < Mb && pinc >= thr);
           const int t = okm ? __ffs(okm) : Mb;  // prefix digits [0, t)
           const double Ctd = t > 0 ? __shfl_sync(FULL, pinc, t - 1) : 1.0;
           const long long Ct = (long long)Ctd;
-          const int Rsi = (int)(Rdd / Ctd + 0.5);
+          // R / C_t: an exact integer <= 64 (float quotient error ~1e-7 of it: rounding is safe)
+          const int Rsi = __float2int_rn(__fdividef((float)Rdd, (float)Ctd));
           // per-lane prefix digits (digit t-1 least significant) of the lane's first prefix
           // index (= lane), and the digits of the stride 32, for an incremental add per round:
           // digit m of c = floor(c / pv_m) mod r_m, pv_m = Ct / pinc_m (place value)
-          if (lane < t) c_pv[lane] = __float_as_int(1.0f / (float)(Ctd / pinc));  // 1 / pv_m
+          if (lane < t) c_pv[lane] = __float_as_int(__fdividef((float)pinc, (float)Ctd));  // 1 / pv_m
           __syncwarp();
           for (int m = 0; m < t; ++m) {
             const float ipv = __int_as_float(c_pv[m]), ir = c_inv[m];
