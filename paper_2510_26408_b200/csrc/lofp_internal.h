@@ -69,8 +69,9 @@ struct __align__(16) PlanFactor {
   int32_t crow;
   int32_t base;
   int8_t dy, dx;
-  uint16_t chain;   // factors of chain levels: bits 0-3 key bytes from chain levels,
-                    // bits 4-7 of those from its own level, bits 8-11 from the previous one
+  uint16_t chain;   // byte selector of the chain engine's pair-table key:
+                    // key = __byte_perm(gathered key, v_m | v_{m-1} << 8, chain), nibble p =
+                    // p (keep), 4 (v_m: the factor's own chain level) or 5 (v_{m-1})
   uint8_t slot[4];  // levels of (a, b, c, y) (0xff: constant), to gather a key from the
                     // value bytes (chain factors have no key word while the engine is on)
 };

@@ -274,13 +274,11 @@ __global__ void lofp_plan_kernel(CallArgs a) {
   for (int f = 0; f < nf; ++f) {
     const FacTmp ft = tmp[f];
     int w = cnt[ft.at]++;
-    uint32_t chain = 0;
+    uint32_t chain = 0x3210u;  // identity byte selector
     if (ft.at >= jb)
-      for (int p = 0; p < 4; ++p) {
-        if (ft.s[p] >= jb) chain |= 1u << p;
-        if (ft.s[p] >= jb && ft.s[p] == ft.at) chain |= 16u << p;
-        if (ft.s[p] >= jb && ft.s[p] == ft.at - 1) chain |= 256u << p;
-      }
+      for (int p = 0; p < 4; ++p)
+        if (ft.s[p] >= jb)  // a chain value: the level's own (4) or the previous one's (5)
+          chain = (chain & ~(15u << (4 * p))) | ((ft.s[p] == ft.at ? 4u : 5u) << (4 * p));
     PlanFactor pf;
     pf.crow = (int32_t)(((uint32_t)(uint8_t)(int8_t)(-ft.stride)) | ((uint32_t)(uint8_t)(int8_t)(ft.stride - 1) << 8) |
                         (1u << 16));
@@ -916,11 +914,8 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
               double2 Q = make_double2(1.0, 0.0);
               for (int f = lv.fbeg; f < lv.fend; ++f) {
                 const PlanFactor fd = s_fac[f];
-                int key = gather_key(fd, vcol + 4 * c);
-                const uint32_t cmask = (((fd.chain & 15u) * 0x00204081u) & 0x01010101u) * 0xffu;
-                const uint32_t s01 = (((fd.chain >> 4) & 15u) * 0x00204081u) & 0x01010101u;
-                const uint32_t p01 = (((fd.chain >> 8) & 15u) * 0x00204081u) & 0x01010101u;
-                key = (int)(((uint32_t)key & ~cmask) + (uint32_t)vm * s01 + (uint32_t)vp * p01);
+                const int key = (int)__byte_perm((uint32_t)gather_key(fd, vcol + 4 * c),
+                                                 (uint32_t)vm | ((uint32_t)vp << 8), fd.chain);
                 const int row = __dp4a(key, fd.crow, fd.base);
                 const int o = s_off[row] + __dp4a(key, 0x010000ff, (int)fd.dy);
                 Q = cmul(Q, s_ent[o]);
@@ -1034,17 +1029,15 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
           c_wb[lane] = inc - sz;
           if (lane == 0) c_wb[32] = E;
           __syncwarp();
-          // (2) pair table.  First the chain factors' keys with their chain bytes cleared
-          // (gathered once per chain from the emitter's value bytes), then one entry per
+          // (2) pair table.  First the chain factors' keys (gathered once per chain from the
+          // emitter's value bytes; the chain bytes are replaced below), then one entry per
           // lane per round: W_m(v_{m-1}, v_m) = product of level m's factors.
           const int fc0 = s_lev[jbq].fbeg, nfc = NF - fc0;  // chain factors come last
           uint32_t *ckey = reinterpret_cast<uint32_t *>(cPs);  // (the suffix table comes later)
           const bool pre = nfc <= 2 * LOFP_SUF_ENTRIES;
           if (pre) {
             for (int f = lane; f < nfc; f += 32) {
-              const PlanFactor fd = s_fac[fc0 + f];
-              const uint32_t cmask = (((fd.chain & 15u) * 0x00204081u) & 0x01010101u) * 0xffu;
-              ckey[f] = (uint32_t)gather_key(fd, lbe) & ~cmask;
+              ckey[f] = (uint32_t)gather_key(s_fac[fc0 + f], lbe);
             }
             __syncwarp();
           }
@@ -1054,22 +1047,15 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
               if (m + st < Mb && c_wb[m + st] <= w) m += st;
             const int rm = c_r[m], rel = w - c_wb[m];
             const int ii = (int)(((float)rel + 0.5f) * c_inv[m]), kk = rel - ii * rm;
-            const int vm = c_lo[m] + kk, vp = m > 0 ? c_lo[m - 1] + ii : 0;
+            const uint32_t vmp = (uint32_t)(c_lo[m] + kk) | ((uint32_t)(m > 0 ? c_lo[m - 1] + ii : 0) << 8);
             const PlanLevel lv = s_lev[jbq + m];
             double2 Q = make_double2(1.0, 0.0);
+#pragma unroll 1
             for (int f = lv.fbeg; f < lv.fend; ++f) {
               const PlanFactor fd = s_fac[f];
-              // 4 flag bits -> one 0x01 per flagged byte (bit i moves to bit 8 i)
-              const uint32_t s01 = (((fd.chain >> 4) & 15u) * 0x00204081u) & 0x01010101u;
-              const uint32_t p01 = (((fd.chain >> 8) & 15u) * 0x00204081u) & 0x01010101u;
-              uint32_t base;
-              if (pre) {
-                base = ckey[f - fc0];
-              } else {
-                const uint32_t cmask = (((fd.chain & 15u) * 0x00204081u) & 0x01010101u) * 0xffu;
-                base = (uint32_t)gather_key(fd, lbe) & ~cmask;
-              }
-              const int key = (int)(base + (uint32_t)vm * s01 + (uint32_t)vp * p01);
+              // the chain bytes of the key: v_m and v_{m-1} put in by one byte permutation
+              const uint32_t base = pre ? ckey[f - fc0] : (uint32_t)gather_key(fd, lbe);
+              const int key = (int)__byte_perm(base, vmp, fd.chain);
               const int row = __dp4a(key, fd.crow, fd.base);
               const int o = s_off[row] + __dp4a(key, 0x010000ff, (int)fd.dy);
               Q = cmul(Q, s_ent[o]);
