@@ -1087,6 +1087,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
           // digit m of c = floor(c / pv_m) mod r_m, pv_m = Ct / pinc_m (place value)
           if (lane < t) c_pv[lane] = __float_as_int(__fdividef((float)pinc, (float)Ctd));  // 1 / pv_m
           __syncwarp();
+#pragma unroll 1
           for (int m = 0; m < t; ++m) {
             const float ipv = __int_as_float(c_pv[m]), ir = c_inv[m];
             const int rm = c_r[m];
@@ -1131,6 +1132,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             const bool act = cc < Ct;
             if (c0 > 0) {  // advance this lane's prefix index by 32 (mixed-radix add)
               int carry = 0;
+#pragma unroll 1
               for (int m = t - 1; m >= 0; --m) {
                 int d = c_dig[m * 32 + lane] + c_u32[m] + carry;
                 carry = d >= c_r[m];
