@@ -457,13 +457,12 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
   // chain engine scratch: pair table W, per-lane suffix products, per-digit arrays
   double2 *cW = mbP + 2;                                     // [LOFP_W_MAX]
   double2 *cPs = cW + LOFP_W_MAX;                            // [LOFP_SUF_ENTRIES] suffix table
-  int *c_lo = reinterpret_cast<int *>(cPs + LOFP_SUF_ENTRIES);  // [32]
-  int *c_r = c_lo + 32;                                      // [32]
-  int *c_wb = c_r + 32;                                      // [33]
-  int *c_pv = c_wb + 33;                                     // [32] prefix place values
-  float *c_inv = reinterpret_cast<float *>(c_pv + 32);       // [32] 1 / range size
-  int *c_u32 = reinterpret_cast<int *>(c_inv + 32);              // [32] digits of the stride 32
-  unsigned char *c_dig = reinterpret_cast<unsigned char *>(c_u32 + 32);  // [32 digits][32 lanes]
+  // per chain level m: (range r_m, digit m of the stride 32, pair-table block base, 1 / r_m)
+  int4 *c_lv = reinterpret_cast<int4 *>(cPs + LOFP_SUF_ENTRIES);  // [33]
+  int *c_lo = reinterpret_cast<int *>(c_lv + 33);            // [32] range low ends
+  int *c_wb = c_lo + 32;                                     // [33] block bases (binary search)
+  int *c_pv = c_wb + 33;                                     // [32] 1 / prefix place values
+  unsigned char *c_dig = reinterpret_cast<unsigned char *>(c_pv + 32);  // [32 digits][32 lanes]
   // small-chain batch: per emitting lane (column) its chain's ranges and table offsets
   double2 *sc_proot = reinterpret_cast<double2 *>(
       (reinterpret_cast<uintptr_t>(c_dig + 32 * 32) + 15) & ~uintptr_t(15));  // [32] root products
@@ -1023,9 +1022,8 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
           }
           LOFP_PHASE(1);
           c_lo[lane] = clo;
-          c_r[lane] = crr;
           // reciprocal of the range: floor(n / r) = (int)((n + 0.5) * inv) exactly for n < 2^12
-          c_inv[lane] = __fdividef(1.0f, (float)crr);
+          c_lv[lane] = make_int4(crr, 0, inc - sz, __float_as_int(__fdividef(1.0f, (float)crr)));
           c_wb[lane] = inc - sz;
           if (lane == 0) c_wb[32] = E;
           __syncwarp();
@@ -1045,8 +1043,9 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             int m = 0;
             for (int st = 16; st > 0; st >>= 1)
               if (m + st < Mb && c_wb[m + st] <= w) m += st;
-            const int rm = c_r[m], rel = w - c_wb[m];
-            const int ii = (int)(((float)rel + 0.5f) * c_inv[m]), kk = rel - ii * rm;
+            const int4 lvm = c_lv[m];
+            const int rm = lvm.x, rel = w - lvm.z;
+            const int ii = (int)(((float)rel + 0.5f) * __int_as_float(lvm.w)), kk = rel - ii * rm;
             const uint32_t vmp = (uint32_t)(c_lo[m] + kk) | ((uint32_t)(m > 0 ? c_lo[m - 1] + ii : 0) << 8);
             const PlanLevel lv = s_lev[jbq + m];
             double2 Q = make_double2(1.0, 0.0);
@@ -1089,13 +1088,14 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
           __syncwarp();
 #pragma unroll 1
           for (int m = 0; m < t; ++m) {
-            const float ipv = __int_as_float(c_pv[m]), ir = c_inv[m];
-            const int rm = c_r[m];
+            const int4 lvm = c_lv[m];
+            const float ipv = __int_as_float(c_pv[m]), ir = __int_as_float(lvm.w);
+            const int rm = lvm.x;
             const int q = (int)(((float)lane + 0.5f) * ipv), q32 = (int)((32.0f + 0.5f) * ipv);
             const int d = q - (int)(((float)q + 0.5f) * ir) * rm;
             const int d32 = q32 - (int)(((float)q32 + 0.5f) * ir) * rm;
             c_dig[m * 32 + lane] = (unsigned char)d;
-            if (lane == 0) c_u32[m] = d32;  // digit m of 32
+            if (lane == 0) reinterpret_cast<int *>(c_lv + m)[1] = d32;  // digit m of 32
           }
           LOFP_PHASE(3);
           // suffix table: entry s (digit t most significant) = prod_{m = t+1}^{Mb-1} W_m;
@@ -1104,18 +1104,21 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             const int s0 = sbase + lane, s1 = sbase + lane + 32;
             int rem0 = s0, rem1 = s1;
             double2 Q0 = make_double2(1.0, 0.0), Q1 = Q0;
+            int4 lvm = c_lv[Mb - 1];
             for (int m = Mb - 1; m > t; --m) {  // decode from the last digit
-              const int rm = c_r[m], rp = c_r[m - 1];
-              const float im = c_inv[m], ip = c_inv[m - 1];
+              const int4 lvp = c_lv[m - 1];
+              const int rm = lvm.x, rp = lvp.x;
+              const float im = __int_as_float(lvm.w), ip = __int_as_float(lvp.w);
               const int q0 = (int)(((float)rem0 + 0.5f) * im), q1 = (int)(((float)rem1 + 0.5f) * im);
               const int cur0 = rem0 - q0 * rm, cur1 = rem1 - q1 * rm;
               rem0 = q0;
               rem1 = q1;
               const int nx0 = rem0 - (int)(((float)rem0 + 0.5f) * ip) * rp;  // digit m-1
               const int nx1 = rem1 - (int)(((float)rem1 + 0.5f) * ip) * rp;
-              const int blk_m = c_wb[m + 1] - c_wb[m];  // (lane 31's c_wb = E past the chain)
-              const double2 w0 = cW[c_wb[m] + min(nx0 * rm + cur0, blk_m - 1)];
-              const double2 w1 = cW[c_wb[m] + min(nx1 * rm + cur1, blk_m - 1)];
+              const int blk_m = rp * rm;  // the level's pair-table block (m >= 1)
+              const double2 w0 = cW[lvm.z + min(nx0 * rm + cur0, blk_m - 1)];
+              const double2 w1 = cW[lvm.z + min(nx1 * rm + cur1, blk_m - 1)];
+              lvm = lvp;
               Q0 = cmul(Q0, w0);
               Q1 = cmul(Q1, w1);
               if (COUNTED) ncm += (s0 < Rsi) + (s1 < Rsi);
@@ -1125,7 +1128,8 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
           }
           __syncwarp();
           LOFP_PHASE(7);
-          const int rt = t < Mb ? c_r[t] : 1;
+          const int4 lvt = c_lv[min(t, Mb - 1)];
+          const int rt = t < Mb ? lvt.x : 1;
           const int blk = Rsi / rt;  // suffix entries per value of digit t
           for (long long c0 = 0; c0 < Ct; c0 += 32) {
             const long long cc = c0 + lane;
@@ -1134,9 +1138,10 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
               int carry = 0;
 #pragma unroll 1
               for (int m = t - 1; m >= 0; --m) {
-                int d = c_dig[m * 32 + lane] + c_u32[m] + carry;
-                carry = d >= c_r[m];
-                d -= carry ? c_r[m] : 0;
+                const int2 rd = *reinterpret_cast<const int2 *>(c_lv + m);  // (r_m, digit of 32)
+                int d = c_dig[m * 32 + lane] + rd.y + carry;
+                carry = d >= rd.x;
+                d -= carry ? rd.x : 0;
                 c_dig[m * 32 + lane] = (unsigned char)d;
               }
             }
@@ -1144,7 +1149,8 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             int vprev = 0;
             for (int m = 0; m < t; ++m) {
               const int d = c_dig[m * 32 + lane];
-              const int idx = c_wb[m] + (m > 0 ? vprev * c_r[m] : 0) + d;
+              const int4 lv = c_lv[m];
+              const int idx = lv.z + (m > 0 ? vprev * lv.x : 0) + d;
               P = cmul(P, cW[idx]);
               if (COUNTED) ncm += act;
               vprev = d;  // digit (offset from the level's low end)
@@ -1158,7 +1164,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
               continue;
             }
             for (int dt = 0; dt < rt; ++dt) {
-              const double2 Q = cmul(P, cW[c_wb[t] + (t > 0 ? vprev * rt : 0) + dt]);
+              const double2 Q = cmul(P, cW[lvt.z + (t > 0 ? vprev * rt : 0) + dt]);
               if (COUNTED) ncm += act;
               const double2 *sf = cPs + dt * blk;
               double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
