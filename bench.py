@@ -41,17 +41,21 @@ def parse():
     p.add_argument("--impl", choices=["lofp", "reference"], default="lofp")
     p.add_argument("--config", type=int, default=4)
     p.add_argument("--outputs", type=int, default=0, help="limit the batch to its first N outputs")
+    p.add_argument("--hero", action="store_true",
+                   help="configs[4] hero sample: its 8 largest uncapped outputs (2.2e11-2.5e11 paths each)")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-paths", type=float, default=6e7, help="paths in the cpu_baseline sample")
     return p.parse_args()
 
 
-def workload(idx: int, limit: int = 0):
+def workload(idx: int, limit: int = 0, hero: bool = False):
     import lofp_inputs as li
     c = li.config(idx)
     d = np.load(os.path.join(DATA, f"cfg{idx}.npz"))
-    if "T_cond" in d.files:
+    if hero:  # uncapped single-output scaling sample (configs[4] only)
+        T, P, kind = d["T_hero"].astype(np.int32), d["P_hero"].astype(np.uint64), "hero (uncapped)"
+    elif "T_cond" in d.files:
         T, P, kind = d["T_cond"].astype(np.int32), d["P_cond"].astype(np.uint64), "conditioned"
     else:
         T, P, kind = d["T_literal"].astype(np.int32), d["P_literal"].astype(np.uint64), "literal"
@@ -123,11 +127,11 @@ def cpu_sample(c, T, P, budget):
     return sel
 
 
-def run_oracle(c, T, P, sel):
+def run_oracle(c, T, P, sel, threads=0):
     import oracle
     oracle.build()
     t0 = time.perf_counter()
-    oracle.path_sum(c.M, c.layers, c.S, T[sel])
+    oracle.path_sum(c.M, c.layers, c.S, T[sel], threads=threads)
     dt = time.perf_counter() - t0
     return float(P[sel].astype(np.float64).sum()), dt
 
@@ -136,7 +140,7 @@ def reference_arm(args, rank, world):
     """--impl reference: the CPU oracle as it stands, on the host cores, rank 0 only."""
     if rank != 0:
         return
-    c, T, P, kind = workload(args.config, args.outputs)
+    c, T, P, kind = workload(args.config, args.outputs)  # (no hero sample: hours on the CPU)
     sel = cpu_sample(c, T, P, args.cpu_paths / 4)
     cores = os.cpu_count() or 1
     for _ in range(args.warmup):
@@ -180,7 +184,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    c, T_all, P_all, kind = workload(args.config, args.outputs)
+    c, T_all, P_all, kind = workload(args.config, args.outputs, args.hero)
     mine = shard(P_all, rank, world)
     T, P = T_all[mine], P_all[mine]
     circ = Circuit(c.M, c.layers)
@@ -275,11 +279,16 @@ def main():
                 "kernel_ms": enum_mean, "kernel_share_of_step": enum_mean / (t_local / args.steps)}
 
     cpu = None
-    if not args.no_cpu and world == 1:
+    if not args.no_cpu and world == 1 and not args.hero:  # (hero trees: hours on the CPU)
         sel = cpu_sample(c, T_all, P_all, args.cpu_paths)
         p, dt = run_oracle(c, T_all, P_all, sel)
+        # one core (after the all-core run: the oracle's thread setting persists)
+        sel1 = cpu_sample(c, T_all, P_all, args.cpu_paths / 24)
+        p1, dt1 = run_oracle(c, T_all, P_all, sel1, threads=1)
         cpu = {"value": p / dt, "unit": "paths/s", "cores": os.cpu_count(), "kind": "oracle",
-               "sample": f"{len(sel)} smallest-path outputs of the batch ({p:.3e} paths), {dt:.1f} s"}
+               "sample": f"{len(sel)} smallest-path outputs of the batch ({p:.3e} paths), {dt:.1f} s",
+               "one_core": {"value": p1 / dt1, "unit": "paths/s",
+                            "sample": f"{len(sel1)} smallest-path outputs ({p1:.3e} paths), {dt1:.1f} s"}}
 
     line = {
         "metric": "paths/s", "value": value, "unit": "paths/s", "n_gpus": world, "steps": args.steps,

@@ -11,6 +11,8 @@ Stored per config:
                          from stream 2 kept iff structurally reachable and
                          P(T) <= P_CAP, until the batch is full.
   draws                : how many stream-2 candidates were drawn to fill T_cond.
+  T_hero, P_hero       : configs[4] only: the 8 largest-P reachable outputs of 32768
+                         uncapped stream-3 draws (single-output scaling).
 
 usage: python scripts/make_batches.py [config indices...]
 """
@@ -71,6 +73,24 @@ def conditioned(c, chunk):
     return np.array(keepT, dtype=np.uint8), np.array(keepP, dtype=np.uint64), draws
 
 
+def hero(c, n=8, chunks=8, chunk=4096):
+    """Uncapped single-output scaling sample: the n largest-P structurally
+    reachable outputs among chunks x chunk draws of stream 3 (same distribution as the
+    conditioned batch, no path cap)."""
+    rng = np.random.default_rng([c.seed, 3])
+    src = [i for i in range(c.M) if c.S[i] > 0]
+    Ts, Ps = [], []
+    for _ in range(chunks):
+        T = li.displaced_patterns(c.M, src, 4, chunk, rng)[0]
+        cand = T[oracle.reachable(c.M, c.layers, c.S, T)]
+        if len(cand):
+            Ts.append(cand)
+            Ps.append(counts_u64(c, cand))
+    T, P = np.concatenate(Ts), np.concatenate(Ps)
+    top = np.argsort(P.astype(np.float64), kind="stable")[::-1][:n]
+    return T[top].astype(np.uint8), P[top], chunks * chunk
+
+
 def main(which):
     os.makedirs(os.path.join(ROOT, "data"), exist_ok=True)
     for i in which:
@@ -83,6 +103,9 @@ def main(which):
             chunk = {2: 1 << 20, 3: 4096, 4: 4096}[i]
             Tc, Pc, draws = conditioned(c, chunk)
             out.update(T_cond=Tc, P_cond=Pc, draws=np.int64(draws))
+        if i == 4:
+            Th, Ph, hd = hero(c)
+            out.update(T_hero=Th, P_hero=Ph, hero_draws=np.int64(hd))
         path = os.path.join(ROOT, "data", f"cfg{i}.npz")
         np.savez_compressed(path, **out)
         msg = f"cfg{i}: literal {len(T)} (sum P = {int(P.astype(object).sum()):.3e})"

@@ -159,6 +159,22 @@ def test_conditioned_batch_full_size_sampled_values(lofp, idx):
     assert ok, err
 
 
+def test_hero_outputs_single_output_scaling(lofp):
+    """configs[4] uncapped 'hero' sample: the 8 largest-P reachable outputs of
+    32768 draws, 2.2e11-2.5e11 paths each, so every output's tree is split over the whole
+    GPU through the work queue.  Exact path counts against the oracle's transfer count,
+    values against the Ryser permanent (eq. (1) = Per(U[T,S]) / sqrt(prod S! T!))."""
+    c = li.config(4)
+    d = load(4)
+    T = d["T_hero"].astype(np.int32)
+    got, cnt, st, _ = run(lofp, c.M, c.layers, c.S, T)
+    assert np.array_equal(cnt, d["P_hero"])
+    assert st["spills"] > 0  # the trees were shared between warps
+    ref = oracle.amplitudes_permanent(c.M, c.layers, c.S, T)
+    ok, err = tol_ok(got, ref)
+    assert ok, err
+
+
 def test_config2_literal_structural_zeros(lofp):
     c = li.config(2)
     d = load(2)
