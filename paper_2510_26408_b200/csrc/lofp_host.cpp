@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -331,8 +332,32 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
     // scatter entries past a level's own list: vals, keys and stack follow inside the
     // warp's region, so those reads never leave it)
     a.plan_smem = (int)round16(sizeof(PlanHead) + (size_t)(maxL + maxF) * 16 + 2 * (size_t)maxS);
-    a.chain_on = hc->nchain > 0 && !std::getenv("LOFP_NO_CHAIN") &&
-                 (2ull * (unsigned long long)hc->nchain >= hc->nfeas || std::getenv("LOFP_FORCE_CHAIN"));
+    // Chain engine (R17): on when most outputs have chains of >= LOFP_CHAIN_RBOX box paths.
+    // Otherwise, if most outputs have the chain structure with chains of moderate size
+    // (geometric-mean box >= 2^LOFP_SHORT_CHAIN_LOG2 paths), every such output gets the
+    // engine with the short chains batched (R20; the plans are rebuilt with those
+    // thresholds).  Environment overrides (tests) disable this choice.
+    const bool env_chain = std::getenv("LOFP_NO_CHAIN") || std::getenv("LOFP_FORCE_CHAIN") ||
+                           std::getenv("LOFP_CHAIN_RBOX") || std::getenv("LOFP_CHAIN_RMIN") ||
+                           std::getenv("LOFP_SMALL_PATHS");
+    const double mlog = hc->nchain_ok > 0 ? (double)hc->rbox_log16 / 16.0 / hc->nchain_ok : 0.0;
+    bool short_chains = false;
+    if (!env_chain && 2ull * (unsigned long long)hc->nchain < hc->nfeas &&
+        2ull * (unsigned long long)hc->nchain_ok >= hc->nfeas && mlog >= LOFP_SHORT_CHAIN_LOG2) {
+      a.chain_rbox = 1.0;
+      a.chain_rmin = 1;
+      a.small_paths = 256;
+      // the plan kernel counts the feasible outputs and the outstanding work: reset those
+      CK(cudaMemsetAsync(reinterpret_cast<char *>(a.ctr) + offsetof(Counters, nfeas), 0, sizeof(unsigned long long),
+                         stream), "reset counters");
+      CK(cudaMemsetAsync(reinterpret_cast<char *>(a.ctr) + offsetof(Counters, outstanding), 0,
+                         sizeof(unsigned long long), stream), "reset counters");
+      CK(lofp_launch_plan(a, stream), "plan kernel (short chains)");
+      short_chains = true;
+    }
+    a.chain_on = short_chains ||
+                 (hc->nchain > 0 && !std::getenv("LOFP_NO_CHAIN") &&
+                  (2ull * (unsigned long long)hc->nchain >= hc->nfeas || std::getenv("LOFP_FORCE_CHAIN")));
     // key words per lane: every attached factor (none while the engine is on)
     a.maxfac = a.chain_on ? 0 : maxF;
     (void)maxK;

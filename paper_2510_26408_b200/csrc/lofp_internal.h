@@ -31,6 +31,7 @@
 #define LOFP_W_MAX 128         // chain pair-table entries per warp (else: plain DFS)
 #ifndef LOFP_CHAIN_RMIN
 #define LOFP_CHAIN_RMIN 32     // fewest paths of a chain enumerated by the engine (else: plain DFS)
+#define LOFP_SHORT_CHAIN_LOG2 7.0  // short-chain mode: geometric-mean chain box >= 2^this paths
 #endif
 #define LOFP_SUF_ENTRIES 64     // chain suffix-table entries per warp
 #define LOFP_ENUM_MAX_THREADS 640  // largest block of the enumeration kernel
@@ -120,6 +121,8 @@ struct Counters {
   int32_t maxS;                    // largest per-output scatter-list length
   int32_t maxK;                    // largest per-output count of non-chain factors
   int32_t nchain;                  // outputs whose plan has a chain
+  int32_t nchain_ok;               // outputs whose last free layer has the chain structure
+  unsigned long long rbox_log16;   // sum over those of 16 log2(chain box product)
 };
 
 // A queued subtree: output `out`, levels [0, j0) fixed to prefix[], level j0 ranging

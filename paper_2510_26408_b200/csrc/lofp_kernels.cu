@@ -253,6 +253,10 @@ __global__ void lofp_plan_kernel(CallArgs a) {
     // the paths of every chain subtree of this output)
     double rbox = 1.0;
     for (int m = cand; m < L; ++m) rbox *= (double)((int)lev[m].hi - (int)lev[m].lo + 1);
+    if (ok && L - cand >= LOFP_CHAIN_MIN) {
+      atomicAdd(&a.ctr->nchain_ok, 1);
+      atomicAdd(&a.ctr->rbox_log16, (unsigned long long)(16.0 * log2(rbox)));
+    }
     if (ok && L - cand >= LOFP_CHAIN_MIN && rbox >= a.chain_rbox) jb = cand;
   }
   // scatter entries per level: those of chain factors go last (<= 15 per level, and the
