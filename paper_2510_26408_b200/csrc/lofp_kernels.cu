@@ -336,11 +336,6 @@ __global__ void lofp_plan_kernel(CallArgs a) {
 // ---------------------------------------------------------------------------
 // path enumeration
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ unsigned lanemask_lt() {
-  unsigned m;
-  asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-  return m;
-}
 
 __device__ __forceinline__ unsigned long long vload(const unsigned long long *p) {
   return *reinterpret_cast<const volatile unsigned long long *>(p);
@@ -912,7 +907,6 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
               const int rm = sc_r[m * 32 + c], rel = loc - sc_wb[m * 32 + c];
               const int ii = (int)(((float)rel + 0.5f) * __frcp_rn((float)rm)), kk = rel - ii * rm;
               const int vm = sc_lo[m * 32 + c] + kk, vp = m > 0 ? sc_lo[(m - 1) * 32 + c] + ii : 0;
-              const unsigned char *kbc = kcol + 4 * c;
               const PlanLevel lv = s_lev[jbq + m];
               double2 Q = make_double2(1.0, 0.0);
               for (int f = lv.fbeg; f < lv.fend; ++f) {
@@ -966,7 +960,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
         while (pend) {
           const int em = __ffs(pend) - 1;
           pend &= pend - 1;
-          const unsigned char *lbe = vcol + 4 * em, *kbe = kcol + 4 * em;
+          const unsigned char *lbe = vcol + 4 * em;
           const double2 Proot = make_double2(__shfl_sync(FULL, Pb.x, em), __shfl_sync(FULL, Pb.y, em));
           const int Mb = L - jbq;
           int clo = 0, crr = 1;
