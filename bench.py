@@ -305,7 +305,7 @@ def main():
         "gpu_launches": 4 * args.steps,
         "clocks": clk,
         "stats": {k: vst[k] for k in ("feasible", "items", "spills", "donations", "overflows", "levels",
-                                      "table_entries", "smem_bytes", "grid_blocks", "block_threads")},
+                                      "table_entries", "smem_bytes", "grid_blocks", "block_threads", "engine")},
     }
     print(json.dumps(line), flush=True)
     if world > 1:

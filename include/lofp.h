@@ -138,6 +138,8 @@ typedef struct {
   int32_t bad_rows;       /* rows with a negative entry (their amplitude is NaN) */
   int32_t max_factors;    /* largest number of attached BS elements of one output */
   int32_t max_scatter;    /* largest number of key bytes written per level value, one output */
+  int32_t engine;         /* 0: depth-first walk only; 1: chain engine (R17); 2: chain engine
+                             with the short chains batched (short-chain mode) */
   float enum_ms;          /* device time of the enumeration kernel (CUDA events) */
   float total_ms;         /* device time from the first to the last kernel */
 } lofp_run_stats;

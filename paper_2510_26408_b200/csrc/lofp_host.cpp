@@ -387,6 +387,7 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
     ctx->stats.smem_bytes = (int32_t)smem;
     ctx->stats.max_factors = maxF;
     ctx->stats.max_scatter = maxS;
+    ctx->stats.engine = a.chain_on ? (a.small_paths > 0 ? 2 : 1) : 0;
     ctx->stats.grid_blocks = grid;
     ctx->stats.block_threads = block;
     CK(lofp_launch_enum(a, counts != nullptr, grid, block, smem, stream), "enumeration kernel");

@@ -355,3 +355,18 @@ def test_paper_correctness_protocol_gpu(lofp, case):
     ref, leaves = oracle.path_sum(6, layers, S, T, return_leaves=True)
     assert np.array_equal(cnt, leaves)
     assert tol_ok(got, ref)[0]
+
+
+@pytest.mark.parametrize("idx,engine", [(2, 2), (3, 0), (4, 1)])
+def test_engine_choice_per_batch(lofp, idx, engine):
+    """The host picks the enumeration mode from the batch's plans:
+    configs[4] the chain engine, configs[2] the short-chain mode, configs[3] the walk; the
+    values of the first outputs match the Ryser permanent in every mode."""
+    c = li.config(idx)
+    d = load(idx)
+    T = d["T_cond"][:64].astype(np.int32)
+    got, _, st, _ = run(lofp, c.M, c.layers, c.S, T, counted=False)
+    assert st["engine"] == engine
+    ref = oracle.amplitudes_permanent(c.M, c.layers, c.S, T[:8])
+    ok, err = tol_ok(got[:8], ref)
+    assert ok, err
