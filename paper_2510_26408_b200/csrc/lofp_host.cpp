@@ -332,7 +332,8 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
     // scatter entries past a level's own list: vals, keys and stack follow inside the
     // warp's region, so those reads never leave it)
     a.plan_smem = (int)round16(sizeof(PlanHead) + (size_t)(maxL + maxF) * 16 + 2 * (size_t)maxS);
-    // Chain engine (R17): on when most outputs have chains of >= LOFP_CHAIN_RBOX box paths.
+    // Chain engine (R17): on when most outputs have chains of >= LOFP_CHAIN_MODE_RBOX box
+    // paths (then every output whose chain box is >= LOFP_CHAIN_RBOX gets its chain).
     // Otherwise, if most outputs have the chain structure with chains of moderate size
     // (geometric-mean box >= 2^LOFP_SHORT_CHAIN_LOG2 paths), every such output gets the
     // engine with the short chains batched (R20; the plans are rebuilt with those
@@ -342,7 +343,7 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
                            std::getenv("LOFP_SMALL_PATHS");
     const double mlog = hc->nchain_ok > 0 ? (double)hc->rbox_log16 / 16.0 / hc->nchain_ok : 0.0;
     bool short_chains = false;
-    if (!env_chain && 2ull * (unsigned long long)hc->nchain < hc->nfeas &&
+    if (!env_chain && 2ull * (unsigned long long)hc->nchain_big < hc->nfeas &&
         2ull * (unsigned long long)hc->nchain_ok >= hc->nfeas && mlog >= LOFP_SHORT_CHAIN_LOG2) {
       a.chain_rbox = 1.0;
       a.chain_rmin = 1;
@@ -357,7 +358,7 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
     }
     a.chain_on = short_chains ||
                  (hc->nchain > 0 && !std::getenv("LOFP_NO_CHAIN") &&
-                  (2ull * (unsigned long long)hc->nchain >= hc->nfeas || std::getenv("LOFP_FORCE_CHAIN")));
+                  (2ull * (unsigned long long)hc->nchain_big >= hc->nfeas || std::getenv("LOFP_FORCE_CHAIN")));
     // key words per lane: every attached factor (none while the engine is on)
     a.maxfac = a.chain_on ? 0 : maxF;
     (void)maxK;

@@ -24,13 +24,14 @@
 #define LOFP_ITEM_PREFIX 224  // prefix bytes an item can carry (>= LOFP_MAX_LEVELS)
 #define LOFP_SPILL_MIN_DIST 6  // global-queue spills only for branches >= this many levels above the leaf level
 #define LOFP_CHAIN_MIN 4       // shortest chain handed to the chain engine
-#define LOFP_CHAIN_RBOX 1024   // smallest box product (paths bound) of an output's chain
+#define LOFP_CHAIN_RBOX 256    // smallest box product (paths bound) of an output's chain
+#define LOFP_CHAIN_MODE_RBOX 1024.0  // batch mode: chain engine if most outputs' chain box >= this
 #define LOFP_SMALL_LEVELS 16   // chains with <= this many levels and
 #define LOFP_SMALL_PATHS 0     // < this many paths are enumerated in batches (0: off; the
                                // batched mode is slower than the walk on the configs measured)
 #define LOFP_W_MAX 128         // chain pair-table entries per warp (else: plain DFS)
 #ifndef LOFP_CHAIN_RMIN
-#define LOFP_CHAIN_RMIN 32     // fewest paths of a chain enumerated by the engine (else: plain DFS)
+#define LOFP_CHAIN_RMIN 8      // fewest paths of a chain enumerated by the engine (else: plain DFS)
 #define LOFP_SHORT_CHAIN_LOG2 7.0  // short-chain mode: geometric-mean chain box >= 2^this paths
 #endif
 #define LOFP_SUF_ENTRIES 64     // chain suffix-table entries per warp
@@ -122,6 +123,7 @@ struct Counters {
   int32_t maxK;                    // largest per-output count of non-chain factors
   int32_t nchain;                  // outputs whose plan has a chain
   int32_t nchain_ok;               // outputs whose last free layer has the chain structure
+  int32_t nchain_big;              // those whose chain box >= LOFP_CHAIN_MODE_RBOX
   unsigned long long rbox_log16;   // sum over those of 16 log2(chain box product)
 };
 

@@ -255,6 +255,7 @@ __global__ void lofp_plan_kernel(CallArgs a) {
     for (int m = cand; m < L; ++m) rbox *= (double)((int)lev[m].hi - (int)lev[m].lo + 1);
     if (ok && L - cand >= LOFP_CHAIN_MIN) {
       atomicAdd(&a.ctr->nchain_ok, 1);
+      if (rbox >= LOFP_CHAIN_MODE_RBOX) atomicAdd(&a.ctr->nchain_big, 1);
       atomicAdd(&a.ctr->rbox_log16, (unsigned long long)(16.0 * log2(rbox)));
     }
     if (ok && L - cand >= LOFP_CHAIN_MIN && rbox >= a.chain_rbox) jb = cand;
