@@ -302,7 +302,7 @@ def main():
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": 4 * args.steps,
+        "gpu_launches": int(vst["launches"]) * args.steps,  # this library's kernels per call
         "clocks": clk,
         "stats": {k: vst[k] for k in ("feasible", "items", "spills", "donations", "overflows", "levels",
                                       "table_entries", "smem_bytes", "grid_blocks", "block_threads", "engine")},

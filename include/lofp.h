@@ -140,6 +140,7 @@ typedef struct {
   int32_t max_scatter;    /* largest number of key bytes written per level value, one output */
   int32_t engine;         /* 0: depth-first walk only; 1: chain engine (R17); 2: chain engine
                              with the short chains batched (short-chain mode) */
+  int32_t launches;       /* kernels launched by the call (prep, tables, plan(s), enumeration) */
   float enum_ms;          /* device time of the enumeration kernel (CUDA events) */
   float total_ms;         /* device time from the first to the last kernel */
 } lofp_run_stats;

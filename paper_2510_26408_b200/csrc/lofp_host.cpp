@@ -250,6 +250,7 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
   CK(cudaMemcpyAsync(ctx->d_cumS.p, cs, M + 1, cudaMemcpyHostToDevice, stream), "upload cumS");
   CK(cudaMemsetAsync(a.ctr, 0, sizeof(Counters), stream), "reset counters");
   CK(lofp_launch_prep(a, stream), "prep kernel");
+  ctx->stats.launches += a.B > 0 ? 1 : 0;
   // (sync 1) the batch's per-mode maximum sizes the tables
   CK(ctx->h_ctr.ensure(sizeof(Counters)), "alloc pinned counters");
   CK(cudaMemcpyAsync(ctx->h_ctr.p, a.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, stream), "read tmax");
@@ -318,6 +319,7 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
 
   CK(lofp_launch_tables(a, stream), "table kernel");
   CK(lofp_launch_plan(a, stream), "plan kernel");
+  ctx->stats.launches += (a.nentries > 0 ? 1 : 0) + (a.B > 0 ? 1 : 0);
   // (sync 2) the largest per-output plan sizes the enumeration kernel's shared memory
   CK(cudaMemcpyAsync(ctx->h_ctr.p, a.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, stream), "read plan sizes");
   CK(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
@@ -354,6 +356,7 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
       CK(cudaMemsetAsync(reinterpret_cast<char *>(a.ctr) + offsetof(Counters, outstanding), 0,
                          sizeof(unsigned long long), stream), "reset counters");
       CK(lofp_launch_plan(a, stream), "plan kernel (short chains)");
+      ++ctx->stats.launches;
       short_chains = true;
     }
     a.chain_on = short_chains ||
@@ -392,6 +395,7 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
     ctx->stats.grid_blocks = grid;
     ctx->stats.block_threads = block;
     CK(lofp_launch_enum(a, counts != nullptr, grid, block, smem, stream), "enumeration kernel");
+    ++ctx->stats.launches;
   }
   CK(cudaEventRecord(ctx->ev_enum1, stream), "cudaEventRecord");
   CK(cudaMemcpyAsync(ctx->h_ctr.p, a.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, stream), "read counters");

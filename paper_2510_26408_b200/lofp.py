@@ -31,6 +31,7 @@ class lofp_run_stats(ctypes.Structure):
                 ("smem_bytes", ctypes.c_int32), ("grid_blocks", ctypes.c_int32),
                 ("block_threads", ctypes.c_int32), ("bad_rows", ctypes.c_int32),
                 ("max_factors", ctypes.c_int32), ("max_scatter", ctypes.c_int32), ("engine", ctypes.c_int32),
+                ("launches", ctypes.c_int32),
                 ("enum_ms", ctypes.c_float), ("total_ms", ctypes.c_float)]
 
 
