@@ -1099,8 +1099,28 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
           LOFP_PHASE(3);
           // suffix table: entry s (digit t most significant) = prod_{m = t+1}^{Mb-1} W_m;
           // entries lane and lane + 32 are built together (two independent chains)
-          for (int sbase = 0; sbase < Rsi; sbase += 64) {
-            const int s0 = sbase + lane, s1 = sbase + lane + 32;
+          if (Rsi <= 32) {  // one entry per lane
+            const int s0 = lane;
+            int rem0 = s0;
+            double2 Q0 = make_double2(1.0, 0.0);
+            int4 lvm = c_lv[Mb - 1];
+            for (int m = Mb - 1; m > t; --m) {  // decode from the last digit
+              const int4 lvp = c_lv[m - 1];
+              const int rm = lvm.x, rp = lvp.x;
+              const float im = __int_as_float(lvm.w), ip = __int_as_float(lvp.w);
+              const int q0 = (int)(((float)rem0 + 0.5f) * im);
+              const int cur0 = rem0 - q0 * rm;
+              rem0 = q0;
+              const int nx0 = rem0 - (int)(((float)rem0 + 0.5f) * ip) * rp;  // digit m-1
+              const int blk_m = rp * rm;  // the level's pair-table block (m >= 1)
+              const double2 w0 = cW[lvm.z + min(nx0 * rm + cur0, blk_m - 1)];
+              lvm = lvp;
+              Q0 = cmul(Q0, w0);
+              if (COUNTED) ncm += (s0 < Rsi);
+            }
+            if (s0 < Rsi) cPs[s0] = Q0;
+          } else {
+            const int s0 = lane, s1 = lane + 32;
             int rem0 = s0, rem1 = s1;
             double2 Q0 = make_double2(1.0, 0.0), Q1 = Q0;
             int4 lvm = c_lv[Mb - 1];
