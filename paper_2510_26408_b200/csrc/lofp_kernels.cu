@@ -1083,18 +1083,21 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
           // per-lane prefix digits (digit t-1 least significant) of the lane's first prefix
           // index (= lane), and the digits of the stride 32, for an incremental add per round:
           // digit m of c = floor(c / pv_m) mod r_m, pv_m = Ct / pinc_m (place value)
-          if (lane < t) c_pv[lane] = __float_as_int(__fdividef((float)pinc, (float)Ctd));  // 1 / pv_m
+          if (lane < t) {  // lane m: 1 / pv_m and digit m of the stride 32
+            const float ipv = __fdividef((float)pinc, (float)Ctd), ir = __fdividef(1.0f, (float)crr);
+            c_pv[lane] = __float_as_int(ipv);
+            const int q32 = (int)((32.0f + 0.5f) * ipv);
+            reinterpret_cast<int *>(c_lv + lane)[1] = q32 - (int)(((float)q32 + 0.5f) * ir) * crr;
+          }
           __syncwarp();
 #pragma unroll 1
           for (int m = 0; m < t; ++m) {
             const int4 lvm = c_lv[m];
             const float ipv = __int_as_float(c_pv[m]), ir = __int_as_float(lvm.w);
             const int rm = lvm.x;
-            const int q = (int)(((float)lane + 0.5f) * ipv), q32 = (int)((32.0f + 0.5f) * ipv);
+            const int q = (int)(((float)lane + 0.5f) * ipv);
             const int d = q - (int)(((float)q + 0.5f) * ir) * rm;
-            const int d32 = q32 - (int)(((float)q32 + 0.5f) * ir) * rm;
             c_dig[m * 32 + lane] = (unsigned char)d;
-            if (lane == 0) reinterpret_cast<int *>(c_lv + m)[1] = d32;  // digit m of 32
           }
           LOFP_PHASE(3);
           // suffix table: entry s (digit t most significant) = prod_{m = t+1}^{Mb-1} W_m;
