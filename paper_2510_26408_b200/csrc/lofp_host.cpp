@@ -367,7 +367,7 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
     (void)maxK;
     a.warp_bytes = (int)round16((size_t)a.plan_smem + (size_t)a.vals_slots * 32 + (size_t)a.maxfac * 128 +
                                 (size_t)(a.chain_on ? LOFP_STK_CHAIN : LOFP_STK) * 32 * 20 + 32 +
-                                (a.chain_on ? (size_t)LOFP_W_MAX * 16 + (size_t)LOFP_SUF_ENTRIES * 16 + 33 * 16 + 97 * 4 + 1024 +
+                                (a.chain_on ? (size_t)LOFP_W_MAX * 16 + (size_t)LOFP_SUF_ENTRIES * 16 + 33 * 16 + 65 * 4 + 1024 +
                                                   (a.small_paths > 0 ? 512 + 264 + 4 * 32 * LOFP_SMALL_LEVELS + 16 : 0)
                                             : 0));
     int grid = 0, block = 0;

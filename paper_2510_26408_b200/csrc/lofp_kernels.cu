@@ -457,10 +457,9 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
   // chain engine scratch: pair table W, per-lane suffix products, per-digit arrays
   double2 *cW = mbP + 2;                                     // [LOFP_W_MAX]
   double2 *cPs = cW + LOFP_W_MAX;                            // [LOFP_SUF_ENTRIES] suffix table
-  // per chain level m: (range r_m, digit m of the stride 32, pair-table block base, 1 / r_m)
+  // per chain level m: (range r_m, low end / digit m of the stride 32, pair-table block base, 1 / r_m)
   int4 *c_lv = reinterpret_cast<int4 *>(cPs + LOFP_SUF_ENTRIES);  // [33]
-  int *c_lo = reinterpret_cast<int *>(c_lv + 33);            // [32] range low ends
-  int *c_wb = c_lo + 32;                                     // [33] block bases (binary search)
+  int *c_wb = reinterpret_cast<int *>(c_lv + 33);            // [33] block bases (binary search)
   int *c_pv = c_wb + 33;                                     // [32] 1 / prefix place values
   unsigned char *c_dig = reinterpret_cast<unsigned char *>(c_pv + 32);  // [32 digits][32 lanes]
   // small-chain batch: per emitting lane (column) its chain's ranges and table offsets
@@ -1020,9 +1019,8 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             continue;
           }
           LOFP_PHASE(1);
-          c_lo[lane] = clo;
           // reciprocal of the range: floor(n / r) = (int)((n + 0.5) * inv) exactly for n < 2^12
-          c_lv[lane] = make_int4(crr, 0, inc - sz, __float_as_int(__fdividef(1.0f, (float)crr)));
+          c_lv[lane] = make_int4(crr, clo, inc - sz, __float_as_int(__fdividef(1.0f, (float)crr)));  // (.y: low end until the split)
           c_wb[lane] = inc - sz;
           if (lane == 0) c_wb[32] = E;
           __syncwarp();
@@ -1045,7 +1043,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             const int4 lvm = c_lv[m];
             const int rm = lvm.x, rel = w - lvm.z;
             const int ii = (int)(((float)rel + 0.5f) * __int_as_float(lvm.w)), kk = rel - ii * rm;
-            const uint32_t vmp = (uint32_t)(c_lo[m] + kk) | ((uint32_t)(m > 0 ? c_lo[m - 1] + ii : 0) << 8);
+            const uint32_t vmp = (uint32_t)(lvm.y + kk) | ((uint32_t)(m > 0 ? c_lv[m - 1].y + ii : 0) << 8);
             const PlanLevel lv = s_lev[jbq + m];
             double2 Q = make_double2(1.0, 0.0);
 #pragma unroll 1
