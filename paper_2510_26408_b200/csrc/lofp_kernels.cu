@@ -1088,7 +1088,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             reinterpret_cast<int *>(c_lv + lane)[1] = q32 - (int)(((float)q32 + 0.5f) * ir) * crr;
           }
           __syncwarp();
-#pragma unroll 2
+#pragma unroll 4
           for (int m = 0; m < t; ++m) {
             const int4 lvm = c_lv[m];
             const float ipv = __int_as_float(c_pv[m]), ir = __int_as_float(lvm.w);
