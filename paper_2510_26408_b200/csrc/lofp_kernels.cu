@@ -1167,6 +1167,7 @@ __global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(Cal
             }
             double2 P = Proot;
             int vprev = 0;
+#pragma unroll 4
             for (int m = 0; m < t; ++m) {
               const int d = c_dig[m * 32 + lane];
               const int4 lv = c_lv[m];
