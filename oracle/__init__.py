@@ -34,7 +34,7 @@ def build(force: bool = False) -> str:
     if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
         tmp = _LIB_PATH + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-std=gnu11",
-                               "-o", tmp, _SRC, "-lm"])
+                               "-o", tmp, _SRC, "-lquadmath", "-lm"])
         os.replace(tmp, _LIB_PATH)
     return _LIB_PATH
 
@@ -53,6 +53,8 @@ def _load():
         lib.oracle_circuit_unitary.argtypes = circ + [_f64p, _f64p, _f64p]
         lib.oracle_amplitude_permanent.argtypes = circ + [_f64p, _f64p, _i32p, c_long, _i32p, c_int, c_int, _f64p]
         lib.oracle_path_sum.argtypes = circ + [_f64p, _f64p, _i32p, c_long, _i32p, c_int, c_int, _f64p, _u64p]
+        lib.oracle_path_sum_gates.argtypes = circ + [_f64p, _f64p, _i32p, c_long, _i32p, c_int, c_int, c_int,
+                                                     _i32p, _i32p, _f64p, _f64p, _f64p, _u64p]
         lib.oracle_cone_sets.argtypes = circ + [c_int, c_int, _i32p, _i32p]
         lib.oracle_reachable.argtypes = circ + [_i32p, c_long, _i32p, c_int, _u8p]
         lib.oracle_count_paths.argtypes = circ + [_i32p, c_long, _i32p, c_int, c_long, _u64p, _i32p]
@@ -138,15 +140,27 @@ def amplitudes_permanent(M, layers, S, T, method: str = "ryser", threads: int = 
 PRUNE_NONE, PRUNE_CONE, PRUNE_BOX = 0, 1, 2
 
 
-def path_sum(M, layers, S, T, prune: int = PRUNE_BOX, threads: int = 0, return_leaves: bool = False):
-    """Eq. (1) for every row of T; optionally the number of valid paths summed."""
+def path_sum(M, layers, S, T, prune: int = PRUNE_BOX, threads: int = 0, return_leaves: bool = False,
+             gates=()):
+    """Eq. (1) for every row of T; optionally the number of valid paths summed.
+
+    ``gates``: photon-number-preserving phase gates, tuples
+    ``(mode, after_layer, a, b)`` multiplying every path by exp(i (a n + b n^2)), n = the
+    photons in ``mode`` after layer ``after_layer`` (0 = on the input).
+    """
     bpl, ma, mb, th, ph = _flatten(layers)
     S = _state(S, M)
     T = _batch(T, M)
     B = T.shape[0]
     out = np.zeros(B * 2)
     leaves = np.zeros(max(B, 1), dtype=np.uint64)
-    rc = _load().oracle_path_sum(M, len(layers), bpl, ma, mb, th, ph, S, B, T, prune, threads, out, leaves)
+    G = len(gates)
+    gm = np.array([g[0] for g in gates] or [0], dtype=np.int32)
+    gl = np.array([g[1] for g in gates] or [0], dtype=np.int32)
+    ga = np.array([g[2] for g in gates] or [0.0], dtype=np.float64)
+    gb = np.array([g[3] for g in gates] or [0.0], dtype=np.float64)
+    rc = _load().oracle_path_sum_gates(M, len(layers), bpl, ma, mb, th, ph, S, B, T, prune, threads, G,
+                                       gm, gl, ga, gb, out, leaves)
     _check(rc, "path_sum")
     amps = out.view(np.complex128)
     return (amps, leaves[:B].copy()) if return_leaves else amps

@@ -6,10 +6,14 @@
  * includes, links or calls anything here, and this file includes nothing from it.
  *
  * Everything is plain, slow and written from the paper (arXiv 2510.26408, PAPER.md
- * lines "P:n"); arithmetic is `long double` (x87 80-bit) complex.
+ * lines "P:n"); arithmetic is `long double` (x87 80-bit) complex, except the
+ * Appendix-A element, which is summed in __float128 (113-bit significand) because its
+ * alternating t-sum cancels catastrophically at high photon numbers (DESIGN.md reading
+ * R18: a precision choice only; the formula is the paper's).
  *
  *   oracle_bs_element      Appendix A, the printed factorial (y1-x2+t)!
- *                          of P:406 read as (x2-y1+t)! (reading R1).
+ *                          of P:406 read as (x2-y1+t)! (reading R1); summed
+ *                          in __float128 (reading R18).
  *   oracle_naive_permanent definition of the permanent, sum over all n!
  *                          permutations.
  *   oracle_ryser_permanent Ryser's formula in Gray-code order.
@@ -21,6 +25,9 @@
  *                          path.  prune 0 = none (final check against T only),
  *                          1 = the paper's past/future light-cone upper bounds,
  *                          2 = the cumulative light-cone box (reading R5).
+ *   oracle_path_sum_gates  the same recursion with photon-number-preserving phase gates
+ *                          exp(i (a n + b n^2)) on a mode after a layer (reading
+ *                          R19), multiplied in when the layer that precedes them ends.
  *   oracle_cone_bound      the per-waveguide bound of P:164.
  *   oracle_count_paths     exact number of valid paths (the number of terms of eq. (1))
  *                          by a transfer over cuts with explicit constraint checks
@@ -32,6 +39,7 @@
  */
 #include <complex.h>
 #include <math.h>
+#include <quadmath.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -44,6 +52,7 @@ typedef long double complex C;
 
 #define ORACLE_MAXM 256
 #define ORACLE_MAXD 64
+#define ORACLE_MAXN 120 /* photons (uint8-safe; the ABI's LOFP_MAX_PHOTONS) */
 
 /* ------------------------------------------------------------------------- */
 /* small helpers                                                              */
@@ -53,13 +62,6 @@ static R fact(int n) {
   R f = 1.0L;
   for (int i = 2; i <= n; ++i) f *= (R)i;
   return f;
-}
-
-/* z^n with integer n >= 0 and 0^0 = 1 (P:384 exponents may be zero at theta = 0, pi/2). */
-static C ipow(C z, int n) {
-  C r = 1.0L;
-  for (int i = 0; i < n; ++i) r *= z;
-  return r;
 }
 
 /* eq. bs_matrix: BS = [[cos t, -e^{-i phi} sin t], [e^{i phi} sin t, cos t]]. */
@@ -76,26 +78,62 @@ static void bs_matrix(double theta, double phi, C u[4]) {
  *   1/sqrt(x1!x2!y1!y2!) * sum_t [y1! x1! / (t! (y1-t)!)] [y2! x2! / ((x1-t)! (x2-y1+t)!)]
  *                         U11^t U12^(y1-t) U21^(x1-t) U22^(x2-y1+t)
  * with max(0, y1-x2, x1-y2) <= t <= min(x1, y1).  Zero when photon number
- * is not conserved ("valid path"). */
-static C bs_element_u(const C u[4], int x1, int x2, int y1, int y2) {
-  if (x1 < 0 || x2 < 0 || y1 < 0 || y2 < 0 || x1 + x2 != y1 + y2) return 0.0L;
+ * is not conserved ("valid path").  Summed term by term in __float128 (reading
+ * R18): the terms alternate in sign and exceed the result by up to ~1e17 at 120
+ * photons, which a 64-bit significand cannot absorb. */
+typedef __float128 Q;
+typedef __complex128 QC;
+
+static Q QFACT[ORACLE_MAXN + 1]; /* n! in __float128, filled when the library loads */
+
+__attribute__((constructor)) static void qfact_init(void) {
+  QFACT[0] = 1.0Q;
+  for (int i = 1; i <= ORACLE_MAXN; ++i) QFACT[i] = QFACT[i - 1] * (Q)i;
+}
+
+static Q qfact(int n) { return QFACT[n]; }
+
+static void bs_matrix_q(double theta, double phi, QC u[4]) {
+  Q c = cosq((Q)theta), s = sinq((Q)theta);
+  QC e = cosq((Q)phi) + 1.0Qi * sinq((Q)phi);
+  u[0] = c;              /* U11 */
+  u[1] = -conjq(e) * s;  /* U12 */
+  u[2] = e * s;          /* U21 */
+  u[3] = c;              /* U22 */
+}
+
+/* The t-sum of Appendix A with the powers U_ij^p tabulated (p <= n; 0^0 = 1). */
+static QC bs_element_q(const QC u[4], int x1, int x2, int y1, int y2) {
+  if (x1 < 0 || x2 < 0 || y1 < 0 || y2 < 0 || x1 + x2 != y1 + y2) return 0.0Q;
+  int n = x1 + x2;
+  QC pw[4][ORACLE_MAXN + 1];
+  for (int k = 0; k < 4; ++k) {
+    pw[k][0] = 1.0Q;
+    for (int p = 1; p <= n; ++p) pw[k][p] = pw[k][p - 1] * u[k];
+  }
   int tlo = 0;
   if (y1 - x2 > tlo) tlo = y1 - x2;
   if (x1 - y2 > tlo) tlo = x1 - y2;
   int thi = x1 < y1 ? x1 : y1;
-  C per = 0.0L;
+  QC per = 0.0Q;
   for (int t = tlo; t <= thi; ++t) {
-    R comb = (fact(y1) * fact(x1) / (fact(t) * fact(y1 - t))) *
-             (fact(y2) * fact(x2) / (fact(x1 - t) * fact(x2 - y1 + t)));
-    per += comb * ipow(u[0], t) * ipow(u[1], y1 - t) * ipow(u[2], x1 - t) * ipow(u[3], x2 - y1 + t);
+    Q comb = (qfact(y1) * qfact(x1) / (qfact(t) * qfact(y1 - t))) *
+             (qfact(y2) * qfact(x2) / (qfact(x1 - t) * qfact(x2 - y1 + t)));
+    per += comb * pw[0][t] * pw[1][y1 - t] * pw[2][x1 - t] * pw[3][x2 - y1 + t];
   }
-  return per / sqrtl(fact(x1) * fact(x2) * fact(y1) * fact(y2));
+  return per / sqrtq(qfact(x1) * qfact(x2) * qfact(y1) * qfact(y2));
+}
+
+static C bs_element_theta(double theta, double phi, int x1, int x2, int y1, int y2) {
+  QC u[4];
+  bs_matrix_q(theta, phi, u);
+  QC a = bs_element_q(u, x1, x2, y1, y2);
+  return (R)crealq(a) + I * (R)cimagq(a);
 }
 
 void oracle_bs_element(double theta, double phi, int x1, int x2, int y1, int y2, double out[2]) {
-  C u[4];
-  bs_matrix(theta, phi, u);
-  C a = bs_element_u(u, x1, x2, y1, y2);
+  if (x1 + x2 > ORACLE_MAXN || y1 + y2 > ORACLE_MAXN) { out[0] = out[1] = NAN; return; }
+  C a = bs_element_theta(theta, phi, x1, x2, y1, y2);
   out[0] = (double)creall(a);
   out[1] = (double)cimagl(a);
 }
@@ -381,6 +419,9 @@ typedef struct {
   const C *elem;      /* per-BS element cache [nbs][tri(N)] */
   const int *tri_off; /* offset of photon number n inside a BS's cache */
   int tri_size;
+  int ngates;         /* photon-number-preserving phase gates */
+  const int *g_mode, *g_after;
+  const double *g_a, *g_b;
   int occ[ORACLE_MAXM];
   C acc;
   uint64_t leaves;
@@ -392,6 +433,21 @@ static C elem_of(const pathsum_t *p, int b, int x1, int x2, int y1) {
   return p->elem[(size_t)b * p->tri_size + p->tri_off[n] + x1 * (n + 1) + y1];
 }
 
+/* Phase gates ("nonlinear phase gates are also photon-number preserving"): a
+ * gate on mode m after layer j (j = 0: on the input) multiplies the path by
+ * exp(i (a n + b n^2)), n = the photons in mode m after layer j.  b = 0 is a linear
+ * phase shifter, b != 0 a Kerr-type nonlinear phase (reading R19). */
+static C gate_factor(const pathsum_t *p, int after_layer) {
+  C f = 1.0L;
+  for (int g = 0; g < p->ngates; ++g) {
+    if (p->g_after[g] != after_layer) continue;
+    R n = (R)p->occ[p->g_mode[g]];
+    R arg = (R)p->g_a[g] * n + (R)p->g_b[g] * n * n;
+    f *= cosl(arg) + I * sinl(arg);
+  }
+  return f;
+}
+
 /* Recursion over the BS in layer order ("a systematic way to enumerate all possible
  * valid paths"): BS b gets every output split y1 = 0..x1+x2 (photon number is
  * conserved at each BS); the product of BS elements along the path is
@@ -401,6 +457,7 @@ static void pathsum_rec(pathsum_t *p, int layer, int b, C prod) {
   const circuit_t *c = p->c;
   if (b == p->layer_start[layer + 1]) { /* layer finished */
     ++layer;
+    if (p->ngates) prod *= gate_factor(p, layer);
     if (layer == c->D) {
       for (int i = 0; i < c->M; ++i) if (p->occ[i] != p->T[i]) return; /* invalid path */
       p->acc += prod;
@@ -435,13 +492,28 @@ static void pathsum_rec(pathsum_t *p, int layer, int b, C prod) {
   }
 }
 
+/* Largest photon number that can enter BS i (of layer l, 0-based): the input photons
+ * of its past light cone, capped at N.  Sizes the element cache only. */
+static int bs_cap(const circuit_t *c, const int *layer_start, const int *S, int l, int i, int N) {
+  unsigned char in[ORACLE_MAXM];
+  memset(in, 0, sizeof(in));
+  in[c->ma[i]] = in[c->mb[i]] = 1;
+  for (int k = l - 1; k >= 0; --k)
+    for (int j = layer_start[k]; j < layer_start[k + 1]; ++j)
+      if (in[c->ma[j]] || in[c->mb[j]]) in[c->ma[j]] = in[c->mb[j]] = 1;
+  int s = 0;
+  for (int m = 0; m < c->M; ++m) if (in[m]) s += S[m];
+  return s < N ? s : N;
+}
+
 /* Batch entry: amplitudes (and leaf counts = number of valid paths reached) for B
- * output patterns.  Returns 0, or -1 bad circuit / -2 bad state / -3 prune 2 on a
- * non-nearest-neighbour circuit. */
-int oracle_path_sum(int M, int D, const int *bs_per_layer, const int *ma, const int *mb,
-                    const double *theta, const double *phi, const int *S, long B,
-                    const int *T /* [B][M] */, int prune, int nthreads, double *out /* [B][2] */,
-                    uint64_t *leaves /* [B] or NULL */) {
+ * output patterns, with optional phase gates.  Returns 0, or -1 bad circuit / -2 bad
+ * state / -3 prune 2 on a non-nearest-neighbour circuit / -5 bad gate. */
+int oracle_path_sum_gates(int M, int D, const int *bs_per_layer, const int *ma, const int *mb,
+                          const double *theta, const double *phi, const int *S, long B,
+                          const int *T /* [B][M] */, int prune, int nthreads, int ngates,
+                          const int *g_mode, const int *g_after, const double *g_a, const double *g_b,
+                          double *out /* [B][2] */, uint64_t *leaves /* [B] or NULL */) {
   circuit_t c = {M, D, 0, bs_per_layer, ma, mb, theta, phi};
   int nbs = circuit_check(&c);
   if (nbs < 0) return -1;
@@ -449,27 +521,35 @@ int oracle_path_sum(int M, int D, const int *bs_per_layer, const int *ma, const 
   if (prune == 2 && !is_nn(&c)) return -3;
   int N = 0;
   for (int i = 0; i < M; ++i) { if (S[i] < 0) return -2; N += S[i]; }
-  if (N > 64) return -2;
+  if (N > ORACLE_MAXN) return -2;
+  for (int g = 0; g < ngates; ++g)
+    if (g_mode[g] < 0 || g_mode[g] >= M || g_after[g] < 0 || g_after[g] > D) return -5;
   int ls[ORACLE_MAXD + 1];
   ls[0] = 0;
   for (int l = 0; l < D; ++l) ls[l + 1] = ls[l] + bs_per_layer[l];
-  /* per-BS cache of Appendix-A elements for every (x1, x2, y1) with x1 + x2 <= N */
+  /* per-BS cache of Appendix-A elements for every (x1, x2, y1) with x1 + x2 <= cap(BS) */
   int *tri_off = (int *)malloc(sizeof(int) * (size_t)(N + 2));
   tri_off[0] = 0;
   for (int n = 0; n <= N; ++n) tri_off[n + 1] = tri_off[n] + (n + 1) * (n + 1);
   int tri = tri_off[N + 1];
+  int *cap = (int *)malloc(sizeof(int) * (size_t)(nbs > 0 ? nbs : 1));
+  for (int l = 0; l < D; ++l)
+    for (int i = ls[l]; i < ls[l + 1]; ++i) cap[i] = bs_cap(&c, ls, S, l, i, N);
   C *elem = (C *)malloc(sizeof(C) * (size_t)(nbs > 0 ? nbs : 1) * tri);
-  for (int b = 0; b < nbs; ++b) {
-    C u[4];
-    bs_matrix(theta[b], phi[b], u);
-    for (int n = 0; n <= N; ++n)
-      for (int x1 = 0; x1 <= n; ++x1)
-        for (int y1 = 0; y1 <= n; ++y1)
-          elem[(size_t)b * tri + tri_off[n] + x1 * (n + 1) + y1] = bs_element_u(u, x1, n - x1, y1, n - y1);
-  }
-  int rc = 0;
 #ifdef _OPENMP
   if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for collapse(2) schedule(dynamic, 1)
+#endif
+  for (int b = 0; b < nbs; ++b)
+    for (int n = 0; n <= N; ++n) {
+      if (n > cap[b]) continue;
+      for (int x1 = 0; x1 <= n; ++x1)
+        for (int y1 = 0; y1 <= n; ++y1)
+          elem[(size_t)b * tri + tri_off[n] + x1 * (n + 1) + y1] =
+              bs_element_theta(theta[b], phi[b], x1, n - x1, y1, n - y1);
+    }
+  int rc = 0;
+#ifdef _OPENMP
 #pragma omp parallel for schedule(dynamic, 1)
 #endif
   for (long q = 0; q < B; ++q) {
@@ -490,6 +570,11 @@ int oracle_path_sum(int M, int D, const int *bs_per_layer, const int *ma, const 
     p->elem = elem;
     p->tri_off = tri_off;
     p->tri_size = tri;
+    p->ngates = ngates;
+    p->g_mode = g_mode;
+    p->g_after = g_after;
+    p->g_a = g_a;
+    p->g_b = g_b;
     if (prune == 1) {
       bound = (int *)malloc(sizeof(int) * (size_t)(D + 1) * M);
       for (int j = 0; j <= D; ++j)
@@ -504,12 +589,13 @@ int oracle_path_sum(int M, int D, const int *bs_per_layer, const int *ma, const 
     }
     for (int i = 0; i < M; ++i) p->occ[i] = S[i];
     p->acc = 0.0L;
+    C start = ngates ? gate_factor(p, 0) : 1.0L;
     if (D == 0) {
       int same = 1;
       for (int i = 0; i < M; ++i) if (S[i] != Tq[i]) same = 0;
-      if (same) { p->acc = 1.0L; p->leaves = 1; }
+      if (same) { p->acc = start; p->leaves = 1; }
     } else {
-      pathsum_rec(p, 0, 0, 1.0L);
+      pathsum_rec(p, 0, 0, start);
     }
     out[2 * q] = (double)creall(p->acc);
     out[2 * q + 1] = (double)cimagl(p->acc);
@@ -518,8 +604,17 @@ int oracle_path_sum(int M, int D, const int *bs_per_layer, const int *ma, const 
     free(p);
   }
   free(elem);
+  free(cap);
   free(tri_off);
   return rc;
+}
+
+int oracle_path_sum(int M, int D, const int *bs_per_layer, const int *ma, const int *mb,
+                    const double *theta, const double *phi, const int *S, long B,
+                    const int *T /* [B][M] */, int prune, int nthreads, double *out /* [B][2] */,
+                    uint64_t *leaves /* [B] or NULL */) {
+  return oracle_path_sum_gates(M, D, bs_per_layer, ma, mb, theta, phi, S, B, T, prune, nthreads, 0,
+                               NULL, NULL, NULL, NULL, out, leaves);
 }
 
 /* ------------------------------------------------------------------------- */
