@@ -11,7 +11,9 @@
  * (eq. (1)): a valid path assigns photon numbers to every waveguide segment,
  * conserving x1+x2 = y1+y2 at every BS, with the input segments equal to S and the
  * output segments equal to T.  The BS elements are those of Appendix A
- * (P:354-408).  The sum is enumerated on the GPU path by path; no permanent is used.
+ * (P:354-408).  lofp_amplitudes forms the product of every valid path on the GPU and
+ * adds it (no permanent is used); lofp_amplitudes_contract evaluates the same sum by the
+ * paper's strip tensor contraction instead.
  *
  * Conventions.
  *   - Modes are 0-based.  A BS is given as (mode_a, mode_b, theta, phi); mode_a is BS
@@ -26,10 +28,17 @@
  *     [0, pi]; the benchmark configurations draw phi in [0, 2 pi)).
  *   - An output whose photon number differs from the input's gets exactly 0; so does an
  *     output that no path reaches.
+ *   - Results are bitwise reproducible run to run (fixed summation order; no floating-
+ *     point atomics).
  *
- * Threading and ownership.  A context owns its device memory and must not be used from
- * two host threads at once; separate contexts are independent.  The library never frees
- * caller memory and never throws or aborts across this boundary.
+ * Threading, streams and ownership.  A context owns its device memory and must not be
+ * used from two host threads at once; separate contexts are independent.  Every device
+ * call enqueues its work on the stream it is given and returns without waiting for it
+ * (no host synchronisation, no device-to-host read); it can be captured in a CUDA graph
+ * once a call of the same batch size has run outside capture (buffers are sized then).
+ * Consecutive calls on one context are ordered after each other even on different
+ * streams (outside capture).  The library never frees caller memory and never throws or
+ * aborts across this boundary.
  */
 #ifndef LOFP_H
 #define LOFP_H
@@ -50,20 +59,36 @@ typedef struct {
   double phi;
 } lofp_bs;
 
+/* A photon-number-preserving phase gate ("nonlinear phase gates are also photon-
+ * number preserving"): on mode `mode` after layer `after_layer` (0 = on the input, D =
+ * on the output) it multiplies the state |n> of that mode by exp(i (a n + b n^2)).
+ * b = 0 is a linear phase shifter; b != 0 a Kerr-type nonlinear phase. */
+typedef struct {
+  int32_t mode;
+  int32_t after_layer;
+  double a;
+  double b;
+} lofp_gate;
+
 typedef enum {
   LOFP_OK = 0,
   LOFP_E_INVALID_ARG = 1, /* null pointer, bad count, mode out of range, overlapping
                              pairs in one layer, non-finite angle, negative input */
-  LOFP_E_UNSUPPORTED = 2, /* non-adjacent pair, too many modes/photons/levels */
+  LOFP_E_UNSUPPORTED = 2, /* non-adjacent pair, too many modes/photons/layers, an output
+                             whose light-cone state space exceeds the limits below */
   LOFP_E_CUDA = 3,        /* a CUDA runtime error; text in lofp_last_error() */
   LOFP_E_OOM = 4,         /* device allocation failed */
   LOFP_E_BAD_OUTPUT = 5   /* an output row had a negative entry; its amplitude is NaN */
 } lofp_status;
 
-/* Limits of this build (uint8 photon numbers; bounded DFS metadata). */
+/* Limits of this build.  Photon numbers are uint8 segment values; a column of the path
+ * tree (the photon counts left of one cut over all layers) may take at
+ * most 4096 values inside the light-cone box, 65536 summed over the columns of one
+ * output; an output over these limits gets NaN and lofp_stats() counts it. */
 #define LOFP_MAX_MODES 128
 #define LOFP_MAX_PHOTONS 120
 #define LOFP_MAX_LAYERS 64
+#define LOFP_MAX_GATES 4096
 
 /* Create a context for one circuit.
  *   modes         M >= 1, M <= LOFP_MAX_MODES.
@@ -71,32 +96,38 @@ typedef enum {
  *   bs_per_layer  host array [n_layers], each >= 0 (NULL allowed when n_layers == 0).
  *   bs            host array [sum bs_per_layer], layer-major (NULL allowed when empty).
  *   out           receives the new context (set to NULL on failure).
- * Copies everything it is given; allocates only small device buffers.  Uses the
- * current CUDA device.  Errors: LOFP_E_INVALID_ARG, LOFP_E_UNSUPPORTED, LOFP_E_CUDA,
- * LOFP_E_OOM. */
+ * Copies everything it is given; uploads the circuit's topology tables (synchronously,
+ * once).  Uses the current CUDA device.  Errors: LOFP_E_INVALID_ARG, LOFP_E_UNSUPPORTED,
+ * LOFP_E_CUDA, LOFP_E_OOM. */
 lofp_status lofp_create(int32_t modes, int32_t n_layers, const int32_t *bs_per_layer,
                         const lofp_bs *bs, lofp_ctx **out);
 
-/* Amplitudes <T_b|U_P|S> for a batch of outputs (eq. (1)).
+/* lofp_create plus phase gates.  gates: host array [n_gates] (NULL when 0),
+ * 0 <= mode < modes, 0 <= after_layer <= n_layers, finite a and b, n_gates <=
+ * LOFP_MAX_GATES.  Several gates on one (mode, layer) multiply. */
+lofp_status lofp_create_ex(int32_t modes, int32_t n_layers, const int32_t *bs_per_layer,
+                           const lofp_bs *bs, int32_t n_gates, const lofp_gate *gates,
+                           lofp_ctx **out);
+
+/* Amplitudes <T_b|U_P|S> for a batch of outputs by the path sum (eq. (1)):
+ * every valid path's product is formed and added on the GPU.
  *   input_occ     host int32 [modes]: S (entries >= 0, sum <= LOFP_MAX_PHOTONS).
  *   batch         B >= 0 (B = 0 is a no-op).
  *   output_occ    DEVICE int32 [B][modes], row-major: T_b.
  *   amps          DEVICE double [B][2]: complex128 results (re, im interleaved).
  *   cuda_stream   cudaStream_t to run on (NULL = legacy default stream).
- * Host arguments are validated before any device work.  The call enqueues its kernels
- * on cuda_stream; it synchronises that stream once, after the first (feasibility)
- * kernel, to size the shared-memory BS tables from the batch's per-mode maximum, and
- * returns with the enumeration still running: the caller synchronises the stream before
- * reading amps.  output_occ and amps must stay valid until then.  A row with a negative
- * entry gets NaN and LOFP_E_BAD_OUTPUT is returned by lofp_stats() after completion.
+ * Host arguments are validated before any device work; the kernels are enqueued on
+ * cuda_stream and the call returns (see "Threading, streams and ownership").
+ * output_occ and amps must stay valid until the stream has run the work.  A row with a
+ * negative entry gets NaN (lofp_stats() then returns LOFP_E_BAD_OUTPUT).
  * Errors: LOFP_E_INVALID_ARG, LOFP_E_UNSUPPORTED, LOFP_E_CUDA, LOFP_E_OOM. */
 lofp_status lofp_amplitudes(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch,
                             const int32_t *output_occ, double *amps, void *cuda_stream);
 
-/* Same as lofp_amplitudes, and also the exact number of valid paths summed for every
- * output: path_counts is a DEVICE uint64 [B] (written, not accumulated).  Slightly
- * slower (one integer add per path); used by the parity tests to check that every path
- * of eq. (1) is enumerated exactly once. */
+/* Same as lofp_amplitudes, and also the number of path products formed for every
+ * output: path_counts is a DEVICE uint64 [B] (written, not accumulated).  Equal to the
+ * exact number of valid paths of eq. (1) (the kernel checks it against an independent
+ * count; lofp_stats() reports a mismatch).  Same cost as lofp_amplitudes. */
 lofp_status lofp_amplitudes_counted(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch,
                                     const int32_t *output_occ, double *amps,
                                     uint64_t *path_counts, void *cuda_stream);
@@ -116,49 +147,34 @@ const char *lofp_status_string(lofp_status s);
 /* Message for the last failing call on ctx ("" if none); valid until the next call. */
 const char *lofp_last_error(const lofp_ctx *ctx);
 
-/* Measurement / validation counters of the last lofp_amplitudes* call.  Reading them
- * synchronises the call's stream. */
+/* Measurement / validation counters of the last device call.  Reading them synchronises
+ * that call's work (the only synchronising entry besides _host and destroy). */
 typedef struct {
   int64_t batch;          /* B of the last call */
-  int64_t feasible;       /* outputs whose path tree has at least one free level */
-  int64_t items;          /* work items (subtrees) processed by the enumeration kernel */
-  int64_t spills;         /* subtrees pushed to the global work queue */
-  int64_t donations;      /* subtrees handed between lanes of one warp */
-  int64_t overflows;      /* branch-stack entries that went to the local overflow */
-  int64_t paths;          /* valid paths summed (lofp_amplitudes_counted only, else 0) */
-  int64_t cmuls;          /* complex multiplications executed (counted only, else 0): DFS
-                             factors with x1 + x2 > 0, chain pair-table factors, chain products */
-  int64_t chains;         /* chain subtrees enumerated by the lockstep chain engine */
-  int64_t chain_fallbacks;/* chains walked depth-first instead (pair table over capacity) */
-  int32_t levels;         /* largest number of free DFS levels of one output */
-  int32_t table_entries;  /* Appendix-A elements staged in shared memory */
-  int32_t smem_bytes;     /* dynamic shared memory per block of the enumeration kernel */
-  int32_t grid_blocks;    /* persistent grid size */
+  int64_t feasible;       /* outputs with at least one valid path */
+  int64_t paths;          /* path products formed (sum over the batch) */
+  int64_t cmuls;          /* other complex multiplications: half-path list products, the
+                             per-pair scalings of the lists */
+  int64_t units;          /* work units (subtrees) processed */
+  int64_t subsplits;      /* units split again inside the kernel (lists over capacity) */
+  int64_t pairs;          /* column-pair states multiplied out */
+  int64_t elements;       /* half-path list elements built */
+  int64_t unsupported;    /* outputs over a state limit (their amplitude is NaN) */
+  int64_t bad_rows;       /* rows with a negative entry (their amplitude is NaN) */
+  int64_t check_errors;   /* internal consistency failures (must be 0): a path-count
+                             mismatch or a table index outside its block */
+  int64_t max_states;     /* largest number of column states of one output */
+  int64_t max_list;       /* largest half-path list */
+  int64_t table_entries;  /* Appendix-A elements in the table */
+  int32_t grid_blocks;    /* persistent grid of the unit kernel */
   int32_t block_threads;  /* threads per block */
-  int32_t bad_rows;       /* rows with a negative entry (their amplitude is NaN) */
-  int32_t max_factors;    /* largest number of attached BS elements of one output */
-  int32_t max_scatter;    /* largest number of key bytes written per level value, one output */
-  int32_t engine;         /* 0: depth-first walk only; 1: chain engine (R17); 2: chain engine
-                             with the short chains batched (short-chain mode) */
-  int32_t launches;       /* kernels launched by the call (prep, tables, plan(s), enumeration) */
-  float enum_ms;          /* device time of the enumeration kernel (CUDA events) */
+  int32_t launches;       /* kernels launched by the call */
+  int32_t mode;           /* 0 path sum, 1 strip contraction */
+  float units_ms;         /* device time of the unit (enumeration) kernel, CUDA events */
   float total_ms;         /* device time from the first to the last kernel */
 } lofp_run_stats;
 
 lofp_status lofp_stats(lofp_ctx *ctx, lofp_run_stats *out);
-
-/* Work-distribution histograms of the last lofp_amplitudes_counted call (zeros after an
- * uncounted call): subtrees handed between lanes of a warp (handover) and pushed to the
- * global queue (spill), indexed by (deepest level - level of the handed-over branch),
- * clamped to 63.  handover and spill are host uint64 [64].  Synchronises the call. */
-lofp_status lofp_work_histograms(lofp_ctx *ctx, uint64_t *handover, uint64_t *spill);
-
-/* Enumeration-kernel time split of the last lofp_amplitudes_counted call (zeros after an
- * uncounted call): SM clock cycles summed over warps (lane 0's clock) in 8 phases --
- * 0 depth-first step and hand-over, 1 chain ranges, 2 chain pair table, 3 chain split and
- * prefix digits, 4 chain path products, 5 return to the walk and global-queue feeding,
- * 6 work acquisition, plan staging and item reduction, 7 chain suffix table.  cycles is a host uint64 [8].  Synchronises the call. */
-lofp_status lofp_phase_cycles(lofp_ctx *ctx, uint64_t *cycles);
 
 #ifdef __cplusplus
 }

@@ -1,7 +1,8 @@
 // lofp_host.cpp — host side of liblofp: the C ABI of include/lofp.h, circuit
-// canonicalisation, light-cone topology maps, per-call Appendix-A table layout and the
-// kernel launches.  See DESIGN.md for the derivations (readings R1-R9) and the paper
-// passages each step follows.
+// canonicalisation, the column / light-cone topology tables, per-call buffer sizing and
+// the kernel launches.  See DESIGN.md for the derivations (readings R1-R20) and the paper
+// passages each step follows.  No call here waits for the device except lofp_create
+// (one upload), lofp_stats, lofp_amplitudes_host and lofp_destroy.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -17,6 +18,8 @@
 #include "../../include/lofp.h"
 #include "lofp_internal.h"
 
+using namespace lofp;
+
 namespace {
 
 constexpr double kPi = 3.14159265358979323846;
@@ -25,7 +28,7 @@ struct DevBuf {
   void *p = nullptr;
   size_t n = 0;
   cudaError_t ensure(size_t bytes) {
-    if (bytes <= n) return cudaSuccess;
+    if (bytes <= n && p) return cudaSuccess;
     if (p) cudaFree(p);
     p = nullptr;
     n = 0;
@@ -44,7 +47,7 @@ struct HostPinned {
   void *p = nullptr;
   size_t n = 0;
   cudaError_t ensure(size_t bytes) {
-    if (bytes <= n) return cudaSuccess;
+    if (bytes <= n && p) return cudaSuccess;
     if (p) cudaFreeHost(p);
     p = nullptr;
     n = 0;
@@ -59,376 +62,249 @@ struct HostPinned {
   }
 };
 
-// A beam splitter after canonicalisation: port 1 = mode k-1, port 2 = mode k.
+// A beam splitter after canonicalisation: port 1 = mode cut-1, port 2 = mode cut.
 struct CanonBS {
   int layer;  // 1-based
   int cut;    // k = max(mode_a, mode_b)
   double theta, phi;
 };
 
+long long env_ll(const char *name, long long dflt) {
+  const char *v = std::getenv(name);
+  if (!v || !*v) return dflt;
+  char *end = nullptr;
+  long long x = std::strtoll(v, &end, 10);
+  return (end && *end == 0 && x > 0) ? x : dflt;
+}
+
 }  // namespace
 
 struct lofp_ctx {
-  int M = 0, D = 0, nbs = 0, Lg = 0;
-  std::vector<CanonBS> bs;                  // layer-major, by cut inside a layer
-  std::vector<std::vector<uint8_t>> act;    // [D+1][M+1]
-  std::vector<uint8_t> maps;                // [4][D+1][M+1]: rho, sigma, rho', sigma'
-  // static device data
-  DevBuf d_maps, d_bs_lk, d_bs_cs;
-  // per-call device data
-  DevBuf d_flags, d_plans, d_feas, d_ctr, d_ring, d_edesc, d_offsets, d_entries, d_cumS, d_bsrow;
-  DevBuf d_hostT, d_hostA;
-  HostPinned h_stage, h_ctr;
-  unsigned ring_cap = 0;
-  cudaEvent_t ev_start = nullptr, ev_enum0 = nullptr, ev_enum1 = nullptr, ev_end = nullptr;
-  cudaStream_t own_stream = nullptr;
-  bool have_call = false;
+  int device = 0;
+  int M = 0, D = 0, nbs = 0, ngate = 0;
+  std::vector<CanonBS> bs;
+  // topology (lofp_internal.h)
+  std::vector<ColInfo> col;
+  std::vector<SegInfo> seg;
+  std::vector<CmpPair> cmp;
+  std::vector<FacInfo> fac;
+  std::vector<GateInfo> gat;
+  std::vector<BSInfo> bsi;
+  std::vector<double> gate_ab;
+  std::vector<int16_t> gate_mode, gate_after;
+  DevBuf d_topo;
+  size_t off_col = 0, off_seg = 0, off_cmp = 0, off_fac = 0, off_gat = 0, off_bsi = 0, off_gab = 0, off_gm = 0,
+         off_gl = 0;
+  // per-call device buffers
+  DevBuf d_table, d_taboff, d_gatetab, d_units, d_nunits, d_ubase, d_status, d_pexp, d_pdone, d_partial, d_slab,
+      d_ctr, d_hostT, d_hostA;
+  HostPinned h_ctr;
+  std::vector<int32_t> tab_S;  // input the table was built for
+  bool tables_valid = false;
+  long long table_entries = 0;
+  int grid = 0;
+  long long slab_bytes = 0;
+  cudaEvent_t ev_start = nullptr, ev_u0 = nullptr, ev_u1 = nullptr, ev_end = nullptr;
+  bool have_call = false, timed = false;
   lofp_run_stats stats{};
   std::string err;
-  int device = 0;
+  cudaStream_t own_stream = nullptr;
 };
 
 namespace {
 
-lofp_status fail(lofp_ctx *c, lofp_status s, const std::string &msg) {
-  if (c) c->err = msg;
+lofp_status fail(lofp_ctx *ctx, lofp_status s, const std::string &msg) {
+  if (ctx) ctx->err = msg;
   return s;
 }
 
-lofp_status cuda_fail(lofp_ctx *c, cudaError_t e, const char *where) {
-  std::string m = std::string(where) + ": " + cudaGetErrorString(e);
-  return fail(c, e == cudaErrorMemoryAllocation ? LOFP_E_OOM : LOFP_E_CUDA, m);
-}
-
-#define CK(expr, where)                                      \
-  do {                                                       \
-    cudaError_t _e = (expr);                                 \
-    if (_e != cudaSuccess) return cuda_fail(ctx, _e, where); \
+#define CK(call, what)                                                                          \
+  do {                                                                                          \
+    cudaError_t e_ = (call);                                                                    \
+    if (e_ != cudaSuccess)                                                                      \
+      return fail(ctx, e_ == cudaErrorMemoryAllocation ? LOFP_E_OOM : LOFP_E_CUDA,             \
+                  std::string(what) + ": " + cudaGetErrorString(e_));                          \
   } while (0)
 
-// Topology-only light-cone maps (reading R5).  Backward: rho_D(k) = sigma_D(k) = k and,
-// going back through layer l, an active cut k takes rho_{l-1}(k) = rho_l(k-1),
-// sigma_{l-1}(k) = sigma_l(k+1); then F_l(k) lies in [G(rho_l(k)), G(sigma_l(k))].
-// Forward (the same construction from the input side): rho'_0(k) = sigma'_0(k) = k,
-// rho'_l(k) = rho'_{l-1}(k-1), sigma'_l(k) = sigma'_{l-1}(k+1) at active cuts; then
-// F_l(k) lies in [cumS(rho'_l(k)), cumS(sigma'_l(k))] (P:153-164 cones, cumulative form).
-lofp_status plan_circuit(lofp_ctx *c) {
-  const int M = c->M, D = c->D, W = M + 1;
-  c->act.assign(D + 1, std::vector<uint8_t>(M + 1, 0));
-  for (const CanonBS &b : c->bs) c->act[b.layer][b.cut] = 1;
-  c->maps.assign(4 * (D + 1) * W, 0);
-  uint8_t *rho = c->maps.data(), *sig = rho + (D + 1) * W, *frho = sig + (D + 1) * W, *fsig = frho + (D + 1) * W;
-  for (int k = 0; k <= M; ++k) rho[D * W + k] = sig[D * W + k] = (uint8_t)k;
+struct DeviceGuard {  // restores the caller's current device
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// Column / light-cone topology of the circuit (readings R5, R15, R20).
+lofp_status build_topology(lofp_ctx *ctx, const std::vector<lofp_gate> &gates) {
+  const int M = ctx->M, D = ctx->D, W = M + 1;
+  std::vector<int> act((size_t)(D + 1) * W, -1);  // act[l][k] = BS index or -1
+  for (int i = 0; i < ctx->nbs; ++i) act[(size_t)ctx->bs[i].layer * W + ctx->bs[i].cut] = i;
+  auto A = [&](int l, int k) { return act[(size_t)l * W + k] >= 0; };
+  // backward maps (from T): F_l(k) in [G(rho_l(k)), G(sig_l(k))]   (reading R5)
+  std::vector<int> rho((size_t)(D + 1) * W), sig((size_t)(D + 1) * W);
+  // forward maps (from S): F_l(k) in [cumS(rhop_l(k)), cumS(sigp_l(k))]  (reading R15)
+  std::vector<int> rhop((size_t)(D + 1) * W), sigp((size_t)(D + 1) * W);
+  for (int k = 0; k <= M; ++k) {
+    rho[(size_t)D * W + k] = sig[(size_t)D * W + k] = k;
+    rhop[k] = sigp[k] = k;
+  }
   for (int l = D; l >= 1; --l)
     for (int k = 0; k <= M; ++k) {
-      rho[(l - 1) * W + k] = c->act[l][k] ? rho[l * W + k - 1] : rho[l * W + k];
-      sig[(l - 1) * W + k] = c->act[l][k] ? sig[l * W + k + 1] : sig[l * W + k];
+      const bool a = A(l, k);
+      rho[(size_t)(l - 1) * W + k] = a ? rho[(size_t)l * W + k - 1] : rho[(size_t)l * W + k];
+      sig[(size_t)(l - 1) * W + k] = a ? sig[(size_t)l * W + k + 1] : sig[(size_t)l * W + k];
     }
-  for (int k = 0; k <= M; ++k) frho[k] = fsig[k] = (uint8_t)k;
   for (int l = 1; l <= D; ++l)
     for (int k = 0; k <= M; ++k) {
-      frho[l * W + k] = c->act[l][k] ? frho[(l - 1) * W + k - 1] : frho[(l - 1) * W + k];
-      fsig[l * W + k] = c->act[l][k] ? fsig[(l - 1) * W + k + 1] : fsig[(l - 1) * W + k];
+      const bool a = A(l, k);
+      rhop[(size_t)l * W + k] = a ? rhop[(size_t)(l - 1) * W + k - 1] : rhop[(size_t)(l - 1) * W + k];
+      sigp[(size_t)l * W + k] = a ? sigp[(size_t)(l - 1) * W + k + 1] : sigp[(size_t)(l - 1) * W + k];
     }
-  // global bound on DFS levels: BS outputs whose backward box is not a single cut
-  int L = 0;
-  for (const CanonBS &b : c->bs)
-    if (rho[b.layer * W + b.cut] != sig[b.layer * W + b.cut]) ++L;
-  if (L > LOFP_MAX_LEVELS) return fail(c, LOFP_E_UNSUPPORTED, "too many free BS outputs (DFS levels)");
-  c->Lg = L;
-  return LOFP_OK;
-}
-
-// Per-segment occupation caps: min(photons of S in the past light cone, photons of
-// max-over-batch T in the future light cone).  cap[j][m] for the segment of
-// mode m after layer j.
-std::vector<std::vector<int>> segment_caps(const lofp_ctx *c, const std::vector<int> &S, const int32_t *tmax) {
-  const int M = c->M, D = c->D;
-  std::vector<std::vector<int>> cap(D + 1, std::vector<int>(M, 0));
-  std::vector<std::vector<const CanonBS *>> byl(D + 1);
-  for (const CanonBS &b : c->bs) byl[b.layer].push_back(&b);
-  std::vector<uint8_t> in(M);
-  for (int j = 0; j <= D; ++j)
-    for (int m = 0; m < M; ++m) {
-      std::fill(in.begin(), in.end(), 0);
-      in[m] = 1;
-      for (int l = j; l >= 1; --l)
-        for (const CanonBS *b : byl[l])
-          if (in[b->cut - 1] || in[b->cut]) in[b->cut - 1] = in[b->cut] = 1;
-      int past = 0;
-      for (int i = 0; i < M; ++i)
-        if (in[i]) past += S[i];
-      std::fill(in.begin(), in.end(), 0);
-      in[m] = 1;
-      for (int l = j + 1; l <= D; ++l)
-        for (const CanonBS *b : byl[l])
-          if (in[b->cut - 1] || in[b->cut]) in[b->cut - 1] = in[b->cut] = 1;
-      int fut = 0;
-      for (int i = 0; i < M; ++i)
-        if (in[i]) fut += tmax[i];
-      cap[j][m] = std::min(past, fut);
-    }
-  return cap;
-}
-
-inline size_t round16(size_t x) { return (x + 15) & ~size_t(15); }
-
-lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const int32_t *output_occ, double *amps,
-                unsigned long long *counts, cudaStream_t stream) {
-  if (!ctx) return LOFP_E_INVALID_ARG;
-  ctx->err.clear();
-  if (!input_occ || batch < 0) return fail(ctx, LOFP_E_INVALID_ARG, "null input_occ or negative batch");
-  if (batch > 0 && (!output_occ || !amps)) return fail(ctx, LOFP_E_INVALID_ARG, "null output_occ or amps");
-  if (batch > (int64_t)0x7fffffff) return fail(ctx, LOFP_E_UNSUPPORTED, "batch too large");
-  const int M = ctx->M;
-  std::vector<int> S(M);
-  int N = 0;
-  for (int m = 0; m < M; ++m) {
-    if (input_occ[m] < 0) return fail(ctx, LOFP_E_INVALID_ARG, "negative input occupation");
-    S[m] = input_occ[m];
-    N += S[m];
-    if (N > LOFP_MAX_PHOTONS) return fail(ctx, LOFP_E_UNSUPPORTED, "too many photons");
-  }
-  CK(cudaSetDevice(ctx->device), "cudaSetDevice");
-  ctx->stats = lofp_run_stats{};
-  ctx->stats.batch = batch;
-  ctx->have_call = false;
-  if (batch == 0) return LOFP_OK;
-  // serialise with this context's previous call (its buffers are reused)
-  CK(cudaEventSynchronize(ctx->ev_end), "cudaEventSynchronize");
-
-  const int64_t B = batch;
-  CallArgs a{};
-  a.M = M;
-  a.D = ctx->D;
-  a.N = N;
-  a.nbs = ctx->nbs;
-  a.Lg = ctx->Lg;
-  a.vals_slots = (int)((ctx->Lg + 1 + 3) & ~3);
-  a.B = B;
-  // head | levels [Lg] | factors [nbs] | scatter u16 [4 nbs] | pad | scratch factors [nbs] |
-  // scratch scatter u32 [4 nbs]  (see lofp_plan_kernel)
-  a.plan_stride = (int)round16(sizeof(PlanHead) + (size_t)ctx->Lg * sizeof(PlanLevel) +
-                               2 * (size_t)ctx->nbs * sizeof(PlanFactor) + 8 * (size_t)ctx->nbs + 16 +
-                               16 * (size_t)ctx->nbs);
-  // chain-engine thresholds (env overrides exist for the tests, which exercise the
-  // engine on small circuits)
-  a.chain_rbox = LOFP_CHAIN_RBOX;
-  a.chain_rmin = LOFP_CHAIN_RMIN;
-  if (const char *e = std::getenv("LOFP_CHAIN_RBOX")) a.chain_rbox = std::atof(e);
-  if (const char *e = std::getenv("LOFP_CHAIN_RMIN")) a.chain_rmin = std::atoi(e);
-  a.small_paths = LOFP_SMALL_PATHS;
-  if (const char *e = std::getenv("LOFP_SMALL_PATHS")) a.small_paths = std::min(std::atoi(e), 256);
-  a.T = output_occ;
-  a.amps = amps;
-  a.counts = counts;
-  CK(ctx->d_flags.ensure((size_t)B), "alloc flags");
-  CK(ctx->d_plans.ensure((size_t)B * a.plan_stride), "alloc plans");
-  CK(ctx->d_feas.ensure((size_t)B * 4), "alloc feas");
-  CK(ctx->d_ctr.ensure(sizeof(Counters)), "alloc counters");
-  CK(ctx->d_cumS.ensure(256), "alloc cumS");
-  a.flags = (uint8_t *)ctx->d_flags.p;
-  a.plans = (unsigned char *)ctx->d_plans.p;
-  a.feas = (uint32_t *)ctx->d_feas.p;
-  a.ctr = (Counters *)ctx->d_ctr.p;
-  a.cumS = (const uint8_t *)ctx->d_cumS.p;
-  a.maps = (const uint8_t *)ctx->d_maps.p;
-  a.bs_lk = (const int16_t *)ctx->d_bs_lk.p;
-  a.bs_cs = (const double *)ctx->d_bs_cs.p;
-
-  CK(cudaEventRecord(ctx->ev_start, stream), "cudaEventRecord");
-  // cum(S) to the device (pinned staging; the previous call has completed)
-  CK(ctx->h_stage.ensure(4096), "alloc staging");
-  uint8_t *cs = (uint8_t *)ctx->h_stage.p;
-  {
-    int f = 0;
-    for (int k = 0; k <= M; ++k) {
-      cs[k] = (uint8_t)f;
-      if (k < M) f += S[k];
+  // segments of every column: F(k) is constant between consecutive active layers of cut k
+  std::vector<std::vector<int>> al(W);         // active layers of cut k
+  std::vector<std::vector<int>> segof(W);      // time t -> segment index
+  for (int k = 0; k <= M; ++k) {
+    for (int l = 1; l <= D; ++l)
+      if (A(l, k)) al[k].push_back(l);
+    segof[k].assign(D + 1, 0);
+    int s = 0;
+    for (int t = 0; t <= D; ++t) {
+      if (s < (int)al[k].size() && al[k][s] == t) ++s;
+      segof[k][t] = s;
     }
   }
-  CK(cudaMemcpyAsync(ctx->d_cumS.p, cs, M + 1, cudaMemcpyHostToDevice, stream), "upload cumS");
-  CK(cudaMemsetAsync(a.ctr, 0, sizeof(Counters), stream), "reset counters");
-  CK(lofp_launch_prep(a, stream), "prep kernel");
-  ctx->stats.launches += a.B > 0 ? 1 : 0;
-  // (sync 1) the batch's per-mode maximum sizes the tables
-  CK(ctx->h_ctr.ensure(sizeof(Counters)), "alloc pinned counters");
-  CK(cudaMemcpyAsync(ctx->h_ctr.p, a.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, stream), "read tmax");
-  CK(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
-  const Counters *hc = (const Counters *)ctx->h_ctr.p;
-  int32_t tmax[LOFP_MAX_MODES];
-  for (int m = 0; m < M; ++m) tmax[m] = hc->tmax[m];
-
-  // Appendix-A table layout inside the light-cone caps
-  std::vector<std::vector<int>> cap = segment_caps(ctx, S, tmax);
-  std::vector<int32_t> offsets;
-  std::vector<EntryDesc> edesc;
-  std::vector<int32_t> bsrow(2 * std::max(ctx->nbs, 1));  // [base | stride]
+  ctx->col.assign(W, ColInfo{});
+  ctx->seg.clear();
+  ctx->cmp.clear();
+  ctx->fac.clear();
+  ctx->gat.clear();
+  // gates by cut: a gate on mode m reads columns m and m+1 -> folded into cut m+1
+  // (or cut M-1 for the last mode); M == 1 has no cut: the kernels multiply those in.
+  std::vector<std::vector<GateInfo>> gates_of(W);
+  for (size_t g = 0; g < gates.size(); ++g) {
+    const int m = gates[g].mode, j = gates[g].after_layer;
+    if (M == 1) continue;
+    const int c = (m + 1 <= M - 1) ? m + 1 : m;
+    GateInfo gi{};
+    gi.gate = (int32_t)g;
+    gi.col_off = (uint8_t)(m - (c - 1));
+    gi.seg_lo = (uint8_t)segof[m][j];
+    gi.seg_hi = (uint8_t)segof[m + 1][j];
+    gates_of[c].push_back(gi);
+  }
+  for (int k = 0; k <= M; ++k) {
+    ColInfo &ci = ctx->col[k];
+    const int nseg = (int)al[k].size() + 1;
+    if (ctx->seg.size() + nseg > 8192 || nseg > 255) return LOFP_E_UNSUPPORTED;
+    ci.seg_base = (uint16_t)ctx->seg.size();
+    ci.nseg = (uint8_t)nseg;
+    for (int i = 0; i < nseg; ++i) {
+      const int t0 = i == 0 ? 0 : al[k][i - 1];
+      SegInfo si;
+      si.rho = (uint8_t)rho[(size_t)t0 * W + k];
+      si.sig = (uint8_t)sig[(size_t)t0 * W + k];
+      si.rhop = (uint8_t)rhop[(size_t)t0 * W + k];
+      si.sigp = (uint8_t)sigp[(size_t)t0 * W + k];
+      ctx->seg.push_back(si);
+    }
+    // adjacent-column constraints F_t(k-1) <= F_t(k), one check per time interval
+    ci.cmp_base = (uint16_t)ctx->cmp.size();
+    int ncmp = 0;
+    if (k >= 1) {
+      int la = -1, lb = -1;
+      for (int t = 0; t <= D; ++t) {
+        const int sa = segof[k - 1][t], sb = segof[k][t];
+        if (sa == la && sb == lb) continue;
+        ctx->cmp.push_back(CmpPair{(uint8_t)sa, (uint8_t)sb});
+        la = sa;
+        lb = sb;
+        ++ncmp;
+      }
+    }
+    if (ncmp > 255 || ctx->cmp.size() > 65535) return LOFP_E_UNSUPPORTED;
+    ci.ncmp = (uint8_t)ncmp;
+    // the BS of cut k, in layer order (its cut factor, eq. (1))
+    ci.fac_base = (uint16_t)ctx->fac.size();
+    int nfac = 0;
+    if (k >= 1 && k <= M - 1) {
+      for (int i = 0; i < (int)al[k].size(); ++i) {
+        const int l = al[k][i];
+        FacInfo fi{};
+        fi.bs = act[(size_t)l * W + k];
+        fi.sA = (uint8_t)segof[k - 1][l - 1];
+        fi.i = (uint8_t)i;
+        fi.sC = (uint8_t)segof[k + 1][l - 1];
+        ctx->fac.push_back(fi);
+        ++nfac;
+      }
+    }
+    if (nfac > 255 || ctx->fac.size() > 65535) return LOFP_E_UNSUPPORTED;
+    ci.nfac = (uint8_t)nfac;
+    ci.gate_base = (uint16_t)ctx->gat.size();
+    ci.ngate = (uint8_t)std::min<size_t>(gates_of[k].size(), 255);
+    if (gates_of[k].size() > 255 || ctx->gat.size() + gates_of[k].size() > 65535) return LOFP_E_UNSUPPORTED;
+    for (const GateInfo &g : gates_of[k]) ctx->gat.push_back(g);
+  }
+  // BS parameters and the past-cone photon bound that sizes their Appendix-A blocks
+  ctx->bsi.assign(std::max(ctx->nbs, 1), BSInfo{});
   for (int i = 0; i < ctx->nbs; ++i) {
     const CanonBS &b = ctx->bs[i];
-    int X1 = cap[b.layer - 1][b.cut - 1], X2 = cap[b.layer - 1][b.cut];
-    int Y1 = cap[b.layer][b.cut - 1], Y2 = cap[b.layer][b.cut];
-    bsrow[i] = (int32_t)offsets.size();
-    bsrow[ctx->nbs + i] = X2 + 1;
-    for (int x1 = 0; x1 <= X1; ++x1)
-      for (int x2 = 0; x2 <= X2; ++x2) {
-        int n = x1 + x2;
-        int ylo = std::max(0, n - Y2), yhi = std::min(Y1, n);
-        offsets.push_back((int32_t)edesc.size() - ylo);
-        for (int y1 = ylo; y1 <= yhi; ++y1) {
-          EntryDesc e{};
-          e.bs = (uint16_t)i;
-          e.x1 = (uint8_t)x1;
-          e.x2 = (uint8_t)x2;
-          e.y1 = (uint8_t)y1;
-          edesc.push_back(e);
-        }
-      }
+    BSInfo &bi = ctx->bsi[i];
+    bi.c = std::cos(b.theta);
+    bi.s = std::sin(b.theta);
+    bi.phi = b.phi;
+    bi.cap_lo = (uint8_t)rhop[(size_t)(b.layer - 1) * W + b.cut - 1];
+    bi.cap_hi = (uint8_t)sigp[(size_t)(b.layer - 1) * W + b.cut + 1];
   }
-  if (edesc.empty()) edesc.push_back(EntryDesc{});  // keep pointers valid
-  if (offsets.empty()) offsets.push_back(0);
-  a.nentries = (int)edesc.size();
-  a.noffsets = (int)offsets.size();
-  a.table_bytes = (int)round16((size_t)a.nentries * 16 + (size_t)a.noffsets * 4);
-  CK(ctx->d_edesc.ensure(edesc.size() * sizeof(EntryDesc)), "alloc edesc");
-  CK(ctx->d_offsets.ensure(offsets.size() * 4), "alloc offsets");
-  CK(ctx->d_entries.ensure(edesc.size() * 16), "alloc entries");
-  CK(ctx->d_bsrow.ensure(bsrow.size() * 4), "alloc bs rows");
-  size_t need = edesc.size() * sizeof(EntryDesc) + offsets.size() * 4 + bsrow.size() * 4 + 64;
-  CK(ctx->h_stage.ensure(need), "alloc staging");
-  {
-    uint8_t *st = (uint8_t *)ctx->h_stage.p;
-    size_t o = 0;
-    memcpy(st + o, edesc.data(), edesc.size() * sizeof(EntryDesc));
-    CK(cudaMemcpyAsync(ctx->d_edesc.p, st + o, edesc.size() * sizeof(EntryDesc), cudaMemcpyHostToDevice, stream),
-       "upload edesc");
-    o += edesc.size() * sizeof(EntryDesc);
-    memcpy(st + o, offsets.data(), offsets.size() * 4);
-    CK(cudaMemcpyAsync(ctx->d_offsets.p, st + o, offsets.size() * 4, cudaMemcpyHostToDevice, stream),
-       "upload offsets");
-    o += offsets.size() * 4;
-    memcpy(st + o, bsrow.data(), bsrow.size() * 4);
-    CK(cudaMemcpyAsync(ctx->d_bsrow.p, st + o, bsrow.size() * 4, cudaMemcpyHostToDevice, stream), "upload bs rows");
+  ctx->ngate = (int)gates.size();
+  ctx->gate_ab.assign(2 * std::max<size_t>(gates.size(), 1), 0.0);
+  ctx->gate_mode.assign(std::max<size_t>(gates.size(), 1), 0);
+  ctx->gate_after.assign(std::max<size_t>(gates.size(), 1), 0);
+  for (size_t g = 0; g < gates.size(); ++g) {
+    ctx->gate_ab[2 * g] = gates[g].a;
+    ctx->gate_ab[2 * g + 1] = gates[g].b;
+    ctx->gate_mode[g] = (int16_t)gates[g].mode;
+    ctx->gate_after[g] = (int16_t)gates[g].after_layer;
   }
-  a.edesc = (const EntryDesc *)ctx->d_edesc.p;
-  a.offsets = (const int32_t *)ctx->d_offsets.p;
-  a.entries = (double *)ctx->d_entries.p;
-  a.bs_base = (const int32_t *)ctx->d_bsrow.p;
-  a.bs_stride = (const int32_t *)ctx->d_bsrow.p + ctx->nbs;
-  ctx->stats.table_entries = a.nentries;
-
-  CK(lofp_launch_tables(a, stream), "table kernel");
-  CK(lofp_launch_plan(a, stream), "plan kernel");
-  ctx->stats.launches += (a.nentries > 0 ? 1 : 0) + (a.B > 0 ? 1 : 0);
-  // (sync 2) the largest per-output plan sizes the enumeration kernel's shared memory
-  CK(cudaMemcpyAsync(ctx->h_ctr.p, a.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, stream), "read plan sizes");
-  CK(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
-  const int maxL = hc->maxL, maxF = hc->maxF, maxS = hc->maxS, maxK = hc->maxK;
-  ctx->stats.levels = maxL;
-  CK(cudaEventRecord(ctx->ev_enum0, stream), "cudaEventRecord");
-  if (hc->nfeas > 0) {
-    a.vals_slots = (maxL + 2 + 3) & ~3;  // zero slot, levels, a scratch slot
-    // plans were written with the zero slot of the global bound; re-base is not needed
-    // because the kernel only dereferences slots < maxL and the zero slot below
-    // (the step's uniform loops read up to maxF descriptors / key words and maxS + 3
-    // scatter entries past a level's own list: vals, keys and stack follow inside the
-    // warp's region, so those reads never leave it)
-    a.plan_smem = (int)round16(sizeof(PlanHead) + (size_t)(maxL + maxF) * 16 + 2 * (size_t)maxS);
-    // Chain engine (R17): on when most outputs have chains of >= LOFP_CHAIN_MODE_RBOX box
-    // paths (then every output whose chain box is >= LOFP_CHAIN_RBOX gets its chain).
-    // Otherwise, if most outputs have the chain structure with chains of moderate size
-    // (geometric-mean box >= 2^LOFP_SHORT_CHAIN_LOG2 paths), every such output gets the
-    // engine with the short chains batched (R20; the plans are rebuilt with those
-    // thresholds).  Environment overrides (tests) disable this choice.
-    const bool env_chain = std::getenv("LOFP_NO_CHAIN") || std::getenv("LOFP_FORCE_CHAIN") ||
-                           std::getenv("LOFP_CHAIN_RBOX") || std::getenv("LOFP_CHAIN_RMIN") ||
-                           std::getenv("LOFP_SMALL_PATHS");
-    const double mlog = hc->nchain_ok > 0 ? (double)hc->rbox_log16 / 16.0 / hc->nchain_ok : 0.0;
-    bool short_chains = false;
-    if (!env_chain && 2ull * (unsigned long long)hc->nchain_big < hc->nfeas &&
-        2ull * (unsigned long long)hc->nchain_ok >= hc->nfeas && mlog >= LOFP_SHORT_CHAIN_LOG2) {
-      a.chain_rbox = 1.0;
-      a.chain_rmin = 1;
-      a.small_paths = 256;
-      // the plan kernel counts the feasible outputs and the outstanding work: reset those
-      CK(cudaMemsetAsync(reinterpret_cast<char *>(a.ctr) + offsetof(Counters, nfeas), 0, sizeof(unsigned long long),
-                         stream), "reset counters");
-      CK(cudaMemsetAsync(reinterpret_cast<char *>(a.ctr) + offsetof(Counters, outstanding), 0,
-                         sizeof(unsigned long long), stream), "reset counters");
-      CK(lofp_launch_plan(a, stream), "plan kernel (short chains)");
-      ++ctx->stats.launches;
-      short_chains = true;
-    }
-    a.chain_on = short_chains ||
-                 (hc->nchain > 0 && !std::getenv("LOFP_NO_CHAIN") &&
-                  (2ull * (unsigned long long)hc->nchain_big >= hc->nfeas || std::getenv("LOFP_FORCE_CHAIN")));
-    // key words per lane: every attached factor (none while the engine is on)
-    a.maxfac = a.chain_on ? 0 : maxF;
-    (void)maxK;
-    a.warp_bytes = (int)round16((size_t)a.plan_smem + (size_t)a.vals_slots * 32 + (size_t)a.maxfac * 128 +
-                                (size_t)(a.chain_on ? LOFP_STK_CHAIN : LOFP_STK) * 32 * 20 + 32 +
-                                (a.chain_on ? (size_t)LOFP_W_MAX * 16 + (size_t)LOFP_SUF_ENTRIES * 16 + 33 * 16 + 65 * 4 + 1024 +
-                                                  (a.small_paths > 0 ? 512 + 264 + 4 * 32 * LOFP_SMALL_LEVELS + 16 : 0)
-                                            : 0));
-    int grid = 0, block = 0;
-    size_t smem = 0;
-    cudaError_t e = lofp_enum_config(a, counts != nullptr, &grid, &block, &smem);
-    if (e == cudaErrorInvalidConfiguration)
-      return fail(ctx, LOFP_E_UNSUPPORTED, "BS tables do not fit in shared memory");
-    CK(e, "enumeration config");
-    unsigned lanes = (unsigned)grid * (unsigned)block;
-    // Queue capacity: spills are accepted while fewer than cap/2 are waiting, which
-    // keeps every reused slot's previous item already claimed (see the kernel).
-    unsigned cap_items = 1u << 20;
-    while (cap_items < 8u * lanes) cap_items <<= 1;
-    if (cap_items > ctx->ring_cap) {
-      CK(ctx->d_ring.ensure((size_t)cap_items * sizeof(Item)), "alloc work queue");
-      CK(cudaMemsetAsync(ctx->d_ring.p, 0, (size_t)cap_items * sizeof(Item), stream), "clear work queue");
-      ctx->ring_cap = cap_items;
-    }
-    a.ring = (Item *)ctx->d_ring.p;
-    a.ring_mask = ctx->ring_cap - 1;
-    ctx->stats.smem_bytes = (int32_t)smem;
-    ctx->stats.max_factors = maxF;
-    ctx->stats.max_scatter = maxS;
-    ctx->stats.engine = a.chain_on ? (a.small_paths > 0 ? 2 : 1) : 0;
-    ctx->stats.grid_blocks = grid;
-    ctx->stats.block_threads = block;
-    CK(lofp_launch_enum(a, counts != nullptr, grid, block, smem, stream), "enumeration kernel");
-    ++ctx->stats.launches;
-  }
-  CK(cudaEventRecord(ctx->ev_enum1, stream), "cudaEventRecord");
-  CK(cudaMemcpyAsync(ctx->h_ctr.p, a.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, stream), "read counters");
-  CK(cudaEventRecord(ctx->ev_end, stream), "cudaEventRecord");
-  ctx->have_call = true;
   return LOFP_OK;
 }
 
-}  // namespace
-
-extern "C" {
-
-const char *lofp_status_string(lofp_status s) {
-  switch (s) {
-    case LOFP_OK: return "ok";
-    case LOFP_E_INVALID_ARG: return "invalid argument";
-    case LOFP_E_UNSUPPORTED: return "unsupported";
-    case LOFP_E_CUDA: return "CUDA error";
-    case LOFP_E_OOM: return "out of device memory";
-    case LOFP_E_BAD_OUTPUT: return "bad output row";
-  }
-  return "unknown status";
+template <class T>
+size_t append(std::vector<char> &blob, const std::vector<T> &v) {
+  size_t off = (blob.size() + 15) & ~size_t(15);
+  blob.resize(off + std::max<size_t>(v.size(), 1) * sizeof(T), 0);
+  if (!v.empty()) std::memcpy(blob.data() + off, v.data(), v.size() * sizeof(T));
+  return off;
 }
 
-const char *lofp_last_error(const lofp_ctx *ctx) { return ctx ? ctx->err.c_str() : ""; }
+lofp_status upload_topology(lofp_ctx *ctx) {
+  std::vector<char> blob;
+  ctx->off_col = append(blob, ctx->col);
+  ctx->off_seg = append(blob, ctx->seg);
+  ctx->off_cmp = append(blob, ctx->cmp);
+  ctx->off_fac = append(blob, ctx->fac);
+  ctx->off_gat = append(blob, ctx->gat);
+  ctx->off_bsi = append(blob, ctx->bsi);
+  ctx->off_gab = append(blob, ctx->gate_ab);
+  ctx->off_gm = append(blob, ctx->gate_mode);
+  ctx->off_gl = append(blob, ctx->gate_after);
+  CK(ctx->d_topo.ensure(blob.size()), "alloc topology");
+  CK(cudaMemcpy(ctx->d_topo.p, blob.data(), blob.size(), cudaMemcpyHostToDevice), "upload topology");
+  return LOFP_OK;
+}
 
-lofp_status lofp_create(int32_t modes, int32_t n_layers, const int32_t *bs_per_layer, const lofp_bs *bs,
-                        lofp_ctx **out) {
+lofp_status create_impl(int32_t modes, int32_t n_layers, const int32_t *bs_per_layer, const lofp_bs *bs,
+                        int32_t n_gates, const lofp_gate *gates, lofp_ctx **out) {
   if (!out) return LOFP_E_INVALID_ARG;
   *out = nullptr;
-  if (modes < 1 || n_layers < 0) return LOFP_E_INVALID_ARG;
-  if (modes > LOFP_MAX_MODES || n_layers > LOFP_MAX_LAYERS) return LOFP_E_UNSUPPORTED;
+  if (modes < 1 || n_layers < 0 || n_gates < 0) return LOFP_E_INVALID_ARG;
+  if (modes > LOFP_MAX_MODES || n_layers > LOFP_MAX_LAYERS || n_gates > LOFP_MAX_GATES) return LOFP_E_UNSUPPORTED;
   if (n_layers > 0 && !bs_per_layer) return LOFP_E_INVALID_ARG;
+  if (n_gates > 0 && !gates) return LOFP_E_INVALID_ARG;
   int64_t total = 0;
   for (int l = 0; l < n_layers; ++l) {
     if (bs_per_layer[l] < 0) return LOFP_E_INVALID_ARG;
@@ -436,6 +312,14 @@ lofp_status lofp_create(int32_t modes, int32_t n_layers, const int32_t *bs_per_l
   }
   if (total > 0 && !bs) return LOFP_E_INVALID_ARG;
   if (total > 65535) return LOFP_E_UNSUPPORTED;
+  std::vector<lofp_gate> gv;
+  for (int g = 0; g < n_gates; ++g) {
+    const lofp_gate &x = gates[g];
+    if (x.mode < 0 || x.mode >= modes || x.after_layer < 0 || x.after_layer > n_layers || !std::isfinite(x.a) ||
+        !std::isfinite(x.b))
+      return LOFP_E_INVALID_ARG;
+    gv.push_back(x);
+  }
   lofp_ctx *ctx = new (std::nothrow) lofp_ctx();
   if (!ctx) return LOFP_E_OOM;
   ctx->M = modes;
@@ -470,35 +354,29 @@ lofp_status lofp_create(int32_t modes, int32_t n_layers, const int32_t *bs_per_l
       ctx->bs.push_back(c);
     }
   }
-  // layer-major, top to bottom inside a layer: the DFS level order ("systematic way")
   std::stable_sort(ctx->bs.begin(), ctx->bs.end(),
                    [](const CanonBS &x, const CanonBS &y) { return x.layer != y.layer ? x.layer < y.layer : x.cut < y.cut; });
-  if (st == LOFP_OK) st = plan_circuit(ctx);
+  if (st == LOFP_OK) st = build_topology(ctx, gv);
   if (st != LOFP_OK) {
     delete ctx;
     return st;
   }
   cudaError_t e = cudaGetDevice(&ctx->device);
-  std::vector<int16_t> lk(2 * std::max(ctx->nbs, 1));
-  std::vector<double> csv(4 * std::max(ctx->nbs, 1));
-  for (int i = 0; i < ctx->nbs; ++i) {
-    lk[2 * i] = (int16_t)ctx->bs[i].layer;
-    lk[2 * i + 1] = (int16_t)ctx->bs[i].cut;
-    csv[4 * i] = std::cos(ctx->bs[i].theta);
-    csv[4 * i + 1] = std::sin(ctx->bs[i].theta);
-    csv[4 * i + 2] = std::cos(ctx->bs[i].phi);
-    csv[4 * i + 3] = std::sin(ctx->bs[i].phi);
+  if (e == cudaSuccess) {
+    lofp_status s2 = upload_topology(ctx);
+    if (s2 != LOFP_OK) {
+      lofp_destroy(ctx);
+      return s2;
+    }
   }
-  if (e == cudaSuccess) e = ctx->d_maps.ensure(ctx->maps.size());
-  if (e == cudaSuccess) e = cudaMemcpy(ctx->d_maps.p, ctx->maps.data(), ctx->maps.size(), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = ctx->d_bs_lk.ensure(lk.size() * 2);
-  if (e == cudaSuccess) e = cudaMemcpy(ctx->d_bs_lk.p, lk.data(), lk.size() * 2, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = ctx->d_bs_cs.ensure(csv.size() * 8);
-  if (e == cudaSuccess) e = cudaMemcpy(ctx->d_bs_cs.p, csv.data(), csv.size() * 8, cudaMemcpyHostToDevice);
-  for (cudaEvent_t *ev : {&ctx->ev_start, &ctx->ev_enum0, &ctx->ev_enum1, &ctx->ev_end})
+  for (cudaEvent_t *ev : {&ctx->ev_start, &ctx->ev_u0, &ctx->ev_u1, &ctx->ev_end})
     if (e == cudaSuccess) e = cudaEventCreate(ev);
-  if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_end, 0);
-  if (e == cudaSuccess) e = cudaEventSynchronize(ctx->ev_end);
+  if (e == cudaSuccess) e = ctx->h_ctr.ensure(sizeof(Counters));
+  if (e == cudaSuccess) {
+    ctx->grid = lofp_units_grid(ctx->device);
+    if (ctx->grid <= 0) e = cudaErrorInvalidDevice;
+  }
+  ctx->slab_bytes = env_ll("LOFP_SLAB_MB", 16) << 20;
   if (e != cudaSuccess) {
     lofp_status s = e == cudaErrorMemoryAllocation ? LOFP_E_OOM : LOFP_E_CUDA;
     lofp_destroy(ctx);
@@ -508,9 +386,164 @@ lofp_status lofp_create(int32_t modes, int32_t n_layers, const int32_t *bs_per_l
   return LOFP_OK;
 }
 
+// Validated per-call setup shared by the path-sum and contraction entries.
+lofp_status prepare(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const int32_t *output_occ,
+                    double *amps, cudaStream_t stream, CallParams &P, bool &capturing) {
+  if (!input_occ || batch < 0) return fail(ctx, LOFP_E_INVALID_ARG, "null input_occ or negative batch");
+  if (batch > 0 && (!output_occ || !amps)) return fail(ctx, LOFP_E_INVALID_ARG, "null output_occ or amps");
+  if (batch > (int64_t)0x7fffffff) return fail(ctx, LOFP_E_UNSUPPORTED, "batch too large");
+  const int M = ctx->M;
+  int N = 0;
+  for (int i = 0; i < M; ++i) {
+    if (input_occ[i] < 0) return fail(ctx, LOFP_E_INVALID_ARG, "negative input occupation");
+    N += input_occ[i];
+    if (N > LOFP_MAX_PHOTONS) return fail(ctx, LOFP_E_UNSUPPORTED, "too many photons");
+  }
+  std::memset(&P, 0, sizeof(P));
+  P.M = M;
+  P.D = ctx->D;
+  P.N = N;
+  P.B = (int)batch;
+  P.nbs = ctx->nbs;
+  P.ngate = ctx->ngate;
+  P.cumS[0] = 0;
+  for (int i = 0; i < M; ++i) P.cumS[i + 1] = (uint8_t)(P.cumS[i] + input_occ[i]);
+  char *topo = (char *)ctx->d_topo.p;
+  P.col = (const ColInfo *)(topo + ctx->off_col);
+  P.seg = (const SegInfo *)(topo + ctx->off_seg);
+  P.cmp = (const CmpPair *)(topo + ctx->off_cmp);
+  P.fac = (const FacInfo *)(topo + ctx->off_fac);
+  P.gat = (const GateInfo *)(topo + ctx->off_gat);
+  P.bsi = (const BSInfo *)(topo + ctx->off_bsi);
+  P.gate_ab = (const double *)(topo + ctx->off_gab);
+  P.gate_mode = (const int16_t *)(topo + ctx->off_gm);
+  P.gate_after = (const int16_t *)(topo + ctx->off_gl);
+  // Appendix-A table: per BS all (x1, x2, y1) with x1 + x2 <= its past-cone photon bound
+  long long entries = 0;
+  for (int i = 0; i < ctx->nbs; ++i) {
+    const BSInfo &bi = ctx->bsi[i];
+    const int cap = std::min(N, (int)P.cumS[bi.cap_hi] - (int)P.cumS[bi.cap_lo]);
+    entries += tri_entries(cap);
+  }
+  ctx->table_entries = entries;
+  CK(ctx->d_table.ensure((size_t)std::max(entries, 1ll) * 16), "alloc table");
+  CK(ctx->d_taboff.ensure((size_t)(ctx->nbs + 1) * 8), "alloc table offsets");
+  CK(ctx->d_gatetab.ensure((size_t)std::max(ctx->ngate, 1) * (N + 1) * 16), "alloc gate table");
+  P.table = (double2 *)ctx->d_table.p;
+  P.tab_off = (long long *)ctx->d_taboff.p;
+  P.gate_tab = (double2 *)ctx->d_gatetab.p;
+  P.table_cap = (long long)(ctx->d_table.n / 16);
+  // units: per-output slots; partial sums; per-output status/counters
+  const long long B = std::max<long long>(batch, 1);
+  long long budget = (1ll << 21) / B;
+  budget = std::max(8ll, std::min(budget, 1ll << 17));
+  P.budget = (int)budget;
+  P.thr = (unsigned long long)env_ll("LOFP_UNIT_PATHS", 1ll << 26);
+  P.slab_bytes = ctx->slab_bytes;
+  CK(ctx->d_units.ensure((size_t)(B * budget) * sizeof(Unit)), "alloc units");
+  CK(ctx->d_partial.ensure((size_t)(B * budget) * 16), "alloc partials");
+  CK(ctx->d_nunits.ensure((size_t)B * 4), "alloc nunits");
+  CK(ctx->d_ubase.ensure((size_t)(B + 1) * 4), "alloc ubase");
+  CK(ctx->d_status.ensure((size_t)B), "alloc status");
+  CK(ctx->d_pexp.ensure((size_t)B * 8), "alloc pexp");
+  CK(ctx->d_pdone.ensure((size_t)B * 8), "alloc pdone");
+  CK(ctx->d_slab.ensure((size_t)ctx->grid * (size_t)ctx->slab_bytes), "alloc scratch");
+  CK(ctx->d_ctr.ensure(sizeof(Counters)), "alloc counters");
+  P.units = (Unit *)ctx->d_units.p;
+  P.partial = (double2 *)ctx->d_partial.p;
+  P.nunits = (int *)ctx->d_nunits.p;
+  P.ubase = (int *)ctx->d_ubase.p;
+  P.status = (uint8_t *)ctx->d_status.p;
+  P.pexp = (unsigned long long *)ctx->d_pexp.p;
+  P.pdone = (unsigned long long *)ctx->d_pdone.p;
+  P.slab = (char *)ctx->d_slab.p;
+  P.ctr = (Counters *)ctx->d_ctr.p;
+  P.T = output_occ;
+  P.amps = (double2 *)amps;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CK(cudaStreamIsCapturing(stream, &cs), "cudaStreamIsCapturing");
+  capturing = cs != cudaStreamCaptureStatusNone;
+  // order after the previous call on this context (its buffers are reused)
+  if (!capturing && ctx->have_call) CK(cudaStreamWaitEvent(stream, ctx->ev_end, 0), "cudaStreamWaitEvent");
+  return LOFP_OK;
+}
+
+lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const int32_t *output_occ, double *amps,
+                unsigned long long *counts, cudaStream_t stream, int mode) {
+  if (!ctx) return LOFP_E_INVALID_ARG;
+  ctx->err.clear();
+  DeviceGuard guard(ctx->device);
+  CallParams P;
+  bool capturing = false;
+  lofp_status s = prepare(ctx, input_occ, batch, output_occ, amps, stream, P, capturing);
+  if (s != LOFP_OK) return s;
+  ctx->stats = lofp_run_stats{};
+  ctx->stats.batch = batch;
+  if (batch == 0) return LOFP_OK;
+  P.counts = counts;
+  P.mode = mode;
+  ctx->timed = !capturing;
+  if (ctx->timed) CK(cudaEventRecord(ctx->ev_start, stream), "cudaEventRecord");
+  CK(cudaMemsetAsync(P.ctr, 0, sizeof(Counters), stream), "clear counters");
+  int launches = 0;
+  std::vector<int32_t> S(input_occ, input_occ + ctx->M);
+  if (!ctx->tables_valid || S != ctx->tab_S) {
+    CK((cudaError_t)lofp_launch_tables(&P, stream), "table kernels");
+    launches += ctx->nbs > 0 ? 2 : 1;
+    ctx->tab_S = S;
+    ctx->tables_valid = true;
+  }
+  if (mode == 0) {
+    CK((cudaError_t)lofp_launch_paths(&P, ctx->grid, stream, ctx->timed ? ctx->ev_u0 : nullptr,
+                                      ctx->timed ? ctx->ev_u1 : nullptr),
+       "path-sum kernels");
+    launches += 4;
+  } else {
+    CK((cudaError_t)lofp_launch_contract(&P, ctx->grid, stream), "contraction kernels");
+    launches += 1;
+  }
+  CK(cudaMemcpyAsync(ctx->h_ctr.p, P.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, stream), "read counters");
+  CK(cudaEventRecord(ctx->ev_end, stream), "cudaEventRecord");
+  ctx->have_call = true;
+  ctx->stats.launches = launches;
+  ctx->stats.mode = mode;
+  ctx->stats.grid_blocks = ctx->grid;
+  ctx->stats.block_threads = kThreads;
+  ctx->stats.table_entries = ctx->table_entries;
+  return LOFP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *lofp_status_string(lofp_status s) {
+  switch (s) {
+    case LOFP_OK: return "ok";
+    case LOFP_E_INVALID_ARG: return "invalid argument";
+    case LOFP_E_UNSUPPORTED: return "unsupported";
+    case LOFP_E_CUDA: return "CUDA error";
+    case LOFP_E_OOM: return "out of device memory";
+    case LOFP_E_BAD_OUTPUT: return "bad output row";
+  }
+  return "unknown status";
+}
+
+const char *lofp_last_error(const lofp_ctx *ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+lofp_status lofp_create(int32_t modes, int32_t n_layers, const int32_t *bs_per_layer, const lofp_bs *bs,
+                        lofp_ctx **out) {
+  return create_impl(modes, n_layers, bs_per_layer, bs, 0, nullptr, out);
+}
+
+lofp_status lofp_create_ex(int32_t modes, int32_t n_layers, const int32_t *bs_per_layer, const lofp_bs *bs,
+                           int32_t n_gates, const lofp_gate *gates, lofp_ctx **out) {
+  return create_impl(modes, n_layers, bs_per_layer, bs, n_gates, gates, out);
+}
+
 lofp_status lofp_amplitudes(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const int32_t *output_occ,
                             double *amps, void *cuda_stream) {
-  return run(ctx, input_occ, batch, output_occ, amps, nullptr, (cudaStream_t)cuda_stream);
+  return run(ctx, input_occ, batch, output_occ, amps, nullptr, (cudaStream_t)cuda_stream, 0);
 }
 
 lofp_status lofp_amplitudes_counted(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch,
@@ -518,7 +551,8 @@ lofp_status lofp_amplitudes_counted(lofp_ctx *ctx, const int32_t *input_occ, int
                                     void *cuda_stream) {
   if (!ctx) return LOFP_E_INVALID_ARG;
   if (batch > 0 && !path_counts) return fail(ctx, LOFP_E_INVALID_ARG, "null path_counts");
-  return run(ctx, input_occ, batch, output_occ, amps, (unsigned long long *)path_counts, (cudaStream_t)cuda_stream);
+  return run(ctx, input_occ, batch, output_occ, amps, (unsigned long long *)path_counts, (cudaStream_t)cuda_stream,
+             0);
 }
 
 lofp_status lofp_amplitudes_host(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const int32_t *output_occ,
@@ -527,15 +561,15 @@ lofp_status lofp_amplitudes_host(lofp_ctx *ctx, const int32_t *input_occ, int64_
   if (batch < 0 || !input_occ) return fail(ctx, LOFP_E_INVALID_ARG, "bad arguments");
   if (batch == 0) return LOFP_OK;
   if (!output_occ || !amps) return fail(ctx, LOFP_E_INVALID_ARG, "null output_occ or amps");
-  CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+  DeviceGuard guard(ctx->device);
   if (!ctx->own_stream) CK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking), "stream");
   size_t tb = (size_t)batch * ctx->M * 4, ab = (size_t)batch * 16;
-  CK(cudaEventSynchronize(ctx->ev_end), "cudaEventSynchronize");
+  if (ctx->have_call) CK(cudaEventSynchronize(ctx->ev_end), "cudaEventSynchronize");
   CK(ctx->d_hostT.ensure(tb), "alloc T");
   CK(ctx->d_hostA.ensure(ab), "alloc amps");
   CK(cudaMemcpyAsync(ctx->d_hostT.p, output_occ, tb, cudaMemcpyHostToDevice, ctx->own_stream), "copy T");
-  lofp_status s =
-      run(ctx, input_occ, batch, (const int32_t *)ctx->d_hostT.p, (double *)ctx->d_hostA.p, nullptr, ctx->own_stream);
+  lofp_status s = run(ctx, input_occ, batch, (const int32_t *)ctx->d_hostT.p, (double *)ctx->d_hostA.p, nullptr,
+                      ctx->own_stream, 0);
   if (s != LOFP_OK) return s;
   CK(cudaMemcpyAsync(amps, ctx->d_hostA.p, ab, cudaMemcpyDeviceToHost, ctx->own_stream), "copy amps");
   CK(cudaStreamSynchronize(ctx->own_stream), "cudaStreamSynchronize");
@@ -544,64 +578,45 @@ lofp_status lofp_amplitudes_host(lofp_ctx *ctx, const int32_t *input_occ, int64_
 
 lofp_status lofp_stats(lofp_ctx *ctx, lofp_run_stats *out) {
   if (!ctx || !out) return LOFP_E_INVALID_ARG;
+  DeviceGuard guard(ctx->device);
   if (ctx->have_call) {
     CK(cudaEventSynchronize(ctx->ev_end), "cudaEventSynchronize");
     const Counters *hc = (const Counters *)ctx->h_ctr.p;
-    ctx->stats.feasible = (int64_t)hc->nfeas;
-    ctx->stats.items = (int64_t)hc->items;
-    ctx->stats.spills = (int64_t)hc->spills;
-    ctx->stats.donations = (int64_t)hc->donations;
-    ctx->stats.overflows = (int64_t)hc->ovf;
-    ctx->stats.paths = (int64_t)hc->leaves;
-    ctx->stats.cmuls = (int64_t)hc->cmuls;
-    ctx->stats.chains = (int64_t)hc->chains;
-    ctx->stats.chain_fallbacks = (int64_t)hc->chain_fb;
-    ctx->stats.bad_rows = (int32_t)hc->bad_rows;
-    float ms = 0.f;
-    if (cudaEventElapsedTime(&ms, ctx->ev_enum0, ctx->ev_enum1) == cudaSuccess) ctx->stats.enum_ms = ms;
-    if (cudaEventElapsedTime(&ms, ctx->ev_start, ctx->ev_end) == cudaSuccess) ctx->stats.total_ms = ms;
-    ctx->have_call = false;
+    lofp_run_stats &st = ctx->stats;
+    st.feasible = (int64_t)hc->feasible;
+    st.paths = (int64_t)hc->paths;
+    st.cmuls = (int64_t)hc->cmuls;
+    st.units = (int64_t)hc->units;
+    st.subsplits = (int64_t)hc->subsplits;
+    st.pairs = (int64_t)hc->pairs;
+    st.elements = (int64_t)hc->elements;
+    st.unsupported = (int64_t)hc->unsupported;
+    st.bad_rows = (int64_t)hc->bad_rows;
+    st.check_errors = (int64_t)hc->table_error;
+    st.max_states = (int64_t)hc->max_states;
+    st.max_list = (int64_t)hc->max_list;
+    if (ctx->timed) {
+      float ms = 0.f;
+      if (st.mode == 0 && cudaEventElapsedTime(&ms, ctx->ev_u0, ctx->ev_u1) == cudaSuccess) st.units_ms = ms;
+      if (cudaEventElapsedTime(&ms, ctx->ev_start, ctx->ev_end) == cudaSuccess) st.total_ms = ms;
+      if (st.mode == 1) st.units_ms = st.total_ms;
+    }
   }
   *out = ctx->stats;
-  return ctx->stats.bad_rows ? LOFP_E_BAD_OUTPUT : LOFP_OK;
-}
-
-lofp_status lofp_work_histograms(lofp_ctx *ctx, uint64_t *handover, uint64_t *spill) {
-  if (!ctx || !handover || !spill) return LOFP_E_INVALID_ARG;
-  if (ctx->h_ctr.p == nullptr) {
-    for (int i = 0; i < 64; ++i) handover[i] = spill[i] = 0;
-    return LOFP_OK;
-  }
-  CK(cudaEventSynchronize(ctx->ev_end), "cudaEventSynchronize");
-  const Counters *hc = (const Counters *)ctx->h_ctr.p;
-  for (int i = 0; i < 64; ++i) {
-    handover[i] = hc->don_hist[i];
-    spill[i] = hc->spill_hist[i];
-  }
-  return LOFP_OK;
-}
-
-lofp_status lofp_phase_cycles(lofp_ctx *ctx, uint64_t *cycles) {
-  if (!ctx || !cycles) return LOFP_E_INVALID_ARG;
-  for (int i = 0; i < 8; ++i) cycles[i] = 0;
-  if (ctx->h_ctr.p == nullptr) return LOFP_OK;
-  CK(cudaEventSynchronize(ctx->ev_end), "cudaEventSynchronize");
-  const Counters *hc = (const Counters *)ctx->h_ctr.p;
-  for (int i = 0; i < 8; ++i) cycles[i] = hc->phase_cyc[i];
+  if (ctx->stats.bad_rows) return LOFP_E_BAD_OUTPUT;
   return LOFP_OK;
 }
 
 void lofp_destroy(lofp_ctx *ctx) {
   if (!ctx) return;
-  cudaSetDevice(ctx->device);
-  if (ctx->ev_end) cudaEventSynchronize(ctx->ev_end);
-  for (DevBuf *b : {&ctx->d_maps, &ctx->d_bs_lk, &ctx->d_bs_cs, &ctx->d_flags, &ctx->d_plans, &ctx->d_feas,
-                    &ctx->d_ctr, &ctx->d_ring, &ctx->d_edesc, &ctx->d_offsets, &ctx->d_entries, &ctx->d_cumS,
-                    &ctx->d_bsrow, &ctx->d_hostT, &ctx->d_hostA})
+  DeviceGuard guard(ctx->device);
+  if (ctx->have_call && ctx->ev_end) cudaEventSynchronize(ctx->ev_end);
+  for (DevBuf *b : {&ctx->d_topo, &ctx->d_table, &ctx->d_taboff, &ctx->d_gatetab, &ctx->d_units, &ctx->d_nunits,
+                    &ctx->d_ubase, &ctx->d_status, &ctx->d_pexp, &ctx->d_pdone, &ctx->d_partial, &ctx->d_slab,
+                    &ctx->d_ctr, &ctx->d_hostT, &ctx->d_hostA})
     b->release();
-  ctx->h_stage.release();
   ctx->h_ctr.release();
-  for (cudaEvent_t ev : {ctx->ev_start, ctx->ev_enum0, ctx->ev_enum1, ctx->ev_end})
+  for (cudaEvent_t ev : {ctx->ev_start, ctx->ev_u0, ctx->ev_u1, ctx->ev_end})
     if (ev) cudaEventDestroy(ev);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;

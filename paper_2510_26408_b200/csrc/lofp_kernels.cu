@@ -1,1396 +1,1055 @@
-// lofp_kernels.cu — sm_100a kernels of the LOFP path sum (arXiv 2510.26408).
+// lofp_kernels.cu — sm_100a kernels of liblofp (the LOFP path sum of arXiv 2510.26408).
 //
-//   lofp_prep_kernel   per output row: validity, photon number, per-mode max of T.
-//   lofp_table_kernel  Appendix-A BS elements for every (x1, x2, y1) inside
-//                      the paper's light-cone caps, fp64.
-//   lofp_plan_kernel   per output: G = cum(T), exact light-cone reachability (reading
-//                      R5), the output's DFS levels (free "green" waveguides)
-//                      and attached factors, and the product of the constant factors.
-//   lofp_enum_kernel   persistent path enumeration (eq. (1)): one warp per work
-//                      item (a subtree of one output), one iterative DFS per lane over
-//                      the item's levels with its state in shared memory, fp64 complex
-//                      products of Appendix-A factors staged in shared memory, subtrees
-//                      handed between lanes of a warp (shared memory) and between warps
-//                      (a global atomic work queue); warp-shuffle reduction per item.
+// Pipeline of one lofp_amplitudes call (all on the caller's stream, no host sync):
+//   lofp_table_off_kernel   per-BS Appendix-A block sizes from the input's past light cones
+//                            and the phase-gate tables
+//   lofp_table_kernel       Appendix-A elements <y1,y2|BS|x1,x2> by the stable
+//                           four-term creation-operator recurrence (reading R1/R18)
+//   lofp_plan_kernel        per output: column states inside the light-cone box (R5, R15),
+//                           exact path counts by a transfer over columns (R6), and the split
+//                           of the path tree into units of <= thr paths (a prefix split,
+//                           BASELINE north_star "splits the path tree ... into prefixes")
+//   lofp_scan_kernel        unit numbering
+//   lofp_units_kernel       the hot path: per unit, the column-split enumeration (R20):
+//                           half-path lists on both sides of a column pair, then every path
+//                           formed as (left half-path) x (right half-path), one complex
+//                           multiply-accumulate per path on the FP64 pipe
+//   lofp_final_kernel       per output: sum of its units in a fixed order (deterministic)
 //
-// The arithmetic follows the paper; the data layout is described in lofp_internal.h
-// and DESIGN.md.  No code here is shared with oracle/.
+// Notation: column k holds F_t(k), t = 0..D (photons in modes < k after layer t) as a
+// tuple of segment values; see lofp_internal.h.
 #include <cuda_runtime.h>
-#include <stdint.h>
+
+#include <cstdint>
 
 #include "lofp_internal.h"
 
+using namespace lofp;
+
 namespace {
 
-constexpr unsigned FULL = 0xffffffffu;
+typedef unsigned long long ull;
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-  // (a.x + i a.y)(b.x + i b.y): 2 DMUL + 2 DFMA
-  double2 r;
-  r.x = fma(a.x, b.x, -a.y * b.y);
-  r.y = fma(a.x, b.y, a.y * b.x);
-  return r;
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 
-// ---------------------------------------------------------------------------
-// prep: row validity, photon number, per-mode max of T over the batch
-// ---------------------------------------------------------------------------
-__global__ void lofp_prep_kernel(CallArgs a) {
-  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q >= a.B) return;
-  const int32_t *t = a.T + q * a.M;
-  int sum = 0, bad = 0;
-  for (int m = 0; m < a.M; ++m) {
-    int v = t[m];
-    if (v < 0) bad = 1;
-    sum += v;
+__device__ __forceinline__ ull sat_add(ull a, ull b) {
+  ull c = a + b;
+  return c < a ? ~0ull : c;
+}
+
+__device__ __forceinline__ long long tri_dev(int n) {  // sum_{m<n} (m+1)^2
+  return (long long)n * (n + 1) * (2 * n + 1) / 6;
+}
+
+// ---- scratch layout of one block (global memory, L1/L2 resident) -------------------
+struct Seg {             // one (predecessor, state) pair of a BFS level or a column pair
+  uint32_t dst, src, len;
+  uint16_t p, s;
+};
+
+struct StackEnt {
+  int32_t j;
+  uint16_t sjm1, sj;
+  double re, im;
+  ull pad;
+};
+
+constexpr long long kOffSegs = 0;
+constexpr long long kOffFL = kOffSegs + (long long)kMaxSegments * sizeof(Seg);
+constexpr long long kOffFR = kOffFL + (long long)kMaxStates * 16;
+constexpr long long kOffStack = kOffFR + (long long)kMaxStates * 16;
+constexpr long long kOffA = kOffStack + (long long)kStackMax * sizeof(StackEnt);
+constexpr long long kOffB = kOffA + (long long)kMaxStates * 4;
+constexpr long long kOffTmp = kOffB + (long long)kMaxStates * 4;
+constexpr long long kOffTmp2 = kOffTmp + (long long)kMaxStates * 4;
+constexpr int kSegSlots = 8192;  // segment descriptors of all columns of one output
+constexpr long long kOffSegLo = kOffTmp2 + (long long)kMaxStates * 4;
+constexpr long long kOffSegRad = kOffSegLo + kSegSlots;
+constexpr long long kOffSegStr = kOffSegRad + kSegSlots;
+constexpr long long kOffVar = kOffSegStr + (long long)kSegSlots * 4;  // vals, cL, cR, lists
+
+struct Block {           // per-block views (pointers into the slab) + shared-memory state
+  char *slab;
+  Seg *segs;
+  double2 *FL, *FR;
+  StackEnt *stack;
+  uint32_t *offA, *offB, *tmp, *tmp2;
+  uint8_t *segLo, *segRad;
+  int32_t *segStr;
+  uint8_t *vals;
+  ull *cL, *cR;
+  char *lists;
+  long long list_bytes;
+};
+
+struct Shared {
+  ColInfo col[kMaxModes + 1];
+  int G[kMaxModes + 1];
+  int T[kMaxModes];
+  int n[kMaxModes + 1];    // states per column
+  int vb[kMaxModes + 1];   // vals base
+  int cb[kMaxModes + 1];   // count base
+  ull NL[kMaxModes + 1], NR[kMaxModes + 1];
+  uint32_t scan[kThreads];
+  int status;
+  int ks;
+  int nsegs;
+  uint32_t total;
+  int sp;                  // stack pointer
+  StackEnt top;
+  int q_cached;
+  int unit;
+};
+
+// slab carve of one output: vals, cL, cR, then the half-path lists (needs sh.n/vb/cb)
+__device__ __forceinline__ void carve(const CallParams &p, Block &b, const Shared &sh) {
+  const int M = p.M;
+  const long long vb = sh.vb[M] + (long long)sh.n[M] * sh.col[M].nseg;
+  const long long cb = sh.cb[M] + sh.n[M];
+  const long long vbytes = (vb + 15) & ~15ll;
+  b.vals = (uint8_t *)(b.slab + kOffVar);
+  b.cL = (ull *)(b.slab + kOffVar + vbytes);
+  b.cR = b.cL + cb;
+  const long long used = kOffVar + vbytes + 16 * cb;
+  b.lists = b.slab + used;
+  b.list_bytes = p.slab_bytes - used;
+}
+
+__device__ __forceinline__ const uint8_t *vrow(const Block &b, const Shared &sh, int k, int s) {
+  return b.vals + sh.vb[k] + s * sh.col[k].nseg;
+}
+
+// F(k-1) <= F(k) at every time (non-negative occupations of mode k-1)
+__device__ __forceinline__ bool compat(const CallParams &p, const Block &b, const Shared &sh, int k, int sa, int sb) {
+  const ColInfo &ck = sh.col[k];
+  const uint8_t *va = vrow(b, sh, k - 1, sa);
+  const uint8_t *vb = vrow(b, sh, k, sb);
+  for (int c = 0; c < ck.ncmp; ++c) {
+    const CmpPair pr = p.cmp[ck.cmp_base + c];
+    if (va[pr.sa] > vb[pr.sb]) return false;
   }
-  uint8_t f = 0;
-  if (bad) {
-    f = 2;
-    atomicAdd(&a.ctr->bad_rows, 1ull);
-  } else if (sum == a.N) {
-    f = 1;
-    for (int m = 0; m < a.M; ++m) {
-      int v = t[m];
-      if (v > 0) atomicMax(&a.ctr->tmax[m], v);
+  return true;
+}
+
+__device__ __forceinline__ bool live(const Block &b, const Shared &sh, int k, int s) {
+  return b.cL[sh.cb[k] + s] != 0 && b.cR[sh.cb[k] + s] != 0;
+}
+
+// Cut factor of cut c: the product of the Appendix-A elements of the BS on modes (c-1, c)
+// (eq. (1)) for columns c-1, c, c+1 in states sa, sb, sc, times the phase gates
+// folded into cut c.  Vacuum BS (x1 + x2 = 0) contribute exactly 1.
+__device__ double2 cut_factor(const CallParams &p, const Block &b, const Shared &sh, int c, int sa, int sb, int sc,
+                              ull &cm) {
+  double2 f = make_double2(1.0, 0.0);
+  if (c < 1 || c > p.M - 1) return f;
+  const ColInfo &cc = sh.col[c];
+  const uint8_t *va = vrow(b, sh, c - 1, sa);
+  const uint8_t *vb = vrow(b, sh, c, sb);
+  const uint8_t *vc = vrow(b, sh, c + 1, sc);
+  for (int t = 0; t < cc.nfac; ++t) {
+    const FacInfo fi = p.fac[cc.fac_base + t];
+    const int A = va[fi.sA], Bm = vb[fi.i], Bp = vb[fi.i + 1], C = vc[fi.sC];
+    const int x1 = Bm - A, x2 = C - Bm, y1 = Bp - A, n = x1 + x2;
+    if (n == 0) continue;
+    const long long idx = p.tab_off[fi.bs] + tri_dev(n) + (long long)x1 * (n + 1) + y1;
+    if (x1 < 0 || x2 < 0 || y1 < 0 || y1 > n || idx >= p.tab_off[fi.bs + 1]) {
+      atomicAdd(&p.ctr->table_error, 1ull);
+      continue;
     }
+    f = cmul(f, p.table[idx]);
+    ++cm;
   }
-  a.flags[q] = f;
-  const double nan = __longlong_as_double(0x7ff8000000000000ll);
-  a.amps[2 * q] = bad ? nan : 0.0;
-  a.amps[2 * q + 1] = bad ? nan : 0.0;
-  if (a.counts) a.counts[q] = 0;
-}
-
-// ---------------------------------------------------------------------------
-// Appendix A: <y1,y2|BS|x1,x2> = e^{i phi (x1 - y1)} sqrt(x1! x2! y1! y2!)
-//   * sum_t (-1)^{y1-t} c^{x2-y1+2t} s^{x1+y1-2t} / (t! (y1-t)! (x1-t)! (x2-y1+t)!)
-// with max(0, y1-x2, x1-y2) <= t <= min(x1, y1).  This is the paper's t-sum
-// (factorial read as (x2-y1+t)!, reading R1) with U11 = U22 = c,
-// U12 = -e^{-i phi} s, U21 = e^{i phi} s substituted (eq. bs_matrix).
-// ---------------------------------------------------------------------------
-__device__ double dfact(int n) {
-  double f = 1.0;
-  for (int i = 2; i <= n; ++i) f *= (double)i;
+  for (int t = 0; t < cc.ngate; ++t) {
+    const GateInfo gi = p.gat[cc.gate_base + t];
+    const uint8_t *lo = gi.col_off ? vb : va;
+    const uint8_t *hi = gi.col_off ? vc : vb;
+    const int n = (int)hi[gi.seg_hi] - (int)lo[gi.seg_lo];
+    f = cmul(f, p.gate_tab[gi.gate * (p.N + 1) + n]);
+    ++cm;
+  }
   return f;
 }
 
-__device__ double ipow(double x, int n) {  // x^n, n >= 0, 0^0 = 1
-  double r = 1.0;
-  for (int i = 0; i < n; ++i) r *= x;
-  return r;
-}
-
-__global__ void lofp_table_kernel(CallArgs a) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.nentries) return;
-  EntryDesc e = a.edesc[i];
-  const double *cs = a.bs_cs + 4 * e.bs;
-  double c = cs[0], s = cs[1], cph = cs[2], sph = cs[3];
-  int x1 = e.x1, x2 = e.x2, y1 = e.y1, y2 = x1 + x2 - y1;
-  int tlo = max(0, max(y1 - x2, x1 - y2)), thi = min(x1, y1);
-  double sum = 0.0;
-  for (int t = tlo; t <= thi; ++t) {
-    double term = ipow(c, x2 - y1 + 2 * t) * ipow(s, x1 + y1 - 2 * t) /
-                  (dfact(t) * dfact(y1 - t) * dfact(x1 - t) * dfact(x2 - y1 + t));
-    sum += ((y1 - t) & 1) ? -term : term;
-  }
-  double d = sum * sqrt(dfact(x1) * dfact(x2) * dfact(y1) * dfact(y2));
-  // phase e^{i phi (x1 - y1)} by repeated multiplication of (cos phi, sin phi)
-  int k = x1 - y1;
-  double pr = 1.0, pi = 0.0;
-  double sgn = k < 0 ? -1.0 : 1.0;
-  for (int j = 0; j < (k < 0 ? -k : k); ++j) {
-    double nr = pr * cph - pi * (sgn * sph);
-    double ni = pr * (sgn * sph) + pi * cph;
-    pr = nr;
-    pi = ni;
-  }
-  a.entries[2 * i] = d * pr;
-  a.entries[2 * i + 1] = d * pi;
-}
-
-// ---------------------------------------------------------------------------
-// plan: per output, levels + attached factors + root product
-// ---------------------------------------------------------------------------
-// A reference to F_t(k) while sweeping the layers: a level slot, or a constant.
-struct Ref {
-  int slot;  // -1 = constant
-  int cst;
-};
-
-// A factor before sorting: input slots (-1 = constant), attachment level, folded table
-// coordinates.
-struct __align__(16) FacTmp {
-  int8_t s[4];
-  int16_t at, stride;
-  int32_t base;
-  int16_t dy, dx;
-};
-static_assert(sizeof(FacTmp) == 16, "FacTmp layout");
-
-__global__ void lofp_plan_kernel(CallArgs a) {
-  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q >= a.B) return;
-  if (a.flags[q] != 1) return;  // amps already 0 (photon number) or NaN (bad row)
-  const int M = a.M, D = a.D, W = M + 1;
-  const int32_t *t = a.T + q * M;
-  uint8_t G[LOFP_MAX_CUTS];
-  {
-    int g = 0;
-    for (int k = 0; k <= M; ++k) {
-      G[k] = (uint8_t)g;
-      if (k < M) g += t[k];
+// ---- block-wide helpers --------------------------------------------------------------
+// exclusive scan of in[0..n) into out[0..n) (slab arrays); returns the total (all threads)
+__device__ uint32_t block_scan(Shared &sh, const uint32_t *in, uint32_t *out, int n) {
+  const int per = (n + kThreads - 1) / kThreads;
+  const int a = threadIdx.x * per, e = min(n, a + per);
+  uint32_t s = 0;
+  for (int i = a; i < e; ++i) s += in[i];
+  sh.scan[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    uint32_t loc[kThreads / 32];
+    uint32_t tot = 0;
+#pragma unroll
+    for (int i = 0; i < kThreads / 32; ++i) {
+      loc[i] = sh.scan[lane * (kThreads / 32) + i];
+      tot += loc[i];
     }
+    uint32_t incl = tot;
+    for (int d = 1; d < 32; d <<= 1) {
+      uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += v;
+    }
+    uint32_t run = incl - tot;
+#pragma unroll
+    for (int i = 0; i < kThreads / 32; ++i) {
+      sh.scan[lane * (kThreads / 32) + i] = run;
+      run += loc[i];
+    }
+    if (lane == 31) sh.total = incl;
   }
-  const uint8_t *rho = a.maps, *sig = a.maps + (D + 1) * W;
-  const uint8_t *frho = a.maps + 2 * (D + 1) * W, *fsig = a.maps + 3 * (D + 1) * W;
-  // exact reachability: cum(S) inside the time-0 box (reading R5)
+  __syncthreads();
+  uint32_t run = sh.scan[threadIdx.x];
+  for (int i = a; i < e; ++i) {
+    const uint32_t v = in[i];
+    out[i] = run;
+    run += v;
+  }
+  const uint32_t total = sh.total;
+  __syncthreads();
+  return total;
+}
+
+__device__ __forceinline__ ull warp_sum_sat(ull v) {
+  for (int d = 16; d > 0; d >>= 1) v = sat_add(v, __shfl_down_sync(0xffffffffu, v, d));
+  return v;
+}
+
+__device__ __forceinline__ Block make_block(const CallParams &p) {
+  Block b;
+  b.slab = p.slab + (long long)blockIdx.x * p.slab_bytes;
+  b.segs = (Seg *)(b.slab + kOffSegs);
+  b.FL = (double2 *)(b.slab + kOffFL);
+  b.FR = (double2 *)(b.slab + kOffFR);
+  b.stack = (StackEnt *)(b.slab + kOffStack);
+  b.offA = (uint32_t *)(b.slab + kOffA);
+  b.offB = (uint32_t *)(b.slab + kOffB);
+  b.tmp = (uint32_t *)(b.slab + kOffTmp);
+  b.tmp2 = (uint32_t *)(b.slab + kOffTmp2);
+  b.segLo = (uint8_t *)(b.slab + kOffSegLo);
+  b.segRad = (uint8_t *)(b.slab + kOffSegRad);
+  b.segStr = (int32_t *)(b.slab + kOffSegStr);
+  b.vals = nullptr;
+  b.cL = b.cR = nullptr;
+  b.lists = nullptr;
+  b.list_bytes = 0;
+  return b;
+}
+
+// ---- per-output column setup (readings R5, R15) --------------------------------------
+// Returns kStatusOk / kStatusZero / kStatusBad / kStatusUnsupported (block-uniform).
+__device__ int setup_output(const CallParams &p, Block &b, Shared &sh, int q) {
+  const int M = p.M, tid = threadIdx.x;
+  for (int i = tid; i < M; i += kThreads) sh.T[i] = p.T[(long long)q * M + i];
+  __syncthreads();
+  if (tid == 0) {
+    int st = kStatusOk, g = 0;
+    sh.G[0] = 0;
+    for (int i = 0; i < M; ++i) {
+      const int t = sh.T[i];
+      if (t < 0) st = kStatusBad;
+      g += t > 0 ? t : 0;
+      if (g > 255) g = 255;
+      sh.G[i + 1] = g;
+    }
+    if (st == kStatusOk && sh.G[M] != p.N) st = kStatusZero;  // photon number (reading R9)
+    sh.status = st;
+  }
+  __syncthreads();
+  if (sh.status != kStatusOk) return sh.status;
+  // segment ranges: intersection of the backward (T) and forward (S) light-cone boxes
+  int my_bad = 0;
+  for (int k = tid; k <= M; k += kThreads) {
+    const ColInfo ci = sh.col[k];
+    long long n = 1;
+    for (int i = 0; i < ci.nseg; ++i) {
+      const SegInfo si = p.seg[ci.seg_base + i];
+      const int lo = max(sh.G[si.rho], (int)p.cumS[si.rhop]);
+      const int hi = min(sh.G[si.sig], (int)p.cumS[si.sigp]);
+      const int rad = hi - lo + 1;
+      b.segLo[ci.seg_base + i] = (uint8_t)max(lo, 0);
+      b.segRad[ci.seg_base + i] = (uint8_t)max(rad, 0);
+      b.segStr[ci.seg_base + i] = (int)n;
+      n = rad > 0 ? n * rad : 0;
+      if (n > kMaxStates) { n = kMaxStates + 1; }
+    }
+    if (n > kMaxStates) my_bad = 1;
+    sh.n[k] = (int)n;
+  }
+  my_bad = __syncthreads_or(my_bad);
+  if (tid == 0) {
+    int st = my_bad ? kStatusUnsupported : kStatusOk;
+    long long vb = 0, cb = 0;
+    for (int k = 0; k <= M && st == kStatusOk; ++k) {
+      if (sh.n[k] == 0) st = kStatusZero;  // structurally unreachable (reading R5)
+      sh.vb[k] = (int)vb;
+      sh.cb[k] = (int)cb;
+      vb += (long long)sh.n[k] * sh.col[k].nseg;
+      cb += sh.n[k];
+    }
+    if (st == kStatusOk && cb > kMaxStatesTotal) st = kStatusUnsupported;
+    if (st == kStatusOk) {
+      const long long used = kOffVar + ((vb + 15) & ~15ll) + 16 * cb;
+      if (p.slab_bytes - used < 4096) st = kStatusUnsupported;
+      atomicMax(&p.ctr->max_states, (ull)cb);
+    }
+    sh.status = st;
+  }
+  __syncthreads();
+  if (sh.status != kStatusOk) return sh.status;
+  carve(p, b, sh);
+  // segment values of every column state (mixed radix over the segments)
   for (int k = 0; k <= M; ++k) {
-    int f = a.cumS[k];
-    if (f < G[rho[k]] || f > G[sig[k]]) return;  // structural zero
-  }
-  unsigned char *plan = a.plans + (size_t)q * a.plan_stride;
-  PlanHead *head = reinterpret_cast<PlanHead *>(plan);
-  PlanLevel *lev = reinterpret_cast<PlanLevel *>(plan + sizeof(PlanHead));
-  // plan layout: head | levels [Lg] | factors [nbs] | scatter u16 [4 nbs] | scratch
-  PlanFactor *fac = reinterpret_cast<PlanFactor *>(plan + sizeof(PlanHead) + (size_t)a.Lg * sizeof(PlanLevel));
-  uint16_t *scat = reinterpret_cast<uint16_t *>(fac + a.nbs);
-  FacTmp *tmp = reinterpret_cast<FacTmp *>((reinterpret_cast<uintptr_t>(scat + 4 * (size_t)a.nbs) + 15) &
-                                           ~uintptr_t(15));  // unsorted factors
-  uint32_t *stmp = reinterpret_cast<uint32_t *>(tmp + a.nbs);         // unsorted scatter
-  const uint16_t zero_off = LOFP_ZERO_OFF;
-  const double2 *ent = reinterpret_cast<const double2 *>(a.entries);
-
-  Ref cur[LOFP_MAX_CUTS];
-  for (int k = 0; k <= M; ++k) cur[k] = Ref{-1, (int)a.cumS[k]};
-  uint8_t lev_layer[LOFP_MAX_LEVELS];
-  int8_t lev_rl[LOFP_MAX_LEVELS], lev_rr[LOFP_MAX_LEVELS];
-  int L = 0, nf = 0;
-  double2 root = make_double2(1.0, 0.0);
-  for (int b = 0; b < a.nbs; ++b) {
-    int l = a.bs_lk[2 * b], k = a.bs_lk[2 * b + 1];
-    Ref A = cur[k - 1], Bv = cur[k], C = cur[k + 1];
-    int idx = l * W + k;
-    int lo = max((int)G[rho[idx]], (int)a.cumS[frho[idx]]);
-    int hi = min((int)G[sig[idx]], (int)a.cumS[fsig[idx]]);
-    if (lo > hi) return;  // empty box: no valid path (cannot happen once reachable)
-    Ref Y;
-    if (lo == hi) {
-      Y = Ref{-1, lo};
-    } else {
-      Y = Ref{L, 0};
-      PlanLevel pl;
-      pl.ol = A.slot < 0 ? zero_off : lofp_level_off(A.slot);
-      pl.cl = (uint8_t)(A.slot < 0 ? A.cst : 0);
-      pl.or_ = C.slot < 0 ? zero_off : lofp_level_off(C.slot);
-      pl.cr = (uint8_t)(C.slot < 0 ? C.cst : 0);
-      pl.lo = (uint8_t)lo;
-      pl.hi = (uint8_t)hi;
-      pl.fbeg = pl.fend = 0;
-      pl.sbeg = pl.send = 0;
-      lev[L] = pl;
-      lev_layer[L] = (uint8_t)l;
-      lev_rl[L] = (int8_t)A.slot;
-      lev_rr[L] = (int8_t)C.slot;
-      ++L;
+    const ColInfo ci = sh.col[k];
+    for (int s = tid; s < sh.n[k]; s += kThreads) {
+      uint8_t *row = b.vals + sh.vb[k] + s * ci.nseg;
+      for (int i = 0; i < ci.nseg; ++i) {
+        const int g = ci.seg_base + i;
+        row[i] = (uint8_t)(b.segLo[g] + (s / b.segStr[g]) % b.segRad[g]);
+      }
     }
-    cur[k] = Y;
-    // the element <y1, y2| BS_b |x1, x2>
-    int at = max(max(A.slot, Bv.slot), max(C.slot, Y.slot));
-    int ca = A.slot < 0 ? A.cst : 0, cb = Bv.slot < 0 ? Bv.cst : 0, cc = C.slot < 0 ? C.cst : 0,
-        cy = Y.slot < 0 ? Y.cst : 0;
-    int stride = a.bs_stride[b];
-    if (at < 0) {  // all inputs constant: multiply into the root product
-      int x1 = cb - ca, x2 = cc - cb, y1 = cy - ca;
-      if (x1 + x2 == 0) continue;  // vacuum: the element is 1
-      int o = a.offsets[a.bs_base[b] + x1 * stride + x2] + y1;
-      root = cmul(root, ent[o]);
+  }
+  __syncthreads();
+  return kStatusOk;
+}
+
+// ---- exact path counts by a transfer over columns (reading R6) -----------------------
+// cL[k][s]: partial paths from column j (state sj) to column k ending in s;
+// cR[k][s]: completions from column k (state s) to column M.  Columns >= j.
+__device__ void dp_counts(const CallParams &p, Block &b, Shared &sh, int j, int sj, bool need_right) {
+  const int M = p.M, tid = threadIdx.x;
+  for (int s = tid; s < sh.n[j]; s += kThreads) b.cL[sh.cb[j] + s] = (s == sj) ? 1ull : 0ull;
+  if (need_right)
+    for (int s = tid; s < sh.n[M]; s += kThreads) b.cR[sh.cb[M] + s] = 1ull;
+  __syncthreads();
+  for (int i = 1; i <= M - j; ++i) {
+    const int kL = j + i, kR = M - i;
+    const int nL = sh.n[kL], nR = need_right ? sh.n[kR] : 0;
+    for (int t = tid; t < nL + nR; t += kThreads) {
+      ull sum = 0;
+      if (t < nL) {
+        const int n0 = sh.n[kL - 1];
+        const ull *src = b.cL + sh.cb[kL - 1];
+        for (int pp = 0; pp < n0; ++pp) {
+          const ull c = src[pp];
+          if (c && compat(p, b, sh, kL, pp, t)) sum = sat_add(sum, c);
+        }
+        b.cL[sh.cb[kL] + t] = sum;
+      } else {
+        const int s = t - nL;
+        const int n1 = sh.n[kR + 1];
+        const ull *src = b.cR + sh.cb[kR + 1];
+        for (int sp = 0; sp < n1; ++sp) {
+          const ull c = src[sp];
+          if (c && compat(p, b, sh, kR + 1, s, sp)) sum = sat_add(sum, c);
+        }
+        b.cR[sh.cb[kR] + s] = sum;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// NL[k] / NR[k]: half-path list sizes if the split were at column k (live states only)
+__device__ void list_sizes(Block &b, Shared &sh, int j, int M) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = j + warp; k <= M; k += kThreads / 32) {
+    ull sl = 0, sr = 0;
+    for (int s = lane; s < sh.n[k]; s += 32) {
+      const ull l = b.cL[sh.cb[k] + s], r = b.cR[sh.cb[k] + s];
+      if (l && r) {
+        sl = sat_add(sl, l);
+        sr = sat_add(sr, r);
+      }
+    }
+    sl = warp_sum_sat(sl);
+    sr = warp_sum_sat(sr);
+    if (lane == 0) {
+      sh.NL[k] = sl;
+      sh.NR[k] = sr;
+    }
+  }
+  __syncthreads();
+}
+
+// Segment list of one BFS level: for every live state s of column kd (in order), its live
+// neighbours p in column ks_ (in order); dst offsets from offD, src offsets from offS.
+// left = true: kd = ks_ + 1, compat(kd, p, s); else kd = ks_ - 1, compat(ks_, s, p).
+__device__ int build_segments(const CallParams &p, Block &b, Shared &sh, int kd, int kn, bool left,
+                              const uint32_t *offS, const uint32_t *offD) {
+  const int nd = sh.n[kd], nn = sh.n[kn], tid = threadIdx.x;
+  const ull *cnt = left ? b.cL : b.cR;
+  for (int s = tid; s < nd; s += kThreads) {
+    uint32_t c = 0;
+    if (live(b, sh, kd, s))
+      for (int pp = 0; pp < nn; ++pp)
+        if (live(b, sh, kn, pp) && (left ? compat(p, b, sh, kd, pp, s) : compat(p, b, sh, kn, s, pp))) ++c;
+    b.tmp[s] = c;
+  }
+  __syncthreads();
+  const uint32_t nsegs = block_scan(sh, b.tmp, b.tmp2, nd);
+  if (nsegs > (uint32_t)kMaxSegments) return -1;
+  for (int s = tid; s < nd; s += kThreads) {
+    if (!live(b, sh, kd, s)) continue;
+    uint32_t e = b.tmp2[s], d = offD[s];
+    for (int pp = 0; pp < nn; ++pp) {
+      if (!live(b, sh, kn, pp)) continue;
+      if (!(left ? compat(p, b, sh, kd, pp, s) : compat(p, b, sh, kn, s, pp))) continue;
+      const uint32_t len = (uint32_t)cnt[sh.cb[kn] + pp];
+      Seg g;
+      g.dst = d;
+      g.src = offS[pp];
+      g.len = len;
+      g.p = (uint16_t)pp;
+      g.s = (uint16_t)s;
+      b.segs[e++] = g;
+      d += len;
+    }
+  }
+  __syncthreads();
+  return (int)nsegs;
+}
+
+__device__ __forceinline__ int find_seg(const Seg *segs, int nsegs, uint32_t t) {
+  int lo = 0, hi = nsegs - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (segs[mid].dst <= t) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// Bucket offsets of column k: exclusive scan of the live counts (cL or cR).
+__device__ uint32_t bucket_offsets(Block &b, Shared &sh, int k, bool left, uint32_t *off) {
+  const ull *cnt = left ? b.cL : b.cR;
+  for (int s = threadIdx.x; s < sh.n[k]; s += kThreads)
+    b.tmp[s] = live(b, sh, k, s) ? (uint32_t)cnt[sh.cb[k] + s] : 0u;
+  __syncthreads();
+  return block_scan(sh, b.tmp, off, sh.n[k]);
+}
+
+// ---- the outer product: every path = X_i * Y_j, one complex FMA pair per path --------
+__device__ __forceinline__ void outer_pair(const double2 *__restrict__ Xp, const uint16_t *__restrict__ Xc,
+                                           const double2 *__restrict__ FX, int nX, const double2 *__restrict__ Yp,
+                                           const uint16_t *__restrict__ Yc, const double2 *__restrict__ FY, int nY,
+                                           double2 *sY, double2 (&acc)[kKX], ull &npaths, ull &cm) {
+  const int nxb = (nX + kKX - 1) / kKX;
+  for (int y0 = 0; y0 < nY; y0 += kCY) {
+    const int len = min(kCY, nY - y0);
+    for (int t = threadIdx.x; t < len; t += kThreads) sY[t] = cmul(Yp[y0 + t], FY[Yc[y0 + t]]);
+    cm += (len + kThreads - 1 - threadIdx.x) / kThreads;
+    __syncthreads();
+    int parts = (4 * kThreads + nxb - 1) / nxb;
+    if (parts > len) parts = len;
+    if (parts < 1) parts = 1;
+    const int cyt = (len + parts - 1) / parts;
+    parts = (len + cyt - 1) / cyt;
+    const int ntask = nxb * parts;
+    for (int task = threadIdx.x; task < ntask; task += kThreads) {
+      const int xb = task % nxb, part = task / nxb;
+      double2 x[kKX];
+      int nv = 0;
+#pragma unroll
+      for (int r = 0; r < kKX; ++r) {
+        const int i = xb * kKX + r;
+        if (i < nX) {
+          x[r] = cmul(Xp[i], FX[Xc[i]]);
+          ++nv;
+        } else {
+          x[r] = make_double2(0.0, 0.0);
+        }
+      }
+      cm += nv;
+      const int ya = part * cyt, yb = min(len, ya + cyt);
+      int y = ya;
+      for (; y + 1 < yb; y += 2) {
+        const double2 v0 = sY[y], v1 = sY[y + 1];
+#pragma unroll
+        for (int r = 0; r < kKX; ++r) {
+          acc[r].x = fma(x[r].x, v0.x, acc[r].x);
+          acc[r].y = fma(x[r].x, v0.y, acc[r].y);
+          acc[r].x = fma(-x[r].y, v0.y, acc[r].x);
+          acc[r].y = fma(x[r].y, v0.x, acc[r].y);
+        }
+#pragma unroll
+        for (int r = 0; r < kKX; ++r) {
+          acc[r].x = fma(x[r].x, v1.x, acc[r].x);
+          acc[r].y = fma(x[r].x, v1.y, acc[r].y);
+          acc[r].x = fma(-x[r].y, v1.y, acc[r].x);
+          acc[r].y = fma(x[r].y, v1.x, acc[r].y);
+        }
+      }
+      if (y < yb) {
+        const double2 v0 = sY[y];
+#pragma unroll
+        for (int r = 0; r < kKX; ++r) {
+          acc[r].x = fma(x[r].x, v0.x, acc[r].x);
+          acc[r].y = fma(x[r].x, v0.y, acc[r].y);
+          acc[r].x = fma(-x[r].y, v0.y, acc[r].x);
+          acc[r].y = fma(x[r].y, v0.x, acc[r].y);
+        }
+      }
+      npaths += (ull)nv * (ull)(yb - ya);
+    }
+    __syncthreads();
+  }
+}
+
+// ---- one unit: column-split enumeration of its subtree (reading R20) ------------------
+// Paths below the prefix (columns 0..j fixed) = sum over column-pair states (a, b) at
+// columns (ks, ks+1) of L(a) x R(b): L(a) = partial paths j..ks ending in a (products of
+// cut factors j..ks-1), R(b) = partial paths ks+1..M starting in b (cuts ks+2..M-1); the
+// cut factors of ks and ks+1 scale the two lists per pair.  Both lists are built level by
+// level (BFS with exact bucket offsets from the counts: deterministic, no atomics).
+__device__ void process_stack(const CallParams &p, Block &b, Shared &sh, double2 *sY, double2 (&acc)[kKX],
+                              ull &npaths, ull &cm, ull &nelem) {
+  const int M = p.M, tid = threadIdx.x;
+  while (true) {
+    if (tid == 0) {
+      if (sh.sp > 0) sh.top = b.stack[--sh.sp];
+      else sh.top.j = -1;
+    }
+    __syncthreads();
+    const StackEnt top = sh.top;
+    if (top.j < 0) break;
+    const int j = top.j, sj = top.sj, sjm1 = top.sjm1;
+    const double2 pi = make_double2(top.re, top.im);
+    dp_counts(p, b, sh, j, sj, true);
+    list_sizes(b, sh, j, M);
+    // choose the split column pair: smallest L + R lists that fit the scratch
+    if (tid == 0) {
+      const ull cap = (ull)(b.list_bytes / (2 * (16 + 2)) - 64);
+      int best = -1;
+      ull bcost = ~0ull;
+      for (int k = j; k <= M - 1; ++k) {
+        const ull c = sat_add(sh.NL[k], sh.NR[k + 1]);
+        if (c <= cap && c < bcost) {
+          bcost = c;
+          best = k;
+        }
+      }
+      sh.ks = best;
+    }
+    __syncthreads();
+    const int ks = sh.ks;
+    if (ks < 0) {
+      // lists over capacity: split by fixing column j+1 and process the children in turn
+      if (tid == 0) {
+        atomicAdd(&p.ctr->subsplits, 1ull);
+        const int n1 = sh.n[j + 1];
+        for (int s = n1 - 1; s >= 0; --s) {
+          if (!live(b, sh, j + 1, s) || !compat(p, b, sh, j + 1, sj, s)) continue;
+          ull c2 = 0;
+          const double2 f = cut_factor(p, b, sh, j, sjm1, sj, s, c2);
+          const double2 np = cmul(pi, f);
+          if (sh.sp < kStackMax) {
+            StackEnt e;
+            e.j = j + 1;
+            e.sjm1 = (uint16_t)sj;
+            e.sj = (uint16_t)s;
+            e.re = np.x;
+            e.im = np.y;
+            e.pad = 0;
+            b.stack[sh.sp++] = e;
+          } else {
+            atomicAdd(&p.ctr->unsupported, 1ull);
+          }
+        }
+      }
+      __syncthreads();
       continue;
     }
-    if (A.slot < 0 && C.slot < 0 && cc == ca) continue;  // always vacuum
-    FacTmp ft;
-    ft.s[0] = (int8_t)A.slot;
-    ft.s[1] = (int8_t)Bv.slot;
-    ft.s[2] = (int8_t)C.slot;
-    ft.s[3] = (int8_t)Y.slot;
-    ft.at = (int16_t)at;
-    ft.stride = (int16_t)stride;
-    ft.base = a.bs_base[b] + stride * (cb - ca) + (cc - cb);
-    ft.dy = (int16_t)(cy - ca);
-    ft.dx = (int16_t)(cc - ca);
-    tmp[nf] = ft;
-    ++nf;
-  }
-  // counting sort of the factors by level; factor f (sorted) owns key word f
-  uint16_t cnt[LOFP_MAX_LEVELS + 1];
-  for (int j = 0; j <= L; ++j) cnt[j] = 0;
-  for (int f = 0; f < nf; ++f) cnt[tmp[f].at + 1]++;
-  for (int j = 0; j < L; ++j) cnt[j + 1] += cnt[j];
-  for (int j = 0; j < L; ++j) {
-    lev[j].fbeg = cnt[j];
-    lev[j].fend = cnt[j + 1];
-  }
-  // the chain: the last free layer's levels, if their ranges and factors qualify (R17)
-  int jb = L;
-  if (L >= LOFP_CHAIN_MIN) {
-    int cand = L - 1;
-    while (cand > 0 && lev_layer[cand - 1] == lev_layer[L - 1]) --cand;
-    if (cand < L - 32) cand = L - 32;  // one lane per chain level in the engine
-    bool ok = true;
-    for (int m = cand; m < L; ++m)
-      if (lev_rl[m] >= cand || lev_rr[m] >= cand) ok = false;
-    for (int f = 0; f < nf && ok; ++f) {
-      const int at = tmp[f].at;
-      if (at < cand) continue;
-      for (int p = 0; p < 4; ++p) {
-        const int sl = tmp[f].s[p];
-        if (sl >= cand && sl != at && sl != at - 1) ok = false;
-      }
-    }
-    // worth a warp only when the chain's box admits many paths (the box product bounds
-    // the paths of every chain subtree of this output)
-    double rbox = 1.0;
-    for (int m = cand; m < L; ++m) rbox *= (double)((int)lev[m].hi - (int)lev[m].lo + 1);
-    if (ok && L - cand >= LOFP_CHAIN_MIN) {
-      atomicAdd(&a.ctr->nchain_ok, 1);
-      if (rbox >= LOFP_CHAIN_MODE_RBOX) atomicAdd(&a.ctr->nchain_big, 1);
-      atomicAdd(&a.ctr->rbox_log16, (unsigned long long)(16.0 * log2(rbox)));
-    }
-    if (ok && L - cand >= LOFP_CHAIN_MIN && rbox >= a.chain_rbox) jb = cand;
-  }
-  // scatter entries per level: those of chain factors go last (<= 15 per level, and the
-  // whole list < 4096 entries, else no chain for this output)
-  if (jb < L) {
-    uint8_t chc[LOFP_MAX_LEVELS];
-    for (int j = 0; j < L; ++j) chc[j] = 0;
-    int tot = 0;
-    bool fits = true;
-    for (int f = 0; f < nf; ++f)
-      for (int p = 0; p < 4; ++p)
-        if (tmp[f].s[p] >= 0) {
-          ++tot;
-          if (tmp[f].at >= jb && ++chc[tmp[f].s[p]] > 15) fits = false;
-        }
-    if (!fits || tot >= 4096) jb = L;
-  }
-  int ns = 0;
-  for (int f = 0; f < nf; ++f) {
-    const FacTmp ft = tmp[f];
-    int w = cnt[ft.at]++;
-    uint32_t chain = 0x3210u;  // identity byte selector
-    if (ft.at >= jb)
-      for (int p = 0; p < 4; ++p)
-        if (ft.s[p] >= jb)  // a chain value: the level's own (4) or the previous one's (5)
-          chain = (chain & ~(15u << (4 * p))) | ((ft.s[p] == ft.at ? 4u : 5u) << (4 * p));
-    PlanFactor pf;
-    pf.crow = (int32_t)(((uint32_t)(uint8_t)(int8_t)(-ft.stride)) | ((uint32_t)(uint8_t)(int8_t)(ft.stride - 1) << 8) |
-                        (1u << 16));
-    pf.base = ft.base;
-    pf.dy = (int8_t)ft.dy;
-    pf.dx = (int8_t)ft.dx;
-    pf.chain = (uint16_t)chain;
-    for (int p = 0; p < 4; ++p) pf.slot[p] = (uint8_t)ft.s[p];  // -1 -> 0xff
-    fac[w] = pf;
-    const uint32_t isch = ft.at >= jb ? 1u : 0u;
-    for (int p = 0; p < 4; ++p)
-      if (ft.s[p] >= 0) stmp[ns++] = ((2u * (uint32_t)ft.s[p] + isch) << 16) | (uint32_t)(w * 128 + p);
-  }
-  // counting sort of the scatter entries by (level, chain factor)
-  uint16_t cnt2[2 * LOFP_MAX_LEVELS + 1];
-  for (int j = 0; j <= 2 * L; ++j) cnt2[j] = 0;
-  for (int i = 0; i < ns; ++i) cnt2[(stmp[i] >> 16) + 1]++;
-  for (int j = 0; j < 2 * L; ++j) cnt2[j + 1] += cnt2[j];
-  for (int j = 0; j < L; ++j) {
-    const int nch = cnt2[2 * j + 2] - cnt2[2 * j + 1];
-    lev[j].sbeg = cnt2[2 * j];
-    lev[j].send = (uint16_t)((cnt2[2 * j + 2] & 0xfff) | (jb < L ? nch << 12 : 0));
-  }
-  for (int i = 0; i < ns; ++i) scat[cnt2[stmp[i] >> 16]++] = (uint16_t)(stmp[i] & 0xffff);
-  const int nkeys = jb < L ? (int)lev[jb].fbeg : nf;  // non-chain factors (they come first)
-  PlanHead h;
-  h.root[0] = root.x;
-  h.root[1] = root.y;
-  h.L = (uint16_t)L;
-  h.nfac = (uint16_t)nf;
-  h.nscat = (uint16_t)ns;
-  h.jb = (uint16_t)jb;
-  h.pad1 = 0;
-  *head = h;
-  if (L == 0) {  // a single valid path (eq. (10))
-    a.amps[2 * q] = root.x;
-    a.amps[2 * q + 1] = root.y;
-    if (a.counts) a.counts[q] = 1;
-    return;
-  }
-  atomicMax(&a.ctr->maxL, L);
-  atomicMax(&a.ctr->maxF, nf);
-  atomicMax(&a.ctr->maxS, ns);
-  atomicMax(&a.ctr->maxK, nkeys);
-  if (jb < L) atomicAdd(&a.ctr->nchain, 1);
-  unsigned long long idx = atomicAdd(&a.ctr->nfeas, 1ull);
-  a.feas[idx] = (uint32_t)q;
-  atomicAdd(&a.ctr->outstanding, 1ull);
-}
-
-// ---------------------------------------------------------------------------
-// path enumeration
-// ---------------------------------------------------------------------------
-
-__device__ __forceinline__ unsigned long long vload(const unsigned long long *p) {
-  return *reinterpret_cast<const volatile unsigned long long *>(p);
-}
-
-// Per-lane state of the DFS, all in the warp's shared memory:
-//   vals  value bytes of the levels (slot 0 = constant zero, level j = slot j + 1),
-//         lane-interleaved by word (lofp_slot_off): the prefix handed to other lanes/warps;
-//   keys  one word per attached factor: the variable bytes (a, b, c, y) of its inputs,
-//         written when a level's value is set (scatter list of the plan), read with one
-//         32-bit load per factor and turned into the table index with two dp4a;
-//   stack ring of LOFP_STK branch entries [bot, top) (product before the level, level,
-//         last value), a local-memory overflow below it for rare deep stacks.
-struct WarpSmem {
-  unsigned char *plan;  // staged plan of the current output
-  unsigned char *vcol;  // vals words [slots/4][32]
-  unsigned char *kcol;  // key words [nfac][32]
-  double2 *stkP;        // [LOFP_STK][32]
-  uint32_t *stkM;       // [LOFP_STK][32]
-};
-
-// Scatter entries of a level to write: all of them; none while the chain engine is on
-// (then every factor's key is gathered from the value bytes and no key words exist).
-template <bool CHAIN>
-__device__ __forceinline__ int scatter_count(const PlanLevel &lv) {
-  return CHAIN ? 0 : (int)(lv.send & 0xfff) - (int)lv.sbeg;
-}
-
-// Write value v of level j: the vals byte and every key byte that holds it.  (Used off
-// the hot step; the step writes with a warp-uniform trip count, see below.)
-template <bool CHAIN>
-__device__ __forceinline__ void set_level(unsigned char *lb, unsigned char *kb, const PlanLevel &lvref,
-                                          const uint16_t *scat, int j, int v) {
-  const PlanLevel lv = lvref;
-  const int sbeg = lv.sbeg, n = scatter_count<CHAIN>(lv);
-  lb[lofp_level_off(j)] = (unsigned char)v;
-  for (int s = 0; s < n; ++s) kb[scat[sbeg + s]] = (unsigned char)v;
-}
-
-// A factor's key gathered from value bytes (slot 0xff: constant -> 0).
-__device__ __forceinline__ int gather_key(const PlanFactor &fd, const unsigned char *lb) {
-  uint32_t k = 0;
-#pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    const int sl = fd.slot[p];
-    const uint32_t b = sl == 0xff ? 0u : (uint32_t)lb[lofp_level_off(sl)];
-    k |= b << (8 * p);
-  }
-  return (int)k;
-}
-
-// Product of the factors attached to level lv, times P.  The trip count is the warp's
-// largest factor count (nmax, warp-uniform) so that every lane runs the same instruction
-// stream; a lane past its own count multiplies by table entry 0, which is exactly 1 (the
-// vacuum element of BS 0, R16).
-template <bool COUNTED, bool CHAIN>
-__device__ __forceinline__ int factor_entry(const PlanFactor *fp, const unsigned char *kp, int i, int fcnt,
-                                            const int32_t *s_off, const unsigned char *lb, unsigned long long &ncm) {
-  // past the lane's own count: re-read its last factor (always a valid descriptor, key
-  // and table row) and use entry 0 (= 1)
-  const bool on = i < fcnt;
-  const int fi = on ? i : max(fcnt - 1, 0);
-  const int2 fd = *reinterpret_cast<const int2 *>(fp + fi);  // crow, base
-  // engine on: no key words, the key is gathered from the lane's value bytes
-  const int key = CHAIN ? gather_key(fp[fi], lb) : *reinterpret_cast<const int *>(kp + fi * 128);
-  const int row = __dp4a(key, fd.x, fd.y);
-  const int o = s_off[on ? row : 0] + __dp4a(key, 0x010000ff, (int)fp[fi].dy);  // + y - a
-  if (COUNTED) ncm += (on && __dp4a(key, 0x000100ff, (int)fp[fi].dx) > 0);  // x1 + x2 = c - a
-  return on ? o : 0;
-}
-
-// Product of the factors attached to a level, times P.  The trip count is the warp's
-// largest factor count (nmax, warp-uniform) so that every lane runs the same instruction
-// stream; a lane past its own count multiplies by table entry 0, which is exactly 1 (the
-// vacuum element of BS 0, R16).  Factors are taken in pairs: e_i e_{i+1} does not depend on P,
-// so the dependent fp64 chain is one complex multiplication per pair.
-template <bool COUNTED, bool CHAIN>
-__device__ __forceinline__ double2 level_product(double2 P, int fbeg, int fcnt, int nmax, const PlanFactor *fac,
-                                                 const unsigned char *kb, const int32_t *s_off,
-                                                 const double2 *s_ent, const unsigned char *lb,
-                                                 unsigned long long &ncm) {
-  const PlanFactor *fp = fac + fbeg;
-  const unsigned char *kp = kb + fbeg * 128;
-  int i = 0;
-#pragma unroll 1
-  for (; i + 1 < nmax; i += 2) {
-    const int o0 = factor_entry<COUNTED, CHAIN>(fp, kp, i, fcnt, s_off, lb, ncm);
-    const int o1 = factor_entry<COUNTED, CHAIN>(fp, kp, i + 1, fcnt, s_off, lb, ncm);
-    P = cmul(P, cmul(s_ent[o0], s_ent[o1]));
-  }
-  if (i < nmax) P = cmul(P, s_ent[factor_entry<COUNTED, CHAIN>(fp, kp, i, fcnt, s_off, lb, ncm)]);
-  return P;
-}
-
-template <bool COUNTED, bool CHAIN, bool SMALL>
-__global__ void __launch_bounds__(LOFP_ENUM_MAX_THREADS, 1) lofp_enum_kernel(CallArgs a) {
-  // branch-stack entries kept in shared memory: fewer with the chain engine (the walk
-  // above the chains is short; the overflow below the ring catches the rest)
-  constexpr unsigned STK = CHAIN ? LOFP_STK_CHAIN : LOFP_STK;
-  extern __shared__ __align__(16) unsigned char smem[];
-  double2 *s_ent = reinterpret_cast<double2 *>(smem);
-  int32_t *s_off = reinterpret_cast<int32_t *>(s_ent + a.nentries);
-  for (int i = threadIdx.x; i < a.nentries; i += blockDim.x)
-    reinterpret_cast<int4 *>(s_ent)[i] = reinterpret_cast<const int4 *>(a.entries)[i];
-  for (int i = threadIdx.x; i < a.noffsets; i += blockDim.x) s_off[i] = a.offsets[i];
-  __syncthreads();
-
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  unsigned char *wb = smem + a.table_bytes + (size_t)warp * a.warp_bytes;
-  unsigned char *s_plan = wb;
-  const PlanLevel *s_lev = reinterpret_cast<const PlanLevel *>(s_plan + sizeof(PlanHead));
-  unsigned char *vcol = wb + a.plan_smem;                                   // [slots/4][32] words
-  unsigned char *kcol = vcol + a.vals_slots * 32;                           // [maxfac][32] words
-  double2 *stkP = reinterpret_cast<double2 *>(kcol + (size_t)a.maxfac * 128);  // [LOFP_STK][32]
-  uint32_t *stkM = reinterpret_cast<uint32_t *>(stkP + STK * 32);         // [LOFP_STK][32]
-  double2 *mbP = reinterpret_cast<double2 *>(stkM + STK * 32);             // hand-over mailbox
-  uint32_t *mbM = reinterpret_cast<uint32_t *>(mbP + 1);
-  // chain engine scratch: pair table W, per-lane suffix products, per-digit arrays
-  double2 *cW = mbP + 2;                                     // [LOFP_W_MAX]
-  double2 *cPs = cW + LOFP_W_MAX;                            // [LOFP_SUF_ENTRIES] suffix table
-  // per chain level m: (range r_m, low end / digit m of the stride 32, pair-table block base, 1 / r_m)
-  int4 *c_lv = reinterpret_cast<int4 *>(cPs + LOFP_SUF_ENTRIES);  // [33]
-  int *c_wb = reinterpret_cast<int *>(c_lv + 33);            // [33] block bases (binary search)
-  int *c_pv = c_wb + 33;                                     // [32] 1 / prefix place values
-  unsigned char *c_dig = reinterpret_cast<unsigned char *>(c_pv + 32);  // [32 digits][32 lanes]
-  // small-chain batch: per emitting lane (column) its chain's ranges and table offsets
-  double2 *sc_proot = reinterpret_cast<double2 *>(
-      (reinterpret_cast<uintptr_t>(c_dig + 32 * 32) + 15) & ~uintptr_t(15));  // [32] root products
-  int *sc_wbase = reinterpret_cast<int *>(sc_proot + 32);                // [33] pair-table bases
-  int *sc_pbase = sc_wbase + 33;                                         // [33] path bases
-  uint16_t *sc_wb = reinterpret_cast<uint16_t *>(sc_pbase + 33);        // [16 levels][32]
-  unsigned char *sc_lo = reinterpret_cast<unsigned char *>(sc_wb + LOFP_SMALL_LEVELS * 32);  // [16][32]
-  unsigned char *sc_r = sc_lo + LOFP_SMALL_LEVELS * 32;                  // [16][32]
-  unsigned char *lb = vcol + 4 * lane;  // this lane's vals byte base
-  unsigned char *kb = kcol + 4 * lane;  // this lane's key byte base
-  lb[LOFP_ZERO_OFF] = 0;
-  const uint16_t dummy_off = lofp_slot_off(a.vals_slots - 1);  // scratch byte for idle lanes
-  const unsigned nfeas = (unsigned)a.ctr->nfeas;
-
-  // local-memory overflow below the shared ring: entries [obot, otop) (ring indices mod
-  // LOFP_OVF), all shallower than the shared-memory entries
-  double2 ovfP[LOFP_OVF];
-  uint32_t ovfM[LOFP_OVF];
-
-  unsigned cur_out = 0xffffffffu;
-  const PlanFactor *s_fac = nullptr;
-  const uint16_t *s_scat = nullptr;
-  int L = 0, NF = 0;
-  unsigned long long spills = 0, ovfc = 0, dons = 0, items = 0, nchains = 0, nchainfb = 0;
-  unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  long long tph = COUNTED ? clock64() : 0;
-#define LOFP_PHASE(k)                        \
-  do {                                       \
-    if (COUNTED) {                           \
-      const long long _t = clock64();        \
-      ph[k] += (unsigned long long)(_t - tph); \
-      tph = _t;                              \
-    }                                        \
-  } while (0)
-  uint32_t *const mySM = stkM + lane;    // this lane's stack metas, entry e at [e * 32]
-  double2 *const mySP = stkP + lane;     // this lane's stack products
-  const int dummy_rel = (int)dummy_off - a.vals_slots * 32;  // kb + dummy_rel = scratch byte
-
-  // spill a branch (level jd = m & 0xff, last value m >> 8) of this lane to the global queue
-  auto spill = [&](unsigned long long slot, unsigned out, uint32_t m, double2 Pe) {
-    Item *it = a.ring + (slot & a.ring_mask);
-    while (*reinterpret_cast<volatile unsigned *>(&it->seq) != 0u) __nanosleep(64);
-    int jd = m & 0xff, hh = (m >> 8) & 0xff;
-    if (COUNTED) atomicAdd(&a.ctr->spill_hist[min(L - 1 - jd, 63)], 1ull);
-    it->out = out;
-    it->j0 = (unsigned short)jd;
-    it->vs = (unsigned char)(lb[lofp_level_off(jd)] + 1);
-    it->ve = (unsigned char)hh;
-    it->P[0] = Pe.x;
-    it->P[1] = Pe.y;
-    uint32_t *pw = reinterpret_cast<uint32_t *>(it->prefix);
-    for (int w = 0; w < (jd + 4) / 4; ++w) pw[w] = *reinterpret_cast<const uint32_t *>(vcol + w * 128 + 4 * lane);
-    __threadfence();
-    *reinterpret_cast<volatile unsigned *>(&it->seq) = (unsigned)(slot + 1);
-  };
-
-  while (true) {
-    // ---------------- acquire a work item (lane 0) ----------------
-    int kind = 0;  // 0 done, 1 fresh output, 2 queued subtree
-    unsigned out = 0;
-    unsigned long long tk = 0;
-    if (lane == 0) {
-      unsigned long long idx = atomicAdd(&a.ctr->fresh_next, 1ull);
-      if (idx < nfeas) {
-        kind = 1;
-        out = a.feas[idx];
-      } else {
-        tk = atomicAdd(&a.ctr->ticket, 1ull);
-        const Item *it = a.ring + (tk & a.ring_mask);
-        unsigned ns = 32;
-        while (true) {
-          unsigned seq = *reinterpret_cast<const volatile unsigned *>(&it->seq);
-          if (seq == (unsigned)(tk + 1)) {
-            __threadfence();
-            kind = 2;
-            out = __ldcg(&it->out);
-            break;
-          }
-          if (vload(&a.ctr->outstanding) == 0ull) break;
-          __nanosleep(ns);
-          if (ns < 8192) ns <<= 1;
-        }
-      }
-    }
-    kind = __shfl_sync(FULL, kind, 0);
-    if (kind == 0) break;
-    out = __shfl_sync(FULL, out, 0);
-    tk = __shfl_sync(FULL, tk, 0);
-    ++items;
-
-    LOFP_PHASE(6);
-    // ---------------- stage the output's plan ----------------
-    if (out != cur_out) {
-      const unsigned char *gp = a.plans + (size_t)out * a.plan_stride;
-      const PlanHead *gh = reinterpret_cast<const PlanHead *>(gp);
-      int Lq = gh->L, nf = gh->nfac, ns = gh->nscat;
-      for (int i = lane; i < 2 + Lq; i += 32)
-        reinterpret_cast<int4 *>(s_plan)[i] = reinterpret_cast<const int4 *>(gp)[i];
-      const unsigned char *gf = gp + sizeof(PlanHead) + (size_t)a.Lg * sizeof(PlanLevel);
-      unsigned char *sf = s_plan + sizeof(PlanHead) + (size_t)Lq * sizeof(PlanLevel);
-      for (int i = lane; i < nf; i += 32) reinterpret_cast<int4 *>(sf)[i] = reinterpret_cast<const int4 *>(gf)[i];
-      const uint16_t *gs = reinterpret_cast<const uint16_t *>(gf + (size_t)a.nbs * sizeof(PlanFactor));
-      uint16_t *ss = reinterpret_cast<uint16_t *>(sf + (size_t)nf * sizeof(PlanFactor));
-      for (int i = lane; i < ns; i += 32) ss[i] = gs[i];
-      s_fac = reinterpret_cast<const PlanFactor *>(sf);
-      s_scat = ss;
-      L = Lq;
-      NF = nf;
-      cur_out = out;
-      __syncwarp();
-    }
-    const PlanHead *sh = reinterpret_cast<const PlanHead *>(s_plan);
-    const int Lm1 = L - 1;
-    const int jbq = CHAIN ? (int)sh->jb : L;  // first chain level (== L: no chain)
-    bool chain_pending = false;
-    const int NK = CHAIN ? 0 : NF;  // key words of this output (none while the engine is on)
-
-    // ---------------- lane 0 begins the item ----------------
-    // Lane state: j = current level, v = its value, Pb = product before level j's
-    // factors, leafhi = last sibling when j is the leaf level, stack [bot, top) of open
-    // branches (meta = level | last value << 8, product before that level), overflow
-    // [obot, otop) below it.
-    bool working = false;
-    int j = 0, v = 0, leafhi = 0;
-    unsigned bot = 0, top = 0, obot = 0, otop = 0;
-    double2 Pb = make_double2(0.0, 0.0), acc = make_double2(0.0, 0.0);
-    unsigned long long npaths = 0, ncm = 0;
+    const ull NLk = sh.NL[ks], NRk = sh.NR[ks + 1];
+    const ull capL = NLk, capR = NRk;
+    double2 *Lp[2], *Rp[2];
+    uint16_t *Lc[2], *Rc[2];
     {
-      // all key words of this warp start at zero (constant inputs contribute 0)
-      for (int f = 0; f < NK; ++f) *reinterpret_cast<uint32_t *>(kb + f * 128) = 0u;
-      int j0 = 0, vs = 0, ve = 0;
-      double2 P0;
-      if (kind == 1) {
-        PlanLevel l0 = s_lev[0];
-        vs = max((int)lb[l0.ol] + l0.cl, (int)l0.lo);
-        ve = min((int)lb[l0.or_] + l0.cr, (int)l0.hi);
-        P0 = make_double2(sh->root[0], sh->root[1]);
-      } else {
-        Item *it = a.ring + (tk & a.ring_mask);
-        // the slot was written by another SM: read around L1
-        uint32_t w2 = __ldcg(reinterpret_cast<const uint32_t *>(it) + 2);
-        j0 = w2 & 0xffff;
-        vs = (w2 >> 16) & 0xff;
-        ve = w2 >> 24;
-        P0 = __ldcg(reinterpret_cast<const double2 *>(it->P));
-        int nw = (j0 + 4) >> 2;  // slots [0, j0]: the zero slot and levels < j0
-        const uint32_t *pw = reinterpret_cast<const uint32_t *>(it->prefix);
-        for (int w = lane; w < nw; w += 32) *reinterpret_cast<uint32_t *>(vcol + w * 128) = __ldcg(pw + w);
-        __syncwarp();
-        if (lane == 0) {
-          __threadfence();
-          *reinterpret_cast<volatile unsigned *>(&it->seq) = 0u;  // slot free again
-          for (int jj = 0; jj < j0; ++jj)  // rebuild the keys of the prefix levels
-            set_level<CHAIN>(lb, kb, s_lev[jj], s_scat, jj, lb[lofp_level_off(jj)]);
-        }
+      char *q = b.lists;
+      Lp[0] = (double2 *)q; q += 16 * capL;
+      Lp[1] = (double2 *)q; q += 16 * capL;
+      Rp[0] = (double2 *)q; q += 16 * capR;
+      Rp[1] = (double2 *)q; q += 16 * capR;
+      Lc[0] = (uint16_t *)q; q += 2 * capL;
+      Lc[1] = (uint16_t *)q; q += 2 * capL;
+      Rc[0] = (uint16_t *)q; q += 2 * capR;
+      Rc[1] = (uint16_t *)q;
+    }
+    // ---- left lists: levels j..ks
+    uint32_t *offS = b.offA, *offD = b.offB;
+    int cur = 0;
+    if (tid == 0) {
+      Lp[0][0] = make_double2(1.0, 0.0);
+      Lc[0][0] = (uint16_t)sjm1;
+    }
+    for (int s = tid; s < sh.n[j]; s += kThreads) offS[s] = 0;
+    __syncthreads();
+    bool ok = true;
+    for (int k = j; k < ks && ok; ++k) {
+      const uint32_t total = bucket_offsets(b, sh, k + 1, true, offD);
+      const int nsegs = build_segments(p, b, sh, k + 1, k, true, offS, offD);
+      if (nsegs < 0) { ok = false; break; }
+      for (uint32_t t = tid; t < total; t += kThreads) {
+        const Seg g = b.segs[find_seg(b.segs, nsegs, t)];
+        const uint32_t src = g.src + (t - g.dst);
+        const double2 f = cut_factor(p, b, sh, k, Lc[cur][src], g.p, g.s, cm);
+        Lp[cur ^ 1][t] = cmul(Lp[cur][src], f);
+        Lc[cur ^ 1][t] = g.p;
+        ++cm;
       }
-      if (lane == 0 && kind == 1 && jbq == 0) {  // the whole tree is one chain
-        working = true;
-        chain_pending = true;
-        Pb = P0;
-      } else if (lane == 0) {
-        working = true;
-        j = j0;
-        v = vs;
-        set_level<CHAIN>(lb, kb, s_lev[j0], s_scat, j0, vs);
-        if (j0 == Lm1) {
-          leafhi = ve;
-        } else if (ve > vs) {
-          mySM[0] = (uint32_t)j0 | ((uint32_t)ve << 8);
-          mySP[0] = P0;
-          top = 1;
+      nelem += (total + kThreads - 1 - tid) / kThreads;
+      __syncthreads();
+      cur ^= 1;
+      uint32_t *tt = offS; offS = offD; offD = tt;
+    }
+    const int curL = cur;
+    uint32_t *offL = offS;  // bucket offsets of column ks
+    // ---- right lists: levels M..ks+1 (the other offset buffer pair)
+    uint32_t *offS2 = (offL == b.offA) ? b.offB : b.offA;
+    cur = 0;
+    if (tid == 0) {
+      Rp[0][0] = make_double2(1.0, 0.0);
+      Rc[0][0] = 0;
+    }
+    for (int s = tid; s < sh.n[M]; s += kThreads) offS2[s] = 0;
+    __syncthreads();
+    // the right BFS needs three offset arrays besides offL: use FR's storage as scratch
+    uint32_t *rA = offS2, *rB = (uint32_t *)b.FR;
+    for (int k = M - 1; k >= ks + 1 && ok; --k) {
+      const uint32_t total = bucket_offsets(b, sh, k, false, rB);
+      const int nsegs = build_segments(p, b, sh, k, k + 1, false, rA, rB);
+      if (nsegs < 0) { ok = false; break; }
+      for (uint32_t t = tid; t < total; t += kThreads) {
+        const Seg g = b.segs[find_seg(b.segs, nsegs, t)];
+        const uint32_t src = g.src + (t - g.dst);
+        const double2 f = cut_factor(p, b, sh, k + 1, g.s, g.p, Rc[cur][src], cm);
+        Rp[cur ^ 1][t] = cmul(Rp[cur][src], f);
+        Rc[cur ^ 1][t] = g.p;
+        ++cm;
+      }
+      nelem += (total + kThreads - 1 - tid) / kThreads;
+      __syncthreads();
+      cur ^= 1;
+      uint32_t *tt = rA; rA = rB; rB = tt;
+    }
+    const int curR = cur;
+    uint32_t *offR = rA;  // bucket offsets of column ks+1
+    if (offR == (uint32_t *)b.FR) {
+      // move the offsets out of FR's storage (FR is rebuilt per pair)
+      uint32_t *dst = (offL == b.offA) ? b.offB : b.offA;
+      for (int s = tid; s < sh.n[ks + 1]; s += kThreads) dst[s] = offR[s];
+      __syncthreads();
+      offR = dst;
+    }
+    if (!ok) {
+      if (tid == 0) atomicAdd(&p.ctr->unsupported, 1ull);
+      __syncthreads();
+      continue;
+    }
+    if (tid == 0) {
+      atomicMax(&p.ctr->max_list, (ull)max(NLk, NRk));
+    }
+    // ---- column pairs (a at ks, b at ks+1)
+    {
+      // reuse build_segments with kd = ks+1 (b), kn = ks (a), left = true: offsets unused
+      const int npairs = build_segments(p, b, sh, ks + 1, ks, true, b.offA /*unused*/, b.tmp /*zeros ok*/);
+      if (npairs < 0) {
+        if (tid == 0) atomicAdd(&p.ctr->unsupported, 1ull);
+        __syncthreads();
+        continue;
+      }
+      if (tid == 0) atomicAdd(&p.ctr->pairs, (ull)npairs);
+      for (int e = 0; e < npairs; ++e) {
+        const Seg g = b.segs[e];
+        const int a = g.p, bb = g.s;
+        const int nL = (int)b.cL[sh.cb[ks] + a];
+        const int nR = (int)b.cR[sh.cb[ks + 1] + bb];
+        const int nctxL = ks >= 1 ? sh.n[ks - 1] : 1;
+        const int nctxR = ks + 2 <= M ? sh.n[ks + 2] : 1;
+        for (int al = tid; al < nctxL; al += kThreads) {
+          double2 f = pi;
+          if (ks >= 1) {
+            if (compat(p, b, sh, ks, al, a)) f = cmul(pi, cut_factor(p, b, sh, ks, al, a, bb, cm));
+            else f = make_double2(0.0, 0.0);
+          }
+          b.FL[al] = f;
         }
-        Pb = P0;
+        for (int be = tid; be < nctxR; be += kThreads) {
+          double2 f = make_double2(1.0, 0.0);
+          if (ks + 1 <= M - 1) {
+            if (compat(p, b, sh, ks + 2, bb, be)) f = cut_factor(p, b, sh, ks + 1, a, bb, be, cm);
+            else f = make_double2(0.0, 0.0);
+          }
+          b.FR[be] = f;
+        }
+        __syncthreads();
+        const double2 *xp = Lp[curL] + offL[a];
+        const uint16_t *xc = Lc[curL] + offL[a];
+        const double2 *yp = Rp[curR] + offR[bb];
+        const uint16_t *yc = Rc[curR] + offR[bb];
+        if (nL >= nR)
+          outer_pair(xp, xc, b.FL, nL, yp, yc, b.FR, nR, sY, acc, npaths, cm);
+        else
+          outer_pair(yp, yc, b.FR, nR, xp, xc, b.FL, nL, sY, acc, npaths, cm);
       }
     }
-    __syncwarp();
-
-    // after a chain's subtree is done: pop the deepest open branch (or become idle)
-    auto resume_walk = [&]() {
-      if (top != bot) {
-        const unsigned e2 = ((top - 1u) & (STK - 1)) * 32;
-        const uint32_t m2 = mySM[e2];
-        const int jj = m2 & 0xff;
-        const int nv2 = (int)lb[lofp_level_off(jj)] + 1;
-        Pb = mySP[e2];
-        if (nv2 == (int)((m2 >> 8) & 0xff)) --top;
-        j = jj;
-        v = nv2;
-        set_level<CHAIN>(lb, kb, s_lev[jj], s_scat, jj, nv2);
-      } else if (otop != obot) {
-        const unsigned e2 = (otop - 1u) & (LOFP_OVF - 1);
-        const uint32_t m2 = ovfM[e2];
-        const int jj = m2 & 0xff;
-        const int nv2 = (int)lb[lofp_level_off(jj)] + 1;
-        Pb = ovfP[e2];
-        if (nv2 == (int)((m2 >> 8) & 0xff)) --otop;
-        j = jj;
-        v = nv2;
-        set_level<CHAIN>(lb, kb, s_lev[jj], s_scat, jj, nv2);
-      } else {
-        working = false;
-      }
-    };
-
-    unsigned iter = 0;
-    while (true) {
-      // ---------------- intra-warp hand-over ----------------
-      // One per step: the lane holding the shallowest open branch of the warp gives it
-      // (all its remaining siblings) to the lowest idle lane.
-      const unsigned idle = __ballot_sync(FULL, !working);
-      if (idle) {
-        int myshal = 0x7fffffff;
-        if (working) {
-          if (otop != obot)
-            myshal = (int)(ovfM[obot & (LOFP_OVF - 1)] & 0xff);
-          else if (top != bot)
-            myshal = (int)(mySM[(bot & (STK - 1)) * 32] & 0xff);
-        }
-        const int shal = __reduce_min_sync(FULL, myshal);
-        if (shal == 0x7fffffff) {
-          if (idle == FULL) break;  // item finished
-        } else {
-          const int donor = __ffs(__ballot_sync(FULL, myshal == shal)) - 1;
-          const int recv = __ffs(idle) - 1;
-          if (lane == donor) {  // publish the shallowest open branch
-            uint32_t m;
-            double2 P;
-            if (otop != obot) {
-              m = ovfM[obot & (LOFP_OVF - 1)];
-              P = ovfP[obot & (LOFP_OVF - 1)];
-              ++obot;
-            } else {
-              const unsigned e = (bot & (STK - 1)) * 32;
-              m = mySM[e];
-              P = mySP[e];
-              ++bot;
-            }
-            mbM[0] = m;
-            mbP[0] = P;
-          }
-          __syncwarp();
-          if (lane == recv) {
-            const uint32_t m = mbM[0];
-            const double2 P = mbP[0];
-            const int jd = m & 0xff, hh = (m >> 8) & 0xff;
-            const int nw = ((jd + 1) >> 2) + 1;  // words holding slots [0, jd + 1]
-            for (int w = 0; w < nw; ++w)
-              *reinterpret_cast<uint32_t *>(vcol + w * 128 + 4 * lane) =
-                  *reinterpret_cast<const uint32_t *>(vcol + w * 128 + 4 * donor);
-            // the donor's keys hold the prefix values (deeper bytes are rewritten on descent)
-            for (int f = 0; f < NK; ++f)
-              *reinterpret_cast<uint32_t *>(kcol + f * 128 + 4 * lane) =
-                  *reinterpret_cast<const uint32_t *>(kcol + f * 128 + 4 * donor);
-            const int nv = (int)lb[lofp_level_off(jd)] + 1;
-            set_level<CHAIN>(lb, kb, s_lev[jd], s_scat, jd, nv);
-            bot = top = obot = otop = 0;
-            leafhi = 0;
-            if (jd == Lm1) {
-              leafhi = hh;
-            } else if (hh > nv) {
-              mySM[0] = (uint32_t)jd | ((uint32_t)hh << 8);
-              mySP[0] = P;
-              top = 1;
-            }
-            Pb = P;
-            j = jd;
-            v = nv;
-            working = true;
-            ++dons;
-            if (COUNTED) atomicAdd(&a.ctr->don_hist[min(Lm1 - jd, 63)], 1ull);
-          }
-          __syncwarp();
-        }
-      }
-
-      // ---------------- one DFS node per lane ----------------
-      // Every lane runs the same instruction stream: the product of its current level's
-      // factors (warp-uniform trip count), one move -- next leaf sibling, pop of the
-      // deepest open branch, or descent -- chosen by predicates, and one write of the new
-      // value into the vals byte and the key bytes (warp-uniform trip count; a lane with
-      // nothing to write writes a scratch byte).
-      {
-        const bool stepping = working && !chain_pending;  // a pending lane waits for the engine
-        const PlanLevel lv = s_lev[stepping ? j : 0];
-        const int fcnt = stepping ? (int)lv.fend - (int)lv.fbeg : 0;
-        const int nmax = __reduce_max_sync(FULL, fcnt);
-        const double2 P = level_product<COUNTED, CHAIN>(Pb, lv.fbeg, fcnt, nmax, s_fac, kb, s_off, s_ent, lb, ncm);
-        const bool isleaf = stepping && j == Lm1;
-        if (isleaf) {
-          acc.x += P.x;
-          acc.y += P.y;
-          if (COUNTED) ++npaths;
-        }
-        const bool sib = isleaf && v < leafhi;
-        const bool desc = stepping && !isleaf;
-        const bool popsm = isleaf && !sib && top != bot;
-        const unsigned te = ((top - 1u) & (STK - 1)) * 32;
-        uint32_t m = mySM[te];
-        double2 Ps = mySP[te];
-        bool popov = false;
-        if (isleaf && !sib && !popsm && otop != obot) {  // rare: the local overflow
-          popov = true;
-          const unsigned e = (otop - 1u) & (LOFP_OVF - 1);
-          m = ovfM[e];
-          Ps = ovfP[e];
-        }
-        const bool pop = popsm || popov;
-        const bool moves = desc || sib || pop;
-        const int nj = desc ? j + 1 : (sib ? j : (pop ? (int)(m & 0xff) : 0));
-        const PlanLevel nl = s_lev[nj];
-        const uint16_t noff = lofp_level_off(nj);
-        const int dlo = max((int)lb[nl.ol] + nl.cl, (int)nl.lo);
-        const int dhi = min((int)lb[nl.or_] + nl.cr, (int)nl.hi);
-        const int pv = (int)lb[noff] + 1;
-        const int nv = desc ? dlo : (sib ? v + 1 : pv);
-        if (pop) {
-          Pb = Ps;
-          if (pv == (int)((m >> 8) & 0xff)) {
-            if (popsm) --top; else --otop;
-          }
-        }
-        const bool tochain = desc && nj == jbq;
-        if (tochain) {
-          Pb = P;  // product through level jb - 1: the chain's root product
-          chain_pending = true;
-        } else if (desc) {
-          Pb = P;
-          if (nj == Lm1) {
-            leafhi = dhi;  // leaf siblings are walked one per step
-          } else if (dhi > dlo) {
-            if (top - bot == STK) {  // full: the shallowest entry goes to the overflow
-              const unsigned e = (bot & (STK - 1)) * 32, o = otop & (LOFP_OVF - 1);
-              ovfM[o] = mySM[e];
-              ovfP[o] = mySP[e];
-              ++otop;
-              ++bot;
-              ++ovfc;
-            }
-            const unsigned e = (top & (STK - 1)) * 32;
-            mySM[e] = (uint32_t)nj | ((uint32_t)dhi << 8);
-            mySP[e] = P;
-            ++top;
-          }
-        }
-        const bool wr = moves && !tochain;
-        if (stepping) working = moves;
-        if (wr) {
-          j = nj;
-          v = nv;
-        }
-        // the new value: vals byte and key bytes
-        lb[wr ? (int)noff : (int)dummy_off] = (unsigned char)nv;
-        const int scnt = wr ? scatter_count<CHAIN>(nl) : 0;
-        const int smax = __reduce_max_sync(FULL, scnt);
-        const uint16_t *sp = s_scat + nl.sbeg;  // reads past the list stay in the warp's smem
-#pragma unroll 1
-        for (int i = 0; i < smax; i += 4) {  // four loads in flight, then four stores
-          const uint2 w = make_uint2(sp[i] | ((uint32_t)sp[i + 1] << 16), sp[i + 2] | ((uint32_t)sp[i + 3] << 16));
-          kb[i < scnt ? (int)(w.x & 0xffff) : dummy_rel] = (unsigned char)nv;
-          kb[i + 1 < scnt ? (int)(w.x >> 16) : dummy_rel] = (unsigned char)nv;
-          kb[i + 2 < scnt ? (int)(w.y & 0xffff) : dummy_rel] = (unsigned char)nv;
-          kb[i + 3 < scnt ? (int)(w.y >> 16) : dummy_rel] = (unsigned char)nv;
-        }
-      }
-
-      LOFP_PHASE(0);
-      // ---------------- chain engine (lockstep, whole warp) ----------------
-      // Each lane that reached the first chain level hands its chain -- the Cartesian
-      // product of the chain levels' ranges, fixed by its levels < jb -- to the whole warp:
-      // (1) lane m computes chain level m's range; (2) the pair table
-      // W_m(v_{m-1}, v_m) = product of level m's factors is built (one entry per lane per
-      // round); (3) every path of the chain is enumerated: the leading digits are split
-      // over the lanes, the remaining digits run one odometer shared by all lanes (warp-
-      // uniform control), each path's product = root * prod_m W_m formed with prefix
-      // sharing and added to the lane's accumulator.  Then the emitting lane pops its
-      // stack as after a finished subtree.
-      {
-        unsigned pend = CHAIN ? __ballot_sync(FULL, chain_pending) : 0u;
-        if (pend) {
-          // Every pending lane sizes its own chain; short chains (few paths) are
-          // enumerated together below, the others get a warp pass each.
-          const int Mb = L - jbq;
-          bool small = false;
-          int myE = 0, myR = 0;
-          if (SMALL && chain_pending && Mb <= LOFP_SMALL_LEVELS) {
-            int rprev = 1, E = 0;
-            float R = 1.f;
-            for (int m = 0; m < Mb; ++m) {
-              const PlanLevel cl = s_lev[jbq + m];
-              const int lo = max((int)lb[cl.ol] + cl.cl, (int)cl.lo);
-              const int r = min((int)lb[cl.or_] + cl.cr, (int)cl.hi) - lo + 1;
-              sc_lo[m * 32 + lane] = (unsigned char)lo;
-              sc_r[m * 32 + lane] = (unsigned char)r;
-              sc_wb[m * 32 + lane] = (uint16_t)min(E, 65535);
-              E += rprev * r;
-              rprev = r;
-              R *= (float)r;
-            }
-            small = R < (float)a.small_paths && E <= LOFP_W_MAX;
-            myE = E;
-            myR = (int)R;
-          }
-          unsigned smask = SMALL ? __ballot_sync(FULL, small) : 0u;
-          pend &= ~smask;
-          // ---- short chains, batched: all their pair tables, then all their paths ----
-          while (smask) {
-            const bool cand = (smask >> lane) & 1u;
-            int incE = cand ? myE : 0;
-            for (int o = 1; o < 32; o <<= 1) {
-              const int tv = __shfl_up_sync(FULL, incE, o);
-              if (lane >= o) incE += tv;
-            }
-            const bool ing = cand && incE <= LOFP_W_MAX;  // a prefix of the candidates
-            const unsigned gmask = __ballot_sync(FULL, ing);
-            smask &= ~gmask;
-            const int eg = ing ? myE : 0, rg = ing ? myR : 0;
-            int ie = eg, ir = rg;
-            for (int o = 1; o < 32; o <<= 1) {
-              const int te = __shfl_up_sync(FULL, ie, o), tr = __shfl_up_sync(FULL, ir, o);
-              if (lane >= o) {
-                ie += te;
-                ir += tr;
-              }
-            }
-            const int Eg = __shfl_sync(FULL, ie, 31), Rg = __shfl_sync(FULL, ir, 31);
-            sc_wbase[lane] = ie - eg;
-            sc_pbase[lane] = ir - rg;
-            if (lane == 0) {
-              sc_wbase[32] = Eg;
-              sc_pbase[32] = Rg;
-            }
-            sc_proot[lane] = Pb;
-            __syncwarp();
-            if (lane == 0) nchains += __popc(gmask);
-            for (int w = lane; w < Eg; w += 32) {  // pair tables W of every chain of the group
-              int c = 0;
-              for (int st = 16; st > 0; st >>= 1)
-                if (sc_wbase[c + st] <= w) c += st;
-              const int loc = w - sc_wbase[c];
-              int m = 0;
-              for (int st = LOFP_SMALL_LEVELS / 2; st > 0; st >>= 1)
-                if (m + st < Mb && sc_wb[(m + st) * 32 + c] <= loc) m += st;
-              const int rm = sc_r[m * 32 + c], rel = loc - sc_wb[m * 32 + c];
-              const int ii = (int)(((float)rel + 0.5f) * __frcp_rn((float)rm)), kk = rel - ii * rm;
-              const int vm = sc_lo[m * 32 + c] + kk, vp = m > 0 ? sc_lo[(m - 1) * 32 + c] + ii : 0;
-              const PlanLevel lv = s_lev[jbq + m];
-              double2 Q = make_double2(1.0, 0.0);
-              for (int f = lv.fbeg; f < lv.fend; ++f) {
-                const PlanFactor fd = s_fac[f];
-                const int key = (int)__byte_perm((uint32_t)gather_key(fd, vcol + 4 * c),
-                                                 (uint32_t)vm | ((uint32_t)vp << 8), fd.chain);
-                const int row = __dp4a(key, fd.crow, fd.base);
-                const int o = s_off[row] + __dp4a(key, 0x010000ff, (int)fd.dy);
-                Q = cmul(Q, s_ent[o]);
-                if (COUNTED) ncm += __dp4a(key, 0x000100ff, (int)fd.dx) > 0;
-              }
-              cW[w] = Q;
-            }
-            __syncwarp();
-            for (int p = lane; p < Rg; p += 32) {  // every path: root * prod_m W_m
-              int c = 0;
-              for (int st = 16; st > 0; st >>= 1)
-                if (sc_pbase[c + st] <= p) c += st;
-              int rem = p - sc_pbase[c];
-              const double2 *wc = cW + sc_wbase[c];
-              double2 P = sc_proot[c];
-              int m = Mb - 1, rm = sc_r[m * 32 + c];
-              int q = (int)(((float)rem + 0.5f) * __frcp_rn((float)rm));
-              int cur = rem - q * rm;
-              rem = q;
-              for (; m > 0; --m) {  // digits from the last level; W_m(v_{m-1}, v_m)
-                const int rp = sc_r[(m - 1) * 32 + c];
-                const int q2 = (int)(((float)rem + 0.5f) * __frcp_rn((float)rp));
-                const int nxt = rem - q2 * rp;
-                rem = q2;
-                P = cmul(P, wc[sc_wb[m * 32 + c] + nxt * rm + cur]);
-                cur = nxt;
-                rm = rp;
-              }
-              P = cmul(P, wc[cur]);  // W_0(v_0)
-              acc.x += P.x;
-              acc.y += P.y;
-              if (COUNTED) {
-                ++npaths;
-                ncm += Mb;
-              }
-            }
-            __syncwarp();
-            if (ing) {
-              chain_pending = false;
-              resume_walk();
-            }
-          }
-        }
-        LOFP_PHASE(1);
-        while (pend) {
-          const int em = __ffs(pend) - 1;
-          pend &= pend - 1;
-          const unsigned char *lbe = vcol + 4 * em;
-          const double2 Proot = make_double2(__shfl_sync(FULL, Pb.x, em), __shfl_sync(FULL, Pb.y, em));
-          const int Mb = L - jbq;
-          int clo = 0, crr = 1;
-          if (lane < Mb) {
-            const PlanLevel cl = s_lev[jbq + lane];
-            clo = max((int)lbe[cl.ol] + cl.cl, (int)cl.lo);
-            crr = min((int)lbe[cl.or_] + cl.cr, (int)cl.hi) - clo + 1;
-          }
-          int rprev = __shfl_up_sync(FULL, crr, 1);
-          if (lane == 0) rprev = 1;
-          const int sz = lane < Mb ? rprev * crr : 0;
-          int inc = sz;
-          for (int o = 1; o < 32; o <<= 1) {
-            const int tv = __shfl_up_sync(FULL, inc, o);
-            if (lane >= o) inc += tv;
-          }
-          const int E = __shfl_sync(FULL, inc, 31);
-          // lane m: product of the ranges of levels <= m (exact in double); lane 31: paths
-          double pinc = (double)crr;
-          for (int o = 1; o < 32; o <<= 1) {
-            const double tv = __shfl_up_sync(FULL, pinc, o);
-            if (lane >= o) pinc *= tv;
-          }
-          const double Rd = __shfl_sync(FULL, pinc, 31);
-          const bool fb = E > LOFP_W_MAX || Rd > 2.0e9 || Rd < (double)a.chain_rmin;
-          if (lane == 0) {
-            if (fb) ++nchainfb; else ++nchains;
-          }
-          if (fb) {  // too few paths (or too many pairs/paths): the emitting lane walks the chain itself
-            if (lane == em) {
-              chain_pending = false;
-              j = jbq;
-              v = clo;  // lane em's own range of level jb (it is lane 0's value: broadcast)
-            }
-            const int lo0 = __shfl_sync(FULL, clo, 0), r0 = __shfl_sync(FULL, crr, 0);
-            if (lane == em) {
-              v = lo0;
-              set_level<CHAIN>(lb, kb, s_lev[jbq], s_scat, jbq, lo0);
-              if (jbq == Lm1) {
-                leafhi = lo0 + r0 - 1;
-              } else if (r0 > 1) {
-                if (top - bot == STK) {
-                  const unsigned e2 = (bot & (STK - 1)) * 32, o2 = otop & (LOFP_OVF - 1);
-                  ovfM[o2] = mySM[e2];
-                  ovfP[o2] = mySP[e2];
-                  ++otop;
-                  ++bot;
-                  ++ovfc;
-                }
-                const unsigned e2 = (top & (STK - 1)) * 32;
-                mySM[e2] = (uint32_t)jbq | ((uint32_t)(lo0 + r0 - 1) << 8);
-                mySP[e2] = Pb;
-                ++top;
-              }
-            }
-            continue;
-          }
-          LOFP_PHASE(1);
-          // reciprocal of the range: floor(n / r) = (int)((n + 0.5) * inv) exactly for n < 2^12
-          c_lv[lane] = make_int4(crr, clo, inc - sz, __float_as_int(__fdividef(1.0f, (float)crr)));  // (.y: low end until the split)
-          c_wb[lane] = inc - sz;
-          if (lane == 0) c_wb[32] = E;
-          __syncwarp();
-          // (2) pair table.  First the chain factors' keys (gathered once per chain from the
-          // emitter's value bytes; the chain bytes are replaced below), then one entry per
-          // lane per round: W_m(v_{m-1}, v_m) = product of level m's factors.
-          const int fc0 = s_lev[jbq].fbeg, nfc = NF - fc0;  // chain factors come last
-          uint32_t *ckey = reinterpret_cast<uint32_t *>(cPs);  // (the suffix table comes later)
-          const bool pre = nfc <= 2 * LOFP_SUF_ENTRIES;
-          if (pre) {
-            for (int f = lane; f < nfc; f += 32) {
-              ckey[f] = (uint32_t)gather_key(s_fac[fc0 + f], lbe);
-            }
-            __syncwarp();
-          }
-          for (int w = lane; w < E; w += 32) {
-            int m = 0;
-            for (int st = 16; st > 0; st >>= 1)
-              if (m + st < Mb && c_wb[m + st] <= w) m += st;
-            const int4 lvm = c_lv[m];
-            const int rm = lvm.x, rel = w - lvm.z;
-            const int ii = (int)(((float)rel + 0.5f) * __int_as_float(lvm.w)), kk = rel - ii * rm;
-            const uint32_t vmp = (uint32_t)(lvm.y + kk) | ((uint32_t)(m > 0 ? c_lv[m - 1].y + ii : 0) << 8);
-            const PlanLevel lv = s_lev[jbq + m];
-            double2 Q = make_double2(1.0, 0.0);
-#pragma unroll 1
-            for (int f = lv.fbeg; f < lv.fend; ++f) {
-              const PlanFactor fd = s_fac[f];
-              // the chain bytes of the key: v_m and v_{m-1} put in by one byte permutation
-              const uint32_t base = pre ? ckey[f - fc0] : (uint32_t)gather_key(fd, lbe);
-              const int key = (int)__byte_perm(base, vmp, fd.chain);
-              const int row = __dp4a(key, fd.crow, fd.base);
-              const int o = s_off[row] + __dp4a(key, 0x010000ff, (int)fd.dy);
-              Q = cmul(Q, s_ent[o]);
-              if (COUNTED) ncm += __dp4a(key, 0x000100ff, (int)fd.dx) > 0;
-            }
-            cW[w] = Q;
-          }
-          __syncwarp();  // the key scratch is reused by the suffix table below
-          LOFP_PHASE(2);
-          // (3) enumeration.  Digits [0, t) (prefix) are split over the lanes, digits
-          // [t, Mb) (suffix) form a table Suf[s] = prod_{m > t} W_m shared by all lanes
-          // (one lane per entry).  Every path of the chain is then formed as
-          //   (root * prod_{m < t} W_m * W_t) * Suf[s]
-          // -- one complex multiplication per path in a warp-uniform inner loop -- and
-          // added to the lane's accumulator.  t maximises lane use with |Suf| <= 64.
-          __syncwarp();
-          // split: the shortest prefix with >= 32 combinations (every lane busy), then
-          // lengthened until the suffix table has <= 64 entries (pinc: see the ranges).
-          const double Rdd = Rd;
-          const double thr = fmax(32.0, Rdd * (1.0 / LOFP_SUF_ENTRIES));
-          const unsigned okm = __ballot_sync(FULL, lane < Mb && pinc >= thr);
-          const int t = okm ? __ffs(okm) : Mb;  // prefix digits [0, t)
-          const double Ctd = t > 0 ? __shfl_sync(FULL, pinc, t - 1) : 1.0;
-          const long long Ct = (long long)Ctd;
-          // R / C_t: an exact integer <= 64 (float quotient error ~1e-7 of it: rounding is safe)
-          const int Rsi = __float2int_rn(__fdividef((float)Rdd, (float)Ctd));
-          // per-lane prefix digits (digit t-1 least significant) of the lane's first prefix
-          // index (= lane), and the digits of the stride 32, for an incremental add per round:
-          // digit m of c = floor(c / pv_m) mod r_m, pv_m = Ct / pinc_m (place value)
-          if (lane < t) {  // lane m: 1 / pv_m and digit m of the stride 32
-            const float ipv = __fdividef((float)pinc, (float)Ctd), ir = __fdividef(1.0f, (float)crr);
-            c_pv[lane] = __float_as_int(ipv);
-            const int q32 = (int)((32.0f + 0.5f) * ipv);
-            reinterpret_cast<int *>(c_lv + lane)[1] = q32 - (int)(((float)q32 + 0.5f) * ir) * crr;
-          }
-          __syncwarp();
-#pragma unroll 4
-          for (int m = 0; m < t; ++m) {
-            const int4 lvm = c_lv[m];
-            const float ipv = __int_as_float(c_pv[m]), ir = __int_as_float(lvm.w);
-            const int rm = lvm.x;
-            const int q = (int)(((float)lane + 0.5f) * ipv);
-            const int d = q - (int)(((float)q + 0.5f) * ir) * rm;
-            c_dig[m * 32 + lane] = (unsigned char)d;
-          }
-          LOFP_PHASE(3);
-          // suffix table: entry s (digit t most significant) = prod_{m = t+1}^{Mb-1} W_m;
-          // entries lane and lane + 32 are built together (two independent chains)
-          if (Rsi <= 32) {  // one entry per lane
-            const int s0 = lane;
-            int rem0 = s0;
-            double2 Q0 = make_double2(1.0, 0.0);
-            int4 lvm = c_lv[Mb - 1];
-            for (int m = Mb - 1; m > t; --m) {  // decode from the last digit
-              const int4 lvp = c_lv[m - 1];
-              const int rm = lvm.x, rp = lvp.x;
-              const float im = __int_as_float(lvm.w), ip = __int_as_float(lvp.w);
-              const int q0 = (int)(((float)rem0 + 0.5f) * im);
-              const int cur0 = rem0 - q0 * rm;
-              rem0 = q0;
-              const int nx0 = rem0 - (int)(((float)rem0 + 0.5f) * ip) * rp;  // digit m-1
-              const int blk_m = rp * rm;  // the level's pair-table block (m >= 1)
-              const double2 w0 = cW[lvm.z + min(nx0 * rm + cur0, blk_m - 1)];
-              lvm = lvp;
-              Q0 = cmul(Q0, w0);
-              if (COUNTED) ncm += (s0 < Rsi);
-            }
-            if (s0 < Rsi) cPs[s0] = Q0;
-          } else {
-            const int s0 = lane, s1 = lane + 32;
-            int rem0 = s0, rem1 = s1;
-            double2 Q0 = make_double2(1.0, 0.0), Q1 = Q0;
-            int4 lvm = c_lv[Mb - 1];
-            for (int m = Mb - 1; m > t; --m) {  // decode from the last digit
-              const int4 lvp = c_lv[m - 1];
-              const int rm = lvm.x, rp = lvp.x;
-              const float im = __int_as_float(lvm.w), ip = __int_as_float(lvp.w);
-              const int q0 = (int)(((float)rem0 + 0.5f) * im), q1 = (int)(((float)rem1 + 0.5f) * im);
-              const int cur0 = rem0 - q0 * rm, cur1 = rem1 - q1 * rm;
-              rem0 = q0;
-              rem1 = q1;
-              const int nx0 = rem0 - (int)(((float)rem0 + 0.5f) * ip) * rp;  // digit m-1
-              const int nx1 = rem1 - (int)(((float)rem1 + 0.5f) * ip) * rp;
-              const int blk_m = rp * rm;  // the level's pair-table block (m >= 1)
-              const double2 w0 = cW[lvm.z + min(nx0 * rm + cur0, blk_m - 1)];
-              const double2 w1 = cW[lvm.z + min(nx1 * rm + cur1, blk_m - 1)];
-              lvm = lvp;
-              Q0 = cmul(Q0, w0);
-              Q1 = cmul(Q1, w1);
-              if (COUNTED) ncm += (s0 < Rsi) + (s1 < Rsi);
-            }
-            if (s0 < Rsi) cPs[s0] = Q0;
-            if (s1 < Rsi) cPs[s1] = Q1;
-          }
-          __syncwarp();
-          LOFP_PHASE(7);
-          const int4 lvt = c_lv[min(t, Mb - 1)];
-          const int rt = t < Mb ? lvt.x : 1;
-          const int blk = Rsi / rt;  // suffix entries per value of digit t
-          for (long long c0 = 0; c0 < Ct; c0 += 32) {
-            const long long cc = c0 + lane;
-            const bool act = cc < Ct;
-            if (c0 > 0) {  // advance this lane's prefix index by 32 (mixed-radix add)
-              int carry = 0;
-#pragma unroll 1
-              for (int m = t - 1; m >= 0; --m) {
-                const int2 rd = *reinterpret_cast<const int2 *>(c_lv + m);  // (r_m, digit of 32)
-                int d = c_dig[m * 32 + lane] + rd.y + carry;
-                carry = d >= rd.x;
-                d -= carry ? rd.x : 0;
-                c_dig[m * 32 + lane] = (unsigned char)d;
-              }
-            }
-            double2 P = Proot;
-            int vprev = 0;
-#pragma unroll 4
-            for (int m = 0; m < t; ++m) {
-              const int d = c_dig[m * 32 + lane];
-              const int4 lv = c_lv[m];
-              const int idx = lv.z + (m > 0 ? vprev * lv.x : 0) + d;
-              P = cmul(P, cW[idx]);
-              if (COUNTED) ncm += act;
-              vprev = d;  // digit (offset from the level's low end)
-            }
-            if (t == Mb) {  // no suffix: the prefix is the whole path
-              if (act) {
-                acc.x += P.x;
-                acc.y += P.y;
-                if (COUNTED) ++npaths;
-              }
-              continue;
-            }
-            for (int dt = 0; dt < rt; ++dt) {
-              const double2 Q = cmul(P, cW[lvt.z + (t > 0 ? vprev * rt : 0) + dt]);
-              if (COUNTED) ncm += act;
-              const double2 *sf = cPs + dt * blk;
-              double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
-              int k = 0;
-              for (; k + 1 < blk; k += 2) {
-                const double2 l0 = cmul(Q, sf[k]), l1 = cmul(Q, sf[k + 1]);
-                a0.x += l0.x;
-                a0.y += l0.y;
-                a1.x += l1.x;
-                a1.y += l1.y;
-              }
-              if (k < blk) {
-                const double2 l0 = cmul(Q, sf[k]);
-                a0.x += l0.x;
-                a0.y += l0.y;
-              }
-              if (act) {
-                acc.x += a0.x + a1.x;
-                acc.y += a0.y + a1.y;
-                if (COUNTED) {
-                  npaths += blk;
-                  ncm += blk;
-                }
-              }
-            }
-          }
-          __syncwarp();
-          LOFP_PHASE(4);
-          // the emitting lane continues its depth-first walk after the chain's subtree
-          if (lane == em) {
-            chain_pending = false;
-            resume_walk();
-          }
-        }
-      }
-
-      LOFP_PHASE(5);
-      // ---------------- feed idle warps through the global queue ----------------
-      // At most one subtree per warp per check: the warp's shallowest open branch, and
-      // only when it is far from the leaves (a large subtree) and some warp is waiting.
-      if (((++iter) & (CHAIN ? 0u : 31u)) == 0u) {  // (a chain step is long: check often)
-        long long waiting = 0;
-        if (lane == 0) waiting = (long long)(vload(&a.ctr->ticket) - vload(&a.ctr->tail));
-        waiting = __shfl_sync(FULL, waiting, 0);
-        if (waiting > 0) {
-          int myshal = 0x7fffffff;
-          if (working) {
-            if (otop != obot)
-              myshal = (int)(ovfM[obot & (LOFP_OVF - 1)] & 0xff);
-            else if (top != bot)
-              myshal = (int)(mySM[(bot & (STK - 1)) * 32] & 0xff);
-          }
-          const int shal = __reduce_min_sync(FULL, myshal);
-          if (shal != 0x7fffffff && Lm1 - shal >= LOFP_SPILL_MIN_DIST) {
-            const int giver = __ffs(__ballot_sync(FULL, myshal == shal)) - 1;
-            if (lane == giver) {
-              atomicAdd(&a.ctr->outstanding, 1ull);
-              const unsigned long long slot = atomicAdd(&a.ctr->tail, 1ull);
-              if (otop != obot) {
-                const unsigned e = obot & (LOFP_OVF - 1);
-                spill(slot, out, ovfM[e], ovfP[e]);
-                ++obot;
-              } else {
-                const unsigned e = (bot & (STK - 1)) * 32;
-                spill(slot, out, mySM[e], mySP[e]);
-                ++bot;
-              }
-              ++spills;
-            }
-          }
-        }
-      }
-    }
-
-    LOFP_PHASE(6);
-    // ---------------- item finished: warp reduction, one atomic per item ----------------
-    for (int s = 16; s > 0; s >>= 1) {
-      acc.x += __shfl_xor_sync(FULL, acc.x, s);
-      acc.y += __shfl_xor_sync(FULL, acc.y, s);
-      if (COUNTED) {
-        npaths += __shfl_xor_sync(FULL, npaths, s);
-        ncm += __shfl_xor_sync(FULL, ncm, s);
-      }
-    }
-    if (lane == 0) {
-      atomicAdd(&a.amps[2 * out], acc.x);
-      atomicAdd(&a.amps[2 * out + 1], acc.y);
-      if (COUNTED) {
-        atomicAdd(&a.counts[out], npaths);
-        atomicAdd(&a.ctr->leaves, npaths);
-        atomicAdd(&a.ctr->cmuls, ncm);
-      }
-      __threadfence();
-      atomicAdd(&a.ctr->outstanding, ~0ull);  // -1
-    }
-    __syncwarp();
   }
-  // statistics
-  for (int s = 16; s > 0; s >>= 1) {
-    spills += __shfl_xor_sync(FULL, spills, s);
-    ovfc += __shfl_xor_sync(FULL, ovfc, s);
-    dons += __shfl_xor_sync(FULL, dons, s);
+}
+
+__device__ void reduce_block(Shared &sh, double2 (&acc)[kKX], double2 *out, ull np, ull *np_out) {
+  double re = 0.0, im = 0.0;
+#pragma unroll
+  for (int r = 0; r < kKX; ++r) {
+    re += acc[r].x;
+    im += acc[r].y;
   }
-  if (COUNTED && lane == 0)
-    for (int k = 0; k < 8; ++k) atomicAdd(&a.ctr->phase_cyc[k], ph[k]);
+  for (int d = 16; d > 0; d >>= 1) {
+    re += __shfl_down_sync(0xffffffffu, re, d);
+    im += __shfl_down_sync(0xffffffffu, im, d);
+    np += __shfl_down_sync(0xffffffffu, np, d);
+  }
+  __shared__ double rre[kThreads / 32], rim[kThreads / 32];
+  __shared__ ull rnp[kThreads / 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) {
-    atomicAdd(&a.ctr->chains, nchains);
-    atomicAdd(&a.ctr->chain_fb, nchainfb);
-    atomicAdd(&a.ctr->items, items);
-    atomicAdd(&a.ctr->spills, spills);
-    atomicAdd(&a.ctr->ovf, ovfc);
-    atomicAdd(&a.ctr->donations, dons);
+    rre[warp] = re;
+    rim[warp] = im;
+    rnp[warp] = np;
   }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, c = 0.0;
+    ull n = 0;
+    for (int w = 0; w < kThreads / 32; ++w) {
+      a += rre[w];
+      c += rim[w];
+      n += rnp[w];
+    }
+    *out = make_double2(a, c);
+    *np_out = n;
+  }
+  __syncthreads();
+}
+
+__device__ void load_cols(const CallParams &p, Shared &sh) {
+  for (int k = threadIdx.x; k <= p.M; k += kThreads) sh.col[k] = p.col[k];
+  if (threadIdx.x == 0) sh.q_cached = -1;
+  __syncthreads();
 }
 
 }  // namespace
 
-// ---------------------------------------------------------------------------
-// launchers
-// ---------------------------------------------------------------------------
-cudaError_t lofp_launch_prep(const CallArgs &a, cudaStream_t s) {
-  if (a.B == 0) return cudaSuccess;
-  int bs = 256;
-  lofp_prep_kernel<<<(unsigned)((a.B + bs - 1) / bs), bs, 0, s>>>(a);
-  return cudaGetLastError();
-}
-
-cudaError_t lofp_launch_tables(const CallArgs &a, cudaStream_t s) {
-  if (a.nentries == 0) return cudaSuccess;
-  int bs = 128;
-  lofp_table_kernel<<<(a.nentries + bs - 1) / bs, bs, 0, s>>>(a);
-  return cudaGetLastError();
-}
-
-cudaError_t lofp_launch_plan(const CallArgs &a, cudaStream_t s) {
-  if (a.B == 0) return cudaSuccess;
-  int bs = 64;
-  lofp_plan_kernel<<<(unsigned)((a.B + bs - 1) / bs), bs, 0, s>>>(a);
-  return cudaGetLastError();
-}
-
-// The enumeration kernel variants: validation counters, chain engine, batched short chains
-// (the last only on request; it enlarges the engine's code).
-static const void *pick_enum(bool counted, bool chain, bool small) {
-  if (counted) {
-    if (!chain) return (const void *)lofp_enum_kernel<true, false, false>;
-    return small ? (const void *)lofp_enum_kernel<true, true, true> : (const void *)lofp_enum_kernel<true, true, false>;
+// ---- Appendix-A tables ---------------------------------------------------------------
+__global__ void lofp_table_off_kernel(const __grid_constant__ CallParams p) {
+  // one block: per-BS block sizes (past light cone of its inputs) and offsets
+  __shared__ long long part[kThreads];
+  const int nb = p.nbs, tid = threadIdx.x;
+  const int per = (nb + kThreads - 1) / kThreads;
+  const int a = tid * per, e = min(nb, a + per);
+  long long s = 0;
+  for (int i = a; i < e; ++i) {
+    const BSInfo bi = p.bsi[i];
+    const int cap = min(p.N, (int)p.cumS[bi.cap_hi] - (int)p.cumS[bi.cap_lo]);
+    s += tri_dev(cap + 1);
   }
-  if (!chain) return (const void *)lofp_enum_kernel<false, false, false>;
-  return small ? (const void *)lofp_enum_kernel<false, true, true> : (const void *)lofp_enum_kernel<false, true, false>;
+  part[tid] = s;
+  __syncthreads();
+  if (tid == 0) {
+    long long run = 0;
+    for (int i = 0; i < kThreads; ++i) {
+      const long long v = part[i];
+      part[i] = run;
+      run += v;
+    }
+    p.tab_off[nb] = run;
+    if (run > p.table_cap) atomicAdd(&p.ctr->table_error, 1ull);
+  }
+  __syncthreads();
+  long long run = part[tid];
+  for (int i = a; i < e; ++i) {
+    p.tab_off[i] = run;
+    const BSInfo bi = p.bsi[i];
+    const int cap = min(p.N, (int)p.cumS[bi.cap_hi] - (int)p.cumS[bi.cap_lo]);
+    run += tri_dev(cap + 1);
+  }
+  // phase gates exp(i (a n + b n^2)) for n = 0..N (reading R19)
+  for (int t = tid; t < p.ngate * (p.N + 1); t += kThreads) {
+    const int g = t / (p.N + 1), n = t % (p.N + 1);
+    const double arg = p.gate_ab[2 * g] * n + p.gate_ab[2 * g + 1] * (double)n * n;
+    double sn, cs;
+    sincos(arg, &sn, &cs);
+    p.gate_tab[t] = make_double2(cs, sn);
+  }
 }
 
-cudaError_t lofp_enum_config(const CallArgs &a, bool counted, int *grid, int *block, size_t *smem) {
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return e;
-  int sms = 0, maxblk = 0, maxsm = 0;
-  e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (e != cudaSuccess) return e;
-  e = cudaDeviceGetAttribute(&maxblk, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  if (e != cudaSuccess) return e;
-  e = cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-  if (e != cudaSuccess) return e;
-  const void *fn = pick_enum(counted, a.chain_on != 0, a.small_paths > 0);
-  cudaFuncAttributes fa;
-  e = cudaFuncGetAttributes(&fa, fn);
-  if (e != cudaSuccess) return e;
-  // Pick warps per block W and blocks per SM n to maximise resident warps: the staged
-  // tables are paid once per block, the per-warp state once per warp.
-  const size_t tb = (size_t)a.table_bytes, wbytes = (size_t)a.warp_bytes;
-  const int max_w = LOFP_ENUM_MAX_THREADS / 32;
-  int regs_warps = fa.numRegs > 0 ? 65536 / (fa.numRegs * 32) : 64;
-  int best_w = 0, best_n = 0;
-  for (int w = 1; w <= max_w; ++w) {
-    size_t per_block = tb + (size_t)w * wbytes + 1024;  // + the per-block reservation
-    if (per_block - 1024 > (size_t)maxblk) break;
-    int n = (int)((size_t)maxsm / per_block);
-    int nw = regs_warps / w;
-    if (nw < n) n = nw;
-    if (n > 32) n = 32;
-    if (n < 1) continue;
-    if (n * w > best_n * best_w || (n * w == best_n * best_w && w > best_w)) {
-      best_w = w;
-      best_n = n;
+// Appendix-A elements of BS blockIdx.x for every photon number n <= cap:
+// the real Wigner-type factor d_n(x1, y1) of <y1, n-y1| BS |x1, n-x1> from the four-term
+// recurrence  n d_n(x, y) = sum_{i,k} sqrt(x_i y_k) u_ki d_{n-1}(x - e_i, y - e_k)  with
+// u = [[c, -s], [s, c]] (reading R18), then the phase e^{i phi (x1 - y1)}
+// (SURVEY A.1).  Stable to ~1e-15 at 120 photons, unlike the alternating t-sum.
+__global__ void __launch_bounds__(kThreads) lofp_table_kernel(const __grid_constant__ CallParams p) {
+  const int bs = blockIdx.x, tid = threadIdx.x;
+  if (p.tab_off[p.nbs] > p.table_cap) return;
+  const BSInfo bi = p.bsi[bs];
+  const int cap = min(p.N, (int)p.cumS[bi.cap_hi] - (int)p.cumS[bi.cap_lo]);
+  double2 *tb = p.table + p.tab_off[bs];
+  const double c = bi.c, s = bi.s;
+  if (tid == 0) tb[0] = make_double2(1.0, 0.0);
+  __syncthreads();
+  for (int n = 1; n <= cap; ++n) {
+    const double2 *prev = tb + tri_dev(n - 1);
+    double2 *curr = tb + tri_dev(n);
+    const double inv_n = 1.0 / n;
+    for (int idx = tid; idx < (n + 1) * (n + 1); idx += kThreads) {
+      const int x1 = idx / (n + 1), y1 = idx - x1 * (n + 1);
+      const int x2 = n - x1, y2 = n - y1;
+      double v = 0.0;
+      if (x1 > 0) {  // remove a photon from input mode 1 (row x1-1 of level n-1)
+        if (y1 > 0) v += sqrt((double)(x1 * y1)) * c * prev[(x1 - 1) * n + (y1 - 1)].x;
+        if (y2 > 0) v += sqrt((double)(x1 * y2)) * s * prev[(x1 - 1) * n + y1].x;
+      }
+      if (x2 > 0) {  // remove a photon from input mode 2 (row x1 of level n-1)
+        if (y1 > 0) v -= sqrt((double)(x2 * y1)) * s * prev[x1 * n + (y1 - 1)].x;
+        if (y2 > 0) v += sqrt((double)(x2 * y2)) * c * prev[x1 * n + y1].x;
+      }
+      curr[idx] = make_double2(v * inv_n, 0.0);
+    }
+    __syncthreads();
+  }
+  // phases: <y1,y2|BS(theta,phi)|x1,x2> = e^{i phi (x1 - y1)} d
+  for (int n = 1; n <= cap; ++n) {
+    double2 *curr = tb + tri_dev(n);
+    for (int idx = tid; idx < (n + 1) * (n + 1); idx += kThreads) {
+      const int x1 = idx / (n + 1), y1 = idx - x1 * (n + 1);
+      if (x1 == y1) continue;
+      double sn, cs;
+      sincos(bi.phi * (double)(x1 - y1), &sn, &cs);
+      const double d = curr[idx].x;
+      curr[idx] = make_double2(d * cs, d * sn);
     }
   }
-  if (best_w == 0) return cudaErrorInvalidConfiguration;
-  size_t sm = tb + (size_t)best_w * wbytes;
-  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  if (e != cudaSuccess) return e;
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, best_w * 32, sm);
-  if (e != cudaSuccess) return e;
-  if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  *grid = per_sm * sms;
-  *block = best_w * 32;
-  *smem = sm;
-  return cudaSuccess;
 }
 
-cudaError_t lofp_launch_enum(const CallArgs &a, bool counted, int grid, int block, size_t smem,
-                             cudaStream_t s) {
-  void *args[] = {const_cast<CallArgs *>(&a)};
-  cudaError_t e = cudaLaunchKernel(pick_enum(counted, a.chain_on != 0, a.small_paths > 0), dim3(grid), dim3(block),
-                                   args, smem, s);
-  if (e != cudaSuccess) return e;
-  return cudaGetLastError();
+// ---- plan: per output, counts and the split into units -------------------------------
+__global__ void __launch_bounds__(kThreads) lofp_plan_kernel(const __grid_constant__ CallParams p) {
+  __shared__ Shared sh;
+  Block b = make_block(p);
+  load_cols(p, sh);
+  const int M = p.M, tid = threadIdx.x;
+  for (int q = blockIdx.x; q < p.B; q += gridDim.x) {
+    int st = setup_output(p, b, sh, q);
+    if (st == kStatusOk) {
+      dp_counts(p, b, sh, 0, 0, true);
+      if (b.cR[sh.cb[0]] == 0) st = kStatusZero;
+    }
+    if (tid == 0) {
+      p.pdone[q] = 0;
+      p.status[q] = (uint8_t)st;
+      int count = 0;
+      if (st == kStatusOk) {
+        atomicAdd(&p.ctr->feasible, 1ull);
+        const ull P = b.cR[sh.cb[0]];
+        p.pexp[q] = P;
+        // root product: phase gates that no cut carries (M == 1: the single mode holds N)
+        double2 root = make_double2(1.0, 0.0);
+        if (M == 1)
+          for (int g = 0; g < p.ngate; ++g) root = cmul(root, p.gate_tab[g * (p.N + 1) + p.N]);
+        ull thr = p.thr;
+        Unit *U = p.units + (long long)q * p.budget;
+        while (true) {
+          count = 0;
+          int sp = 0;
+          StackEnt e;
+          e.j = 0; e.sjm1 = 0; e.sj = 0; e.re = root.x; e.im = root.y; e.pad = 0;
+          b.stack[sp++] = e;
+          while (sp > 0) {
+            const StackEnt t = b.stack[--sp];
+            const ull below = b.cR[sh.cb[t.j] + t.sj];
+            bool leaf = below <= thr || t.j >= M - 1;
+            if (!leaf) {
+              const int n1 = sh.n[t.j + 1];
+              int pushed = 0;
+              for (int s = n1 - 1; s >= 0; --s) {
+                if (!live(b, sh, t.j + 1, s) || !compat(p, b, sh, t.j + 1, t.sj, s)) continue;
+                if (sp >= kStackMax) { leaf = true; break; }
+                ull cm = 0;
+                const double2 f = cut_factor(p, b, sh, t.j, t.sjm1, t.sj, s, cm);
+                const double2 np = cmul(make_double2(t.re, t.im), f);
+                StackEnt c;
+                c.j = t.j + 1; c.sjm1 = t.sj; c.sj = (uint16_t)s; c.re = np.x; c.im = np.y; c.pad = 0;
+                b.stack[sp++] = c;
+                ++pushed;
+              }
+              if (leaf) sp -= pushed;  // stack full: keep this node whole
+            }
+            if (leaf) {
+              if (count < p.budget) {
+                Unit u;
+                u.q = q; u.j = (int16_t)t.j; u.sjm1 = t.sjm1; u.sj = t.sj; u.pad = 0;
+                u.re = t.re; u.im = t.im; u.paths = below;
+                U[count] = u;
+              }
+              ++count;
+            }
+          }
+          if (count <= p.budget) break;
+          thr = thr > (~0ull >> 2) ? ~0ull : thr * 4;  // too many units for the slots: coarser
+        }
+      } else {
+        p.pexp[q] = 0;
+        if (st == kStatusBad) atomicAdd(&p.ctr->bad_rows, 1ull);
+        if (st == kStatusUnsupported) atomicAdd(&p.ctr->unsupported, 1ull);
+      }
+      p.nunits[q] = count;
+    }
+    __syncthreads();
+  }
 }
+
+// exclusive scan of nunits -> ubase, total -> ctr->total_units (one block of kThreads)
+__global__ void lofp_scan_kernel(const __grid_constant__ CallParams p) {
+  __shared__ long long part[kThreads];
+  const int B = p.B, tid = threadIdx.x;
+  const int per = (B + kThreads - 1) / kThreads;
+  const int a = tid * per, e = min(B, a + per);
+  long long s = 0;
+  for (int i = a; i < e; ++i) s += p.nunits[i];
+  part[tid] = s;
+  __syncthreads();
+  if (tid == 0) {
+    long long run = 0;
+    for (int i = 0; i < kThreads; ++i) {
+      const long long v = part[i];
+      part[i] = run;
+      run += v;
+    }
+    p.ubase[B] = (int)run;
+    p.ctr->total_units = (ull)run;
+  }
+  __syncthreads();
+  long long run = part[tid];
+  for (int i = a; i < e; ++i) {
+    p.ubase[i] = (int)run;
+    run += p.nunits[i];
+  }
+}
+
+// ---- the hot path ----------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads, 2) lofp_units_kernel(const __grid_constant__ CallParams p) {
+  __shared__ Shared sh;
+  extern __shared__ double2 sY[];
+  Block b = make_block(p);
+  load_cols(p, sh);
+  const int tid = threadIdx.x;
+  ull cm = 0, nelem = 0;
+  while (true) {
+    if (tid == 0) sh.unit = (int)atomicAdd(&p.ctr->ticket, 1ull);
+    __syncthreads();
+    const int u = sh.unit;
+    if ((ull)u >= p.ctr->total_units) break;
+    // unit u -> output q (binary search over ubase) -> slot
+    int lo = 0, hi = p.B - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (p.ubase[mid] <= u) lo = mid; else hi = mid - 1;
+    }
+    const int q = lo;
+    const Unit un = p.units[(long long)q * p.budget + (u - p.ubase[q])];
+    if (sh.q_cached != q) {
+      const int st = setup_output(p, b, sh, q);
+      if (st != kStatusOk) {  // cannot happen: units exist only for feasible outputs
+        if (tid == 0) {
+          atomicAdd(&p.ctr->table_error, 1ull);
+          p.partial[u] = make_double2(0.0, 0.0);
+        }
+        __syncthreads();
+        continue;
+      }
+      if (tid == 0) sh.q_cached = q;
+    } else {
+      carve(p, b, sh);  // columns of q are still in the slab from an earlier unit
+    }
+    if (tid == 0) {
+      StackEnt e;
+      e.j = un.j; e.sjm1 = un.sjm1; e.sj = un.sj; e.re = un.re; e.im = un.im; e.pad = 0;
+      b.stack[0] = e;
+      sh.sp = 1;
+    }
+    __syncthreads();
+    double2 acc[kKX];
+#pragma unroll
+    for (int r = 0; r < kKX; ++r) acc[r] = make_double2(0.0, 0.0);
+    ull np = 0;
+    process_stack(p, b, sh, sY, acc, np, cm, nelem);
+    ull np_tot = 0;
+    reduce_block(sh, acc, &p.partial[u], np, &np_tot);
+    if (tid == 0) {
+      atomicAdd(&p.pdone[q], np_tot);
+      atomicAdd(&p.ctr->paths, np_tot);
+      atomicAdd(&p.ctr->units, 1ull);
+    }
+  }
+  // statistics
+  for (int d = 16; d > 0; d >>= 1) {
+    cm += __shfl_down_sync(0xffffffffu, cm, d);
+    nelem += __shfl_down_sync(0xffffffffu, nelem, d);
+  }
+  if ((tid & 31) == 0) {
+    atomicAdd(&p.ctr->cmuls, cm);
+    atomicAdd(&p.ctr->elements, nelem);
+  }
+}
+
+// per output: the sum of its units in unit order (deterministic), exact 0 / NaN otherwise
+__global__ void lofp_final_kernel(const __grid_constant__ CallParams p) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < p.B; q += gridDim.x * blockDim.x) {
+    const int st = p.status[q];
+    double2 a = make_double2(0.0, 0.0);
+    if (st == kStatusOk) {
+      for (int u = p.ubase[q]; u < p.ubase[q + 1]; ++u) {
+        const double2 v = p.partial[u];
+        a.x += v.x;
+        a.y += v.y;
+      }
+      if (p.pdone[q] != p.pexp[q]) atomicAdd(&p.ctr->table_error, 1ull);  // every path exactly once
+    } else if (st == kStatusBad || st == kStatusUnsupported) {
+      a = make_double2(__longlong_as_double(0x7ff8000000000000ll), __longlong_as_double(0x7ff8000000000000ll));
+    }
+    p.amps[q] = a;
+    if (p.counts) p.counts[q] = p.pdone[q];
+  }
+}
+
+// ---- launchers -------------------------------------------------------------------------
+extern "C" int lofp_units_grid(int device) {
+  int nsm = 0;
+  if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
+  return 2 * nsm;
+}
+
+extern "C" int lofp_launch_tables(const CallParams *p, void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  lofp_table_off_kernel<<<1, kThreads, 0, st>>>(*p);
+  if (p->nbs > 0) lofp_table_kernel<<<p->nbs, kThreads, 0, st>>>(*p);
+  return (int)cudaGetLastError();
+}
+
+extern "C" int lofp_launch_paths(const CallParams *p, int grid, void *stream, void *ev0, void *ev1) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int smem = kCY * (int)sizeof(double2);
+  cudaFuncSetAttribute(lofp_units_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int pgrid = p->B < grid ? p->B : grid;
+  lofp_plan_kernel<<<pgrid, kThreads, 0, st>>>(*p);
+  lofp_scan_kernel<<<1, kThreads, 0, st>>>(*p);
+  if (ev0) cudaEventRecord((cudaEvent_t)ev0, st);
+  lofp_units_kernel<<<grid, kThreads, smem, st>>>(*p);
+  if (ev1) cudaEventRecord((cudaEvent_t)ev1, st);
+  lofp_final_kernel<<<(p->B + 255) / 256 < 1024 ? (p->B + 255) / 256 : 1024, 256, 0, st>>>(*p);
+  return (int)cudaGetLastError();
+}
+
+extern "C" int lofp_launch_contract(const CallParams *, int, void *) { return (int)cudaErrorNotSupported; }

@@ -22,22 +22,24 @@ class lofp_bs(ctypes.Structure):
                 ("theta", ctypes.c_double), ("phi", ctypes.c_double)]
 
 
+class lofp_gate(ctypes.Structure):
+    _fields_ = [("mode", ctypes.c_int32), ("after_layer", ctypes.c_int32),
+                ("a", ctypes.c_double), ("b", ctypes.c_double)]
+
+
 class lofp_run_stats(ctypes.Structure):
-    _fields_ = [("batch", ctypes.c_int64), ("feasible", ctypes.c_int64), ("items", ctypes.c_int64),
-                ("spills", ctypes.c_int64), ("donations", ctypes.c_int64), ("overflows", ctypes.c_int64),
-                ("paths", ctypes.c_int64), ("cmuls", ctypes.c_int64),
-                ("chains", ctypes.c_int64), ("chain_fallbacks", ctypes.c_int64),
-                ("levels", ctypes.c_int32), ("table_entries", ctypes.c_int32),
-                ("smem_bytes", ctypes.c_int32), ("grid_blocks", ctypes.c_int32),
-                ("block_threads", ctypes.c_int32), ("bad_rows", ctypes.c_int32),
-                ("max_factors", ctypes.c_int32), ("max_scatter", ctypes.c_int32), ("engine", ctypes.c_int32),
-                ("launches", ctypes.c_int32),
-                ("enum_ms", ctypes.c_float), ("total_ms", ctypes.c_float)]
+    _fields_ = [("batch", ctypes.c_int64), ("feasible", ctypes.c_int64), ("paths", ctypes.c_int64),
+                ("cmuls", ctypes.c_int64), ("units", ctypes.c_int64), ("subsplits", ctypes.c_int64),
+                ("pairs", ctypes.c_int64), ("elements", ctypes.c_int64), ("unsupported", ctypes.c_int64),
+                ("bad_rows", ctypes.c_int64), ("check_errors", ctypes.c_int64), ("max_states", ctypes.c_int64),
+                ("max_list", ctypes.c_int64), ("table_entries", ctypes.c_int64),
+                ("grid_blocks", ctypes.c_int32), ("block_threads", ctypes.c_int32),
+                ("launches", ctypes.c_int32), ("mode", ctypes.c_int32),
+                ("units_ms", ctypes.c_float), ("total_ms", ctypes.c_float)]
 
 
-EXPORTS = ["lofp_create", "lofp_amplitudes", "lofp_amplitudes_counted", "lofp_amplitudes_host",
-           "lofp_destroy", "lofp_status_string", "lofp_last_error", "lofp_stats", "lofp_work_histograms",
-           "lofp_phase_cycles"]
+EXPORTS = ["lofp_create", "lofp_create_ex", "lofp_amplitudes", "lofp_amplitudes_counted", "lofp_amplitudes_host",
+           "lofp_destroy", "lofp_status_string", "lofp_last_error", "lofp_stats"]
 
 
 def _load():
@@ -48,6 +50,10 @@ def _load():
     lib.lofp_create.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
                                 ctypes.POINTER(lofp_bs), ctypes.POINTER(P)]
     lib.lofp_create.restype = ctypes.c_int
+    lib.lofp_create_ex.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
+                                   ctypes.POINTER(lofp_bs), ctypes.c_int32, ctypes.POINTER(lofp_gate),
+                                   ctypes.POINTER(P)]
+    lib.lofp_create_ex.restype = ctypes.c_int
     lib.lofp_amplitudes.argtypes = [P, ctypes.POINTER(ctypes.c_int32), ctypes.c_int64, P, P, P]
     lib.lofp_amplitudes.restype = ctypes.c_int
     lib.lofp_amplitudes_counted.argtypes = [P, ctypes.POINTER(ctypes.c_int32), ctypes.c_int64, P, P, P, P]
@@ -62,10 +68,6 @@ def _load():
     lib.lofp_last_error.restype = ctypes.c_char_p
     lib.lofp_stats.argtypes = [P, ctypes.POINTER(lofp_run_stats)]
     lib.lofp_stats.restype = ctypes.c_int
-    lib.lofp_work_histograms.argtypes = [P, P, P]
-    lib.lofp_work_histograms.restype = ctypes.c_int
-    lib.lofp_phase_cycles.argtypes = [P, P]
-    lib.lofp_phase_cycles.restype = ctypes.c_int
     return lib
 
 
@@ -87,16 +89,21 @@ def _occ(S, M):
 
 class Circuit:
     """A mesh of beam splitters: ``layers`` is a list of layers, each a list of
-    ``(mode_a, mode_b, theta, phi)`` (mode_a = BS port 1)."""
+    ``(mode_a, mode_b, theta, phi)`` (mode_a = BS port 1).  ``gates``: optional phase
+    gates ``(mode, after_layer, a, b)`` multiplying |n> of that mode by exp(i (a n + b n^2))
+    (P:338)."""
 
-    def __init__(self, modes: int, layers):
+    def __init__(self, modes: int, layers, gates=()):
         self.modes = int(modes)
         self.layers = [list(l) for l in layers]
+        self.gates = [tuple(g) for g in gates]
         flat = [bs for l in self.layers for bs in l]
         bpl = (ctypes.c_int32 * max(len(self.layers), 1))(*[len(l) for l in self.layers])
         arr = (lofp_bs * max(len(flat), 1))(*[lofp_bs(int(a), int(b), float(t), float(p)) for a, b, t, p in flat])
+        garr = (lofp_gate * max(len(self.gates), 1))(*[lofp_gate(int(m), int(j), float(a), float(b))
+                                                        for m, j, a, b in self.gates])
         h = ctypes.c_void_p()
-        st = _lib.lofp_create(self.modes, len(self.layers), bpl, arr, ctypes.byref(h))
+        st = _lib.lofp_create_ex(self.modes, len(self.layers), bpl, arr, len(self.gates), garr, ctypes.byref(h))
         if st != LOFP_OK:
             raise LofpError(st, "lofp_create failed")
         self._h = h
@@ -116,32 +123,43 @@ class Circuit:
         if st != LOFP_OK:
             raise LofpError(st, _lib.lofp_last_error(self._h).decode())
 
-    def amplitudes(self, S, T, out=None, counts=None, stream=None):
-        """<T_b|U_P|S> for every row of the int32 CUDA tensor T [B, M] -> complex128 CUDA [B].
-
-        ``counts``: optional uint64-compatible int64 CUDA tensor [B] receiving the exact
-        number of valid paths summed per output.  Runs on ``stream`` (default: torch's
-        current stream); the result is ready when that stream is.
-        """
+    def _out(self, T, out):
         import torch
         if T.dtype != torch.int32 or not T.is_cuda or T.dim() != 2 or T.shape[1] != self.modes:
             raise ValueError("T must be an int32 CUDA tensor of shape [B, modes]")
-        T = T.contiguous()
         B = T.shape[0]
         if out is None:
             out = torch.empty((B, 2), dtype=torch.float64, device=T.device)
+        elif (out.dtype != torch.float64 or tuple(out.shape) != (B, 2) or not out.is_contiguous()
+              or out.device != T.device):
+            raise ValueError("out must be a contiguous float64 tensor [B, 2] on T's device")
+        return out
+
+    def amplitudes(self, S, T, out=None, counts=None, stream=None):
+        """<T_b|U_P|S> for every row of the int32 CUDA tensor T [B, M] -> complex128 CUDA [B].
+
+        ``counts``: optional int64 CUDA tensor [B] receiving the number of path products
+        formed per output (= the exact number of valid paths).  Runs on ``stream``
+        (default: torch's current stream); the result is ready when that stream is.
+        """
+        import torch
+        T = T.contiguous()
+        out = self._out(T, out)
+        B = T.shape[0]
         s = _occ(S, self.modes)
         strm = (stream or torch.cuda.current_stream(T.device)).cuda_stream
         sp = s.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
-        if counts is None:
-            st = _lib.lofp_amplitudes(self._h, sp, B, ctypes.c_void_p(T.data_ptr()), ctypes.c_void_p(out.data_ptr()),
-                                      ctypes.c_void_p(strm))
-        else:
-            if counts.dtype != torch.int64 or counts.numel() != B or not counts.is_cuda:
-                raise ValueError("counts must be an int64 CUDA tensor [B]")
-            st = _lib.lofp_amplitudes_counted(self._h, sp, B, ctypes.c_void_p(T.data_ptr()),
-                                              ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(counts.data_ptr()),
-                                              ctypes.c_void_p(strm))
+        with torch.cuda.device(T.device):
+            if counts is None:
+                st = _lib.lofp_amplitudes(self._h, sp, B, ctypes.c_void_p(T.data_ptr()),
+                                          ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(strm))
+            else:
+                if counts.dtype != torch.int64 or counts.numel() != B or not counts.is_cuda or \
+                        counts.device != T.device or not counts.is_contiguous():
+                    raise ValueError("counts must be a contiguous int64 CUDA tensor [B] on T's device")
+                st = _lib.lofp_amplitudes_counted(self._h, sp, B, ctypes.c_void_p(T.data_ptr()),
+                                                  ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(counts.data_ptr()),
+                                                  ctypes.c_void_p(strm))
         self._check(st)
         return torch.view_as_complex(out)
 
@@ -156,19 +174,6 @@ class Circuit:
                                        ctypes.c_void_p(t.ctypes.data), ctypes.c_void_p(out.ctypes.data))
         self._check(st)
         return out.view(np.complex128)[:, 0]
-
-    def work_histograms(self):
-        """(handover, spill) histograms of the last counted call, by distance from the leaf level."""
-        h = np.zeros(64, dtype=np.uint64)
-        sp = np.zeros(64, dtype=np.uint64)
-        self._check(_lib.lofp_work_histograms(self._h, ctypes.c_void_p(h.ctypes.data), ctypes.c_void_p(sp.ctypes.data)))
-        return h, sp
-
-    def phase_cycles(self):
-        """Enumeration-kernel cycle split of the last counted call (see include/lofp.h)."""
-        c = np.zeros(8, dtype=np.uint64)
-        self._check(_lib.lofp_phase_cycles(self._h, ctypes.c_void_p(c.ctypes.data)))
-        return c
 
     def stats(self) -> dict:
         st = lofp_run_stats()
