@@ -1,17 +1,21 @@
 """Benchmark of the LOFP path sum on B200 (BASELINE.json metric: paths/s and amplitudes/s
 on 1 B200; FP64-pipe fraction of roofline).
 
-One *step* = one call of the hot path (``lofp_amplitudes``: prep, Appendix-A tables,
-per-output plans, path enumeration) over one batch of outputs resident in HBM.  The
-default workload is BASELINE.json configs[4] (M=64, N=24, D=4) with its batch of 16384
-outputs conditioned on structural reachability and at most 1e9 paths per output
-(reading R14; the literal batch is ~100% structural zeros).  ``--config`` picks
-another config (0/1 literal batches, 2-4 conditioned).  Inputs are the seeded synthetic
-batches in data/ (written by scripts/make_batches.py).
+One *step* = one call of the hot path (``lofp_amplitudes``: Appendix-A tables when the
+input changes, per-output column counts and unit split, the column-split enumeration,
+the per-output reduction) over one batch of outputs resident in HBM.  The default
+workload is BASELINE.json configs[4] (M=64, N=24, D=4) with its batch of 16384 outputs
+conditioned on structural reachability and at most 1e9 paths per output (DESIGN.md
+reading R14; the literal batch is ~100% structural zeros for configs[2] and 3e14 paths
+per amplitude for configs[3]).  ``--config`` picks another config (0/1 literal batches,
+2-4 conditioned), ``--literal`` the literal configs[4] batch (12,548 reachable outputs,
+4.9e13 paths), ``--hero`` the 8 largest uncapped configs[4] outputs.  Inputs are the
+seeded synthetic batches in data/ (written by scripts/make_batches.py).
 
 Launch: ``python bench.py [--gpus N --steps K --warmup W]``; N > 1 under torchrun, one
-rank per GPU, outputs sharded across ranks (no collective on the data path; strong
-scaling of a fixed batch).  ``--impl reference`` times the CPU oracle instead.
+rank per GPU, every rank evaluating the whole batch (weak scaling: per-GPU work fixed;
+outputs are independent, so there is no collective on the data path).
+``--impl reference`` times the CPU oracle instead.
 """
 from __future__ import annotations
 
@@ -43,18 +47,24 @@ def parse():
     p.add_argument("--outputs", type=int, default=0, help="limit the batch to its first N outputs")
     p.add_argument("--hero", action="store_true",
                    help="configs[4] hero sample: its 8 largest uncapped outputs (2.2e11-2.5e11 paths each)")
+    p.add_argument("--literal", action="store_true",
+                   help="configs[4] literal batch (reachable outputs only: 12,548 outputs, 4.9e13 paths)")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--cpu-paths", type=float, default=6e7, help="paths in the cpu_baseline sample")
+    p.add_argument("--cpu-paths", type=float, default=3e7, help="paths in the cpu_baseline sample")
     return p.parse_args()
 
 
-def workload(idx: int, limit: int = 0, hero: bool = False):
+def workload(idx: int, limit: int = 0, hero: bool = False, literal: bool = False):
     import lofp_inputs as li
     c = li.config(idx)
     d = np.load(os.path.join(DATA, f"cfg{idx}.npz"))
     if hero:  # uncapped single-output scaling sample (configs[4] only)
         T, P, kind = d["T_hero"].astype(np.int32), d["P_hero"].astype(np.uint64), "hero (uncapped)"
+    elif literal:  # the literal batch, structural zeros dropped (they cost nothing)
+        keep = d["P_literal"] > 0
+        T, P = d["T_literal"][keep].astype(np.int32), d["P_literal"][keep].astype(np.uint64)
+        kind = "literal (reachable rows)"
     elif "T_cond" in d.files:
         T, P, kind = d["T_cond"].astype(np.int32), d["P_cond"].astype(np.uint64), "conditioned"
     else:
@@ -64,10 +74,16 @@ def workload(idx: int, limit: int = 0, hero: bool = False):
     return c, T, P, kind
 
 
-def shard(P, rank, world):
-    """Longest-first round robin over ranks (balanced by exact path counts)."""
-    order = np.argsort(-P.astype(np.float64), kind="stable")
-    return np.sort(order[rank::world])
+def aggregate(t_local_ms, paths_local, outs_local, world, dist=None, device=None):
+    """Max of the ranks' device times, sums of their paths and outputs (the only
+    collectives of the bench: there is none on the data path)."""
+    import torch
+    t = torch.tensor([t_local_ms], dtype=torch.float64, device=device)
+    tot = torch.tensor([paths_local, outs_local], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    return float(t.item()), float(tot[0].item()), float(tot[1].item())
 
 
 class ClockSampler:
@@ -118,13 +134,20 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def cpu_sample(c, T, P, budget):
-    """Smallest-P outputs of the batch up to `budget` paths (a bounded oracle sample)."""
-    order = np.argsort(P.astype(np.float64), kind="stable")
-    cs = np.cumsum(P[order].astype(np.float64))
-    n = max(1, int(np.searchsorted(cs, budget)))
-    sel = np.sort(order[:n])
-    return sel
+def cpu_sample(c, T, P, budget, seed=0):
+    """A seeded random sample of the batch's outputs holding about `budget` paths (outputs
+    larger than a quarter of the budget are skipped so the sample stays bounded)."""
+    order = np.random.default_rng(seed).permutation(len(T))
+    sel, tot = [], 0.0
+    for i in order:
+        p = float(P[i])
+        if p > budget / 4:
+            continue
+        sel.append(int(i))
+        tot += p
+        if tot >= budget:
+            break
+    return np.sort(np.array(sel if sel else [int(np.argmin(P))], dtype=np.int64))
 
 
 def run_oracle(c, T, P, sel, threads=0):
@@ -159,7 +182,8 @@ def reference_arm(args, rank, world):
                                         "sample_outputs": int(len(sel))},
         "amplitudes_per_s": len(sel) * args.steps / tot_s,
         "cpu_baseline": {"value": v, "unit": "paths/s", "cores": cores, "kind": "oracle",
-                         "sample": f"{len(sel)} smallest-path outputs of the batch, {p:.3e} paths per step"},
+                         "sample": f"{len(sel)} outputs drawn at random from the batch (each <= 1/4 of the "
+                                   f"path budget), {p:.3e} paths per step"},
         "e2e": {"value": v, "unit": "paths/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -184,9 +208,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    c, T_all, P_all, kind = workload(args.config, args.outputs, args.hero)
-    mine = shard(P_all, rank, world)
-    T, P = T_all[mine], P_all[mine]
+    c, T, P, kind = workload(args.config, args.outputs, args.hero, args.literal)
     circ = Circuit(c.M, c.layers)
     Td = torch.from_numpy(np.ascontiguousarray(T)).to(dev)
     B = len(T)
@@ -194,15 +216,16 @@ def main():
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    # validation pass (untimed): exact path counts must equal the oracle's (data/), and
-    # the kernel's own count of non-vacuum complex multiplications sizes the roofline
+    # validation pass (untimed): the path products the kernel formed per output must equal
+    # the oracle's exact path counts (data/); its complex-multiplication count sizes the roofline
     counts = torch.zeros(B, dtype=torch.int64, device=dev)
     circ.amplitudes(c.S, Td, out=out, counts=counts)
     torch.cuda.synchronize()
     vst = circ.stats()
     got = counts.cpu().numpy().astype(np.uint64)
-    if not np.array_equal(got, P):
-        raise SystemExit(f"path counts differ from the oracle's on {int((got != P).sum())} outputs")
+    if not np.array_equal(got, P) or vst["check_errors"] or vst["unsupported"]:
+        raise SystemExit(f"path counts differ from the oracle's on {int((got != P).sum())} outputs "
+                         f"(check_errors={vst['check_errors']}, unsupported={vst['unsupported']})")
     cmuls, paths = int(vst["cmuls"]), int(vst["paths"])
 
     for _ in range(args.warmup):
@@ -214,7 +237,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     clocks.start()
-    ms, enum_ms = [], []
+    ms, unit_ms = [], []
     for _ in range(args.steps):
         flush.fill_(1)  # L2 flush outside the timed events
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -223,19 +246,13 @@ def main():
         e1.record(stream)
         e1.synchronize()
         ms.append(e0.elapsed_time(e1))
-        enum_ms.append(circ.stats()["enum_ms"])
+        unit_ms.append(circ.stats()["units_ms"])
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
     t_local = float(np.sum(ms))
-    t = torch.tensor([t_local], dtype=torch.float64, device=dev)
-    tot = torch.tensor([float(P.astype(np.float64).sum()), float(B)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
-    t_max = float(t.item())
-    paths_all, outs_all = float(tot[0].item()), float(tot[1].item())
+    t_max, paths_all, outs_all = aggregate(t_local, float(P.astype(np.float64).sum()), float(B), world, dist, dev)
     value = paths_all * args.steps / (t_max * 1e-3)
 
     # end to end through the public host API: H2D of T, D2H of the amplitudes each step
@@ -260,43 +277,46 @@ def main():
             dist.destroy_process_group()
         return
 
-    # roofline of the dominant kernel (path enumeration): algorithmic FP64 lane
-    # instructions = 4 per non-vacuum complex multiplication + 2 per path (leaf sum),
-    # over its device time (CUDA events on the launching stream, inside liblofp)
+    # roofline of the dominant kernel (the unit kernel): FP64 lane instructions the method
+    # executes in this order = 4 per path (its product formed as a fused complex
+    # multiply-accumulate: 2 DFMA per component) + 4 per other complex multiplication (the
+    # half-path lists and their per-pair scalings: 2 DMUL + 2 DFMA), over the kernel's
+    # device time (CUDA events on the launching stream, recorded inside liblofp)
     lib = ctypes.CDLL(_build.PEAK_LIB)
     lib.lofp_probe_fp64_dfma_rate.restype = ctypes.c_double
     lib.lofp_probe_fp64_dfma_rate.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
     nsm = ctypes.c_int(0)
     peak_meas = lib.lofp_probe_fp64_dfma_rate(5, ctypes.byref(nsm)) / 1e12
-    enum_mean = float(np.mean(enum_ms))
-    alg = 4.0 * cmuls + 2.0 * paths
-    achieved = alg / (enum_mean * 1e-3) / 1e12
+    umean = float(np.mean(unit_ms))
+    alg = 4.0 * paths + 4.0 * cmuls
+    achieved = alg / (umean * 1e-3) / 1e12
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak_meas, "unit": "TFP64-inst/s",
                 "frac": achieved / peak_meas if peak_meas > 0 else None, "traffic": None,
-                "peak_source": f"measured DFMA issue rate (fp64_peak.cu, {nsm.value} SMs, burst)",
+                "peak_source": f"measured DFMA issue rate (fp64_peak.cu, {nsm.value} SMs, burst); "
+                               f"MEASURED_PEAKS.json has no FP64 entry",
                 "nominal_peak": 148 * 64 * 1965e6 / 1e12,
-                "work_per_launch": {"cmuls": cmuls, "paths": paths, "fp64_lane_inst": alg},
-                "kernel_ms": enum_mean, "kernel_share_of_step": enum_mean / (t_local / args.steps)}
+                "work_per_launch": {"paths": paths, "cmuls": cmuls, "fp64_lane_inst": alg},
+                "kernel": "lofp_units_kernel", "kernel_ms": umean,
+                "kernel_share_of_step": umean / (t_local / args.steps)}
 
     cpu = None
     if not args.no_cpu and world == 1 and not args.hero:  # (hero trees: hours on the CPU)
-        sel = cpu_sample(c, T_all, P_all, args.cpu_paths)
-        p, dt = run_oracle(c, T_all, P_all, sel)
-        # one core (after the all-core run: the oracle's thread setting persists)
-        sel1 = cpu_sample(c, T_all, P_all, args.cpu_paths / 24)
-        p1, dt1 = run_oracle(c, T_all, P_all, sel1, threads=1)
+        sel = cpu_sample(c, T, P, args.cpu_paths)
+        p, dt = run_oracle(c, T, P, sel)
+        sel1 = cpu_sample(c, T, P, args.cpu_paths / 24, seed=1)
+        p1, dt1 = run_oracle(c, T, P, sel1, threads=1)
         cpu = {"value": p / dt, "unit": "paths/s", "cores": os.cpu_count(), "kind": "oracle",
-               "sample": f"{len(sel)} smallest-path outputs of the batch ({p:.3e} paths), {dt:.1f} s",
+               "sample": f"{len(sel)} outputs drawn at random from the batch ({p:.3e} paths), {dt:.1f} s",
                "one_core": {"value": p1 / dt1, "unit": "paths/s",
-                            "sample": f"{len(sel1)} smallest-path outputs ({p1:.3e} paths), {dt1:.1f} s"}}
+                            "sample": f"{len(sel1)} random outputs ({p1:.3e} paths), {dt1:.1f} s"}}
 
     line = {
         "metric": "paths/s", "value": value, "unit": "paths/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"configs[{args.config}] {kind} batch: M={c.M} N={c.N} D={c.D}, "
-                               f"{int(outs_all)} outputs, {paths_all:.4e} paths",
-                   "global_batch": int(outs_all), "parallelism": f"outputs sharded over {world} GPU(s)",
+                               f"{B} outputs, {float(P.astype(np.float64).sum()):.4e} paths per GPU",
+                   "global_batch": int(outs_all), "parallelism": f"the batch on each of {world} GPU(s)",
                    "l2": "flushed between steps (256 MiB write)"},
         "amplitudes_per_s": outs_all * args.steps / (t_max * 1e-3),
         "roofline": roofline,
@@ -304,8 +324,8 @@ def main():
         "e2e": e2e,
         "gpu_launches": int(vst["launches"]) * args.steps,  # this library's kernels per call
         "clocks": clk,
-        "stats": {k: vst[k] for k in ("feasible", "items", "spills", "donations", "overflows", "levels",
-                                      "table_entries", "smem_bytes", "grid_blocks", "block_threads", "engine")},
+        "stats": {k: vst[k] for k in ("feasible", "units", "subsplits", "pairs", "elements", "max_list",
+                                      "max_states", "table_entries", "grid_blocks", "block_threads")},
     }
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -99,8 +99,6 @@ struct lofp_ctx {
   DevBuf d_table, d_taboff, d_gatetab, d_units, d_nunits, d_ubase, d_status, d_pexp, d_pdone, d_partial, d_slab,
       d_ctr, d_hostT, d_hostA;
   HostPinned h_ctr;
-  std::vector<int32_t> tab_S;  // input the table was built for
-  bool tables_valid = false;
   long long table_entries = 0;
   int grid = 0;
   long long slab_bytes = 0;
@@ -486,13 +484,10 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
   if (ctx->timed) CK(cudaEventRecord(ctx->ev_start, stream), "cudaEventRecord");
   CK(cudaMemsetAsync(P.ctr, 0, sizeof(Counters), stream), "clear counters");
   int launches = 0;
-  std::vector<int32_t> S(input_occ, input_occ + ctx->M);
-  if (!ctx->tables_valid || S != ctx->tab_S) {
-    CK((cudaError_t)lofp_launch_tables(&P, stream), "table kernels");
-    launches += ctx->nbs > 0 ? 2 : 1;
-    ctx->tab_S = S;
-    ctx->tables_valid = true;
-  }
+  // the Appendix-A tables depend on S only through their size; rebuilt every call (a few
+  // microseconds) so that each call, and each graph replay, is self-contained
+  CK((cudaError_t)lofp_launch_tables(&P, stream), "table kernels");
+  launches += ctx->nbs > 0 ? 2 : 1;
   if (mode == 0) {
     CK((cudaError_t)lofp_launch_paths(&P, ctx->grid, stream, ctx->timed ? ctx->ev_u0 : nullptr,
                                       ctx->timed ? ctx->ev_u1 : nullptr),
@@ -502,9 +497,11 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
     CK((cudaError_t)lofp_launch_contract(&P, ctx->grid, stream), "contraction kernels");
     launches += 1;
   }
-  CK(cudaMemcpyAsync(ctx->h_ctr.p, P.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, stream), "read counters");
-  CK(cudaEventRecord(ctx->ev_end, stream), "cudaEventRecord");
-  ctx->have_call = true;
+  if (!capturing) {  // statistics of calls replayed from a graph are not read back
+    CK(cudaMemcpyAsync(ctx->h_ctr.p, P.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, stream), "read counters");
+    CK(cudaEventRecord(ctx->ev_end, stream), "cudaEventRecord");
+    ctx->have_call = true;
+  }
   ctx->stats.launches = launches;
   ctx->stats.mode = mode;
   ctx->stats.grid_blocks = ctx->grid;

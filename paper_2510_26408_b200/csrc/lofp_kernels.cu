@@ -1041,7 +1041,13 @@ extern "C" int lofp_launch_tables(const CallParams *p, void *stream) {
 extern "C" int lofp_launch_paths(const CallParams *p, int grid, void *stream, void *ev0, void *ev1) {
   cudaStream_t st = (cudaStream_t)stream;
   const int smem = kCY * (int)sizeof(double2);
-  cudaFuncSetAttribute(lofp_units_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  static int attr_device_mask = 0;  // set once per device, outside any stream capture
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(attr_device_mask & (1 << (dev & 31)))) {
+    cudaFuncSetAttribute(lofp_units_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr_device_mask |= 1 << (dev & 31);
+  }
   const int pgrid = p->B < grid ? p->B : grid;
   lofp_plan_kernel<<<pgrid, kThreads, 0, st>>>(*p);
   lofp_scan_kernel<<<1, kThreads, 0, st>>>(*p);

@@ -107,6 +107,13 @@ class Circuit:
         if st != LOFP_OK:
             raise LofpError(st, "lofp_create failed")
         self._h = h
+        self.device_index = None  # the CUDA device the context lives on (set on first use)
+        try:
+            import torch
+            if torch.cuda.is_available():
+                self.device_index = torch.cuda.current_device()
+        except ImportError:
+            pass
 
     def close(self):
         if getattr(self, "_h", None):
@@ -127,6 +134,8 @@ class Circuit:
         import torch
         if T.dtype != torch.int32 or not T.is_cuda or T.dim() != 2 or T.shape[1] != self.modes:
             raise ValueError("T must be an int32 CUDA tensor of shape [B, modes]")
+        if self.device_index is not None and T.device.index != self.device_index:
+            raise ValueError(f"T is on {T.device}, the circuit on cuda:{self.device_index}")
         B = T.shape[0]
         if out is None:
             out = torch.empty((B, 2), dtype=torch.float64, device=T.device)
