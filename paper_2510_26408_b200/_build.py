@@ -34,6 +34,20 @@ def _compile(out, sources, deps, force, verbose):
     return out
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+DEBUG_LIB = os.path.join(HERE, "liblofp_debug.so")
+
+
+def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
+    """liblofp.so (and the FP64 peak probe); debug=True also builds liblofp_debug.so, the
+    same sources with device-side bounds checks (-DLOFP_DEBUG), loaded when LOFP_LIB
+    points at it."""
     _compile(PEAK_LIB, [PEAK_SRC], [], force, False)
+    if debug:
+        global NVCC_FLAGS
+        saved = NVCC_FLAGS
+        NVCC_FLAGS = saved + ["-DLOFP_DEBUG"]
+        try:
+            _compile(DEBUG_LIB, SOURCES, HEADERS, force, verbose)
+        finally:
+            NVCC_FLAGS = saved
     return _compile(LIB, SOURCES, HEADERS, force, verbose)

@@ -96,7 +96,7 @@ struct lofp_ctx {
   size_t off_col = 0, off_seg = 0, off_cmp = 0, off_fac = 0, off_gat = 0, off_bsi = 0, off_gab = 0, off_gm = 0,
          off_gl = 0;
   // per-call device buffers
-  DevBuf d_table, d_taboff, d_gatetab, d_units, d_nunits, d_ubase, d_status, d_pexp, d_pdone, d_partial, d_slab,
+  DevBuf d_table, d_taboff, d_gatetab, d_units, d_sched, d_nunits, d_ubase, d_status, d_pexp, d_pdone, d_partial, d_slab,
       d_ctr, d_hostT, d_hostA;
   HostPinned h_ctr;
   long long table_entries = 0;
@@ -436,10 +436,11 @@ lofp_status prepare(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, cons
   long long budget = (1ll << 21) / B;
   budget = std::max(8ll, std::min(budget, 1ll << 17));
   P.budget = (int)budget;
-  P.thr = (unsigned long long)env_ll("LOFP_UNIT_PATHS", 1ll << 26);
+  P.thr = (unsigned long long)env_ll("LOFP_UNIT_PATHS", 1ll << 24);
   P.slab_bytes = ctx->slab_bytes;
   CK(ctx->d_units.ensure((size_t)(B * budget) * sizeof(Unit)), "alloc units");
   CK(ctx->d_partial.ensure((size_t)(B * budget) * 16), "alloc partials");
+  CK(ctx->d_sched.ensure((size_t)(B * budget) * 4), "alloc schedule");
   CK(ctx->d_nunits.ensure((size_t)B * 4), "alloc nunits");
   CK(ctx->d_ubase.ensure((size_t)(B + 1) * 4), "alloc ubase");
   CK(ctx->d_status.ensure((size_t)B), "alloc status");
@@ -449,6 +450,7 @@ lofp_status prepare(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, cons
   CK(ctx->d_ctr.ensure(sizeof(Counters)), "alloc counters");
   P.units = (Unit *)ctx->d_units.p;
   P.partial = (double2 *)ctx->d_partial.p;
+  P.sched = (int *)ctx->d_sched.p;
   P.nunits = (int *)ctx->d_nunits.p;
   P.ubase = (int *)ctx->d_ubase.p;
   P.status = (uint8_t *)ctx->d_status.p;
@@ -492,7 +494,7 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
     CK((cudaError_t)lofp_launch_paths(&P, ctx->grid, stream, ctx->timed ? ctx->ev_u0 : nullptr,
                                       ctx->timed ? ctx->ev_u1 : nullptr),
        "path-sum kernels");
-    launches += 4;
+    launches += 6;
   } else {
     CK((cudaError_t)lofp_launch_contract(&P, ctx->grid, stream), "contraction kernels");
     launches += 1;
@@ -608,7 +610,7 @@ void lofp_destroy(lofp_ctx *ctx) {
   if (!ctx) return;
   DeviceGuard guard(ctx->device);
   if (ctx->have_call && ctx->ev_end) cudaEventSynchronize(ctx->ev_end);
-  for (DevBuf *b : {&ctx->d_topo, &ctx->d_table, &ctx->d_taboff, &ctx->d_gatetab, &ctx->d_units, &ctx->d_nunits,
+  for (DevBuf *b : {&ctx->d_topo, &ctx->d_table, &ctx->d_taboff, &ctx->d_gatetab, &ctx->d_units, &ctx->d_sched, &ctx->d_nunits,
                     &ctx->d_ubase, &ctx->d_status, &ctx->d_pexp, &ctx->d_pdone, &ctx->d_partial, &ctx->d_slab,
                     &ctx->d_ctr, &ctx->d_hostT, &ctx->d_hostA})
     b->release();

@@ -25,8 +25,10 @@ constexpr int kMaxStates = 4096;   // states of one column (uint16 indices)
 constexpr int kMaxStatesTotal = 1 << 16;  // sum over the columns of one output
 constexpr int kMaxSegments = 1 << 16;     // (state, predecessor) pairs of one BFS level
 constexpr int kThreads = 256;      // threads per block of the plan / unit / contraction kernels
-constexpr int kKX = 8;             // X values held in registers per thread (outer product)
-constexpr int kCY = 2048;          // Y values staged in shared memory per chunk
+constexpr int kKX = 8;             // X values held in registers per lane (outer product)
+constexpr int kXT = 32 * kKX;      // X values per warp tile
+constexpr int kYT = 256;           // Y values per warp tile (staged in the warp's shared slice)
+constexpr int kCY = kYT * (kThreads / 32);  // shared memory: one Y slice per warp
 constexpr int kStackMax = 4096;    // sub-split stack entries per block
 
 // ---- topology (lofp_create; constant per circuit) --------------------------------
@@ -97,7 +99,7 @@ struct Counters {        // device counters of one call (zeroed by the host)
   unsigned long long max_states; // largest column state count seen
   unsigned long long max_list;   // largest half-path list built
   unsigned long long contractions; // contraction mode: column-pair states carried
-  unsigned long long pad[1];
+  unsigned long long thr;        // unit size of the call (paths)
 };
 
 enum : uint8_t { kStatusOk = 0, kStatusZero = 1, kStatusBad = 2, kStatusUnsupported = 3 };
@@ -106,7 +108,7 @@ struct CallParams {
   int M, D, N, B, nbs, ngate;
   int budget;            // unit slots per output
   int mode;              // 0 path sum, 1 contraction
-  unsigned long long thr;  // unit size target (paths)
+  unsigned long long thr;  // smallest unit size (paths); the call's is in Counters::thr
   long long slab_bytes;  // per-block scratch in global memory
   long long table_cap;   // entries allocated for the Appendix-A table
   const ColInfo *col;
@@ -127,6 +129,7 @@ struct CallParams {
   Unit *units;               // [B][budget]
   int *nunits;               // [B]
   int *ubase;                // [B+1] (exclusive scan of nunits)
+  int *sched;                // [B][budget]: unit indices, largest size class first
   uint8_t *status;           // [B]
   unsigned long long *pexp;  // [B] exact number of paths (column count, reading R6)
   unsigned long long *pdone; // [B] path products formed

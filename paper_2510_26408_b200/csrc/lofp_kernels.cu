@@ -26,6 +26,23 @@
 
 using namespace lofp;
 
+// Debug build (-DLOFP_DEBUG, liblofp_debug.so): bounds checks that name the failing site.
+#ifdef LOFP_DEBUG
+#include <cstdio>
+#define DCHECK(cond, tag)                                                                        \
+  do {                                                                                           \
+    if (!(cond)) {                                                                               \
+      printf("LOFP_DEBUG %s failed at line %d block %d thread %d\n", tag, __LINE__, blockIdx.x,   \
+             threadIdx.x);                                                                       \
+      __trap();                                                                                  \
+    }                                                                                            \
+  } while (0)
+#else
+#define DCHECK(cond, tag) \
+  do {                    \
+  } while (0)
+#endif
+
 namespace {
 
 typedef unsigned long long ull;
@@ -100,6 +117,7 @@ struct Shared {
   int sp;                  // stack pointer
   StackEnt top;
   int q_cached;
+  int cr_q;                // output whose cR counts are in the slab
   int unit;
 };
 
@@ -246,6 +264,7 @@ __device__ __forceinline__ Block make_block(const CallParams &p) {
 __device__ int setup_output(const CallParams &p, Block &b, Shared &sh, int q) {
   const int M = p.M, tid = threadIdx.x;
   for (int i = tid; i < M; i += kThreads) sh.T[i] = p.T[(long long)q * M + i];
+  if (tid == 0) sh.cr_q = -1;
   __syncthreads();
   if (tid == 0) {
     int st = kStatusOk, g = 0;
@@ -327,9 +346,12 @@ __device__ void dp_counts(const CallParams &p, Block &b, Shared &sh, int j, int 
   if (need_right)
     for (int s = tid; s < sh.n[M]; s += kThreads) b.cR[sh.cb[M] + s] = 1ull;
   __syncthreads();
-  for (int i = 1; i <= M - j; ++i) {
+  // the right counts depend on the output only: computed for every column (they are cached
+  // across the units of one output); the left counts from column j
+  const int iters = need_right ? M : M - j;
+  for (int i = 1; i <= iters; ++i) {
     const int kL = j + i, kR = M - i;
-    const int nL = sh.n[kL], nR = need_right ? sh.n[kR] : 0;
+    const int nL = kL <= M ? sh.n[kL] : 0, nR = need_right ? sh.n[kR] : 0;
     for (int t = tid; t < nL + nR; t += kThreads) {
       ull sum = 0;
       if (t < nL) {
@@ -407,6 +429,7 @@ __device__ int build_segments(const CallParams &p, Block &b, Shared &sh, int kd,
       g.len = len;
       g.p = (uint16_t)pp;
       g.s = (uint16_t)s;
+      DCHECK(e < (uint32_t)kMaxSegments, "segs");
       b.segs[e++] = g;
       d += len;
     }
@@ -434,71 +457,46 @@ __device__ uint32_t bucket_offsets(Block &b, Shared &sh, int k, bool left, uint3
 }
 
 // ---- the outer product: every path = X_i * Y_j, one complex FMA pair per path --------
-__device__ __forceinline__ void outer_pair(const double2 *__restrict__ Xp, const uint16_t *__restrict__ Xc,
-                                           const double2 *__restrict__ FX, int nX, const double2 *__restrict__ Yp,
-                                           const uint16_t *__restrict__ Yc, const double2 *__restrict__ FY, int nY,
-                                           double2 *sY, double2 (&acc)[kKX], ull &npaths, ull &cm) {
-  const int nxb = (nX + kKX - 1) / kKX;
-  for (int y0 = 0; y0 < nY; y0 += kCY) {
-    const int len = min(kCY, nY - y0);
-    for (int t = threadIdx.x; t < len; t += kThreads) sY[t] = cmul(Yp[y0 + t], FY[Yc[y0 + t]]);
-    cm += (len + kThreads - 1 - threadIdx.x) / kThreads;
-    __syncthreads();
-    int parts = (4 * kThreads + nxb - 1) / nxb;
-    if (parts > len) parts = len;
-    if (parts < 1) parts = 1;
-    const int cyt = (len + parts - 1) / parts;
-    parts = (len + cyt - 1) / cyt;
-    const int ntask = nxb * parts;
-    for (int task = threadIdx.x; task < ntask; task += kThreads) {
-      const int xb = task % nxb, part = task / nxb;
-      double2 x[kKX];
-      int nv = 0;
+// A warp holds kKX X values per lane (a tile of kXT = 32 kKX) in registers and streams a
+// tile of up to kYT Y values from its shared-memory slice (broadcast reads): per Y value
+// 1 LDS.128 and 4 kKX DFMA per lane.
+__device__ __forceinline__ void fma_block(const double2 (&x)[kKX], const double2 *__restrict__ sW, uint32_t len,
+                                          double2 (&acc)[kKX]) {
+  uint32_t y = 0;
+  for (; y + 1 < len; y += 2) {
+    const double2 v0 = sW[y], v1 = sW[y + 1];
 #pragma unroll
-      for (int r = 0; r < kKX; ++r) {
-        const int i = xb * kKX + r;
-        if (i < nX) {
-          x[r] = cmul(Xp[i], FX[Xc[i]]);
-          ++nv;
-        } else {
-          x[r] = make_double2(0.0, 0.0);
-        }
-      }
-      cm += nv;
-      const int ya = part * cyt, yb = min(len, ya + cyt);
-      int y = ya;
-      for (; y + 1 < yb; y += 2) {
-        const double2 v0 = sY[y], v1 = sY[y + 1];
-#pragma unroll
-        for (int r = 0; r < kKX; ++r) {
-          acc[r].x = fma(x[r].x, v0.x, acc[r].x);
-          acc[r].y = fma(x[r].x, v0.y, acc[r].y);
-          acc[r].x = fma(-x[r].y, v0.y, acc[r].x);
-          acc[r].y = fma(x[r].y, v0.x, acc[r].y);
-        }
-#pragma unroll
-        for (int r = 0; r < kKX; ++r) {
-          acc[r].x = fma(x[r].x, v1.x, acc[r].x);
-          acc[r].y = fma(x[r].x, v1.y, acc[r].y);
-          acc[r].x = fma(-x[r].y, v1.y, acc[r].x);
-          acc[r].y = fma(x[r].y, v1.x, acc[r].y);
-        }
-      }
-      if (y < yb) {
-        const double2 v0 = sY[y];
-#pragma unroll
-        for (int r = 0; r < kKX; ++r) {
-          acc[r].x = fma(x[r].x, v0.x, acc[r].x);
-          acc[r].y = fma(x[r].x, v0.y, acc[r].y);
-          acc[r].x = fma(-x[r].y, v0.y, acc[r].x);
-          acc[r].y = fma(x[r].y, v0.x, acc[r].y);
-        }
-      }
-      npaths += (ull)nv * (ull)(yb - ya);
+    for (int r = 0; r < kKX; ++r) {
+      acc[r].x = fma(x[r].x, v0.x, acc[r].x);
+      acc[r].y = fma(x[r].x, v0.y, acc[r].y);
+      acc[r].x = fma(-x[r].y, v0.y, acc[r].x);
+      acc[r].y = fma(x[r].y, v0.x, acc[r].y);
     }
-    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kKX; ++r) {
+      acc[r].x = fma(x[r].x, v1.x, acc[r].x);
+      acc[r].y = fma(x[r].x, v1.y, acc[r].y);
+      acc[r].x = fma(-x[r].y, v1.y, acc[r].x);
+      acc[r].y = fma(x[r].y, v1.x, acc[r].y);
+    }
+  }
+  if (y < len) {
+    const double2 v0 = sW[y];
+#pragma unroll
+    for (int r = 0; r < kKX; ++r) {
+      acc[r].x = fma(x[r].x, v0.x, acc[r].x);
+      acc[r].y = fma(x[r].x, v0.y, acc[r].y);
+      acc[r].x = fma(-x[r].y, v0.y, acc[r].x);
+      acc[r].y = fma(x[r].y, v0.x, acc[r].y);
+    }
   }
 }
+
+struct PairInfo {        // one column pair (a, b) of a unit: X = the longer list
+  uint32_t xoff, yoff, nX, nY;
+  uint32_t nxt;          // X tiles
+  uint32_t swap;         // 1: X is the right list
+};
 
 // ---- one unit: column-split enumeration of its subtree (reading R20) ------------------
 // Paths below the prefix (columns 0..j fixed) = sum over column-pair states (a, b) at
@@ -519,16 +517,20 @@ __device__ void process_stack(const CallParams &p, Block &b, Shared &sh, double2
     if (top.j < 0) break;
     const int j = top.j, sj = top.sj, sjm1 = top.sjm1;
     const double2 pi = make_double2(top.re, top.im);
-    dp_counts(p, b, sh, j, sj, true);
+    const bool need_right = sh.cr_q != sh.q_cached;  // cR depends on the output only
+    dp_counts(p, b, sh, j, sj, need_right);
+    if (tid == 0) sh.cr_q = sh.q_cached;
     list_sizes(b, sh, j, M);
     // choose the split column pair: smallest L + R lists that fit the scratch
     if (tid == 0) {
-      const ull cap = (ull)(b.list_bytes / (2 * (16 + 2)) - 64);
       int best = -1;
       ull bcost = ~0ull;
       for (int k = j; k <= M - 1; ++k) {
         const ull c = sat_add(sh.NL[k], sh.NR[k + 1]);
-        if (c <= cap && c < bcost) {
+        // lists (two buffers each side, 18 B per element) + room for 16 pairs' scaling tables
+        const long long nctx = (k >= 1 ? sh.n[k - 1] : 1) + (k + 2 <= M ? sh.n[k + 2] : 1);
+        const long long reserve = 64 + 16 * ((long long)sizeof(PairInfo) + 16 * nctx);
+        if (c < (ull)(b.list_bytes / 36) && 36ll * (long long)c + reserve <= b.list_bytes && c < bcost) {
           bcost = c;
           best = k;
         }
@@ -596,6 +598,8 @@ __device__ void process_stack(const CallParams &p, Block &b, Shared &sh, double2
       for (uint32_t t = tid; t < total; t += kThreads) {
         const Seg g = b.segs[find_seg(b.segs, nsegs, t)];
         const uint32_t src = g.src + (t - g.dst);
+        DCHECK(t < capL && src < capL && t >= g.dst && t - g.dst < g.len, "left bfs");
+        DCHECK(Lc[cur][src] < (k >= 1 ? sh.n[k - 1] : 1) || (k == j), "left ctx");
         const double2 f = cut_factor(p, b, sh, k, Lc[cur][src], g.p, g.s, cm);
         Lp[cur ^ 1][t] = cmul(Lp[cur][src], f);
         Lc[cur ^ 1][t] = g.p;
@@ -626,6 +630,8 @@ __device__ void process_stack(const CallParams &p, Block &b, Shared &sh, double2
       for (uint32_t t = tid; t < total; t += kThreads) {
         const Seg g = b.segs[find_seg(b.segs, nsegs, t)];
         const uint32_t src = g.src + (t - g.dst);
+        DCHECK(t < capR && src < capR && t >= g.dst && t - g.dst < g.len, "right bfs");
+        DCHECK(k + 2 > M || Rc[cur][src] < sh.n[k + 2], "right ctx");
         const double2 f = cut_factor(p, b, sh, k + 1, g.s, g.p, Rc[cur][src], cm);
         Rp[cur ^ 1][t] = cmul(Rp[cur][src], f);
         Rc[cur ^ 1][t] = g.p;
@@ -653,48 +659,118 @@ __device__ void process_stack(const CallParams &p, Block &b, Shared &sh, double2
     if (tid == 0) {
       atomicMax(&p.ctr->max_list, (ull)max(NLk, NRk));
     }
-    // ---- column pairs (a at ks, b at ks+1)
+    // ---- column pairs (a at ks, b at ks+1): all pairs' scaling tables, then warp tiles
     {
       // reuse build_segments with kd = ks+1 (b), kn = ks (a), left = true: offsets unused
-      const int npairs = build_segments(p, b, sh, ks + 1, ks, true, b.offA /*unused*/, b.tmp /*zeros ok*/);
+      const int npairs = build_segments(p, b, sh, ks + 1, ks, true, b.offA /*unused*/, b.tmp /*unused*/);
       if (npairs < 0) {
         if (tid == 0) atomicAdd(&p.ctr->unsupported, 1ull);
         __syncthreads();
         continue;
       }
       if (tid == 0) atomicAdd(&p.ctr->pairs, (ull)npairs);
-      for (int e = 0; e < npairs; ++e) {
-        const Seg g = b.segs[e];
-        const int a = g.p, bb = g.s;
-        const int nL = (int)b.cL[sh.cb[ks] + a];
-        const int nR = (int)b.cR[sh.cb[ks + 1] + bb];
-        const int nctxL = ks >= 1 ? sh.n[ks - 1] : 1;
-        const int nctxR = ks + 2 <= M ? sh.n[ks + 2] : 1;
-        for (int al = tid; al < nctxL; al += kThreads) {
+      const int nctxL = ks >= 1 ? sh.n[ks - 1] : 1;
+      const int nctxR = ks + 2 <= M ? sh.n[ks + 2] : 1;
+      char *pq = b.lists + 36ll * (long long)(NLk + NRk);
+      pq = (char *)(((uintptr_t)pq + 15) & ~(uintptr_t)15);
+      const long long room = (b.lists + b.list_bytes) - pq;
+      const long long per_pair = (long long)sizeof(PairInfo) + 16ll * (nctxL + nctxR);
+      const int batch = (int)min((long long)min(npairs, kMaxStates), (room - 16) / per_pair);
+      DCHECK(batch >= 1, "pair batch");
+      PairInfo *pinfo = (PairInfo *)pq;
+      double2 *FLall = (double2 *)(((uintptr_t)(pq + (long long)sizeof(PairInfo) * batch) + 15) & ~(uintptr_t)15);
+      double2 *FRall = FLall + (long long)nctxL * batch;
+      for (int e0 = 0; e0 < npairs; e0 += batch) {
+        const int e1 = min(npairs, e0 + batch), ne = e1 - e0;
+        for (int e = tid; e < ne; e += kThreads) {
+          const Seg g = b.segs[e0 + e];
+          const int a = g.p, bb = g.s;
+          const uint32_t nL = (uint32_t)b.cL[sh.cb[ks] + a];
+          const uint32_t nR = (uint32_t)b.cR[sh.cb[ks + 1] + bb];
+          PairInfo pi_;
+          pi_.swap = nL < nR;
+          pi_.nX = pi_.swap ? nR : nL;
+          pi_.nY = pi_.swap ? nL : nR;
+          pi_.xoff = pi_.swap ? offR[bb] : offL[a];
+          pi_.yoff = pi_.swap ? offL[a] : offR[bb];
+          pi_.nxt = (pi_.nX + kXT - 1) / kXT;
+          b.tmp[e] = pi_.nxt * ((pi_.nY + kYT - 1) / kYT);
+          pinfo[e] = pi_;
+        }
+        for (int t = tid; t < ne * nctxL; t += kThreads) {
+          const int e = t / nctxL, al = t - e * nctxL;
+          const Seg g = b.segs[e0 + e];
           double2 f = pi;
           if (ks >= 1) {
-            if (compat(p, b, sh, ks, al, a)) f = cmul(pi, cut_factor(p, b, sh, ks, al, a, bb, cm));
+            if (compat(p, b, sh, ks, al, g.p)) f = cmul(pi, cut_factor(p, b, sh, ks, al, g.p, g.s, cm));
             else f = make_double2(0.0, 0.0);
           }
-          b.FL[al] = f;
+          FLall[t] = f;
         }
-        for (int be = tid; be < nctxR; be += kThreads) {
+        for (int t = tid; t < ne * nctxR; t += kThreads) {
+          const int e = t / nctxR, be = t - e * nctxR;
+          const Seg g = b.segs[e0 + e];
           double2 f = make_double2(1.0, 0.0);
           if (ks + 1 <= M - 1) {
-            if (compat(p, b, sh, ks + 2, bb, be)) f = cut_factor(p, b, sh, ks + 1, a, bb, be, cm);
+            if (compat(p, b, sh, ks + 2, g.s, be)) f = cut_factor(p, b, sh, ks + 1, g.p, g.s, be, cm);
             else f = make_double2(0.0, 0.0);
           }
-          b.FR[be] = f;
+          FRall[t] = f;
         }
         __syncthreads();
-        const double2 *xp = Lp[curL] + offL[a];
-        const uint16_t *xc = Lc[curL] + offL[a];
-        const double2 *yp = Rp[curR] + offR[bb];
-        const uint16_t *yc = Rc[curR] + offR[bb];
-        if (nL >= nR)
-          outer_pair(xp, xc, b.FL, nL, yp, yc, b.FR, nR, sY, acc, npaths, cm);
-        else
-          outer_pair(yp, yc, b.FR, nR, xp, xc, b.FL, nL, sY, acc, npaths, cm);
+        const uint32_t ntiles = block_scan(sh, b.tmp, b.tmp2, ne);  // tile offsets per pair
+        // every warp takes every (kThreads/32)-th tile: a static, deterministic assignment
+        const int warp = tid >> 5, lane = tid & 31;
+        double2 *sW = sY + warp * kYT;
+        for (uint32_t t = warp; t < ntiles; t += kThreads / 32) {
+          int lo = 0, hi = ne - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (b.tmp2[mid] <= t) lo = mid; else hi = mid - 1;
+          }
+          const PairInfo pr = pinfo[lo];
+          DCHECK(lo >= 0 && lo < ne && t >= b.tmp2[lo], "tile pair");
+          DCHECK((pr.swap ? (ull)pr.xoff + pr.nX <= capR && (ull)pr.yoff + pr.nY <= capL
+                          : (ull)pr.xoff + pr.nX <= capL && (ull)pr.yoff + pr.nY <= capR), "tile lists");
+          const uint32_t local = t - b.tmp2[lo];
+          const uint32_t xt = local % pr.nxt, yt = local / pr.nxt;
+          const double2 *Xp = (pr.swap ? Rp[curR] : Lp[curL]) + pr.xoff;
+          const uint16_t *Xc = (pr.swap ? Rc[curR] : Lc[curL]) + pr.xoff;
+          const double2 *FX = pr.swap ? FRall + (long long)lo * nctxR : FLall + (long long)lo * nctxL;
+          const double2 *Yp = (pr.swap ? Lp[curL] : Rp[curR]) + pr.yoff;
+          const uint16_t *Yc = (pr.swap ? Lc[curL] : Rc[curR]) + pr.yoff;
+          const double2 *FY = pr.swap ? FLall + (long long)lo * nctxL : FRall + (long long)lo * nctxR;
+          const uint32_t y0 = yt * kYT, len = min((uint32_t)kYT, pr.nY - y0);
+#pragma unroll
+          for (int r = 0; r < kYT / 32; ++r) {
+            const uint32_t jj = lane + 32 * r;
+            if (jj < len) {
+              DCHECK(Yc[y0 + jj] < (pr.swap ? nctxL : nctxR), "Y ctx");
+              sW[jj] = cmul(Yp[y0 + jj], FY[Yc[y0 + jj]]);
+            }
+          }
+          cm += (len + 31 - lane) / 32;
+          const uint32_t x0 = xt * kXT;
+          double2 x[kKX];
+          int nv = 0;
+#pragma unroll
+          for (int r = 0; r < kKX; ++r) {
+            const uint32_t i = x0 + lane + 32 * r;
+            if (i < pr.nX) {
+              DCHECK(Xc[i] < (pr.swap ? nctxR : nctxL), "X ctx");
+              x[r] = cmul(Xp[i], FX[Xc[i]]);
+              ++nv;
+            } else {
+              x[r] = make_double2(0.0, 0.0);
+            }
+          }
+          cm += nv;
+          __syncwarp();
+          fma_block(x, sW, len, acc);
+          npaths += (ull)nv * len;
+          __syncwarp();
+        }
+        __syncthreads();
       }
     }
   }
@@ -834,12 +910,12 @@ __global__ void __launch_bounds__(kThreads) lofp_table_kernel(const __grid_const
   }
 }
 
-// ---- plan: per output, counts and the split into units -------------------------------
+// ---- plan: per output, the column states and the exact path count ---------------------
 __global__ void __launch_bounds__(kThreads) lofp_plan_kernel(const __grid_constant__ CallParams p) {
   __shared__ Shared sh;
   Block b = make_block(p);
   load_cols(p, sh);
-  const int M = p.M, tid = threadIdx.x;
+  const int tid = threadIdx.x;
   for (int q = blockIdx.x; q < p.B; q += gridDim.x) {
     int st = setup_output(p, b, sh, q);
     if (st == kStatusOk) {
@@ -849,60 +925,100 @@ __global__ void __launch_bounds__(kThreads) lofp_plan_kernel(const __grid_consta
     if (tid == 0) {
       p.pdone[q] = 0;
       p.status[q] = (uint8_t)st;
-      int count = 0;
-      if (st == kStatusOk) {
-        atomicAdd(&p.ctr->feasible, 1ull);
-        const ull P = b.cR[sh.cb[0]];
-        p.pexp[q] = P;
-        // root product: phase gates that no cut carries (M == 1: the single mode holds N)
-        double2 root = make_double2(1.0, 0.0);
-        if (M == 1)
-          for (int g = 0; g < p.ngate; ++g) root = cmul(root, p.gate_tab[g * (p.N + 1) + p.N]);
-        ull thr = p.thr;
-        Unit *U = p.units + (long long)q * p.budget;
-        while (true) {
-          count = 0;
-          int sp = 0;
-          StackEnt e;
-          e.j = 0; e.sjm1 = 0; e.sj = 0; e.re = root.x; e.im = root.y; e.pad = 0;
-          b.stack[sp++] = e;
-          while (sp > 0) {
-            const StackEnt t = b.stack[--sp];
-            const ull below = b.cR[sh.cb[t.j] + t.sj];
-            bool leaf = below <= thr || t.j >= M - 1;
-            if (!leaf) {
-              const int n1 = sh.n[t.j + 1];
-              int pushed = 0;
-              for (int s = n1 - 1; s >= 0; --s) {
-                if (!live(b, sh, t.j + 1, s) || !compat(p, b, sh, t.j + 1, t.sj, s)) continue;
-                if (sp >= kStackMax) { leaf = true; break; }
-                ull cm = 0;
-                const double2 f = cut_factor(p, b, sh, t.j, t.sjm1, t.sj, s, cm);
-                const double2 np = cmul(make_double2(t.re, t.im), f);
-                StackEnt c;
-                c.j = t.j + 1; c.sjm1 = t.sj; c.sj = (uint16_t)s; c.re = np.x; c.im = np.y; c.pad = 0;
-                b.stack[sp++] = c;
-                ++pushed;
-              }
-              if (leaf) sp -= pushed;  // stack full: keep this node whole
-            }
-            if (leaf) {
-              if (count < p.budget) {
-                Unit u;
-                u.q = q; u.j = (int16_t)t.j; u.sjm1 = t.sjm1; u.sj = t.sj; u.pad = 0;
-                u.re = t.re; u.im = t.im; u.paths = below;
-                U[count] = u;
-              }
-              ++count;
-            }
-          }
-          if (count <= p.budget) break;
-          thr = thr > (~0ull >> 2) ? ~0ull : thr * 4;  // too many units for the slots: coarser
+      p.pexp[q] = st == kStatusOk ? b.cR[sh.cb[0]] : 0ull;
+      if (st == kStatusOk) atomicAdd(&p.ctr->feasible, 1ull);
+      if (st == kStatusBad) atomicAdd(&p.ctr->bad_rows, 1ull);
+      if (st == kStatusUnsupported) atomicAdd(&p.ctr->unsupported, 1ull);
+    }
+    __syncthreads();
+  }
+}
+
+// unit size: the batch's paths spread over ~8 units per block of the unit kernel, at least
+// p.thr (so small batches still split their big trees, north_star "prefixes")
+__global__ void lofp_thr_kernel(const __grid_constant__ CallParams p, int grid) {
+  __shared__ ull part[kThreads];
+  ull s = 0;
+  for (int q = threadIdx.x; q < p.B; q += kThreads) s = sat_add(s, p.pexp[q]);
+  part[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ull tot = 0;
+    for (int i = 0; i < kThreads; ++i) tot = sat_add(tot, part[i]);
+    ull t = tot / (ull)(8 * grid);
+    p.ctr->thr = t > p.thr ? t : p.thr;
+  }
+}
+
+// split: an output above the unit size becomes the prefix subtrees (columns 0..j fixed)
+// of at most that many paths, in depth-first order; every other feasible output is one unit
+__global__ void __launch_bounds__(kThreads) lofp_split_kernel(const __grid_constant__ CallParams p) {
+  __shared__ Shared sh;
+  Block b = make_block(p);
+  load_cols(p, sh);
+  const int M = p.M, tid = threadIdx.x;
+  for (int q = blockIdx.x; q < p.B; q += gridDim.x) {
+    const int st0 = p.status[q];
+    const ull P = p.pexp[q];
+    Unit *U = p.units + (long long)q * p.budget;
+    // root product: phase gates that no cut carries (M == 1: the single mode holds N)
+    double2 root = make_double2(1.0, 0.0);
+    if (M == 1)
+      for (int g = 0; g < p.ngate; ++g) root = cmul(root, p.gate_tab[g * (p.N + 1) + p.N]);
+    ull thr = p.ctr->thr;
+    if (st0 != kStatusOk || P <= thr) {
+      if (tid == 0) {
+        if (st0 == kStatusOk) {
+          Unit u;
+          u.q = q; u.j = 0; u.sjm1 = 0; u.sj = 0; u.pad = 0; u.re = root.x; u.im = root.y; u.paths = P;
+          U[0] = u;
         }
-      } else {
-        p.pexp[q] = 0;
-        if (st == kStatusBad) atomicAdd(&p.ctr->bad_rows, 1ull);
-        if (st == kStatusUnsupported) atomicAdd(&p.ctr->unsupported, 1ull);
+        p.nunits[q] = st0 == kStatusOk ? 1 : 0;
+      }
+      continue;  // (block-uniform)
+    }
+    setup_output(p, b, sh, q);
+    dp_counts(p, b, sh, 0, 0, true);
+    if (tid == 0) {
+      int count = 0;
+      while (true) {
+        count = 0;
+        int sp = 0;
+        StackEnt e;
+        e.j = 0; e.sjm1 = 0; e.sj = 0; e.re = root.x; e.im = root.y; e.pad = 0;
+        b.stack[sp++] = e;
+        while (sp > 0) {
+          const StackEnt t = b.stack[--sp];
+          const ull below = b.cR[sh.cb[t.j] + t.sj];
+          bool leaf = below <= thr || t.j >= M - 1;
+          if (!leaf) {
+            const int n1 = sh.n[t.j + 1];
+            int pushed = 0;
+            for (int s = n1 - 1; s >= 0; --s) {
+              if (!live(b, sh, t.j + 1, s) || !compat(p, b, sh, t.j + 1, t.sj, s)) continue;
+              if (sp >= kStackMax) { leaf = true; break; }
+              ull cm = 0;
+              const double2 f = cut_factor(p, b, sh, t.j, t.sjm1, t.sj, s, cm);
+              const double2 np = cmul(make_double2(t.re, t.im), f);
+              StackEnt c;
+              c.j = t.j + 1; c.sjm1 = t.sj; c.sj = (uint16_t)s; c.re = np.x; c.im = np.y; c.pad = 0;
+              b.stack[sp++] = c;
+              ++pushed;
+            }
+            if (leaf) sp -= pushed;  // stack full: keep this node whole
+          }
+          if (leaf) {
+            if (count < p.budget) {
+              Unit u;
+              u.q = q; u.j = (int16_t)t.j; u.sjm1 = t.sjm1; u.sj = t.sj; u.pad = 0;
+              u.re = t.re; u.im = t.im; u.paths = below;
+              U[count] = u;
+            }
+            ++count;
+          }
+        }
+        if (count <= p.budget) break;
+        thr = thr > (~0ull >> 2) ? ~0ull : thr * 4;  // too many units for the slots: coarser
       }
       p.nunits[q] = count;
     }
@@ -910,15 +1026,18 @@ __global__ void __launch_bounds__(kThreads) lofp_plan_kernel(const __grid_consta
   }
 }
 
-// exclusive scan of nunits -> ubase, total -> ctr->total_units (one block of kThreads)
+// exclusive scan of nunits -> ubase, total -> ctr->total_units; then the schedule: units
+// by decreasing size class (floor log2 of their path count), largest first (one block)
 __global__ void lofp_scan_kernel(const __grid_constant__ CallParams p) {
   __shared__ long long part[kThreads];
+  __shared__ unsigned int hist[65], base[65];
   const int B = p.B, tid = threadIdx.x;
   const int per = (B + kThreads - 1) / kThreads;
   const int a = tid * per, e = min(B, a + per);
   long long s = 0;
   for (int i = a; i < e; ++i) s += p.nunits[i];
   part[tid] = s;
+  if (tid < 65) hist[tid] = 0;
   __syncthreads();
   if (tid == 0) {
     long long run = 0;
@@ -936,6 +1055,29 @@ __global__ void lofp_scan_kernel(const __grid_constant__ CallParams p) {
     p.ubase[i] = (int)run;
     run += p.nunits[i];
   }
+  __syncthreads();
+  const int U = (int)p.ctr->total_units;
+  // size class of every unit (walk the outputs; unit u of output q is slot q*budget + i)
+  for (int q = tid; q < B; q += kThreads)
+    for (int i = 0; i < p.nunits[q]; ++i) {
+      const ull P = p.units[(long long)q * p.budget + i].paths;
+      atomicAdd(&hist[64 - (P ? 64 - __clzll(P) : 0)], 1u);
+    }
+  __syncthreads();
+  if (tid == 0) {
+    unsigned int r = 0;
+    for (int c = 0; c < 65; ++c) {
+      base[c] = r;
+      r += hist[c];
+    }
+  }
+  __syncthreads();
+  for (int q = tid; q < B; q += kThreads)
+    for (int i = 0; i < p.nunits[q]; ++i) {
+      const ull P = p.units[(long long)q * p.budget + i].paths;
+      const unsigned int pos = atomicAdd(&base[64 - (P ? 64 - __clzll(P) : 0)], 1u);
+      if ((int)pos < U) p.sched[pos] = p.ubase[q] + i;
+    }
 }
 
 // ---- the hot path ----------------------------------------------------------------------
@@ -949,8 +1091,10 @@ __global__ void __launch_bounds__(kThreads, 2) lofp_units_kernel(const __grid_co
   while (true) {
     if (tid == 0) sh.unit = (int)atomicAdd(&p.ctr->ticket, 1ull);
     __syncthreads();
-    const int u = sh.unit;
-    if ((ull)u >= p.ctr->total_units) break;
+    const int k_ = sh.unit;
+    if ((ull)k_ >= p.ctr->total_units) break;
+    const int u = p.sched[k_];
+    DCHECK(u >= 0 && u < (int)p.ctr->total_units, "sched");
     // unit u -> output q (binary search over ubase) -> slot
     int lo = 0, hi = p.B - 1;
     while (lo < hi) {
@@ -958,6 +1102,7 @@ __global__ void __launch_bounds__(kThreads, 2) lofp_units_kernel(const __grid_co
       if (p.ubase[mid] <= u) lo = mid; else hi = mid - 1;
     }
     const int q = lo;
+    DCHECK(u - p.ubase[q] >= 0 && u - p.ubase[q] < p.nunits[q] && p.nunits[q] <= p.budget, "unit slot");
     const Unit un = p.units[(long long)q * p.budget + (u - p.ubase[q])];
     if (sh.q_cached != q) {
       const int st = setup_output(p, b, sh, q);
@@ -1050,6 +1195,8 @@ extern "C" int lofp_launch_paths(const CallParams *p, int grid, void *stream, vo
   }
   const int pgrid = p->B < grid ? p->B : grid;
   lofp_plan_kernel<<<pgrid, kThreads, 0, st>>>(*p);
+  lofp_thr_kernel<<<1, kThreads, 0, st>>>(*p, grid);
+  lofp_split_kernel<<<pgrid, kThreads, 0, st>>>(*p);
   lofp_scan_kernel<<<1, kThreads, 0, st>>>(*p);
   if (ev0) cudaEventRecord((cudaEvent_t)ev0, st);
   lofp_units_kernel<<<grid, kThreads, smem, st>>>(*p);

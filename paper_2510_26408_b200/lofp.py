@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblofp.so")
+LIB_PATH = os.environ.get("LOFP_LIB") or os.path.join(_HERE, "liblofp.so")
 
 LOFP_OK, LOFP_E_INVALID_ARG, LOFP_E_UNSUPPORTED, LOFP_E_CUDA, LOFP_E_OOM, LOFP_E_BAD_OUTPUT = range(6)
 

@@ -229,3 +229,23 @@ def test_wrong_device_or_buffer_rejected(lofp):
         circ.amplitudes(c.S, Td, out=torch.zeros((3, 2), dtype=torch.float64, device="cuda"))
     with pytest.raises(ValueError):
         circ.amplitudes(c.S, Td.cpu())
+
+
+@pytest.mark.parametrize("idx,n,env", [(2, 256, {}), (3, 256, {}), (4, 256, {}),
+                                       (3, 128, {"LOFP_UNIT_PATHS": "100000"}),
+                                       (4, 96, {"LOFP_SLAB_MB": "2", "LOFP_UNIT_PATHS": str(1 << 40)})])
+def test_debug_build_bounds_checks(lofp, idx, n, env):
+    """compute-sanitizer is closed on this pool: the debug build (-DLOFP_DEBUG) checks every
+    list, segment, context, schedule and unit-slot index on the device and traps with the
+    failing site; conditioned slices, small units and forced sub-splits run clean."""
+    import subprocess
+    import sys
+    from paper_2510_26408_b200 import _build
+    assert os.path.exists(_build.DEBUG_LIB), "build() builds liblofp_debug.so"
+    e = dict(os.environ, LOFP_LIB=_build.DEBUG_LIB, **env)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "repro.py"), str(idx), str(n)], env=e,
+                       capture_output=True, text=True, timeout=600)
+    assert "LOFP_DEBUG" not in r.stdout + r.stderr, (r.stdout + r.stderr)[-2000:]
+    assert r.returncode == 0, r.stderr[-2000:]
+    ok = [l for l in r.stdout.splitlines() if l.startswith("ok")]
+    assert ok and ok[0].endswith("True") and ok[0].split()[3] == "0"
