@@ -132,6 +132,21 @@ lofp_status lofp_amplitudes_counted(lofp_ctx *ctx, const int32_t *input_occ, int
                                     const int32_t *output_occ, double *amps,
                                     uint64_t *path_counts, void *cuda_stream);
 
+/* The same amplitudes by the paper's strip tensor contraction (its code path
+ * for every D > 2): the circuit is contracted cut by cut from the top mode to the
+ * bottom one; the state crossing cut k is the pair of light-cone-live columns (photon
+ * counts left of cuts k-1 and k over all layers, the tuples l_{k,j} of P:183-185), each
+ * with its partial amplitude.  Work per output is the number of (column, column, column)
+ * triples instead of the number of paths, so outputs with 1e15+ paths (configs[3] as
+ * drawn) take microseconds; no path products are formed.  Arguments, asynchrony, errors
+ * and NaN/zero rules as lofp_amplitudes.  path_counts: optional DEVICE uint64 [B]
+ * (NULL allowed) receiving the exact number of valid paths of each output (the column
+ * count, saturating at 2^64-1).  An output whose column-pair level exceeds the scratch
+ * gets NaN and is counted as unsupported. */
+lofp_status lofp_amplitudes_contract(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch,
+                                     const int32_t *output_occ, double *amps,
+                                     uint64_t *path_counts, void *cuda_stream);
+
 /* End-to-end convenience: HOST buffers in and out.  Copies output_occ (host int32
  * [B][modes]) to the device, runs lofp_amplitudes on an internal stream, copies the
  * amplitudes back into amps (host double [B][2]) and returns when they are there. */
@@ -166,11 +181,13 @@ typedef struct {
   int64_t max_states;     /* largest number of column states of one output */
   int64_t max_list;       /* largest half-path list */
   int64_t table_entries;  /* Appendix-A elements in the table */
+  int64_t terms;          /* contraction mode: (state, state, state) terms summed */
   int32_t grid_blocks;    /* persistent grid of the unit kernel */
   int32_t block_threads;  /* threads per block */
   int32_t launches;       /* kernels launched by the call */
   int32_t mode;           /* 0 path sum, 1 strip contraction */
-  float units_ms;         /* device time of the unit (enumeration) kernel, CUDA events */
+  float units_ms;         /* device time of the unit (enumeration) kernel, CUDA events;
+                             contraction mode: of the contraction kernel */
   float total_ms;         /* device time from the first to the last kernel */
 } lofp_run_stats;
 

@@ -554,6 +554,13 @@ lofp_status lofp_amplitudes_counted(lofp_ctx *ctx, const int32_t *input_occ, int
              0);
 }
 
+lofp_status lofp_amplitudes_contract(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch,
+                                     const int32_t *output_occ, double *amps, uint64_t *path_counts,
+                                     void *cuda_stream) {
+  return run(ctx, input_occ, batch, output_occ, amps, (unsigned long long *)path_counts,
+             (cudaStream_t)cuda_stream, 1);
+}
+
 lofp_status lofp_amplitudes_host(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const int32_t *output_occ,
                                  double *amps) {
   if (!ctx) return LOFP_E_INVALID_ARG;
@@ -594,6 +601,7 @@ lofp_status lofp_stats(lofp_ctx *ctx, lofp_run_stats *out) {
     st.check_errors = (int64_t)hc->table_error;
     st.max_states = (int64_t)hc->max_states;
     st.max_list = (int64_t)hc->max_list;
+    st.terms = (int64_t)hc->contractions;
     if (ctx->timed) {
       float ms = 0.f;
       if (st.mode == 0 && cudaEventElapsedTime(&ms, ctx->ev_u0, ctx->ev_u1) == cudaSuccess) st.units_ms = ms;

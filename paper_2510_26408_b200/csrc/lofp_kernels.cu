@@ -1205,4 +1205,108 @@ extern "C" int lofp_launch_paths(const CallParams *p, int grid, void *stream, vo
   return (int)cudaGetLastError();
 }
 
-extern "C" int lofp_launch_contract(const CallParams *, int, void *) { return (int)cudaErrorNotSupported; }
+// ---- NEXT-1: the strip tensor contraction --------------------------------
+// The paper contracts the circuit block by block from top to bottom, storing for every
+// tuple l_{k,j} of occupation numbers crossing from block C_k to C_{k+1} its partial
+// amplitude.  Here the blocks are the cuts: the state crossing cut k is the
+// column pair (c_{k-1}, c_k) (the photon counts left of the cut over all layers), and
+//   A_{k+1}(c_k, c_{k+1}) = sum_{c_{k-1}} A_k(c_{k-1}, c_k) f_k(c_{k-1}, c_k, c_{k+1})
+// with f_k the cut factor (the BS of cut k, eq. (1)); the amplitude is the sum of the last
+// level ("the last contraction block ... gives us the wanted amplitude").  Only
+// light-cone-live states are carried ("upper bounds ... using the light cones").
+__global__ void __launch_bounds__(kThreads) lofp_contract_kernel(const __grid_constant__ CallParams p) {
+  __shared__ Shared sh;
+  __shared__ double red_re[kThreads / 32], red_im[kThreads / 32];
+  Block b = make_block(p);
+  load_cols(p, sh);
+  const int M = p.M, tid = threadIdx.x;
+  ull cm = 0, terms = 0;
+  for (int q = blockIdx.x; q < p.B; q += gridDim.x) {
+    int st = setup_output(p, b, sh, q);
+    if (st == kStatusOk) {
+      dp_counts(p, b, sh, 0, 0, true);
+      if (b.cR[sh.cb[0]] == 0) st = kStatusZero;
+    }
+    long long need = 0;
+    if (st == kStatusOk)
+      for (int k = 1; k <= M; ++k) need = max(need, (long long)sh.n[k - 1] * sh.n[k]);
+    if (st == kStatusOk && 2 * 16 * need > b.list_bytes) st = kStatusUnsupported;
+    double re = 0.0, im = 0.0;
+    if (st == kStatusOk) {
+      double2 *A = (double2 *)b.lists, *Bn = A + need;
+      // level 1: the pair (c_0, c_1), c_0 the single state of column 0
+      double2 root = make_double2(1.0, 0.0);
+      if (M == 1)
+        for (int g = 0; g < p.ngate; ++g) root = cmul(root, p.gate_tab[g * (p.N + 1) + p.N]);
+      for (int s1 = tid; s1 < sh.n[1]; s1 += kThreads)
+        A[s1] = (live(b, sh, 1, s1) && compat(p, b, sh, 1, 0, s1)) ? root : make_double2(0.0, 0.0);
+      __syncthreads();
+      for (int k = 1; k <= M - 1; ++k) {  // contract cut k: level (k-1, k) -> (k, k+1)
+        const int nA = sh.n[k - 1], nB = sh.n[k], nC = sh.n[k + 1];
+        for (int t = tid; t < nB * nC; t += kThreads) {
+          const int sb = t / nC, sc = t - sb * nC;
+          double2 sum = make_double2(0.0, 0.0);
+          if (live(b, sh, k, sb) && live(b, sh, k + 1, sc) && compat(p, b, sh, k + 1, sb, sc)) {
+            for (int sa = 0; sa < nA; ++sa) {
+              const double2 a = A[sa * nB + sb];
+              if (a.x == 0.0 && a.y == 0.0) continue;
+              const double2 f = cut_factor(p, b, sh, k, sa, sb, sc, cm);
+              sum.x = fma(a.x, f.x, fma(-a.y, f.y, sum.x));
+              sum.y = fma(a.x, f.y, fma(a.y, f.x, sum.y));
+              ++terms;
+            }
+          }
+          Bn[t] = sum;
+        }
+        __syncthreads();
+        double2 *tt = A; A = Bn; Bn = tt;
+      }
+      // the last level (c_{M-1}, c_M): its sum is the amplitude
+      const int nL = sh.n[M - 1] * sh.n[M];
+      for (int t = tid; t < nL; t += kThreads) {
+        re += A[t].x;
+        im += A[t].y;
+      }
+    }
+    // fixed-order block reduction (deterministic)
+    for (int d = 16; d > 0; d >>= 1) {
+      re += __shfl_down_sync(0xffffffffu, re, d);
+      im += __shfl_down_sync(0xffffffffu, im, d);
+    }
+    if ((tid & 31) == 0) {
+      red_re[tid >> 5] = re;
+      red_im[tid >> 5] = im;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double2 a = make_double2(0.0, 0.0);
+      for (int w = 0; w < kThreads / 32; ++w) {
+        a.x += red_re[w];
+        a.y += red_im[w];
+      }
+      if (st == kStatusBad || st == kStatusUnsupported)
+        a = make_double2(__longlong_as_double(0x7ff8000000000000ll), __longlong_as_double(0x7ff8000000000000ll));
+      p.amps[q] = a;
+      p.status[q] = (uint8_t)st;
+      if (p.counts) p.counts[q] = st == kStatusOk ? b.cR[sh.cb[0]] : 0ull;
+      if (st == kStatusOk) atomicAdd(&p.ctr->feasible, 1ull);
+      if (st == kStatusBad) atomicAdd(&p.ctr->bad_rows, 1ull);
+      if (st == kStatusUnsupported) atomicAdd(&p.ctr->unsupported, 1ull);
+    }
+    __syncthreads();
+  }
+  for (int d = 16; d > 0; d >>= 1) {
+    cm += __shfl_down_sync(0xffffffffu, cm, d);
+    terms += __shfl_down_sync(0xffffffffu, terms, d);
+  }
+  if ((tid & 31) == 0) {
+    atomicAdd(&p.ctr->cmuls, cm);
+    atomicAdd(&p.ctr->contractions, terms);
+  }
+}
+
+extern "C" int lofp_launch_contract(const CallParams *p, int grid, void *stream) {
+  const int g = p->B < grid ? p->B : grid;
+  lofp_contract_kernel<<<g, kThreads, 0, (cudaStream_t)stream>>>(*p);
+  return (int)cudaGetLastError();
+}

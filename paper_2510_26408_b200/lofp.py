@@ -32,13 +32,14 @@ class lofp_run_stats(ctypes.Structure):
                 ("cmuls", ctypes.c_int64), ("units", ctypes.c_int64), ("subsplits", ctypes.c_int64),
                 ("pairs", ctypes.c_int64), ("elements", ctypes.c_int64), ("unsupported", ctypes.c_int64),
                 ("bad_rows", ctypes.c_int64), ("check_errors", ctypes.c_int64), ("max_states", ctypes.c_int64),
-                ("max_list", ctypes.c_int64), ("table_entries", ctypes.c_int64),
+                ("max_list", ctypes.c_int64), ("table_entries", ctypes.c_int64), ("terms", ctypes.c_int64),
                 ("grid_blocks", ctypes.c_int32), ("block_threads", ctypes.c_int32),
                 ("launches", ctypes.c_int32), ("mode", ctypes.c_int32),
                 ("units_ms", ctypes.c_float), ("total_ms", ctypes.c_float)]
 
 
-EXPORTS = ["lofp_create", "lofp_create_ex", "lofp_amplitudes", "lofp_amplitudes_counted", "lofp_amplitudes_host",
+EXPORTS = ["lofp_create", "lofp_create_ex", "lofp_amplitudes", "lofp_amplitudes_counted", "lofp_amplitudes_contract",
+           "lofp_amplitudes_host",
            "lofp_destroy", "lofp_status_string", "lofp_last_error", "lofp_stats"]
 
 
@@ -58,6 +59,8 @@ def _load():
     lib.lofp_amplitudes.restype = ctypes.c_int
     lib.lofp_amplitudes_counted.argtypes = [P, ctypes.POINTER(ctypes.c_int32), ctypes.c_int64, P, P, P, P]
     lib.lofp_amplitudes_counted.restype = ctypes.c_int
+    lib.lofp_amplitudes_contract.argtypes = [P, ctypes.POINTER(ctypes.c_int32), ctypes.c_int64, P, P, P, P]
+    lib.lofp_amplitudes_contract.restype = ctypes.c_int
     lib.lofp_amplitudes_host.argtypes = [P, ctypes.POINTER(ctypes.c_int32), ctypes.c_int64, P, P]
     lib.lofp_amplitudes_host.restype = ctypes.c_int
     lib.lofp_destroy.argtypes = [P]
@@ -169,6 +172,29 @@ class Circuit:
                 st = _lib.lofp_amplitudes_counted(self._h, sp, B, ctypes.c_void_p(T.data_ptr()),
                                                   ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(counts.data_ptr()),
                                                   ctypes.c_void_p(strm))
+        self._check(st)
+        return torch.view_as_complex(out)
+
+    def contract(self, S, T, out=None, counts=None, stream=None):
+        """The same amplitudes by the strip tensor contraction: work per output
+        scales with the light-cone state space, not the number of paths.  ``counts``
+        (optional int64 CUDA tensor [B]) receives the exact number of valid paths."""
+        import torch
+        T = T.contiguous()
+        out = self._out(T, out)
+        B = T.shape[0]
+        s = _occ(S, self.modes)
+        strm = (stream or torch.cuda.current_stream(T.device)).cuda_stream
+        cp = None
+        if counts is not None:
+            if counts.dtype != torch.int64 or counts.numel() != B or counts.device != T.device or \
+                    not counts.is_contiguous():
+                raise ValueError("counts must be a contiguous int64 CUDA tensor [B] on T's device")
+            cp = ctypes.c_void_p(counts.data_ptr())
+        with torch.cuda.device(T.device):
+            st = _lib.lofp_amplitudes_contract(self._h, s.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), B,
+                                               ctypes.c_void_p(T.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                               cp, ctypes.c_void_p(strm))
         self._check(st)
         return torch.view_as_complex(out)
 

@@ -1,0 +1,153 @@
+"""GPU parity of the strip tensor contraction (NEXT-1; lofp_amplitudes_contract).
+
+The contraction evaluates eq. (1) without forming path products, so it reaches outputs no
+enumerator can: configs[3] as literally drawn (BASELINE.json: 2048 outputs of up to 1.5e16
+paths each) is checked output by output against the Ryser permanent (n = 12).  Elsewhere it
+is checked against the oracle path sum and against the GPU path-sum engine.
+Tolerance (BASELINE.json north_star): |a - a_ref| <= 1e-12 + 1e-9 |a_ref|.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import lofp_inputs as li
+import oracle
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def lofp():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    import paper_2510_26408_b200 as pkg
+    return pkg
+
+
+def tol_ok(got, ref):
+    err = np.abs(np.asarray(got) - np.asarray(ref))
+    return bool((err <= 1e-12 + 1e-9 * np.abs(ref)).all()), float(err.max()) if err.size else 0.0
+
+
+def contract(lofp, M, layers, S, T, gates=()):
+    circ = lofp.Circuit(M, layers, gates)
+    Td = torch.from_numpy(np.ascontiguousarray(T, dtype=np.int32)).cuda()
+    counts = torch.zeros(len(T), dtype=torch.int64, device="cuda")
+    a = circ.contract(S, Td, counts=counts)
+    torch.cuda.synchronize()
+    return a.cpu().numpy(), counts.cpu().numpy().astype(np.uint64), circ.stats()
+
+
+def paths(lofp, M, layers, S, T, gates=()):
+    circ = lofp.Circuit(M, layers, gates)
+    a = circ.amplitudes(S, torch.from_numpy(np.ascontiguousarray(T, dtype=np.int32)).cuda())
+    torch.cuda.synchronize()
+    return a.cpu().numpy()
+
+
+def load(idx):
+    return np.load(os.path.join(ROOT, "data", f"cfg{idx}.npz"))
+
+
+def test_config0_and_unitarity(lofp):
+    c = li.config(0)
+    T = c.draw_outputs()
+    got, cnt, st = contract(lofp, c.M, c.layers, c.S, T)
+    ref, leaves = oracle.path_sum(c.M, c.layers, c.S, T, return_leaves=True)
+    assert tol_ok(got, ref)[0]
+    assert np.array_equal(cnt, leaves)
+    assert abs(np.sum(np.abs(got) ** 2) - 1) < 1e-12
+    assert st["mode"] == 1 and st["terms"] > 0
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_circuits_with_gates(lofp, seed):
+    rng = np.random.default_rng(5100 + seed)
+    M = int(rng.integers(1, 10))
+    D = int(rng.integers(0, 8))
+    N = int(rng.integers(0, 6))
+    layers = li.random_nn_circuit(M, D, rng, fill=float(rng.uniform(0.4, 1.0)), reverse_prob=0.4)
+    S = np.zeros(M, dtype=np.int32)
+    for m in rng.integers(0, M, size=N):
+        S[m] += 1
+    gates = [(int(rng.integers(0, M)), int(rng.integers(0, D + 1)), float(rng.uniform(-3, 3)),
+              float(rng.uniform(-1, 1))) for _ in range(int(rng.integers(0, 4)))]
+    T = li.all_outputs(M, N)
+    if len(T) > 300:
+        T = T[rng.choice(len(T), 300, replace=False)]
+    T = np.concatenate([T, np.clip(T[:3] + 1, 0, None)])
+    got, cnt, _ = contract(lofp, M, layers, S, T, gates)
+    ref, leaves = oracle.path_sum(M, layers, S, T, return_leaves=True, gates=gates)
+    ok, err = tol_ok(got, ref)
+    assert ok, err
+    assert np.array_equal(cnt, leaves)
+
+
+def test_config1_literal(lofp):
+    c = li.config(1)
+    d = load(1)
+    T = d["T_literal"].astype(np.int32)
+    got, cnt, _ = contract(lofp, c.M, c.layers, c.S, T)
+    assert np.array_equal(cnt, d["P_literal"])
+    assert tol_ok(got, oracle.path_sum(c.M, c.layers, c.S, T))[0]
+
+
+@pytest.mark.parametrize("idx", [2, 3, 4])
+def test_conditioned_batches_match_path_engine(lofp, idx):
+    """Two GPU algorithms, one sum: the contraction against the path-sum engine on the full
+    conditioned batch, and against Ryser on a sample."""
+    c = li.config(idx)
+    d = load(idx)
+    T = d["T_cond"].astype(np.int32)
+    got, cnt, st = contract(lofp, c.M, c.layers, c.S, T)
+    assert np.array_equal(cnt, d["P_cond"])
+    assert st["unsupported"] == 0
+    assert tol_ok(got, paths(lofp, c.M, c.layers, c.S, T))[0]
+    pick = np.random.default_rng(idx).choice(len(T), 64, replace=False)
+    assert tol_ok(got[pick], oracle.amplitudes_permanent(c.M, c.layers, c.S, T[pick]))[0]
+
+
+def test_config3_literal_batch_all_outputs_vs_ryser(lofp):
+    """configs[3] exactly as BASELINE.json draws it: 2048 outputs, up to 1.5e16 paths each
+    (2.5e18 in total) -- every amplitude against the Ryser permanent (n = 12)."""
+    c = li.config(3)
+    d = load(3)
+    T = d["T_literal"].astype(np.int32)
+    got, cnt, st = contract(lofp, c.M, c.layers, c.S, T)
+    assert np.array_equal(cnt, d["P_literal"])
+    assert st["unsupported"] == 0 and st["check_errors"] == 0
+    ref = oracle.amplitudes_permanent(c.M, c.layers, c.S, T)
+    ok, err = tol_ok(got, ref)
+    assert ok, err
+
+
+def test_config2_literal_batch(lofp):
+    c = li.config(2)
+    d = load(2)
+    T = d["T_literal"].astype(np.int32)
+    got, cnt, _ = contract(lofp, c.M, c.layers, c.S, T)
+    assert np.array_equal(cnt, d["P_literal"])
+    reach = d["P_literal"] > 0
+    assert (got[~reach] == 0).all()
+    ref = oracle.amplitudes_permanent(c.M, c.layers, c.S, T[reach])
+    assert tol_ok(got[reach], ref)[0]
+
+
+@pytest.mark.parametrize("D", [3, 4])
+def test_density_workload_all_densities(lofp, D):
+    """P:318 at every density k = 1..10 (10..100 photons in 10 modes): the contraction and
+    the path-sum engine agree (D = 4, k = 10 is 2.3e11 paths); the oracle at k <= 3."""
+    M = 10
+    layers = li.clements_mesh(M, D, seed=318 + D)
+    for k in range(1, 11):
+        S = np.full(M, k, dtype=np.int32)
+        a, cnt, st = contract(lofp, M, layers, S, S[None, :])
+        b = paths(lofp, M, layers, S, S[None, :])
+        assert np.isfinite(a).all() and st["unsupported"] == 0
+        ok, err = tol_ok(a, b)
+        assert ok, (k, err)
+        if k <= 3:
+            assert tol_ok(a, oracle.path_sum(M, layers, S, S[None, :]))[0]
