@@ -147,6 +147,22 @@ lofp_status lofp_amplitudes_contract(lofp_ctx *ctx, const int32_t *input_occ, in
                                      const int32_t *output_occ, double *amps,
                                      uint64_t *path_counts, void *cuda_stream);
 
+/* All output amplitudes for one input ("simultaneously calculate and store the
+ * amplitudes of all possible output states for a given input").  Writes the
+ * C(N+M-1, M-1) patterns of N = sum(S) photons in M modes to outputs (DEVICE int32
+ * [count][modes], ordered by decreasing T_0, then decreasing T_1, ...) and their
+ * amplitudes to amps (DEVICE double [count][2]) in one stream-ordered call.
+ *   max_outputs   capacity of outputs / amps in rows.
+ *   n_outputs     HOST int64: receives the pattern count (also when it exceeds
+ *                 max_outputs, which returns LOFP_E_INVALID_ARG without device work).
+ *   method        0 = strip contraction (lofp_amplitudes_contract), 1 = path sum
+ *                 (lofp_amplitudes).
+ * Errors: LOFP_E_INVALID_ARG, LOFP_E_UNSUPPORTED (more than 2^31 - 1 patterns),
+ * LOFP_E_CUDA, LOFP_E_OOM. */
+lofp_status lofp_distribution(lofp_ctx *ctx, const int32_t *input_occ, int64_t max_outputs,
+                              int32_t *outputs, double *amps, int64_t *n_outputs,
+                              int32_t method, void *cuda_stream);
+
 /* End-to-end convenience: HOST buffers in and out.  Copies output_occ (host int32
  * [B][modes]) to the device, runs lofp_amplitudes on an internal stream, copies the
  * amplitudes back into amps (host double [B][2]) and returns when they are there. */

@@ -561,6 +561,35 @@ lofp_status lofp_amplitudes_contract(lofp_ctx *ctx, const int32_t *input_occ, in
              (cudaStream_t)cuda_stream, 1);
 }
 
+lofp_status lofp_distribution(lofp_ctx *ctx, const int32_t *input_occ, int64_t max_outputs, int32_t *outputs,
+                              double *amps, int64_t *n_outputs, int32_t method, void *cuda_stream) {
+  if (!ctx) return LOFP_E_INVALID_ARG;
+  ctx->err.clear();
+  if (!input_occ || !n_outputs || max_outputs < 0 || (method != 0 && method != 1))
+    return fail(ctx, LOFP_E_INVALID_ARG, "bad arguments");
+  int N = 0;
+  for (int i = 0; i < ctx->M; ++i) {
+    if (input_occ[i] < 0) return fail(ctx, LOFP_E_INVALID_ARG, "negative input occupation");
+    N += input_occ[i];
+    if (N > LOFP_MAX_PHOTONS) return fail(ctx, LOFP_E_UNSUPPORTED, "too many photons");
+  }
+  // C(N + M - 1, M - 1) patterns, computed exactly with an overflow guard
+  const int n = N + ctx->M - 1, k = std::min(ctx->M - 1, N);
+  unsigned long long c = 1;
+  for (int i = 1; i <= k; ++i) {
+    const unsigned long long num = (unsigned long long)(n - k + i);
+    if (c > (~0ull >> 1) / num) return fail(ctx, LOFP_E_UNSUPPORTED, "too many output patterns");
+    c = c * num / (unsigned long long)i;
+  }
+  if (c > (unsigned long long)0x7fffffff) return fail(ctx, LOFP_E_UNSUPPORTED, "too many output patterns");
+  *n_outputs = (int64_t)c;
+  if ((int64_t)c > max_outputs) return fail(ctx, LOFP_E_INVALID_ARG, "max_outputs is smaller than the pattern count");
+  if (!outputs || !amps) return fail(ctx, LOFP_E_INVALID_ARG, "null outputs or amps");
+  DeviceGuard guard(ctx->device);
+  CK((cudaError_t)lofp_launch_outputs(ctx->M, N, (long long)c, outputs, cuda_stream), "output patterns");
+  return run(ctx, input_occ, (int64_t)c, outputs, amps, nullptr, (cudaStream_t)cuda_stream, method == 0 ? 1 : 0);
+}
+
 lofp_status lofp_amplitudes_host(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const int32_t *output_occ,
                                  double *amps) {
   if (!ctx) return LOFP_E_INVALID_ARG;

@@ -153,6 +153,7 @@ int lofp_launch_tables(const lofp::CallParams *p, void *stream);
 int lofp_launch_paths(const lofp::CallParams *p, int grid, void *stream, void *ev_units0, void *ev_units1);
 int lofp_launch_contract(const lofp::CallParams *p, int grid, void *stream);
 int lofp_units_grid(int device);
+int lofp_launch_outputs(int M, int N, long long count, int32_t *T, void *stream);
 }
 
 #endif  // LOFP_INTERNAL_H

@@ -1310,3 +1310,41 @@ extern "C" int lofp_launch_contract(const CallParams *p, int grid, void *stream)
   lofp_contract_kernel<<<g, kThreads, 0, (cudaStream_t)stream>>>(*p);
   return (int)cudaGetLastError();
 }
+
+// ---- NEXT-2: every output pattern of N photons in M modes ----------------------
+// Pattern r (0 <= r < C(N+M-1, M-1)) in the order of decreasing T_0, then decreasing T_1,
+// ...: unranked independently per thread from the binomial counts of the suffixes.
+__device__ __forceinline__ ull binom_dev(int n, int k) {  // C(n, k), n < 256 (caller bounds it)
+  if (k < 0 || k > n) return 0;
+  if (k > n - k) k = n - k;
+  ull r = 1;
+  for (int i = 1; i <= k; ++i) r = r * (ull)(n - k + i) / (ull)i;
+  return r;
+}
+
+__global__ void lofp_outputs_kernel(int M, int N, long long count, int32_t *T) {
+  for (long long r0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; r0 < count;
+       r0 += (long long)gridDim.x * blockDim.x) {
+    ull r = (ull)r0;
+    int rem = N;
+    int32_t *row = T + r0 * M;
+    for (int i = 0; i < M - 1; ++i) {
+      int v = rem;
+      for (; v > 0; --v) {  // patterns of the remaining modes holding rem - v photons
+        const ull c = binom_dev(rem - v + (M - i - 2), M - i - 2);
+        if (r < c) break;
+        r -= c;
+      }
+      row[i] = v;
+      rem -= v;
+    }
+    row[M - 1] = rem;
+  }
+}
+
+extern "C" int lofp_launch_outputs(int M, int N, long long count, int32_t *T, void *stream) {
+  const long long blocks = (count + 255) / 256;
+  lofp_outputs_kernel<<<(int)(blocks < 4096 ? (blocks > 0 ? blocks : 1) : 4096), 256, 0, (cudaStream_t)stream>>>(
+      M, N, count, T);
+  return (int)cudaGetLastError();
+}

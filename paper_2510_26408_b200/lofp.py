@@ -39,7 +39,7 @@ class lofp_run_stats(ctypes.Structure):
 
 
 EXPORTS = ["lofp_create", "lofp_create_ex", "lofp_amplitudes", "lofp_amplitudes_counted", "lofp_amplitudes_contract",
-           "lofp_amplitudes_host",
+           "lofp_distribution", "lofp_amplitudes_host",
            "lofp_destroy", "lofp_status_string", "lofp_last_error", "lofp_stats"]
 
 
@@ -61,6 +61,9 @@ def _load():
     lib.lofp_amplitudes_counted.restype = ctypes.c_int
     lib.lofp_amplitudes_contract.argtypes = [P, ctypes.POINTER(ctypes.c_int32), ctypes.c_int64, P, P, P, P]
     lib.lofp_amplitudes_contract.restype = ctypes.c_int
+    lib.lofp_distribution.argtypes = [P, ctypes.POINTER(ctypes.c_int32), ctypes.c_int64, P, P,
+                                      ctypes.POINTER(ctypes.c_int64), ctypes.c_int32, P]
+    lib.lofp_distribution.restype = ctypes.c_int
     lib.lofp_amplitudes_host.argtypes = [P, ctypes.POINTER(ctypes.c_int32), ctypes.c_int64, P, P]
     lib.lofp_amplitudes_host.restype = ctypes.c_int
     lib.lofp_destroy.argtypes = [P]
@@ -197,6 +200,28 @@ class Circuit:
                                                cp, ctypes.c_void_p(strm))
         self._check(st)
         return torch.view_as_complex(out)
+
+    def distribution(self, S, method: str = "contract", device=None, stream=None):
+        """Every output pattern of sum(S) photons and its amplitude, computed in one
+        call: returns (T int32 CUDA [count, M], amplitudes complex128 CUDA [count])."""
+        import torch
+        s = _occ(S, self.modes)
+        sp = s.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+        dev = torch.device("cuda", self.device_index if device is None else device)
+        n = ctypes.c_int64(0)
+        _lib.lofp_distribution(self._h, sp, 0, None, None, ctypes.byref(n), 0, None)  # count only
+        count = int(n.value)
+        if count <= 0:
+            self._check(_lib.lofp_distribution(self._h, sp, 0, None, None, ctypes.byref(n), 0, None))
+        T = torch.empty((count, self.modes), dtype=torch.int32, device=dev)
+        out = torch.empty((count, 2), dtype=torch.float64, device=dev)
+        strm = (stream or torch.cuda.current_stream(dev)).cuda_stream
+        with torch.cuda.device(dev):
+            st = _lib.lofp_distribution(self._h, sp, count, ctypes.c_void_p(T.data_ptr()),
+                                        ctypes.c_void_p(out.data_ptr()), ctypes.byref(n),
+                                        0 if method == "contract" else 1, ctypes.c_void_p(strm))
+        self._check(st)
+        return T, torch.view_as_complex(out)
 
     def amplitudes_host(self, S, T) -> np.ndarray:
         """End-to-end call with host buffers (numpy in, numpy out)."""

@@ -151,3 +151,38 @@ def test_density_workload_all_densities(lofp, D):
         assert ok, (k, err)
         if k <= 3:
             assert tol_ok(a, oracle.path_sum(M, layers, S, S[None, :]))[0]
+
+
+@pytest.mark.parametrize("method", ["contract", "paths"])
+def test_distribution_paper_protocol(lofp, method):
+    """NEXT-2: all output amplitudes of one input in one call.  The paper's §III.A
+    protocol: its four 6-mode inputs at depths 3..6, probabilities of every
+    output summing to 1 and their total variation distance to Ryser's far below 1e-13."""
+    for case, (S, D) in enumerate(li.paper_correctness_inputs()):
+        S = np.array(S, dtype=np.int32)
+        layers = li.clements_mesh(6, D, seed=300 + case)
+        circ = lofp.Circuit(6, layers)
+        T, a = circ.distribution(S, method=method)
+        torch.cuda.synchronize()
+        T = T.cpu().numpy()
+        a = a.cpu().numpy()
+        assert np.array_equal(T, li.all_outputs(6, int(S.sum())))  # every pattern, fixed order
+        p = np.abs(a) ** 2
+        assert abs(p.sum() - 1.0) < 1e-12
+        q = np.abs(oracle.amplitudes_permanent(6, layers, S, T)) ** 2
+        assert oracle.tvd(p, q) < 1e-13
+
+
+def test_distribution_config1_unitarity(lofp):
+    """configs[1]'s circuit and input: all C(23, 8) = 490,314 outputs in one call; the
+    probabilities sum to 1 (unitarity) and a sample matches the oracle."""
+    c = li.config(1)
+    circ = lofp.Circuit(c.M, c.layers)
+    T, a = circ.distribution(c.S)
+    torch.cuda.synchronize()
+    T = T.cpu().numpy()
+    a = a.cpu().numpy()
+    assert len(T) == 490314
+    assert abs(np.sum(np.abs(a) ** 2) - 1.0) < 1e-11
+    pick = np.random.default_rng(1).choice(len(T), 200, replace=False)
+    assert tol_ok(a[pick], oracle.path_sum(c.M, c.layers, c.S, T[pick]))[0]
