@@ -198,6 +198,11 @@ typedef struct {
   int64_t max_list;       /* largest half-path list */
   int64_t table_entries;  /* Appendix-A elements in the table */
   int64_t terms;          /* contraction mode: (state, state, state) terms summed */
+  int64_t phase_cycles[8];/* unit kernel, SM clock cycles of each block's thread 0 summed over
+                             blocks: 0 unit fetch / output setup / reduction, 1 path counts and
+                             split choice, 2 left lists, 3 right lists, 4 pair list and
+                             scaling tables, 5 warp tiles (path products), 6 waiting for the
+                             block's other warps after the tiles, 7 stack pop / sub-splits */
   int32_t grid_blocks;    /* persistent grid of the unit kernel */
   int32_t block_threads;  /* threads per block */
   int32_t launches;       /* kernels launched by the call */

@@ -438,6 +438,7 @@ lofp_status prepare(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, cons
   P.budget = (int)budget;
   P.thr = (unsigned long long)env_ll("LOFP_UNIT_PATHS", 1ll << 24);
   P.slab_bytes = ctx->slab_bytes;
+  P.units_per_block = (int)env_ll("LOFP_UNITS_PER_BLOCK", 2);
   CK(ctx->d_units.ensure((size_t)(B * budget) * sizeof(Unit)), "alloc units");
   CK(ctx->d_partial.ensure((size_t)(B * budget) * 16), "alloc partials");
   CK(ctx->d_sched.ensure((size_t)(B * budget) * 4), "alloc schedule");
@@ -631,6 +632,7 @@ lofp_status lofp_stats(lofp_ctx *ctx, lofp_run_stats *out) {
     st.max_states = (int64_t)hc->max_states;
     st.max_list = (int64_t)hc->max_list;
     st.terms = (int64_t)hc->contractions;
+    for (int i = 0; i < 8; ++i) st.phase_cycles[i] = (int64_t)hc->phase[i];
     if (ctx->timed) {
       float ms = 0.f;
       if (st.mode == 0 && cudaEventElapsedTime(&ms, ctx->ev_u0, ctx->ev_u1) == cudaSuccess) st.units_ms = ms;

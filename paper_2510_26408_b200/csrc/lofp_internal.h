@@ -100,6 +100,7 @@ struct Counters {        // device counters of one call (zeroed by the host)
   unsigned long long max_list;   // largest half-path list built
   unsigned long long contractions; // contraction mode: column-pair states carried
   unsigned long long thr;        // unit size of the call (paths)
+  unsigned long long phase[8];   // unit kernel, thread 0's SM clocks per phase
 };
 
 enum : uint8_t { kStatusOk = 0, kStatusZero = 1, kStatusBad = 2, kStatusUnsupported = 3 };
@@ -108,6 +109,7 @@ struct CallParams {
   int M, D, N, B, nbs, ngate;
   int budget;            // unit slots per output
   int mode;              // 0 path sum, 1 contraction
+  int units_per_block;   // unit size = max(thr, total paths / (units_per_block * grid))
   unsigned long long thr;  // smallest unit size (paths); the call's is in Counters::thr
   long long slab_bytes;  // per-block scratch in global memory
   long long table_cap;   // entries allocated for the Appendix-A table

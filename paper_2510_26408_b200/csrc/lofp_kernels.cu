@@ -119,7 +119,19 @@ struct Shared {
   int q_cached;
   int cr_q;                // output whose cR counts are in the slab
   int unit;
+  ull ph[8];               // thread 0's SM clock per phase (lofp_stats phase_cycles)
+  ull tph;
 };
+
+// phase timer of thread 0 (block time split: lofp_run_stats::phase_cycles)
+#define PHASE(sh, i)                          \
+  do {                                        \
+    if (threadIdx.x == 0) {                   \
+      const ull now_ = clock64();             \
+      (sh).ph[i] += now_ - (sh).tph;          \
+      (sh).tph = now_;                        \
+    }                                         \
+  } while (0)
 
 // slab carve of one output: vals, cL, cR, then the half-path lists (needs sh.n/vb/cb)
 __device__ __forceinline__ void carve(const CallParams &p, Block &b, const Shared &sh) {
@@ -498,6 +510,66 @@ struct PairInfo {        // one column pair (a, b) of a unit: X = the longer lis
   uint32_t swap;         // 1: X is the right list
 };
 
+// One BFS level of a half-path list: element t of the new level extends element src of
+// the old one by one column; its product gains one cut factor.  Elements of one segment
+// (predecessor p, state s) differ only in their context state (the column beyond p), so
+// when cheaper the factors are tabulated per (segment, context) first (nseg * nctx cut
+// factors instead of one per element).  Warps take 32 consecutive elements: one binary
+// search per warp, then a short forward scan per lane.
+//   left:  dst column k+1, src column k, factor of cut k  = f(ctx @ k-1, p @ k, s @ k+1)
+//   right: dst column k,   src column k+1, factor of cut k+1 = f(s @ k, p @ k+1, ctx @ k+2)
+template <bool LEFT>
+__device__ void expand_level(const CallParams &p, Block &b, Shared &sh, int k, int nsegs, uint32_t total,
+                             const double2 *__restrict__ srcP, const uint16_t *__restrict__ srcC,
+                             double2 *__restrict__ dstP, uint16_t *__restrict__ dstC, double2 *Fseg,
+                             long long fcap, ull &cm) {
+  const int M = p.M, tid = threadIdx.x;
+  const int cut = LEFT ? k : k + 1;
+  const bool has_factor = cut >= 1 && cut <= M - 1;
+  const int nctx = LEFT ? (k >= 1 ? sh.n[k - 1] : 1) : (k + 2 <= M ? sh.n[k + 2] : 1);
+  const long long ntab = (long long)nsegs * nctx;
+  const bool use_table = has_factor && ntab <= fcap && ntab < (long long)total;
+  if (use_table) {
+    for (long long t = tid; t < ntab; t += kThreads) {
+      const int e = (int)(t / nctx), c = (int)(t - (long long)e * nctx);
+      const Seg g = b.segs[e];
+      double2 f = make_double2(0.0, 0.0);
+      if (LEFT) {
+        if (compat(p, b, sh, k, c, g.p)) f = cut_factor(p, b, sh, k, c, g.p, g.s, cm);
+      } else {
+        if (k + 2 > M || compat(p, b, sh, k + 2, g.p, c)) f = cut_factor(p, b, sh, k + 1, g.s, g.p, c, cm);
+      }
+      Fseg[t] = f;
+    }
+    __syncthreads();
+  }
+  const int warp = tid >> 5, lane = tid & 31;
+  for (uint32_t base = (uint32_t)warp * 32; base < total; base += kThreads) {
+    int e = 0;
+    if (lane == 0) e = find_seg(b.segs, nsegs, base);
+    e = __shfl_sync(0xffffffffu, e, 0);
+    const uint32_t t = base + lane;
+    if (t < total) {
+      while (e + 1 < nsegs && b.segs[e + 1].dst <= t) ++e;
+      const Seg g = b.segs[e];
+      const uint32_t src = g.src + (t - g.dst);
+      DCHECK(t >= g.dst && t - g.dst < g.len, "bfs segment");
+      const int ctx = srcC[src];
+      double2 f = make_double2(1.0, 0.0);
+      if (use_table) {
+        DCHECK(ctx < nctx, "bfs ctx");
+        f = Fseg[(long long)e * nctx + ctx];
+      } else if (has_factor) {
+        f = LEFT ? cut_factor(p, b, sh, k, ctx, g.p, g.s, cm) : cut_factor(p, b, sh, k + 1, g.s, g.p, ctx, cm);
+      }
+      dstP[t] = cmul(srcP[src], f);
+      dstC[t] = g.p;
+      ++cm;
+    }
+  }
+  __syncthreads();
+}
+
 // ---- one unit: column-split enumeration of its subtree (reading R20) ------------------
 // Paths below the prefix (columns 0..j fixed) = sum over column-pair states (a, b) at
 // columns (ks, ks+1) of L(a) x R(b): L(a) = partial paths j..ks ending in a (products of
@@ -518,6 +590,7 @@ __device__ void process_stack(const CallParams &p, Block &b, Shared &sh, double2
     const int j = top.j, sj = top.sj, sjm1 = top.sjm1;
     const double2 pi = make_double2(top.re, top.im);
     const bool need_right = sh.cr_q != sh.q_cached;  // cR depends on the output only
+    PHASE(sh, 7);
     dp_counts(p, b, sh, j, sj, need_right);
     if (tid == 0) sh.cr_q = sh.q_cached;
     list_sizes(b, sh, j, M);
@@ -566,6 +639,7 @@ __device__ void process_stack(const CallParams &p, Block &b, Shared &sh, double2
       __syncthreads();
       continue;
     }
+    PHASE(sh, 1);
     const ull NLk = sh.NL[ks], NRk = sh.NR[ks + 1];
     const ull capL = NLk, capR = NRk;
     double2 *Lp[2], *Rp[2];
@@ -581,6 +655,9 @@ __device__ void process_stack(const CallParams &p, Block &b, Shared &sh, double2
       Rc[0] = (uint16_t *)q; q += 2 * capR;
       Rc[1] = (uint16_t *)q;
     }
+    // scratch after the lists: per-(segment, context) factor tables of the BFS levels
+    double2 *Fscratch = (double2 *)(((uintptr_t)(b.lists + 36ll * (long long)(NLk + NRk)) + 15) & ~(uintptr_t)15);
+    const long long fcap = ((b.lists + b.list_bytes) - (char *)Fscratch) / 16 - 1;
     // ---- left lists: levels j..ks
     uint32_t *offS = b.offA, *offD = b.offB;
     int cur = 0;
@@ -595,21 +672,13 @@ __device__ void process_stack(const CallParams &p, Block &b, Shared &sh, double2
       const uint32_t total = bucket_offsets(b, sh, k + 1, true, offD);
       const int nsegs = build_segments(p, b, sh, k + 1, k, true, offS, offD);
       if (nsegs < 0) { ok = false; break; }
-      for (uint32_t t = tid; t < total; t += kThreads) {
-        const Seg g = b.segs[find_seg(b.segs, nsegs, t)];
-        const uint32_t src = g.src + (t - g.dst);
-        DCHECK(t < capL && src < capL && t >= g.dst && t - g.dst < g.len, "left bfs");
-        DCHECK(Lc[cur][src] < (k >= 1 ? sh.n[k - 1] : 1) || (k == j), "left ctx");
-        const double2 f = cut_factor(p, b, sh, k, Lc[cur][src], g.p, g.s, cm);
-        Lp[cur ^ 1][t] = cmul(Lp[cur][src], f);
-        Lc[cur ^ 1][t] = g.p;
-        ++cm;
-      }
+      DCHECK(total <= capL, "left level size");
+      expand_level<true>(p, b, sh, k, nsegs, total, Lp[cur], Lc[cur], Lp[cur ^ 1], Lc[cur ^ 1], Fscratch, fcap, cm);
       nelem += (total + kThreads - 1 - tid) / kThreads;
-      __syncthreads();
       cur ^= 1;
       uint32_t *tt = offS; offS = offD; offD = tt;
     }
+    PHASE(sh, 2);
     const int curL = cur;
     uint32_t *offL = offS;  // bucket offsets of column ks
     // ---- right lists: levels M..ks+1 (the other offset buffer pair)
@@ -627,18 +696,9 @@ __device__ void process_stack(const CallParams &p, Block &b, Shared &sh, double2
       const uint32_t total = bucket_offsets(b, sh, k, false, rB);
       const int nsegs = build_segments(p, b, sh, k, k + 1, false, rA, rB);
       if (nsegs < 0) { ok = false; break; }
-      for (uint32_t t = tid; t < total; t += kThreads) {
-        const Seg g = b.segs[find_seg(b.segs, nsegs, t)];
-        const uint32_t src = g.src + (t - g.dst);
-        DCHECK(t < capR && src < capR && t >= g.dst && t - g.dst < g.len, "right bfs");
-        DCHECK(k + 2 > M || Rc[cur][src] < sh.n[k + 2], "right ctx");
-        const double2 f = cut_factor(p, b, sh, k + 1, g.s, g.p, Rc[cur][src], cm);
-        Rp[cur ^ 1][t] = cmul(Rp[cur][src], f);
-        Rc[cur ^ 1][t] = g.p;
-        ++cm;
-      }
+      DCHECK(total <= capR, "right level size");
+      expand_level<false>(p, b, sh, k, nsegs, total, Rp[cur], Rc[cur], Rp[cur ^ 1], Rc[cur ^ 1], Fscratch, fcap, cm);
       nelem += (total + kThreads - 1 - tid) / kThreads;
-      __syncthreads();
       cur ^= 1;
       uint32_t *tt = rA; rA = rB; rB = tt;
     }
@@ -659,6 +719,7 @@ __device__ void process_stack(const CallParams &p, Block &b, Shared &sh, double2
     if (tid == 0) {
       atomicMax(&p.ctr->max_list, (ull)max(NLk, NRk));
     }
+    PHASE(sh, 3);
     // ---- column pairs (a at ks, b at ks+1): all pairs' scaling tables, then warp tiles
     {
       // reuse build_segments with kd = ks+1 (b), kn = ks (a), left = true: offsets unused
@@ -719,6 +780,7 @@ __device__ void process_stack(const CallParams &p, Block &b, Shared &sh, double2
         }
         __syncthreads();
         const uint32_t ntiles = block_scan(sh, b.tmp, b.tmp2, ne);  // tile offsets per pair
+        PHASE(sh, 4);
         // every warp takes every (kThreads/32)-th tile: a static, deterministic assignment
         const int warp = tid >> 5, lane = tid & 31;
         double2 *sW = sY + warp * kYT;
@@ -770,7 +832,9 @@ __device__ void process_stack(const CallParams &p, Block &b, Shared &sh, double2
           npaths += (ull)nv * len;
           __syncwarp();
         }
+        PHASE(sh, 5);
         __syncthreads();
+        PHASE(sh, 6);
       }
     }
   }
@@ -945,7 +1009,7 @@ __global__ void lofp_thr_kernel(const __grid_constant__ CallParams p, int grid) 
   if (threadIdx.x == 0) {
     ull tot = 0;
     for (int i = 0; i < kThreads; ++i) tot = sat_add(tot, part[i]);
-    ull t = tot / (ull)(8 * grid);
+    ull t = tot / (ull)(p.units_per_block * grid);
     p.ctr->thr = t > p.thr ? t : p.thr;
   }
 }
@@ -1088,6 +1152,10 @@ __global__ void __launch_bounds__(kThreads, 2) lofp_units_kernel(const __grid_co
   load_cols(p, sh);
   const int tid = threadIdx.x;
   ull cm = 0, nelem = 0;
+  if (tid == 0) {
+    for (int i = 0; i < 8; ++i) sh.ph[i] = 0;
+    sh.tph = clock64();
+  }
   while (true) {
     if (tid == 0) sh.unit = (int)atomicAdd(&p.ctr->ticket, 1ull);
     __syncthreads();
@@ -1139,6 +1207,9 @@ __global__ void __launch_bounds__(kThreads, 2) lofp_units_kernel(const __grid_co
     }
   }
   // statistics
+  PHASE(sh, 0);
+  if (tid == 0)
+    for (int i = 0; i < 8; ++i) atomicAdd(&p.ctr->phase[i], sh.ph[i]);
   for (int d = 16; d > 0; d >>= 1) {
     cm += __shfl_down_sync(0xffffffffu, cm, d);
     nelem += __shfl_down_sync(0xffffffffu, nelem, d);

@@ -33,6 +33,7 @@ class lofp_run_stats(ctypes.Structure):
                 ("pairs", ctypes.c_int64), ("elements", ctypes.c_int64), ("unsupported", ctypes.c_int64),
                 ("bad_rows", ctypes.c_int64), ("check_errors", ctypes.c_int64), ("max_states", ctypes.c_int64),
                 ("max_list", ctypes.c_int64), ("table_entries", ctypes.c_int64), ("terms", ctypes.c_int64),
+                ("phase_cycles", ctypes.c_int64 * 8),
                 ("grid_blocks", ctypes.c_int32), ("block_threads", ctypes.c_int32),
                 ("launches", ctypes.c_int32), ("mode", ctypes.c_int32),
                 ("units_ms", ctypes.c_float), ("total_ms", ctypes.c_float)]
@@ -241,5 +242,6 @@ class Circuit:
         if rc not in (LOFP_OK, LOFP_E_BAD_OUTPUT):
             self._check(rc)
         d = {k: getattr(st, k) for k, _ in lofp_run_stats._fields_}
+        d["phase_cycles"] = list(st.phase_cycles)
         d["status"] = rc
         return d
