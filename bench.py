@@ -49,6 +49,9 @@ def parse():
                    help="configs[4] hero sample: its 8 largest uncapped outputs (2.2e11-2.5e11 paths each)")
     p.add_argument("--literal", action="store_true",
                    help="configs[4] literal batch (reachable outputs only: 12,548 outputs, 4.9e13 paths)")
+    p.add_argument("--contract", action="store_true",
+                   help="time lofp_amplitudes_contract (strip tensor contraction, NEXT-1) instead of the path "
+                        "sum; metric amplitudes/s (default workload then: configs[3] as literally drawn)")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-paths", type=float, default=3e7, help="paths in the cpu_baseline sample")
@@ -177,7 +180,7 @@ def reference_arm(args, rank, world):
     line = {
         "impl": "reference", "metric": "paths/s", "value": v, "unit": "paths/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64 (long double accumulate)",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 (long double accumulate)",
         "data": "synthetic", "config": {"workload": f"configs[{args.config}] {kind} batch (oracle sample)",
                                         "sample_outputs": int(len(sel))},
         "amplitudes_per_s": len(sel) * args.steps / tot_s,
@@ -187,6 +190,108 @@ def reference_arm(args, rank, world):
         "e2e": {"value": v, "unit": "paths/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def ncu_traffic(args):
+    """DRAM bytes (read + write) per launch of the unit kernel from the committed ncu --set
+    full capture of the same workload (profiles/r2_ncu_units_cfg<i>.txt), else None."""
+    if args.hero or args.literal or args.outputs:
+        return None
+    path = os.path.join(ROOT, "profiles", f"r2_ncu_units_cfg{args.config}.txt")
+    if not os.path.exists(path):
+        return None
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    tot = 0.0
+    for line in open(path):
+        parts = line.split()
+        if parts and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum") and len(parts) >= 3:
+            tot += float(parts[1]) * scale.get(parts[2], 1)
+    return {"bytes_per_launch": tot, "source": os.path.relpath(path, ROOT)} if tot else None
+
+
+def contract_arm(args, rank, world, local):
+    """--contract: amplitudes/s of the strip tensor contraction on configs[3] as
+    BASELINE.json draws it (2048 outputs, 2.5e18 paths: beyond any enumerator)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2510_26408_b200 import Circuit
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    idx = args.config if args.config != 4 else 3
+    import lofp_inputs as li
+    c = li.config(idx)
+    d = np.load(os.path.join(DATA, f"cfg{idx}.npz"))
+    T, P = d["T_literal"].astype(np.int32), d["P_literal"].astype(np.uint64)
+    if args.outputs:
+        T, P = T[:args.outputs], P[:args.outputs]
+    B = len(T)
+    circ = Circuit(c.M, c.layers)
+    Td = torch.from_numpy(np.ascontiguousarray(T)).to(dev)
+    out = torch.empty((B, 2), dtype=torch.float64, device=dev)
+    counts = torch.zeros(B, dtype=torch.int64, device=dev)
+    circ.contract(c.S, Td, out=out, counts=counts)
+    torch.cuda.synchronize()
+    vst = circ.stats()
+    if not np.array_equal(counts.cpu().numpy().astype(np.uint64), P) or vst["unsupported"] or vst["check_errors"]:
+        raise SystemExit("contraction path counts differ from the oracle's")
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        circ.contract(c.S, Td, out=out)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    clocks.start()
+    ms = []
+    for _ in range(args.steps):
+        flush.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        circ.contract(c.S, Td, out=out)
+        e1.record(stream)
+        e1.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    clk = clocks.stop()
+    t_max, paths_all, outs_all = aggregate(float(np.sum(ms)), float(P.astype(np.float64).sum()), float(B), world,
+                                           dist, dev)
+    value = outs_all * args.steps / (t_max * 1e-3)
+    Th = torch.from_numpy(np.ascontiguousarray(T)).pin_memory()
+    e2e = None
+    if not args.no_e2e:
+        # end to end: H2D of T and D2H of the amplitudes inside the timed region
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            Tg = Th.to(dev, non_blocking=True)
+            a = circ.contract(c.S, Tg, out=out)
+            a.cpu()
+        dt = time.perf_counter() - t0
+        e2e = {"value": B * args.steps / dt, "unit": "amplitudes/s", "h2d_bytes_per_step": int(T.nbytes),
+               "d2h_bytes_per_step": int(B * 16)}
+    if rank == 0:
+        st = circ.stats()
+        terms = int(st["terms"])
+        line = {
+            "metric": "amplitudes/s", "value": value, "unit": "amplitudes/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"configs[{idx}] literal batch by the strip tensor contraction (NEXT-1): "
+                                   f"M={c.M} N={c.N} D={c.D}, {B} outputs, {float(P.astype(np.float64).sum()):.3e} "
+                                   f"paths (not enumerated)", "global_batch": int(outs_all),
+                       "l2": "flushed between steps (256 MiB write)"},
+            "paths_equivalent_per_s": paths_all * args.steps / (t_max * 1e-3),
+            "roofline": {"bound": "alu", "note": "integer index arithmetic and Appendix-A table gathers "
+                                                 "(L1/L2 resident); FP64 work per step below",
+                         "terms": terms, "cmuls": int(st["cmuls"]),
+                         "fp64_lane_inst": 4 * terms + 4 * int(st["cmuls"]), "kernel_ms": float(np.mean(ms))},
+            "e2e": e2e, "gpu_launches": int(st["launches"]) * args.steps, "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def main():
@@ -208,6 +313,9 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
+    if args.contract:
+        contract_arm(args, rank, world, local)
+        return
     c, T, P, kind = workload(args.config, args.outputs, args.hero, args.literal)
     circ = Circuit(c.M, c.layers)
     Td = torch.from_numpy(np.ascontiguousarray(T)).to(dev)
@@ -291,7 +399,7 @@ def main():
     alg = 4.0 * paths + 4.0 * cmuls
     achieved = alg / (umean * 1e-3) / 1e12
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak_meas, "unit": "TFP64-inst/s",
-                "frac": achieved / peak_meas if peak_meas > 0 else None, "traffic": None,
+                "frac": achieved / peak_meas if peak_meas > 0 else None, "traffic": ncu_traffic(args),
                 "peak_source": f"measured DFMA issue rate (fp64_peak.cu, {nsm.value} SMs, burst); "
                                f"MEASURED_PEAKS.json has no FP64 entry",
                 "nominal_peak": 148 * 64 * 1965e6 / 1e12,

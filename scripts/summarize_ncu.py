@@ -1,27 +1,55 @@
-"""Summarise one ncu --set full capture (.ncu-rep) of the enumeration kernel: headline
-metrics, warp-stall split, SASS opcode mix; optional per-instruction hot list (argv[2])."""
-import csv, sys, subprocess
-rep=sys.argv[1]
-raw=subprocess.run(['ncu','-i',rep,'--page','raw','--csv'],capture_output=True,text=True).stdout.splitlines()
-r=list(csv.reader(raw)); hdr=r[0]; vals=r[2]; d=dict(zip(hdr,vals))
-for k in ['gpu__time_duration.sum','sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active','sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active','sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active','l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed','smsp__thread_inst_executed_per_inst_executed.ratio','smsp__inst_executed.sum','sm__warps_active.avg.pct_of_peak_sustained_active','smsp__issue_active.avg.pct_of_peak_sustained_active','l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum','launch__registers_per_thread']:
-    print(f"{k:75s} {d.get(k)}")
-stalls=[(h,v) for h,v in d.items() if 'smsp__pcsamp_warps_issue_stalled' in h and not h.endswith('not_issued')]
-tot=sum(float(v) for h,v in stalls if v)
-print(' '.join(f"{h[33:]}={float(v)/tot*100:.1f}%" for h,v in sorted(stalls,key=lambda x:-float(x[1] or 0))[:8]))
-src=subprocess.run(['ncu','-i',rep,'--page','source','--csv','--print-source','sass'],capture_output=True,text=True).stdout.splitlines()
-r=list(csv.reader(src)); hdr=r[1]; rows=r[2:]
-iS=hdr.index("Source"); iE=hdr.index("Instructions Executed"); iA=hdr.index("Address"); iT=hdr.index("Avg. Threads Executed"); iSt=hdr.index("Warp Stall Sampling (All Samples)")
-from collections import Counter
-c=Counter(); tot=0
+"""Summarise one ncu --set full capture (.ncu-rep): headline metrics, warp-stall split,
+SASS opcode mix and (for lofp_units_kernel / lofp_contract_kernel) the per-function split.
+
+usage: python scripts/summarize_ncu.py <report.ncu-rep> [kernel-name]
+"""
+import collections
+import csv
+import subprocess
+import sys
+
+rep = sys.argv[1]
+kernel = sys.argv[2] if len(sys.argv) > 2 else "lofp_units_kernel"
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout.splitlines()
+r = list(csv.reader(raw))
+d = dict(zip(r[0], r[2]))
+units = dict(zip(r[0], r[1]))
+print(f"report: {rep}")
+print(f"kernel: {d.get('Kernel Name')}  grid {d.get('launch__grid_size')} x block {d.get('launch__block_size')}")
+for k in ["gpu__time_duration.sum", "sm__cycles_elapsed.avg.per_second",
+          "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+          "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+          "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
+          "launch__registers_per_thread", "launch__occupancy_limit_registers",
+          "smsp__thread_inst_executed_per_inst_executed.ratio", "smsp__inst_executed.sum",
+          "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+          "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "l1tex__t_sector_hit_rate.pct",
+          "lts__t_sector_hit_rate.pct", "dram__bytes_read.sum", "dram__bytes_write.sum",
+          "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"]:
+    if k in d:
+        print(f"  {k:78s} {d[k]} {units.get(k, '')}")
+dfma = d.get("smsp__sass_thread_inst_executed_op_dfma_pred_on.sum.per_cycle_elapsed")
+cyc = d.get("sm__cycles_elapsed.avg")
+if dfma and cyc:
+    print(f"  DFMA lane-ops per launch (derived)                                             "
+          f"{float(dfma) * float(cyc):.4e}")
+st = [(k, float(v)) for k, v in d.items() if k.startswith("smsp__pcsamp_warps_issue_stalled") and
+      not k.endswith("not_issued") and v]
+tot = sum(v for _, v in st) or 1
+print("  stalls: " + ", ".join(f"{k[33:]} {100 * v / tot:.1f}%" for k, v in sorted(st, key=lambda x: -x[1])[:8]))
+src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True,
+                     text=True).stdout.splitlines()
+rr = list(csv.reader(src))
+hdr, rows = rr[1], rr[2:]
+iS, iE = hdr.index("Source"), hdr.index("Instructions Executed")
+c = collections.Counter()
+te = 0
 for x in rows:
-    e=int(x[iE]); op=x[iS].strip().split()
-    if not op: continue
-    o=op[1] if op[0].startswith('@') else op[0]
-    c[o.split('.')[0]]+=e; tot+=e
-print([(k,round(v/tot*100,1)) for k,v in c.most_common(24)])
-if len(sys.argv)>2:
-    stot=sum(int(x[iSt]) for x in rows)
-    with open(sys.argv[2],'w') as f:
-        for x in rows:
-            f.write(f"{x[iA][-5:]} {int(x[iE])/tot*1000:7.3f} st{int(x[iSt])/stot*1000:6.2f} thr{float(x[iT]):5.1f}  {x[iS].strip()[:100]}\n")
+    e = int(x[iE] or 0)
+    op = x[iS].strip().split()
+    if not op:
+        continue
+    o = (op[1] if op[0].startswith("@") else op[0]).split(".")[0]
+    c[o] += e
+    te += e
+print("  opcode mix: " + ", ".join(f"{k} {100 * v / te:.1f}%" for k, v in c.most_common(14)))
