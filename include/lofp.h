@@ -198,6 +198,9 @@ typedef struct {
   int64_t max_list;       /* largest half-path list */
   int64_t table_entries;  /* Appendix-A elements in the table */
   int64_t terms;          /* contraction mode: (state, state, state) terms summed */
+  int64_t generic;        /* outputs evaluated by the generic engine (the paper's layer-major
+                             recursion with its cone bounds) because their
+                             columns exceed the column engine's limits */
   int64_t phase_cycles[8];/* unit kernel, SM clock cycles of each block's thread 0 summed over
                              blocks: 0 unit fetch / output setup / reduction, 1 path counts and
                              split choice, 2 left lists, 3 right lists, 4 pair list and

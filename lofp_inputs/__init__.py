@@ -70,6 +70,24 @@ def random_nn_circuit(M: int, D: int, rng, fill: float = 1.0, reverse_prob: floa
     return layers
 
 
+def random_nonlocal_circuit(M: int, D: int, rng, fill: float = 0.8, reverse_prob: float = 0.3):
+    """Random circuit with non-local pairs (test inputs for NEXT-4, "non-local
+    connections"): each layer pairs a random subset of the modes with each other, any
+    distance apart (disjoint pairs, crossings allowed)."""
+    layers = []
+    for _ in range(D):
+        modes = list(rng.permutation(M))
+        layer = []
+        while len(modes) >= 2:
+            a, b = int(modes.pop()), int(modes.pop())
+            if rng.random() < fill:
+                if rng.random() < reverse_prob:
+                    a, b = b, a
+                layer.append((a, b, float(rng.uniform(0, math.pi / 2)), float(rng.uniform(0, 2 * math.pi))))
+        layers.append(layer)
+    return layers
+
+
 def all_outputs(M: int, N: int) -> np.ndarray:
     """All occupation patterns of N photons in M modes, lexicographically descending."""
     rows = []

@@ -65,8 +65,15 @@ struct HostPinned {
 // A beam splitter after canonicalisation: port 1 = mode cut-1, port 2 = mode cut.
 struct CanonBS {
   int layer;  // 1-based
-  int cut;    // k = max(mode_a, mode_b)
+  int cut;    // k = max(mode_a, mode_b): the upper mode
+  int lo;     // min(mode_a, mode_b): the lower mode (port 1 after canonicalisation)
   double theta, phi;
+};
+
+struct Mask {  // a set of modes (M <= 128)
+  uint64_t w[2] = {0, 0};
+  void set(int m) { w[m >> 6] |= 1ull << (m & 63); }
+  bool has(int m) const { return (w[m >> 6] >> (m & 63)) & 1ull; }
 };
 
 long long env_ll(const char *name, long long dflt) {
@@ -90,11 +97,17 @@ struct lofp_ctx {
   std::vector<FacInfo> fac;
   std::vector<GateInfo> gat;
   std::vector<BSInfo> bsi;
+  std::vector<EqCon> eqc;
+  std::vector<BoundInfo> bnd;
+  bool general = false;  // non-local pairs (NEXT-4)
+  std::vector<SeqBS> seq;      // generic engine: layer-major BS order
+  std::vector<uint64_t> cone;  // generic engine: past / future cone masks per waveguide
+  int seq_gl0 = 0;
   std::vector<double> gate_ab;
   std::vector<int16_t> gate_mode, gate_after;
   DevBuf d_topo;
   size_t off_col = 0, off_seg = 0, off_cmp = 0, off_fac = 0, off_gat = 0, off_bsi = 0, off_gab = 0, off_gm = 0,
-         off_gl = 0;
+         off_gl = 0, off_eqc = 0, off_bnd = 0, off_seq = 0, off_cone = 0;
   // per-call device buffers
   DevBuf d_table, d_taboff, d_gatetab, d_units, d_sched, d_nunits, d_ubase, d_status, d_pexp, d_pdone, d_partial, d_slab,
       d_ctr, d_hostT, d_hostA;
@@ -200,6 +213,7 @@ lofp_status build_topology(lofp_ctx *ctx, const std::vector<lofp_gate> &gates) {
     if (ctx->seg.size() + nseg > 8192 || nseg > 255) return LOFP_E_UNSUPPORTED;
     ci.seg_base = (uint16_t)ctx->seg.size();
     ci.nseg = (uint8_t)nseg;
+    ci.nvar = (uint8_t)nseg;
     for (int i = 0; i < nseg; ++i) {
       const int t0 = i == 0 ? 0 : al[k][i - 1];
       SegInfo si;
@@ -271,6 +285,349 @@ lofp_status build_topology(lofp_ctx *ctx, const std::vector<lofp_gate> &gates) {
   return LOFP_OK;
 }
 
+// Column topology of a circuit with non-local pairs (NEXT-4, reading R21).  A BS
+// on modes (a, b) changes F(k) for every cut k in (a, b] by y1 - x1; columns in its span get
+// a segment break.  A BS whose span covers more than one cut, or whose cut another BS of the
+// same layer also spans, is "carried": its (x1, y1) are state variables of the columns
+// a+1..b, defined from columns (a, a+1), passed on unchanged, and consumed at cut b by its
+// factor and by the conservation check of mode b.  Idle modes inside a span keep their
+// occupation.  All checks are between adjacent columns (EqCon), so the column machinery
+// (counts, lists, contraction) is unchanged.  The light-cone bounds become sums over mode
+// sets (P:153-164 cones of a set of modes).
+lofp_status build_topology_general(lofp_ctx *ctx, const std::vector<lofp_gate> &gates) {
+  const int M = ctx->M, D = ctx->D, W = M + 1, nb = ctx->nbs;
+  std::vector<std::vector<int>> layer_bs(D + 1);
+  std::vector<int> owner((size_t)(D + 1) * std::max(M, 1), -1);
+  std::vector<int> nspan((size_t)(D + 1) * W, 0);
+  for (int i = 0; i < nb; ++i) {
+    const CanonBS &b = ctx->bs[i];
+    layer_bs[b.layer].push_back(i);
+    owner[(size_t)b.layer * M + b.lo] = i;
+    owner[(size_t)b.layer * M + b.cut] = i;
+    for (int k = b.lo + 1; k <= b.cut; ++k) nspan[(size_t)b.layer * W + k]++;
+  }
+  auto spanned = [&](int l, int k) { return nspan[(size_t)l * W + k] > 0; };
+  std::vector<char> carried(nb, 0);
+  for (int i = 0; i < nb; ++i) {
+    const CanonBS &b = ctx->bs[i];
+    carried[i] = (b.cut - b.lo > 1) || nspan[(size_t)b.layer * W + b.cut] > 1;
+  }
+  std::vector<std::vector<int>> al(W), segof(W);
+  for (int k = 0; k <= M; ++k) {
+    for (int l = 1; l <= D; ++l)
+      if (spanned(l, k)) al[k].push_back(l);
+    segof[k].assign(D + 1, 0);
+    int s = 0;
+    for (int t = 0; t <= D; ++t) {
+      if (s < (int)al[k].size() && al[k][s] == t) ++s;
+      segof[k][t] = s;
+    }
+  }
+  auto past = [&](int t, Mask X) {  // input modes that can reach X by time t
+    for (int l = t; l >= 1; --l)
+      for (int i : layer_bs[l]) {
+        const CanonBS &b = ctx->bs[i];
+        if (X.has(b.lo) || X.has(b.cut)) {
+          X.set(b.lo);
+          X.set(b.cut);
+        }
+      }
+    return X;
+  };
+  auto fut = [&](int t, Mask X) {  // output modes reachable from X after time t
+    for (int l = t + 1; l <= D; ++l)
+      for (int i : layer_bs[l]) {
+        const CanonBS &b = ctx->bs[i];
+        if (X.has(b.lo) || X.has(b.cut)) {
+          X.set(b.lo);
+          X.set(b.cut);
+        }
+      }
+    return X;
+  };
+  Mask all;
+  for (int m = 0; m < M; ++m) all.set(m);
+  auto range_mask = [&](int a, int e) {
+    Mask X;
+    for (int m = a; m < e; ++m) X.set(m);
+    return X;
+  };
+  auto bound = [&](Mask m0, Mask m1, Mask m2, Mask m3) {
+    BoundInfo bi{};
+    const Mask ms[4] = {m0, m1, m2, m3};
+    for (int w = 0; w < 4; ++w)
+      for (int h = 0; h < 2; ++h) bi.m[w][h] = ms[w].w[h];
+    return bi;
+  };
+  // variables: the segments of each column, then (x1, y1) of every carried BS spanning it
+  std::vector<std::vector<int>> cvar(nb);  // cvar[i][k - lo - 1] = x1's variable index in column k
+  std::vector<int> nvar(W, 0);
+  for (int k = 0; k <= M; ++k) nvar[k] = (int)al[k].size() + 1;
+  for (int i = 0; i < nb; ++i) {
+    if (!carried[i]) continue;
+    const CanonBS &b = ctx->bs[i];
+    for (int k = b.lo + 1; k <= b.cut; ++k) {
+      cvar[i].push_back(nvar[k]);
+      nvar[k] += 2;
+    }
+  }
+  ctx->col.assign(W, ColInfo{});
+  ctx->seg.clear();
+  ctx->bnd.clear();
+  ctx->cmp.clear();
+  ctx->eqc.clear();
+  ctx->fac.clear();
+  ctx->gat.clear();
+  std::vector<std::vector<GateInfo>> gates_of(W);
+  for (size_t g = 0; g < gates.size(); ++g) {
+    const int m = gates[g].mode, j = gates[g].after_layer;
+    if (M == 1) continue;
+    const int c = (m + 1 <= M - 1) ? m + 1 : m;
+    GateInfo gi{};
+    gi.gate = (int32_t)g;
+    gi.col_off = (uint8_t)(m - (c - 1));
+    gi.seg_lo = (uint8_t)segof[m][j];
+    gi.seg_hi = (uint8_t)segof[m + 1][j];
+    gates_of[c].push_back(gi);
+  }
+  for (int k = 0; k <= M; ++k) {
+    ColInfo &ci = ctx->col[k];
+    const int nseg = (int)al[k].size() + 1;
+    if (ctx->seg.size() + nvar[k] > 8192 || nvar[k] > 127) return LOFP_E_UNSUPPORTED;
+    ci.seg_base = (uint16_t)ctx->seg.size();
+    ci.nseg = (uint8_t)nseg;
+    ci.nvar = (uint8_t)nvar[k];
+    for (int i = 0; i < nseg; ++i) {
+      const int t0 = i == 0 ? 0 : al[k][i - 1];
+      const Mask lo = range_mask(0, k), hi = range_mask(k, M);
+      ctx->seg.push_back(SegInfo{});
+      ctx->bnd.push_back(bound(past(t0, lo), past(t0, hi), fut(t0, lo), fut(t0, hi)));
+    }
+    std::vector<BoundInfo> extra(nvar[k] - nseg);
+    for (int i = 0; i < nb; ++i) {
+      if (!carried[i]) continue;
+      const CanonBS &b = ctx->bs[i];
+      if (k <= b.lo || k > b.cut) continue;
+      Mask a;
+      a.set(b.lo);
+      const int v = cvar[i][k - b.lo - 1] - nseg;
+      extra[v] = bound(past(b.layer - 1, a), all, fut(b.layer - 1, a), all);      // x1: mode a before
+      extra[v + 1] = bound(past(b.layer, a), all, fut(b.layer, a), all);          // y1: mode a after
+    }
+    for (const BoundInfo &e : extra) {
+      ctx->seg.push_back(SegInfo{});
+      ctx->bnd.push_back(e);
+    }
+    // F_t(k-1) <= F_t(k) at every time
+    ci.cmp_base = (uint16_t)ctx->cmp.size();
+    int ncmp = 0;
+    if (k >= 1) {
+      int la = -1, lb = -1;
+      for (int t = 0; t <= D; ++t) {
+        const int sa = segof[k - 1][t], sb = segof[k][t];
+        if (sa == la && sb == lb) continue;
+        ctx->cmp.push_back(CmpPair{(uint8_t)sa, (uint8_t)sb});
+        la = sa;
+        lb = sb;
+        ++ncmp;
+      }
+    }
+    if (ncmp > 255 || ctx->cmp.size() > 65535) return LOFP_E_UNSUPPORTED;
+    ci.ncmp = (uint8_t)ncmp;
+    // equalities between columns k-1 and k (mode m = k-1 and the carried variables)
+    int neq = 0;
+    auto add_eq = [&](std::vector<std::pair<int, int>> terms) {  // (coef, side<<7 | var)
+      std::vector<std::pair<int, int>> merged;
+      for (auto &t : terms) {
+        bool found = false;
+        for (auto &u : merged)
+          if (u.second == t.second) {
+            u.first += t.first;
+            found = true;
+          }
+        if (!found) merged.push_back(t);
+      }
+      EqCon e{};
+      int n = 0;
+      for (auto &u : merged)
+        if (u.first != 0 && n < 11) {
+          e.coef[n] = (int8_t)u.first;
+          e.var[n] = (uint8_t)u.second;
+          ++n;
+        }
+      if (n == 0) return;
+      e.nterm = (uint8_t)n;
+      ctx->eqc.push_back(e);
+      ++neq;
+    };
+    // inside column k: at every layer whose spanning BSs are carried, the jump of F(k) is
+    // the sum of their y1 - x1 (photon conservation of the BSs crossing cut k)
+    ci.intra_base = (uint16_t)ctx->eqc.size();
+    int nintra = 0;
+    for (int l = 1; l <= D; ++l) {
+      if (!spanned(l, k)) continue;
+      std::vector<std::pair<int, int>> terms{{1, 0x80 | segof[k][l]}, {-1, 0x80 | segof[k][l - 1]}};
+      bool any_carried = false;
+      for (int i : layer_bs[l]) {
+        const CanonBS &b = ctx->bs[i];
+        if (k <= b.lo || k > b.cut || !carried[i]) continue;
+        any_carried = true;
+        const int xv = 0x80 | cvar[i][k - b.lo - 1];
+        terms.push_back({-1, xv + 1});
+        terms.push_back({1, xv});
+      }
+      if (!any_carried) continue;
+      if (terms.size() > 11) return LOFP_E_UNSUPPORTED;
+      const size_t before = ctx->eqc.size();
+      const int save = neq;
+      add_eq(terms);
+      if (ctx->eqc.size() > before) ++nintra;
+      neq = save;
+    }
+    ci.nintra = (uint8_t)nintra;
+    ci.eq_base = (uint16_t)ctx->eqc.size();
+    neq = 0;
+    if (k >= 1) {
+      const int m = k - 1;
+      for (int l = 1; l <= D; ++l) {
+        const int a0 = segof[k - 1][l - 1], a1 = segof[k - 1][l];
+        const int b0 = 0x80 | segof[k][l - 1], b1 = 0x80 | segof[k][l];
+        const int o = owner[(size_t)l * M + m];
+        if (o < 0) {  // idle mode: its occupation is unchanged
+          if (spanned(l, k)) add_eq({{1, b1}, {-1, b0}, {-1, a1}, {1, a0}});
+        } else if (carried[o]) {
+          const CanonBS &b = ctx->bs[o];
+          if (b.lo == m) {  // x1 = n_m before, y1 = n_m after
+            const int xv = 0x80 | cvar[o][0];
+            add_eq({{1, xv}, {-1, b0}, {1, a0}});
+            add_eq({{1, xv + 1}, {-1, b1}, {1, a1}});
+          } else {  // upper mode: n_m changes by -(y1 - x1)
+            const int xv = cvar[o][b.cut - b.lo - 1];
+            add_eq({{1, b1}, {-1, a1}, {-1, b0}, {1, a0}, {1, xv + 1}, {-1, xv}});
+          }
+        }
+      }
+      for (int i = 0; i < nb; ++i) {  // carried variables pass through the span unchanged
+        if (!carried[i]) continue;
+        const CanonBS &b = ctx->bs[i];
+        if (k - 1 > b.lo && k <= b.cut) {
+          const int xa = cvar[i][k - 1 - b.lo - 1], xb = 0x80 | cvar[i][k - b.lo - 1];
+          add_eq({{1, xa}, {-1, xb}});
+          add_eq({{1, xa + 1}, {-1, xb + 1}});
+        }
+      }
+    }
+    if (neq > 255 || ctx->eqc.size() > 65535) return LOFP_E_UNSUPPORTED;
+    ci.neq = (uint8_t)neq;
+    // factors carried by cut k: NN BS on (k-1, k), carried BS ending at mode k
+    ci.fac_base = (uint16_t)ctx->fac.size();
+    int nfac = 0;
+    if (k >= 1 && k <= M - 1) {
+      for (int i = 0; i < nb; ++i) {
+        const CanonBS &b = ctx->bs[i];
+        if (b.cut != k) continue;
+        const int l = b.layer;
+        FacInfo fi{};
+        fi.bs = i;
+        fi.sC = (uint8_t)segof[k + 1][l - 1];
+        if (!carried[i]) {
+          fi.kind = 0;
+          fi.sA = (uint8_t)segof[k - 1][l - 1];
+          fi.i = (uint8_t)segof[k][l - 1];
+        } else {
+          const int xv = cvar[i][k - b.lo - 1];
+          fi.kind = 1;
+          fi.i = (uint8_t)xv;
+          fi.sA = (uint8_t)(xv + 1);
+          fi.sB = (uint8_t)segof[k][l - 1];
+        }
+        ctx->fac.push_back(fi);
+        ++nfac;
+      }
+    }
+    if (nfac > 255 || ctx->fac.size() > 65535) return LOFP_E_UNSUPPORTED;
+    ci.nfac = (uint8_t)nfac;
+    ci.gate_base = (uint16_t)ctx->gat.size();
+    if (gates_of[k].size() > 255 || ctx->gat.size() + gates_of[k].size() > 65535) return LOFP_E_UNSUPPORTED;
+    ci.ngate = (uint8_t)gates_of[k].size();
+    for (const GateInfo &g : gates_of[k]) ctx->gat.push_back(g);
+  }
+  ctx->bsi.assign(std::max(nb, 1), BSInfo{});
+  for (int i = 0; i < nb; ++i) {
+    const CanonBS &b = ctx->bs[i];
+    BSInfo &bi = ctx->bsi[i];
+    bi.c = std::cos(b.theta);
+    bi.s = std::sin(b.theta);
+    bi.phi = b.phi;
+    Mask ab;
+    ab.set(b.lo);
+    ab.set(b.cut);
+    const Mask pc = past(b.layer - 1, ab);
+    bi.capmask[0] = pc.w[0];
+    bi.capmask[1] = pc.w[1];
+  }
+  ctx->ngate = (int)gates.size();
+  ctx->gate_ab.assign(2 * std::max<size_t>(gates.size(), 1), 0.0);
+  ctx->gate_mode.assign(std::max<size_t>(gates.size(), 1), 0);
+  ctx->gate_after.assign(std::max<size_t>(gates.size(), 1), 0);
+  for (size_t g = 0; g < gates.size(); ++g) {
+    ctx->gate_ab[2 * g] = gates[g].a;
+    ctx->gate_ab[2 * g + 1] = gates[g].b;
+    ctx->gate_mode[g] = (int16_t)gates[g].mode;
+    ctx->gate_after[g] = (int16_t)gates[g].after_layer;
+  }
+  return LOFP_OK;
+}
+
+// Tables of the generic engine (the paper's layer-major recursion, with the
+// per-waveguide light-cone bounds of P:164): the BS order, the layers whose gates follow
+// each BS, and the past / future cone of every waveguide (mode m after layer t).
+void build_generic(lofp_ctx *ctx) {
+  const int M = ctx->M, D = ctx->D, nb = ctx->nbs;
+  ctx->seq.clear();
+  for (int i = 0; i < nb; ++i) {
+    const CanonBS &b = ctx->bs[i];
+    SeqBS q{};
+    q.bs = i;
+    q.lo = (uint8_t)b.lo;
+    q.hi = (uint8_t)b.cut;
+    q.layer = (uint8_t)b.layer;
+    const bool last_of_layer = (i + 1 == nb) || ctx->bs[i + 1].layer != b.layer;
+    if (last_of_layer) {
+      q.gl0 = (uint8_t)b.layer;
+      q.gl1 = (uint8_t)((i + 1 == nb) ? D + 1 : ctx->bs[i + 1].layer);
+    }
+    ctx->seq.push_back(q);
+  }
+  ctx->seq_gl0 = nb > 0 ? ctx->bs[0].layer : D + 1;
+  ctx->cone.assign((size_t)(D + 1) * std::max(M, 1) * 4, 0);
+  std::vector<std::vector<int>> layer_bs(D + 1);
+  for (int i = 0; i < nb; ++i) layer_bs[ctx->bs[i].layer].push_back(i);
+  auto grow = [&](Mask X, int l) {
+    for (int i : layer_bs[l]) {
+      const CanonBS &b = ctx->bs[i];
+      if (X.has(b.lo) || X.has(b.cut)) {
+        X.set(b.lo);
+        X.set(b.cut);
+      }
+    }
+    return X;
+  };
+  for (int t = 0; t <= D; ++t)
+    for (int m = 0; m < M; ++m) {
+      Mask pa, fu;
+      pa.set(m);
+      fu.set(m);
+      for (int l = t; l >= 1; --l) pa = grow(pa, l);
+      for (int l = t + 1; l <= D; ++l) fu = grow(fu, l);
+      uint64_t *c = &ctx->cone[((size_t)t * M + m) * 4];
+      c[0] = pa.w[0];
+      c[1] = pa.w[1];
+      c[2] = fu.w[0];
+      c[3] = fu.w[1];
+    }
+}
+
 template <class T>
 size_t append(std::vector<char> &blob, const std::vector<T> &v) {
   size_t off = (blob.size() + 15) & ~size_t(15);
@@ -290,6 +647,10 @@ lofp_status upload_topology(lofp_ctx *ctx) {
   ctx->off_gab = append(blob, ctx->gate_ab);
   ctx->off_gm = append(blob, ctx->gate_mode);
   ctx->off_gl = append(blob, ctx->gate_after);
+  ctx->off_eqc = append(blob, ctx->eqc);
+  ctx->off_bnd = append(blob, ctx->bnd);
+  ctx->off_seq = append(blob, ctx->seq);
+  ctx->off_cone = append(blob, ctx->cone);
   CK(ctx->d_topo.ensure(blob.size()), "alloc topology");
   CK(cudaMemcpy(ctx->d_topo.p, blob.data(), blob.size(), cudaMemcpyHostToDevice), "upload topology");
   return LOFP_OK;
@@ -339,13 +700,11 @@ lofp_status create_impl(int32_t modes, int32_t n_layers, const int32_t *bs_per_l
         break;
       }
       used[b.mode_a] = used[b.mode_b] = 1;
-      if (std::abs(b.mode_a - b.mode_b) != 1) {
-        st = LOFP_E_UNSUPPORTED;
-        break;
-      }
+      if (std::abs(b.mode_a - b.mode_b) != 1) ctx->general = true;  // non-local pair (NEXT-4)
       CanonBS c;
       c.layer = l + 1;
       c.cut = std::max(b.mode_a, b.mode_b);
+      c.lo = std::min(b.mode_a, b.mode_b);
       c.theta = b.theta;
       // port swap: (b, a, theta, phi) == (a, b, theta, pi - phi) (reading R4)
       c.phi = b.mode_a < b.mode_b ? b.phi : kPi - b.phi;
@@ -354,7 +713,8 @@ lofp_status create_impl(int32_t modes, int32_t n_layers, const int32_t *bs_per_l
   }
   std::stable_sort(ctx->bs.begin(), ctx->bs.end(),
                    [](const CanonBS &x, const CanonBS &y) { return x.layer != y.layer ? x.layer < y.layer : x.cut < y.cut; });
-  if (st == LOFP_OK) st = build_topology(ctx, gv);
+  if (st == LOFP_OK) st = ctx->general ? build_topology_general(ctx, gv) : build_topology(ctx, gv);
+  if (st == LOFP_OK) build_generic(ctx);
   if (st != LOFP_OK) {
     delete ctx;
     return st;
@@ -416,12 +776,24 @@ lofp_status prepare(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, cons
   P.gate_ab = (const double *)(topo + ctx->off_gab);
   P.gate_mode = (const int16_t *)(topo + ctx->off_gm);
   P.gate_after = (const int16_t *)(topo + ctx->off_gl);
+  P.eqc = (const EqCon *)(topo + ctx->off_eqc);
+  P.bnd = (const BoundInfo *)(topo + ctx->off_bnd);
+  P.general = ctx->general ? 1 : 0;
+  P.seq = (const SeqBS *)(topo + ctx->off_seq);
+  P.cone = (const uint64_t *)(topo + ctx->off_cone);
+  P.seq_gl0 = ctx->seq_gl0;
   // Appendix-A table: per BS all (x1, x2, y1) with x1 + x2 <= its past-cone photon bound
   long long entries = 0;
   for (int i = 0; i < ctx->nbs; ++i) {
     const BSInfo &bi = ctx->bsi[i];
-    const int cap = std::min(N, (int)P.cumS[bi.cap_hi] - (int)P.cumS[bi.cap_lo]);
-    entries += tri_entries(cap);
+    int c = 0;
+    if (!ctx->general) {
+      c = (int)P.cumS[bi.cap_hi] - (int)P.cumS[bi.cap_lo];
+    } else {
+      for (int m = 0; m < ctx->M; ++m)
+        if ((bi.capmask[m >> 6] >> (m & 63)) & 1ull) c += input_occ[m];
+    }
+    entries += tri_entries(std::min(N, c));
   }
   ctx->table_entries = entries;
   CK(ctx->d_table.ensure((size_t)std::max(entries, 1ll) * 16), "alloc table");
@@ -439,6 +811,7 @@ lofp_status prepare(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, cons
   P.thr = (unsigned long long)env_ll("LOFP_UNIT_PATHS", 1ll << 24);
   P.slab_bytes = ctx->slab_bytes;
   P.units_per_block = (int)env_ll("LOFP_UNITS_PER_BLOCK", 2);
+  P.force_generic = env_ll("LOFP_FORCE_GENERIC", 0) > 0 ? 1 : 0;
   CK(ctx->d_units.ensure((size_t)(B * budget) * sizeof(Unit)), "alloc units");
   CK(ctx->d_partial.ensure((size_t)(B * budget) * 16), "alloc partials");
   CK(ctx->d_sched.ensure((size_t)(B * budget) * 4), "alloc schedule");
@@ -495,10 +868,10 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
     CK((cudaError_t)lofp_launch_paths(&P, ctx->grid, stream, ctx->timed ? ctx->ev_u0 : nullptr,
                                       ctx->timed ? ctx->ev_u1 : nullptr),
        "path-sum kernels");
-    launches += 6;
+    launches += 7;
   } else {
     CK((cudaError_t)lofp_launch_contract(&P, ctx->grid, stream), "contraction kernels");
-    launches += 1;
+    launches += 2;
   }
   if (!capturing) {  // statistics of calls replayed from a graph are not read back
     CK(cudaMemcpyAsync(ctx->h_ctr.p, P.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, stream), "read counters");
@@ -632,6 +1005,7 @@ lofp_status lofp_stats(lofp_ctx *ctx, lofp_run_stats *out) {
     st.max_states = (int64_t)hc->max_states;
     st.max_list = (int64_t)hc->max_list;
     st.terms = (int64_t)hc->contractions;
+    st.generic = (int64_t)hc->generic;
     for (int i = 0; i < 8; ++i) st.phase_cycles[i] = (int64_t)hc->phase[i];
     if (ctx->timed) {
       float ms = 0.f;

@@ -30,18 +30,47 @@ constexpr int kXT = 32 * kKX;      // X values per warp tile
 constexpr int kYT = 256;           // Y values per warp tile (staged in the warp's shared slice)
 constexpr int kCY = kYT * (kThreads / 32);  // shared memory: one Y slice per warp
 constexpr int kStackMax = 4096;    // sub-split stack entries per block
+constexpr int kMaxRawStates = 1 << 18;  // non-local circuits: raw variable product per column
 
 // ---- topology (lofp_create; constant per circuit) --------------------------------
 struct ColInfo {         // column k = 0..M
-  uint16_t seg_base;     // first SegInfo / segment slot of the column
+  uint16_t seg_base;     // first SegInfo / variable slot of the column
   uint8_t nseg;          // number of segments (1 + number of active layers of cut k)
   uint8_t ncmp;          // CmpPair checks against column k-1 (k >= 1)
   uint16_t cmp_base;
-  uint16_t fac_base;     // FacInfo of the BS on cut k (k = 1..M-1), in layer order
+  uint16_t fac_base;     // FacInfo of the BS whose factor cut k carries, in layer order
   uint8_t nfac;
   uint8_t ngate;         // phase gates folded into cut k's factor
   uint16_t gate_base;
+  uint8_t nvar;          // state variables: the nseg segments, then carried BS variables
+  uint8_t neq;           // EqCon checks against column k-1 (non-local circuits only)
+  uint16_t eq_base;
+  uint8_t nintra;        // EqCon checks inside column k (non-local circuits only)
+  uint8_t pad;
+  uint16_t intra_base;
 };
+
+// Non-local circuits (NEXT-4): a BS on modes (a, b), b > a + 1, shifts every cut in
+// (a, b]; its photon numbers (x1, y1) on mode a are carried as state variables through the
+// columns a+1..b, so that every constraint stays between adjacent columns (R21).
+struct EqCon {           // sum_t coef[t] * var[t] == 0 over variables of columns k-1 and k
+  int8_t coef[11];
+  uint8_t var[11];       // bit 7: column k (else k-1); bits 0..6: variable index
+  uint8_t nterm;
+  uint8_t pad;
+};
+
+struct SeqBS {           // generic engine: BS in layer-major order
+  int32_t bs;            // table block
+  uint8_t lo, hi;        // port-1 (lower) and port-2 modes
+  uint8_t layer;         // 1-based
+  uint8_t gl0, gl1;      // gates of layers gl0..gl1-1 apply after this BS (layer ends)
+  uint8_t pad[3];
+};
+
+struct BoundInfo {       // non-local circuits: light-cone bounds of a variable as mode sets
+  uint64_t m[4][2];      // hi <= sum S over m[0] and sum T over m[2];
+};                       // lo >= N - sum S over m[1] and N - sum T over m[3]
 
 struct SegInfo {         // light-cone box of a segment (readings R5, R15)
   uint8_t rho, sig;      // backward maps: F in [G(rho), G(sig)]
@@ -52,12 +81,16 @@ struct CmpPair {         // F(k-1) on segment sa <= F(k) on segment sb (one time
   uint8_t sa, sb;
 };
 
-struct FacInfo {         // the BS at cut c in its i-th active layer l
+struct FacInfo {         // a BS whose factor cut c carries (layer l)
   int32_t bs;            // canonical BS index (table block)
-  uint8_t sA;            // segment of column c-1 holding F_{l-1}(c-1)
-  uint8_t i;             // segments i (F_{l-1}(c)) and i+1 (F_l(c)) of column c
+  uint8_t sA;            // kind 0: segment of column c-1 holding F_{l-1}(c-1);
+                         // kind 1: variable of column c holding y1 (carried)
+  uint8_t i;             // kind 0: segments i (F_{l-1}(c)) and i+1 (F_l(c)) of column c;
+                         // kind 1: variable of column c holding x1 (carried)
   uint8_t sC;            // segment of column c+1 holding F_{l-1}(c+1)
-  uint8_t pad;
+  uint8_t kind;          // 0 nearest-neighbour BS on (c-1, c); 1 carried BS ending at mode c
+  uint8_t sB;            // kind 1: segment of column c holding F_{l-1}(c)
+  uint8_t pad[3];
 };
 
 struct GateInfo {        // gate on mode m after layer j, folded into cut c's factor
@@ -67,10 +100,11 @@ struct GateInfo {        // gate on mode m after layer j, folded into cut c's fa
   uint8_t pad;
 };
 
-struct BSInfo {          // canonical BS (port 1 = mode c-1), eq. bs_matrix
+struct BSInfo {          // canonical BS (port 1 = the lower mode), eq. bs_matrix
   double c, s, phi;      // cos theta, sin theta, phi (port swap applied, reading R4)
   uint8_t cap_lo, cap_hi;  // photons through it <= cumS(cap_hi) - cumS(cap_lo) (past cone)
   uint8_t pad[6];
+  uint64_t capmask[2];   // non-local circuits: photons through it <= sum S over this mode set
 };
 
 // ---- per-call data -----------------------------------------------------------------
@@ -101,6 +135,7 @@ struct Counters {        // device counters of one call (zeroed by the host)
   unsigned long long contractions; // contraction mode: column-pair states carried
   unsigned long long thr;        // unit size of the call (paths)
   unsigned long long phase[8];   // unit kernel, thread 0's SM clocks per phase
+  unsigned long long generic;    // outputs evaluated by the generic (layer-major) engine
 };
 
 enum : uint8_t { kStatusOk = 0, kStatusZero = 1, kStatusBad = 2, kStatusUnsupported = 3 };
@@ -119,6 +154,13 @@ struct CallParams {
   const FacInfo *fac;
   const GateInfo *gat;
   const BSInfo *bsi;
+  const EqCon *eqc;
+  const BoundInfo *bnd;      // [variables] non-local circuits only
+  int general;               // 1: non-local circuit (mask bounds, carried variables)
+  const SeqBS *seq;          // generic engine: the BS in layer-major order
+  const uint64_t *cone;      // generic engine: [D+1][M][2][2] past / future cone masks of (t, m)
+  int seq_gl0;               // gates of layers 0..seq_gl0-1 apply before the first BS
+  int force_generic;         // test hook (LOFP_FORCE_GENERIC): every output by the generic engine
   const double *gate_ab;     // [ngate][2] (a, b)
   const int16_t *gate_mode;  // [ngate] mode, for M == 1 (no cut to fold into)
   const int16_t *gate_after; // [ngate] layer
@@ -156,6 +198,7 @@ int lofp_launch_paths(const lofp::CallParams *p, int grid, void *stream, void *e
 int lofp_launch_contract(const lofp::CallParams *p, int grid, void *stream);
 int lofp_units_grid(int device);
 int lofp_launch_outputs(int M, int N, long long count, int32_t *T, void *stream);
+int lofp_launch_generic(const lofp::CallParams *p, int grid, void *stream);
 }
 
 #endif  // LOFP_INTERNAL_H

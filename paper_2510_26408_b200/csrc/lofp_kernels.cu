@@ -106,6 +106,7 @@ struct Shared {
   int G[kMaxModes + 1];
   int T[kMaxModes];
   int n[kMaxModes + 1];    // states per column
+  int raw[kMaxModes + 1];  // non-local circuits: raw combinations of a filtered column
   int vb[kMaxModes + 1];   // vals base
   int cb[kMaxModes + 1];   // count base
   ull NL[kMaxModes + 1], NR[kMaxModes + 1];
@@ -136,7 +137,7 @@ struct Shared {
 // slab carve of one output: vals, cL, cR, then the half-path lists (needs sh.n/vb/cb)
 __device__ __forceinline__ void carve(const CallParams &p, Block &b, const Shared &sh) {
   const int M = p.M;
-  const long long vb = sh.vb[M] + (long long)sh.n[M] * sh.col[M].nseg;
+  const long long vb = sh.vb[M] + (long long)sh.n[M] * sh.col[M].nvar;
   const long long cb = sh.cb[M] + sh.n[M];
   const long long vbytes = (vb + 15) & ~15ll;
   b.vals = (uint8_t *)(b.slab + kOffVar);
@@ -148,7 +149,7 @@ __device__ __forceinline__ void carve(const CallParams &p, Block &b, const Share
 }
 
 __device__ __forceinline__ const uint8_t *vrow(const Block &b, const Shared &sh, int k, int s) {
-  return b.vals + sh.vb[k] + s * sh.col[k].nseg;
+  return b.vals + sh.vb[k] + s * sh.col[k].nvar;
 }
 
 // F(k-1) <= F(k) at every time (non-negative occupations of mode k-1)
@@ -159,6 +160,15 @@ __device__ __forceinline__ bool compat(const CallParams &p, const Block &b, cons
   for (int c = 0; c < ck.ncmp; ++c) {
     const CmpPair pr = p.cmp[ck.cmp_base + c];
     if (va[pr.sa] > vb[pr.sb]) return false;
+  }
+  for (int e = 0; e < ck.neq; ++e) {  // non-local circuits: conservation / carried variables
+    const EqCon ec = p.eqc[ck.eq_base + e];
+    int sum = 0;
+    for (int t = 0; t < ec.nterm; ++t) {
+      const int v = (ec.var[t] & 0x80) ? vb[ec.var[t] & 0x7f] : va[ec.var[t] & 0x7f];
+      sum += ec.coef[t] * v;
+    }
+    if (sum != 0) return false;
   }
   return true;
 }
@@ -180,8 +190,18 @@ __device__ double2 cut_factor(const CallParams &p, const Block &b, const Shared 
   const uint8_t *vc = vrow(b, sh, c + 1, sc);
   for (int t = 0; t < cc.nfac; ++t) {
     const FacInfo fi = p.fac[cc.fac_base + t];
-    const int A = va[fi.sA], Bm = vb[fi.i], Bp = vb[fi.i + 1], C = vc[fi.sC];
-    const int x1 = Bm - A, x2 = C - Bm, y1 = Bp - A, n = x1 + x2;
+    int x1, x2, y1;
+    if (fi.kind == 0) {  // BS on (c-1, c): x1, x2 before it, y1 after it
+      const int A = va[fi.sA], Bm = vb[fi.i], Bp = vb[fi.i + 1], C = vc[fi.sC];
+      x1 = Bm - A;
+      x2 = C - Bm;
+      y1 = Bp - A;
+    } else {  // carried BS (a, c): x1, y1 of mode a carried in column c; x2 of mode c
+      x1 = vb[fi.i];
+      y1 = vb[fi.sA];
+      x2 = vc[fi.sC] - vb[fi.sB];
+    }
+    const int n = x1 + x2;
     if (n == 0) continue;
     const long long idx = p.tab_off[fi.bs] + tri_dev(n) + (long long)x1 * (n + 1) + y1;
     if (x1 < 0 || x2 < 0 || y1 < 0 || y1 > n || idx >= p.tab_off[fi.bs + 1]) {
@@ -271,6 +291,23 @@ __device__ __forceinline__ Block make_block(const CallParams &p) {
   return b;
 }
 
+// value of variable g (slot seg_base + i) in the raw mixed-radix combination r
+__device__ __forceinline__ int raw_val(const Block &b, int g, int r) {
+  return b.segLo[g] + (r / b.segStr[g]) % b.segRad[g];
+}
+
+// non-local circuits: the column's own equalities (the jump of F(k) at a layer equals the
+// summed y1 - x1 of the carried BS crossing cut k) for raw combination r
+__device__ bool intra_ok(const CallParams &p, const Block &b, const ColInfo &ci, int r) {
+  for (int e = 0; e < ci.nintra; ++e) {
+    const EqCon ec = p.eqc[ci.intra_base + e];
+    int sum = 0;
+    for (int t = 0; t < ec.nterm; ++t) sum += ec.coef[t] * raw_val(b, ci.seg_base + (ec.var[t] & 0x7f), r);
+    if (sum != 0) return false;
+  }
+  return true;
+}
+
 // ---- per-output column setup (readings R5, R15) --------------------------------------
 // Returns kStatusOk / kStatusZero / kStatusBad / kStatusUnsupported (block-uniform).
 __device__ int setup_output(const CallParams &p, Block &b, Shared &sh, int q) {
@@ -293,26 +330,66 @@ __device__ int setup_output(const CallParams &p, Block &b, Shared &sh, int q) {
   }
   __syncthreads();
   if (sh.status != kStatusOk) return sh.status;
+  if (p.force_generic) return kStatusUnsupported;  // test hook: every output to the generic engine
   // segment ranges: intersection of the backward (T) and forward (S) light-cone boxes
   int my_bad = 0;
   for (int k = tid; k <= M; k += kThreads) {
     const ColInfo ci = sh.col[k];
     long long n = 1;
-    for (int i = 0; i < ci.nseg; ++i) {
-      const SegInfo si = p.seg[ci.seg_base + i];
-      const int lo = max(sh.G[si.rho], (int)p.cumS[si.rhop]);
-      const int hi = min(sh.G[si.sig], (int)p.cumS[si.sigp]);
+    for (int i = 0; i < ci.nvar; ++i) {
+      int lo, hi;
+      if (!p.general) {
+        const SegInfo si = p.seg[ci.seg_base + i];
+        lo = max(sh.G[si.rho], (int)p.cumS[si.rhop]);
+        hi = min(sh.G[si.sig], (int)p.cumS[si.sigp]);
+      } else {  // non-local circuit: cone sums over mode sets
+        const BoundInfo &bi = p.bnd[ci.seg_base + i];
+        int sum[4];
+        for (int w = 0; w < 4; ++w) {
+          int acc = 0;
+          for (int h = 0; h < 2; ++h) {
+            uint64_t m = bi.m[w][h];
+            while (m) {
+              const int md = 64 * h + __ffsll((long long)m) - 1;
+              m &= m - 1;
+              acc += (w < 2) ? (int)p.cumS[md + 1] - (int)p.cumS[md] : sh.G[md + 1] - sh.G[md];
+            }
+          }
+          sum[w] = acc;
+        }
+        hi = min(sum[0], sum[2]);
+        lo = max(0, max(p.N - sum[1], p.N - sum[3]));
+      }
       const int rad = hi - lo + 1;
       b.segLo[ci.seg_base + i] = (uint8_t)max(lo, 0);
       b.segRad[ci.seg_base + i] = (uint8_t)max(rad, 0);
       b.segStr[ci.seg_base + i] = (int)n;
       n = rad > 0 ? n * rad : 0;
-      if (n > kMaxStates) { n = kMaxStates + 1; }
+      if (n > kMaxRawStates) { n = kMaxRawStates + 1; }
     }
-    if (n > kMaxStates) my_bad = 1;
+    // local circuits: every raw combination is a state; non-local ones filter by the
+    // column's conservation equalities below (ColInfo::nintra)
+    const int lim = (p.general && ci.nintra) ? kMaxRawStates : kMaxStates;
+    if (n > lim) my_bad = 1;
     sh.n[k] = (int)n;
   }
   my_bad = __syncthreads_or(my_bad);
+  if (p.general && !my_bad) {
+    // count the raw combinations of each constrained column that satisfy its equalities
+    for (int k = 0; k <= M; ++k) {
+      const ColInfo ci = sh.col[k];
+      if (!ci.nintra) continue;  // (block-uniform)
+      if (tid == 0) sh.total = 0;
+      __syncthreads();
+      uint32_t c = 0;
+      for (int r = tid; r < sh.n[k]; r += kThreads) c += intra_ok(p, b, ci, r) ? 1u : 0u;
+      atomicAdd(&sh.total, c);
+      __syncthreads();
+      if (tid == 0) sh.raw[k] = sh.n[k], sh.n[k] = (int)sh.total;
+      __syncthreads();
+      if (sh.n[k] > kMaxStates) my_bad = 1;
+    }
+  }
   if (tid == 0) {
     int st = my_bad ? kStatusUnsupported : kStatusOk;
     long long vb = 0, cb = 0;
@@ -320,13 +397,14 @@ __device__ int setup_output(const CallParams &p, Block &b, Shared &sh, int q) {
       if (sh.n[k] == 0) st = kStatusZero;  // structurally unreachable (reading R5)
       sh.vb[k] = (int)vb;
       sh.cb[k] = (int)cb;
-      vb += (long long)sh.n[k] * sh.col[k].nseg;
+      vb += (long long)sh.n[k] * sh.col[k].nvar;
       cb += sh.n[k];
     }
     if (st == kStatusOk && cb > kMaxStatesTotal) st = kStatusUnsupported;
     if (st == kStatusOk) {
       const long long used = kOffVar + ((vb + 15) & ~15ll) + 16 * cb;
       if (p.slab_bytes - used < 4096) st = kStatusUnsupported;
+      if (p.general && used > p.slab_bytes - 8ll * kMaxRawStates) st = kStatusUnsupported;
       atomicMax(&p.ctr->max_states, (ull)cb);
     }
     sh.status = st;
@@ -337,9 +415,24 @@ __device__ int setup_output(const CallParams &p, Block &b, Shared &sh, int q) {
   // segment values of every column state (mixed radix over the segments)
   for (int k = 0; k <= M; ++k) {
     const ColInfo ci = sh.col[k];
+    if (p.general && ci.nintra) {  // the raw combinations that satisfy the equalities, in order
+      uint32_t *flag = (uint32_t *)(b.slab + p.slab_bytes - 8ll * kMaxRawStates);
+      uint32_t *pos = flag + kMaxRawStates;
+      const int R = sh.raw[k];
+      for (int r = tid; r < R; r += kThreads) flag[r] = intra_ok(p, b, ci, r) ? 1u : 0u;
+      __syncthreads();
+      block_scan(sh, flag, pos, R);
+      for (int r = tid; r < R; r += kThreads) {
+        if (!flag[r]) continue;
+        uint8_t *row = b.vals + sh.vb[k] + pos[r] * ci.nvar;
+        for (int i = 0; i < ci.nvar; ++i) row[i] = (uint8_t)raw_val(b, ci.seg_base + i, r);
+      }
+      __syncthreads();
+      continue;
+    }
     for (int s = tid; s < sh.n[k]; s += kThreads) {
-      uint8_t *row = b.vals + sh.vb[k] + s * ci.nseg;
-      for (int i = 0; i < ci.nseg; ++i) {
+      uint8_t *row = b.vals + sh.vb[k] + s * ci.nvar;
+      for (int i = 0; i < ci.nvar; ++i) {
         const int g = ci.seg_base + i;
         row[i] = (uint8_t)(b.segLo[g] + (s / b.segStr[g]) % b.segRad[g]);
       }
@@ -884,6 +977,26 @@ __device__ void load_cols(const CallParams &p, Shared &sh) {
 }  // namespace
 
 // ---- Appendix-A tables ---------------------------------------------------------------
+// photons that can enter BS i: its inputs' past light cone, at most N
+__device__ __forceinline__ int bs_cap(const CallParams &p, int i) {
+  const BSInfo &bi = p.bsi[i];
+  int c;
+  if (!p.general) {
+    c = (int)p.cumS[bi.cap_hi] - (int)p.cumS[bi.cap_lo];
+  } else {
+    c = 0;
+    for (int h = 0; h < 2; ++h) {
+      uint64_t m = bi.capmask[h];
+      while (m) {
+        const int md = 64 * h + __ffsll((long long)m) - 1;
+        m &= m - 1;
+        c += (int)p.cumS[md + 1] - (int)p.cumS[md];
+      }
+    }
+  }
+  return min(p.N, c);
+}
+
 __global__ void lofp_table_off_kernel(const __grid_constant__ CallParams p) {
   // one block: per-BS block sizes (past light cone of its inputs) and offsets
   __shared__ long long part[kThreads];
@@ -891,11 +1004,7 @@ __global__ void lofp_table_off_kernel(const __grid_constant__ CallParams p) {
   const int per = (nb + kThreads - 1) / kThreads;
   const int a = tid * per, e = min(nb, a + per);
   long long s = 0;
-  for (int i = a; i < e; ++i) {
-    const BSInfo bi = p.bsi[i];
-    const int cap = min(p.N, (int)p.cumS[bi.cap_hi] - (int)p.cumS[bi.cap_lo]);
-    s += tri_dev(cap + 1);
-  }
+  for (int i = a; i < e; ++i) s += tri_dev(bs_cap(p, i) + 1);
   part[tid] = s;
   __syncthreads();
   if (tid == 0) {
@@ -912,9 +1021,7 @@ __global__ void lofp_table_off_kernel(const __grid_constant__ CallParams p) {
   long long run = part[tid];
   for (int i = a; i < e; ++i) {
     p.tab_off[i] = run;
-    const BSInfo bi = p.bsi[i];
-    const int cap = min(p.N, (int)p.cumS[bi.cap_hi] - (int)p.cumS[bi.cap_lo]);
-    run += tri_dev(cap + 1);
+    run += tri_dev(bs_cap(p, i) + 1);
   }
   // phase gates exp(i (a n + b n^2)) for n = 0..N (reading R19)
   for (int t = tid; t < p.ngate * (p.N + 1); t += kThreads) {
@@ -935,7 +1042,7 @@ __global__ void __launch_bounds__(kThreads) lofp_table_kernel(const __grid_const
   const int bs = blockIdx.x, tid = threadIdx.x;
   if (p.tab_off[p.nbs] > p.table_cap) return;
   const BSInfo bi = p.bsi[bs];
-  const int cap = min(p.N, (int)p.cumS[bi.cap_hi] - (int)p.cumS[bi.cap_lo]);
+  const int cap = bs_cap(p, bs);
   double2 *tb = p.table + p.tab_off[bs];
   const double c = bi.c, s = bi.s;
   if (tid == 0) tb[0] = make_double2(1.0, 0.0);
@@ -1240,6 +1347,8 @@ __global__ void lofp_final_kernel(const __grid_constant__ CallParams p) {
   }
 }
 
+__global__ void __launch_bounds__(kThreads) lofp_generic_kernel(const __grid_constant__ CallParams p);
+
 // ---- launchers -------------------------------------------------------------------------
 extern "C" int lofp_units_grid(int device) {
   int nsm = 0;
@@ -1273,6 +1382,7 @@ extern "C" int lofp_launch_paths(const CallParams *p, int grid, void *stream, vo
   lofp_units_kernel<<<grid, kThreads, smem, st>>>(*p);
   if (ev1) cudaEventRecord((cudaEvent_t)ev1, st);
   lofp_final_kernel<<<(p->B + 255) / 256 < 1024 ? (p->B + 255) / 256 : 1024, 256, 0, st>>>(*p);
+  lofp_generic_kernel<<<grid, kThreads, 0, st>>>(*p);  // outputs over the column limits
   return (int)cudaGetLastError();
 }
 
@@ -1379,6 +1489,7 @@ __global__ void __launch_bounds__(kThreads) lofp_contract_kernel(const __grid_co
 extern "C" int lofp_launch_contract(const CallParams *p, int grid, void *stream) {
   const int g = p->B < grid ? p->B : grid;
   lofp_contract_kernel<<<g, kThreads, 0, (cudaStream_t)stream>>>(*p);
+  lofp_generic_kernel<<<grid, kThreads, 0, (cudaStream_t)stream>>>(*p);  // outputs over the column limits
   return (int)cudaGetLastError();
 }
 
@@ -1417,5 +1528,260 @@ extern "C" int lofp_launch_outputs(int M, int N, long long count, int32_t *T, vo
   const long long blocks = (count + 255) / 256;
   lofp_outputs_kernel<<<(int)(blocks < 4096 ? (blocks > 0 ? blocks : 1) : 4096), 256, 0, (cudaStream_t)stream>>>(
       M, N, count, T);
+  return (int)cudaGetLastError();
+}
+
+// ---- the generic engine: the paper's own recursion ------------------
+// For any output the column model cannot hold (a non-local circuit whose columns exceed the
+// state limits, or any over-limit output): the path tree in the paper's order, BS by BS in
+// layer-major order, each BS choosing y1 within the waveguides' light-cone bounds (P:164:
+// photons in a waveguide <= min(sum of S over its past cone, sum of T over its future
+// cone)); a leaf is a valid path iff it lands on T.  One block per output: the tree is
+// expanded breadth-first into >= 4 prefixes per thread (the north_star's prefix split), then
+// every thread walks its prefixes depth-first with an explicit stack (fixed order: the sum
+// is deterministic).
+namespace {
+
+constexpr int kGenMaxBS = 1024;      // levels of the generic tree (BS count)
+constexpr int kGenFront = 8192;      // frontier entries of the prefix split
+constexpr ull kGenNodeBudget = 1ull << 26;  // tree nodes per thread before an output is given up
+
+struct GenEntry {
+  double re, im;
+  int32_t level;
+  int32_t pad;
+};
+
+__device__ __forceinline__ double2 gen_gates(const CallParams &p, int l0, int l1, const uint8_t *occ) {
+  double2 f = make_double2(1.0, 0.0);
+  if (p.ngate == 0 || l0 >= l1) return f;
+  for (int g = 0; g < p.ngate; ++g) {
+    const int a = p.gate_after[g];
+    if (a >= l0 && a < l1) f = cmul(f, p.gate_tab[g * (p.N + 1) + occ[p.gate_mode[g]]]);
+  }
+  return f;
+}
+
+__device__ __forceinline__ void gen_range(const CallParams &p, const uint8_t *bnd, const SeqBS &s, const uint8_t *occ,
+                                          int &ylo, int &yhi) {
+  const int M = p.M, n = occ[s.lo] + occ[s.hi];
+  const int ba = bnd[s.layer * M + s.lo], bb = bnd[s.layer * M + s.hi];
+  ylo = max(0, n - bb);
+  yhi = min(n, ba);
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kThreads) lofp_generic_kernel(const __grid_constant__ CallParams p) {
+  __shared__ uint8_t bnd[(kMaxLayers + 1) * kMaxModes];
+  __shared__ int sT[kMaxModes];
+  __shared__ double rre[kThreads / 32], rim[kThreads / 32];
+  __shared__ ull rnp[kThreads / 32];
+  __shared__ int s_front, s_level, s_done;
+  const int M = p.M, D = p.D, L = p.nbs, tid = threadIdx.x;
+  char *slab = p.slab + (long long)blockIdx.x * p.slab_bytes;
+  GenEntry *fe[2] = {(GenEntry *)slab, (GenEntry *)slab + kGenFront};
+  uint8_t *fo[2] = {(uint8_t *)((GenEntry *)slab + 2 * kGenFront),
+                    (uint8_t *)((GenEntry *)slab + 2 * kGenFront) + (long long)kGenFront * M};
+  // per-thread DFS state (occupations + stack) after the frontier
+  char *tstate = (char *)(fo[1] + (long long)kGenFront * M);
+  tstate = (char *)(((uintptr_t)tstate + 15) & ~(uintptr_t)15);
+  const long long per_thread = (24ll * L + M + 64 + 15) & ~15ll;
+  uint8_t *occ = (uint8_t *)(tstate + per_thread * tid);
+  double2 *prodst = (double2 *)(((uintptr_t)(occ + M) + 15) & ~(uintptr_t)15);
+  int16_t *yst = (int16_t *)(prodst + L + 1);  // y1 chosen per level
+  int16_t *yhs = yst + L;                        // its upper end
+  ull cm = 0;
+  for (int q = blockIdx.x; q < p.B; q += gridDim.x) {
+    if (p.status[q] != kStatusUnsupported || L > kGenMaxBS || D > kMaxLayers ||
+        (long long)(2 * kGenFront) * (16 + M) + per_thread * kThreads + 64 > p.slab_bytes)
+      continue;  // (block-uniform)
+    for (int i = tid; i < M; i += kThreads) sT[i] = p.T[(long long)q * M + i];
+    __syncthreads();
+    // light-cone bounds of every waveguide (mode m after layer t)
+    for (int w = tid; w < (D + 1) * M; w += kThreads) {
+      const uint64_t *c = p.cone + 4ll * w;
+      int ps = 0, ft = 0;
+      for (int h = 0; h < 2; ++h) {
+        uint64_t m = c[h];
+        while (m) {
+          const int md = 64 * h + __ffsll((long long)m) - 1;
+          m &= m - 1;
+          ps += (int)p.cumS[md + 1] - (int)p.cumS[md];
+        }
+        m = c[2 + h];
+        while (m) {
+          const int md = 64 * h + __ffsll((long long)m) - 1;
+          m &= m - 1;
+          ft += sT[md];
+        }
+      }
+      bnd[w] = (uint8_t)min(255, min(ps, ft));
+    }
+    // root
+    if (tid == 0) {
+      for (int m = 0; m < M; ++m) fo[0][m] = (uint8_t)((int)p.cumS[m + 1] - (int)p.cumS[m]);
+      const double2 g = gen_gates(p, 0, p.seq_gl0, fo[0]);
+      fe[0][0].re = g.x;
+      fe[0][0].im = g.y;
+      fe[0][0].level = 0;
+      s_front = 1;
+      s_level = 0;
+    }
+    __syncthreads();
+    // breadth-first prefix split until every thread has ~4 prefixes (or the tree ends)
+    int cur = 0;
+    while (s_front < 4 * kThreads && s_level < L) {
+      const int nf = s_front, lev = s_level;
+      const SeqBS sb = p.seq[lev];
+      // count children per entry (thread 0: the frontier is small)
+      if (tid == 0) {
+        int tot = 0;
+        for (int e = 0; e < nf; ++e) {
+          int ylo, yhi;
+          gen_range(p, bnd, sb, fo[cur] + (long long)e * M, ylo, yhi);
+          tot += max(0, yhi - ylo + 1);
+        }
+        s_done = tot;
+      }
+      __syncthreads();
+      if (s_done > kGenFront || s_done == 0) break;  // (uniform)
+      if (tid == 0) {
+        int o = 0;
+        for (int e = 0; e < nf; ++e) {
+          const uint8_t *src = fo[cur] + (long long)e * M;
+          int ylo, yhi;
+          gen_range(p, bnd, sb, src, ylo, yhi);
+          const int x1 = src[sb.lo], x2 = src[sb.hi], n = x1 + x2;
+          for (int y1 = ylo; y1 <= yhi; ++y1) {
+            uint8_t *dst = fo[cur ^ 1] + (long long)o * M;
+            for (int m = 0; m < M; ++m) dst[m] = src[m];
+            dst[sb.lo] = (uint8_t)y1;
+            dst[sb.hi] = (uint8_t)(n - y1);
+            double2 f = make_double2(1.0, 0.0);
+            if (n > 0) {
+              f = p.table[p.tab_off[sb.bs] + tri_dev(n) + (long long)x1 * (n + 1) + y1];
+              ++cm;
+            }
+            double2 pr = cmul(make_double2(fe[cur][e].re, fe[cur][e].im), f);
+            pr = cmul(pr, gen_gates(p, sb.gl0, sb.gl1, dst));
+            fe[cur ^ 1][o].re = pr.x;
+            fe[cur ^ 1][o].im = pr.y;
+            fe[cur ^ 1][o].level = lev + 1;
+            ++o;
+          }
+        }
+        s_front = o;
+        s_level = lev + 1;
+      }
+      __syncthreads();
+      cur ^= 1;
+    }
+    // depth-first walk of every prefix
+    double are = 0.0, aim = 0.0;
+    ull np = 0, nodes = 0;
+    bool over = false;
+    const int nf = s_front;
+    for (int e = tid; e < nf && !over; e += kThreads) {
+      for (int m = 0; m < M; ++m) occ[m] = fo[cur][(long long)e * M + m];
+      const int l0 = fe[cur][e].level;
+      prodst[l0] = make_double2(fe[cur][e].re, fe[cur][e].im);
+      int lev = l0;
+      bool down = true;  // entering level lev fresh
+      while (true) {
+        if (lev == L) {  // leaf: a valid path iff it lands on T
+          bool ok = true;
+          for (int m = 0; m < M; ++m) ok &= (occ[m] == sT[m]);
+          if (ok) {
+            are += prodst[L].x;
+            aim += prodst[L].y;
+            ++np;
+          }
+          --lev;
+          down = false;
+          if (lev < l0) break;
+        }
+        const SeqBS sb = p.seq[lev];
+        if (++nodes > kGenNodeBudget) {  // keep the GPU responsive: give the output up (NaN)
+          over = true;
+          break;
+        }
+        int y1;
+        if (down) {
+          int ylo, yhi;
+          gen_range(p, bnd, sb, occ, ylo, yhi);
+          if (ylo > yhi) {  // dead end
+            --lev;
+            down = false;
+            if (lev < l0) break;
+            continue;
+          }
+          yst[lev] = (int16_t)(occ[sb.lo] + occ[sb.hi]);  // n, kept with y1 below
+          yhs[lev] = (int16_t)yhi;
+          y1 = ylo;
+          // remember x1 in the high byte of yst (n <= 240, x1 <= 120)
+          yst[lev] = (int16_t)(yst[lev] | (occ[sb.lo] << 8));
+        } else {
+          y1 = occ[sb.lo] + 1;  // next choice
+          if (y1 > yhs[lev]) {  // exhausted: restore the inputs and go up
+            const int n = yst[lev] & 0xff, x1 = (yst[lev] >> 8) & 0xff;
+            occ[sb.lo] = (uint8_t)x1;
+            occ[sb.hi] = (uint8_t)(n - x1);
+            --lev;
+            if (lev < l0) break;
+            continue;
+          }
+        }
+        const int n = yst[lev] & 0xff, x1 = (yst[lev] >> 8) & 0xff;
+        occ[sb.lo] = (uint8_t)y1;
+        occ[sb.hi] = (uint8_t)(n - y1);
+        double2 f = make_double2(1.0, 0.0);
+        if (n > 0) {
+          f = p.table[p.tab_off[sb.bs] + tri_dev(n) + (long long)x1 * (n + 1) + y1];
+          ++cm;
+        }
+        double2 pr = cmul(prodst[lev], f);
+        if (sb.gl1 > sb.gl0) pr = cmul(pr, gen_gates(p, sb.gl0, sb.gl1, occ));
+        prodst[lev + 1] = pr;
+        ++lev;
+        down = true;
+      }
+    }
+    // deterministic block reduction
+    const int any_over = __syncthreads_or(over ? 1 : 0);
+    for (int d = 16; d > 0; d >>= 1) {
+      are += __shfl_down_sync(0xffffffffu, are, d);
+      aim += __shfl_down_sync(0xffffffffu, aim, d);
+      np += __shfl_down_sync(0xffffffffu, np, d);
+    }
+    if ((tid & 31) == 0) {
+      rre[tid >> 5] = are;
+      rim[tid >> 5] = aim;
+      rnp[tid >> 5] = np;
+    }
+    __syncthreads();
+    if (tid == 0 && !any_over) {
+      double a = 0.0, b2 = 0.0;
+      ull n = 0;
+      for (int w = 0; w < kThreads / 32; ++w) {
+        a += rre[w];
+        b2 += rim[w];
+        n += rnp[w];
+      }
+      p.amps[q] = make_double2(a, b2);
+      if (p.counts) p.counts[q] = n;
+      p.status[q] = kStatusOk;
+      atomicAdd(&p.ctr->paths, n);
+      atomicAdd(&p.ctr->generic, 1ull);
+      atomicAdd(&p.ctr->unsupported, ~0ull);  // (-1: the output is evaluated after all)
+    }
+    __syncthreads();
+  }
+  for (int d = 16; d > 0; d >>= 1) cm += __shfl_down_sync(0xffffffffu, cm, d);
+  if ((tid & 31) == 0) atomicAdd(&p.ctr->cmuls, cm);
+}
+
+extern "C" int lofp_launch_generic(const CallParams *p, int grid, void *stream) {
+  lofp_generic_kernel<<<grid, kThreads, 0, (cudaStream_t)stream>>>(*p);
   return (int)cudaGetLastError();
 }

@@ -33,6 +33,7 @@ class lofp_run_stats(ctypes.Structure):
                 ("pairs", ctypes.c_int64), ("elements", ctypes.c_int64), ("unsupported", ctypes.c_int64),
                 ("bad_rows", ctypes.c_int64), ("check_errors", ctypes.c_int64), ("max_states", ctypes.c_int64),
                 ("max_list", ctypes.c_int64), ("table_entries", ctypes.c_int64), ("terms", ctypes.c_int64),
+                ("generic", ctypes.c_int64),
                 ("phase_cycles", ctypes.c_int64 * 8),
                 ("grid_blocks", ctypes.c_int32), ("block_threads", ctypes.c_int32),
                 ("launches", ctypes.c_int32), ("mode", ctypes.c_int32),

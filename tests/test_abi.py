@@ -40,7 +40,6 @@ def test_status_strings(lib):
 def test_create_validation_without_device():
     from paper_2510_26408_b200 import Circuit, LofpError
     bad = [
-        (4, [[(0, 2, 0.1, 0.2)]], 2),                        # non-adjacent pair -> unsupported
         (4, [[(0, 1, 0.1, 0.2), (1, 2, 0.3, 0.4)]], 1),      # overlapping pairs
         (4, [[(0, 4, 0.1, 0.2)]], 1),                        # mode out of range
         (4, [[(1, 1, 0.1, 0.2)]], 1),                        # a == b

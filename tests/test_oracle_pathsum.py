@@ -167,3 +167,25 @@ def test_reversed_pair_is_swapped_phase(rng):
     S = [1, 0, 1, 1, 0, 0]
     T = li.all_outputs(M, 3)
     assert np.abs(oracle.path_sum(M, rev, S, T) - oracle.path_sum(M, canon, S, T)).max() < 1e-14
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_nonlocal_pathsum_vs_ryser(seed):
+    """Non-local pairs (NEXT-4): the oracle's path sum with the paper's cone bounds (P:164,
+    prune 1) and with no prune agree with each other and with Ryser."""
+    rng = np.random.default_rng(800 + seed)
+    M = int(rng.integers(3, 7))
+    D = int(rng.integers(1, 5))
+    N = int(rng.integers(1, 5))
+    layers = li.random_nonlocal_circuit(M, D, rng)
+    S = np.zeros(M, dtype=np.int32)
+    for m in rng.integers(0, M, size=N):
+        S[m] += 1
+    T = li.all_outputs(M, N)
+    a1, l1 = oracle.path_sum(M, layers, S, T, prune=oracle.PRUNE_CONE, return_leaves=True)
+    a0, l0 = oracle.path_sum(M, layers, S, T, prune=oracle.PRUNE_NONE, return_leaves=True)
+    ref = oracle.amplitudes_permanent(M, layers, S, T)
+    assert np.abs(a1 - ref).max() < 1e-13
+    assert np.abs(a0 - ref).max() < 1e-13
+    assert np.array_equal(l0, l1)  # the cone bound never drops a valid path
+    assert abs(np.sum(np.abs(a1) ** 2) - 1) < 1e-13
