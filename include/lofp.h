@@ -22,8 +22,8 @@
  *     same element as (mode_b, mode_a, theta, pi - phi) (port swap).
  *   - Layers are applied in the order given (layer 0 first); BS inside one layer must
  *     act on disjoint modes (P:65 planar mesh).  Modes not covered by a layer pass
- *     through unchanged.  This version requires nearest-neighbour pairs
- *     (|mode_a - mode_b| = 1), the locally connected meshes of P:105 and P:144.
+ *     through unchanged.  Pairs may be non-adjacent and may cross ("non-local
+ *     connections"); nearest-neighbour meshes are the fast case.
  *   - theta and phi may be any finite doubles (P:80 states theta in [0, pi/2] and phi in
  *     [0, pi]; the benchmark configurations draw phi in [0, 2 pi)).
  *   - An output whose photon number differs from the input's gets exactly 0; so does an
@@ -74,8 +74,8 @@ typedef enum {
   LOFP_OK = 0,
   LOFP_E_INVALID_ARG = 1, /* null pointer, bad count, mode out of range, overlapping
                              pairs in one layer, non-finite angle, negative input */
-  LOFP_E_UNSUPPORTED = 2, /* non-adjacent pair, too many modes/photons/layers, an output
-                             whose light-cone state space exceeds the limits below */
+  LOFP_E_UNSUPPORTED = 2, /* too many modes/photons/layers/gates, or a circuit whose
+                             column description exceeds the topology limits */
   LOFP_E_CUDA = 3,        /* a CUDA runtime error; text in lofp_last_error() */
   LOFP_E_OOM = 4,         /* device allocation failed */
   LOFP_E_BAD_OUTPUT = 5   /* an output row had a negative entry; its amplitude is NaN */
@@ -84,7 +84,9 @@ typedef enum {
 /* Limits of this build.  Photon numbers are uint8 segment values; a column of the path
  * tree (the photon counts left of one cut over all layers) may take at
  * most 4096 values inside the light-cone box, 65536 summed over the columns of one
- * output; an output over these limits gets NaN and lofp_stats() counts it. */
+ * output; an output over these limits is evaluated by the generic engine (the paper's
+ * layer-major recursion, lofp_run_stats.generic) and gets NaN only if that exceeds its
+ * node budget (lofp_run_stats.unsupported). */
 #define LOFP_MAX_MODES 128
 #define LOFP_MAX_PHOTONS 120
 #define LOFP_MAX_LAYERS 64
@@ -202,10 +204,10 @@ typedef struct {
                              recursion with its cone bounds) because their
                              columns exceed the column engine's limits */
   int64_t phase_cycles[8];/* unit kernel, SM clock cycles of each block's thread 0 summed over
-                             blocks: 0 unit fetch / output setup / reduction, 1 path counts and
-                             split choice, 2 left lists, 3 right lists, 4 pair list and
-                             scaling tables, 5 warp tiles (path products), 6 waiting for the
-                             block's other warps after the tiles, 7 stack pop / sub-splits */
+                             blocks: 0 kernel tail, 1 path counts and split choice, 2 left
+                             lists, 3 right lists, 4 pair list and scaling tables, 5 warp tiles
+                             (path products), 6 waiting for the block's other warps after the
+                             tiles, 7 unit fetch, output setup, stack pops and reduction */
   int32_t grid_blocks;    /* persistent grid of the unit kernel */
   int32_t block_threads;  /* threads per block */
   int32_t launches;       /* kernels launched by the call */
