@@ -565,35 +565,27 @@ __device__ uint32_t bucket_offsets(Block &b, Shared &sh, int k, bool left, uint3
 // A warp holds kKX X values per lane (a tile of kXT = 32 kKX) in registers and streams a
 // tile of up to kYT Y values from its shared-memory slice (broadcast reads): per Y value
 // 1 LDS.128 and 4 kKX DFMA per lane.
+#define LOFP_CFMA(v)                                \
+  _Pragma("unroll") for (int r = 0; r < kKX; ++r) { \
+    acc[r].x = fma(x[r].x, (v).x, acc[r].x);        \
+    acc[r].y = fma(x[r].x, (v).y, acc[r].y);        \
+    acc[r].x = fma(-x[r].y, (v).y, acc[r].x);       \
+    acc[r].y = fma(x[r].y, (v).x, acc[r].y);        \
+  }
+
 __device__ __forceinline__ void fma_block(const double2 (&x)[kKX], const double2 *__restrict__ sW, uint32_t len,
                                           double2 (&acc)[kKX]) {
   uint32_t y = 0;
-  for (; y + 1 < len; y += 2) {
-    const double2 v0 = sW[y], v1 = sW[y + 1];
-#pragma unroll
-    for (int r = 0; r < kKX; ++r) {
-      acc[r].x = fma(x[r].x, v0.x, acc[r].x);
-      acc[r].y = fma(x[r].x, v0.y, acc[r].y);
-      acc[r].x = fma(-x[r].y, v0.y, acc[r].x);
-      acc[r].y = fma(x[r].y, v0.x, acc[r].y);
-    }
-#pragma unroll
-    for (int r = 0; r < kKX; ++r) {
-      acc[r].x = fma(x[r].x, v1.x, acc[r].x);
-      acc[r].y = fma(x[r].x, v1.y, acc[r].y);
-      acc[r].x = fma(-x[r].y, v1.y, acc[r].x);
-      acc[r].y = fma(x[r].y, v1.x, acc[r].y);
-    }
+  for (; y + 3 < len; y += 4) {  // four Y values loaded ahead of their 128 DFMA
+    const double2 v0 = sW[y], v1 = sW[y + 1], v2 = sW[y + 2], v3 = sW[y + 3];
+    LOFP_CFMA(v0)
+    LOFP_CFMA(v1)
+    LOFP_CFMA(v2)
+    LOFP_CFMA(v3)
   }
-  if (y < len) {
+  for (; y < len; ++y) {
     const double2 v0 = sW[y];
-#pragma unroll
-    for (int r = 0; r < kKX; ++r) {
-      acc[r].x = fma(x[r].x, v0.x, acc[r].x);
-      acc[r].y = fma(x[r].x, v0.y, acc[r].y);
-      acc[r].x = fma(-x[r].y, v0.y, acc[r].x);
-      acc[r].y = fma(x[r].y, v0.x, acc[r].y);
-    }
+    LOFP_CFMA(v0)
   }
 }
 
