@@ -310,3 +310,21 @@ def test_paper_correctness_protocol_gpu(lofp, case):
     assert tol_ok(got, ref)[0]
 
 
+
+
+def test_config4_literal_batch(lofp):
+    """configs[4] as BASELINE.json draws it, structural zeros included: 16384 outputs, 12,548
+    reachable (4.9e13 paths).  Every output's path-product count equals the oracle's exact
+    count (0 for the unreachable ones, whose amplitude is exactly 0); a seeded sample of 64
+    reachable outputs matches the Ryser permanent."""
+    c = li.config(4)
+    d = load(4)
+    T = d["T_literal"].astype(np.int32)
+    got, cnt, st, _ = run(lofp, c.M, c.layers, c.S, T)
+    assert np.array_equal(cnt, d["P_literal"])
+    assert st["check_errors"] == 0 and st["unsupported"] == 0
+    assert (got[d["P_literal"] == 0] == 0).all()
+    reach = np.nonzero(d["P_literal"] > 0)[0]
+    pick = np.random.default_rng(44).choice(reach, 64, replace=False)
+    ok, err = tol_ok(got[pick], oracle.amplitudes_permanent(c.M, c.layers, c.S, T[pick]))
+    assert ok, err
