@@ -249,3 +249,30 @@ def test_debug_build_bounds_checks(lofp, idx, n, env):
     assert r.returncode == 0, r.stderr[-2000:]
     ok = [l for l in r.stdout.splitlines() if l.startswith("ok")]
     assert ok and ok[0].endswith("True") and ok[0].split()[3] == "0"
+
+
+def test_context_reuse_new_input_and_two_streams(lofp):
+    """One context, calls with different inputs S (tables rebuilt per call) on two
+    different streams back to back (the second waits for the first's buffers)."""
+    rng = np.random.default_rng(11)
+    M, D = 8, 5
+    layers = li.clements_mesh(M, D, seed=12)
+    circ = lofp.Circuit(M, layers)
+    S1 = np.array([1, 0, 1, 0, 1, 0, 1, 0], dtype=np.int32)
+    S2 = np.array([2, 0, 0, 1, 0, 0, 1, 1], dtype=np.int32)
+    T1 = li.all_outputs(M, 4)
+    T2 = li.all_outputs(M, 5)
+    T1 = T1[rng.choice(len(T1), 200, replace=False)]
+    T2 = T2[rng.choice(len(T2), 200, replace=False)]
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    Td1, Td2 = torch.from_numpy(T1).cuda(), torch.from_numpy(T2).cuda()
+    torch.cuda.synchronize()  # (the copies ran on the default stream)
+    a1 = circ.amplitudes(S1, Td1, stream=s1)
+    a2 = circ.amplitudes(S2, Td2, stream=s2)
+    a3 = circ.contract(S1, Td1, stream=s1)
+    torch.cuda.synchronize()
+    r1 = oracle.path_sum(M, layers, S1, T1)
+    r2 = oracle.path_sum(M, layers, S2, T2)
+    assert tol_ok(a1.cpu().numpy(), r1)[0]
+    assert tol_ok(a2.cpu().numpy(), r2)[0]
+    assert tol_ok(a3.cpu().numpy(), r1)[0]
