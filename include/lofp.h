@@ -34,11 +34,10 @@
  * Threading, streams and ownership.  A context owns its device memory and must not be
  * used from two host threads at once; separate contexts are independent.  Every device
  * call enqueues its work on the stream it is given and returns without waiting for it
- * (no host synchronisation, no device-to-host read).  The one exception: a call that needs
- * larger buffers than any earlier call on the context (a bigger batch, more photons)
- * grows them first with cudaFree/cudaMalloc, which synchronise the device.  A call can
- * therefore be captured in a CUDA graph once a call of the same sizes has run outside
- * capture.
+ * (no host synchronisation, no device-to-host read); buffers that must grow (a bigger
+ * batch or input than before) are reallocated stream-ordered (cudaFreeAsync /
+ * cudaMallocAsync on the call's stream).  A call can be captured in a CUDA graph once a
+ * call of the same sizes has run outside capture (no buffer grows during capture).
  * Consecutive calls on one context are ordered after each other even on different
  * streams (outside capture).  The library never frees caller memory and never throws or
  * aborts across this boundary.

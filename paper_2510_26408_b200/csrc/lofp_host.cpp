@@ -36,6 +36,17 @@ struct DevBuf {
     if (e == cudaSuccess) n = bytes;
     return e;
   }
+  // stream-ordered growth: the old block is freed after the work already queued on the
+  // stream, the new one allocated before the work that follows (no host synchronisation)
+  cudaError_t ensure_async(size_t bytes, cudaStream_t st) {
+    if (bytes <= n && p) return cudaSuccess;
+    if (p) cudaFreeAsync(p, st);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMallocAsync(&p, bytes ? bytes : 16, st);
+    if (e == cudaSuccess) n = bytes;
+    return e;
+  }
   void release() {
     if (p) cudaFree(p);
     p = nullptr;
@@ -757,6 +768,11 @@ lofp_status prepare(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, cons
     N += input_occ[i];
     if (N > LOFP_MAX_PHOTONS) return fail(ctx, LOFP_E_UNSUPPORTED, "too many photons");
   }
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CK(cudaStreamIsCapturing(stream, &cs), "cudaStreamIsCapturing");
+  capturing = cs != cudaStreamCaptureStatusNone;
+  // order after the previous call on this context (its buffers are reused or freed)
+  if (!capturing && ctx->have_call) CK(cudaStreamWaitEvent(stream, ctx->ev_end, 0), "cudaStreamWaitEvent");
   std::memset(&P, 0, sizeof(P));
   P.M = M;
   P.D = ctx->D;
@@ -796,9 +812,9 @@ lofp_status prepare(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, cons
     entries += tri_entries(std::min(N, c));
   }
   ctx->table_entries = entries;
-  CK(ctx->d_table.ensure((size_t)std::max(entries, 1ll) * 16), "alloc table");
-  CK(ctx->d_taboff.ensure((size_t)(ctx->nbs + 1) * 8), "alloc table offsets");
-  CK(ctx->d_gatetab.ensure((size_t)std::max(ctx->ngate, 1) * (N + 1) * 16), "alloc gate table");
+  CK(ctx->d_table.ensure_async((size_t)std::max(entries, 1ll) * 16, stream), "alloc table");
+  CK(ctx->d_taboff.ensure_async((size_t)(ctx->nbs + 1) * 8, stream), "alloc table offsets");
+  CK(ctx->d_gatetab.ensure_async((size_t)std::max(ctx->ngate, 1) * (N + 1) * 16, stream), "alloc gate table");
   P.table = (double2 *)ctx->d_table.p;
   P.tab_off = (long long *)ctx->d_taboff.p;
   P.gate_tab = (double2 *)ctx->d_gatetab.p;
@@ -812,16 +828,16 @@ lofp_status prepare(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, cons
   P.slab_bytes = ctx->slab_bytes;
   P.units_per_block = (int)env_ll("LOFP_UNITS_PER_BLOCK", 2);
   P.force_generic = env_ll("LOFP_FORCE_GENERIC", 0) > 0 ? 1 : 0;
-  CK(ctx->d_units.ensure((size_t)(B * budget) * sizeof(Unit)), "alloc units");
-  CK(ctx->d_partial.ensure((size_t)(B * budget) * 16), "alloc partials");
-  CK(ctx->d_sched.ensure((size_t)(B * budget) * 4), "alloc schedule");
-  CK(ctx->d_nunits.ensure((size_t)B * 4), "alloc nunits");
-  CK(ctx->d_ubase.ensure((size_t)(B + 1) * 4), "alloc ubase");
-  CK(ctx->d_status.ensure((size_t)B), "alloc status");
-  CK(ctx->d_pexp.ensure((size_t)B * 8), "alloc pexp");
-  CK(ctx->d_pdone.ensure((size_t)B * 8), "alloc pdone");
-  CK(ctx->d_slab.ensure((size_t)ctx->grid * (size_t)ctx->slab_bytes), "alloc scratch");
-  CK(ctx->d_ctr.ensure(sizeof(Counters)), "alloc counters");
+  CK(ctx->d_units.ensure_async((size_t)(B * budget) * sizeof(Unit), stream), "alloc units");
+  CK(ctx->d_partial.ensure_async((size_t)(B * budget) * 16, stream), "alloc partials");
+  CK(ctx->d_sched.ensure_async((size_t)(B * budget) * 4, stream), "alloc schedule");
+  CK(ctx->d_nunits.ensure_async((size_t)B * 4, stream), "alloc nunits");
+  CK(ctx->d_ubase.ensure_async((size_t)(B + 1) * 4, stream), "alloc ubase");
+  CK(ctx->d_status.ensure_async((size_t)B, stream), "alloc status");
+  CK(ctx->d_pexp.ensure_async((size_t)B * 8, stream), "alloc pexp");
+  CK(ctx->d_pdone.ensure_async((size_t)B * 8, stream), "alloc pdone");
+  CK(ctx->d_slab.ensure_async((size_t)ctx->grid * (size_t)ctx->slab_bytes, stream), "alloc scratch");
+  CK(ctx->d_ctr.ensure_async(sizeof(Counters), stream), "alloc counters");
   P.units = (Unit *)ctx->d_units.p;
   P.partial = (double2 *)ctx->d_partial.p;
   P.sched = (int *)ctx->d_sched.p;
@@ -834,11 +850,6 @@ lofp_status prepare(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, cons
   P.ctr = (Counters *)ctx->d_ctr.p;
   P.T = output_occ;
   P.amps = (double2 *)amps;
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  CK(cudaStreamIsCapturing(stream, &cs), "cudaStreamIsCapturing");
-  capturing = cs != cudaStreamCaptureStatusNone;
-  // order after the previous call on this context (its buffers are reused)
-  if (!capturing && ctx->have_call) CK(cudaStreamWaitEvent(stream, ctx->ev_end, 0), "cudaStreamWaitEvent");
   return LOFP_OK;
 }
 
