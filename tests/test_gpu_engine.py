@@ -191,6 +191,16 @@ def test_stream_ordered_no_host_sync(lofp):
     s.synchronize()
     ref = oracle.amplitudes_permanent(c.M, c.layers, c.S, T[:4])
     assert tol_ok(a.cpu().numpy()[:4], ref)[0]
+    # a bigger batch grows the buffers (stream-ordered: still no host synchronisation)
+    c2, T2, P2 = _cfg4_slice(1024)
+    Td2 = torch.from_numpy(T2).cuda()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        torch.cuda._sleep(int(2e8))
+        a2 = circ.amplitudes(c.S, Td2, stream=s)
+    assert not s.query()
+    s.synchronize()
+    assert tol_ok(a2.cpu().numpy()[:256], a.cpu().numpy())[0]
 
 
 def test_small_units(lofp, monkeypatch):
