@@ -445,9 +445,11 @@ __device__ int setup_output(const CallParams &p, Block &b, Shared &sh, int q) {
 // ---- exact path counts by a transfer over columns (reading R6) -----------------------
 // cL[k][s]: partial paths from column j (state sj) to column k ending in s;
 // cR[k][s]: completions from column k (state s) to column M.  Columns >= j.
-__device__ void dp_counts(const CallParams &p, Block &b, Shared &sh, int j, int sj, bool need_right) {
+__device__ void dp_counts(const CallParams &p, Block &b, Shared &sh, int j, int sj, bool need_right,
+                          bool need_left = true) {
   const int M = p.M, tid = threadIdx.x;
-  for (int s = tid; s < sh.n[j]; s += kThreads) b.cL[sh.cb[j] + s] = (s == sj) ? 1ull : 0ull;
+  if (need_left)
+    for (int s = tid; s < sh.n[j]; s += kThreads) b.cL[sh.cb[j] + s] = (s == sj) ? 1ull : 0ull;
   if (need_right)
     for (int s = tid; s < sh.n[M]; s += kThreads) b.cR[sh.cb[M] + s] = 1ull;
   __syncthreads();
@@ -456,7 +458,7 @@ __device__ void dp_counts(const CallParams &p, Block &b, Shared &sh, int j, int 
   const int iters = need_right ? M : M - j;
   for (int i = 1; i <= iters; ++i) {
     const int kL = j + i, kR = M - i;
-    const int nL = kL <= M ? sh.n[kL] : 0, nR = need_right ? sh.n[kR] : 0;
+    const int nL = (need_left && kL <= M) ? sh.n[kL] : 0, nR = need_right ? sh.n[kR] : 0;
     for (int t = tid; t < nL + nR; t += kThreads) {
       ull sum = 0;
       if (t < nL) {
@@ -1396,8 +1398,9 @@ __global__ void __launch_bounds__(kThreads) lofp_contract_kernel(const __grid_co
   ull cm = 0, terms = 0;
   for (int q = blockIdx.x; q < p.B; q += gridDim.x) {
     int st = setup_output(p, b, sh, q);
-    if (st == kStatusOk) {
-      dp_counts(p, b, sh, 0, 0, true);
+    const bool with_counts = p.counts != nullptr;
+    if (st == kStatusOk && with_counts) {
+      dp_counts(p, b, sh, 0, 0, true, false);  // completions: the exact path count, and pruning
       if (b.cR[sh.cb[0]] == 0) st = kStatusZero;
     }
     long long need = 0;
@@ -1411,15 +1414,19 @@ __global__ void __launch_bounds__(kThreads) lofp_contract_kernel(const __grid_co
       double2 root = make_double2(1.0, 0.0);
       if (M == 1)
         for (int g = 0; g < p.ngate; ++g) root = cmul(root, p.gate_tab[g * (p.N + 1) + p.N]);
-      for (int s1 = tid; s1 < sh.n[1]; s1 += kThreads)
-        A[s1] = (live(b, sh, 1, s1) && compat(p, b, sh, 1, 0, s1)) ? root : make_double2(0.0, 0.0);
+      uint32_t *nz = b.tmp;  // states of column k with a nonzero entry in the current level
+      for (int s1 = tid; s1 < sh.n[1]; s1 += kThreads) {
+        const bool on = (!with_counts || b.cR[sh.cb[1] + s1] != 0) && compat(p, b, sh, 1, 0, s1);
+        A[s1] = on ? root : make_double2(0.0, 0.0);
+        nz[s1] = on;
+      }
       __syncthreads();
       for (int k = 1; k <= M - 1; ++k) {  // contract cut k: level (k-1, k) -> (k, k+1)
         const int nA = sh.n[k - 1], nB = sh.n[k], nC = sh.n[k + 1];
         for (int t = tid; t < nB * nC; t += kThreads) {
           const int sb = t / nC, sc = t - sb * nC;
           double2 sum = make_double2(0.0, 0.0);
-          if (live(b, sh, k, sb) && live(b, sh, k + 1, sc) && compat(p, b, sh, k + 1, sb, sc)) {
+          if (nz[sb] && (!with_counts || b.cR[sh.cb[k + 1] + sc] != 0) && compat(p, b, sh, k + 1, sb, sc)) {
             for (int sa = 0; sa < nA; ++sa) {
               const double2 a = A[sa * nB + sb];
               if (a.x == 0.0 && a.y == 0.0) continue;
@@ -1430,6 +1437,15 @@ __global__ void __launch_bounds__(kThreads) lofp_contract_kernel(const __grid_co
             }
           }
           Bn[t] = sum;
+        }
+        __syncthreads();
+        for (int sc = tid; sc < nC; sc += kThreads) {  // columns of the new level still carrying
+          uint32_t on = 0;
+          for (int sb = 0; sb < nB && !on; ++sb) {
+            const double2 v = Bn[sb * nC + sc];
+            on = (v.x != 0.0 || v.y != 0.0);
+          }
+          nz[sc] = on;
         }
         __syncthreads();
         double2 *tt = A; A = Bn; Bn = tt;
@@ -1461,7 +1477,7 @@ __global__ void __launch_bounds__(kThreads) lofp_contract_kernel(const __grid_co
         a = make_double2(__longlong_as_double(0x7ff8000000000000ll), __longlong_as_double(0x7ff8000000000000ll));
       p.amps[q] = a;
       p.status[q] = (uint8_t)st;
-      if (p.counts) p.counts[q] = st == kStatusOk ? b.cR[sh.cb[0]] : 0ull;
+      if (with_counts) p.counts[q] = st == kStatusOk ? b.cR[sh.cb[0]] : 0ull;
       if (st == kStatusOk) atomicAdd(&p.ctr->feasible, 1ull);
       if (st == kStatusBad) atomicAdd(&p.ctr->bad_rows, 1ull);
       if (st == kStatusUnsupported) atomicAdd(&p.ctr->unsupported, 1ull);
