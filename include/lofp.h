@@ -167,6 +167,13 @@ lofp_status lofp_distribution(lofp_ctx *ctx, const int32_t *input_occ, int64_t m
                               int32_t *outputs, double *amps, int64_t *n_outputs,
                               int32_t method, void *cuda_stream);
 
+/* Guard against unexpectedly large path trees (SURVEY §5 "failure detection"): path-sum
+ * calls on ctx skip every output with more than max_paths_per_output valid paths (counted
+ * exactly by the plan kernel before any enumeration) and give it NaN; lofp_stats() reports
+ * how many (over_budget).  0 (the default) = no limit.  The contraction and the
+ * distribution are not limited (their cost does not grow with the path count). */
+lofp_status lofp_set_path_budget(lofp_ctx *ctx, uint64_t max_paths_per_output);
+
 /* End-to-end convenience: HOST buffers in and out.  Copies output_occ (host int32
  * [B][modes]) to the device, runs lofp_amplitudes on an internal stream, copies the
  * amplitudes back into amps (host double [B][2]) and returns when they are there. */
@@ -202,6 +209,7 @@ typedef struct {
   int64_t max_list;       /* largest half-path list */
   int64_t table_entries;  /* Appendix-A elements in the table */
   int64_t terms;          /* contraction mode: (state, state, state) terms summed */
+  int64_t over_budget;    /* outputs skipped by lofp_set_path_budget (their amplitude is NaN) */
   int64_t generic;        /* outputs evaluated by the generic engine (the paper's layer-major
                              recursion with its cone bounds) because their
                              columns exceed the column engine's limits */

@@ -14,7 +14,7 @@ PEAK_SRC = os.path.join(CSRC, "fp64_peak.cu")
 PEAK_LIB = os.path.join(HERE, "libfp64peak.so")
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared", "-cudart", "static"]
+              "-Xcompiler", "-fPIC", "-shared", "-cudart", "static", "-ldl"]
 
 
 def nvcc() -> str:

@@ -4,6 +4,7 @@
 // passages each step follows.  No call here waits for the device except lofp_create
 // (one upload), lofp_stats, lofp_amplitudes_host and lofp_destroy.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // tracing: one NVTX range per API call (header-only NVTX v3)
 
 #include <algorithm>
 #include <cmath>
@@ -126,6 +127,7 @@ struct lofp_ctx {
   long long table_entries = 0;
   int grid = 0;
   long long slab_bytes = 0;
+  unsigned long long path_budget = 0;  // lofp_set_path_budget
   cudaEvent_t ev_start = nullptr, ev_u0 = nullptr, ev_u1 = nullptr, ev_end = nullptr;
   bool have_call = false, timed = false;
   lofp_run_stats stats{};
@@ -828,6 +830,7 @@ lofp_status prepare(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, cons
   P.slab_bytes = ctx->slab_bytes;
   P.units_per_block = (int)env_ll("LOFP_UNITS_PER_BLOCK", 2);
   P.force_generic = env_ll("LOFP_FORCE_GENERIC", 0) > 0 ? 1 : 0;
+  P.path_budget = ctx->path_budget;
   CK(ctx->d_units.ensure_async((size_t)(B * budget) * sizeof(Unit), stream), "alloc units");
   CK(ctx->d_partial.ensure_async((size_t)(B * budget) * 16, stream), "alloc partials");
   CK(ctx->d_sched.ensure_async((size_t)(B * budget) * 4, stream), "alloc schedule");
@@ -853,9 +856,15 @@ lofp_status prepare(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, cons
   return LOFP_OK;
 }
 
+struct NvtxRange {  // shows each call (and its kernels) as one range in Nsight Systems
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const int32_t *output_occ, double *amps,
                 unsigned long long *counts, cudaStream_t stream, int mode) {
   if (!ctx) return LOFP_E_INVALID_ARG;
+  NvtxRange range(mode == 0 ? (counts ? "lofp_amplitudes_counted" : "lofp_amplitudes") : "lofp_amplitudes_contract");
   ctx->err.clear();
   DeviceGuard guard(ctx->device);
   CallParams P;
@@ -975,6 +984,12 @@ lofp_status lofp_distribution(lofp_ctx *ctx, const int32_t *input_occ, int64_t m
   return run(ctx, input_occ, (int64_t)c, outputs, amps, nullptr, (cudaStream_t)cuda_stream, method == 0 ? 1 : 0);
 }
 
+lofp_status lofp_set_path_budget(lofp_ctx *ctx, uint64_t max_paths_per_output) {
+  if (!ctx) return LOFP_E_INVALID_ARG;
+  ctx->path_budget = max_paths_per_output;
+  return LOFP_OK;
+}
+
 lofp_status lofp_amplitudes_host(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const int32_t *output_occ,
                                  double *amps) {
   if (!ctx) return LOFP_E_INVALID_ARG;
@@ -1017,6 +1032,7 @@ lofp_status lofp_stats(lofp_ctx *ctx, lofp_run_stats *out) {
     st.max_list = (int64_t)hc->max_list;
     st.terms = (int64_t)hc->contractions;
     st.generic = (int64_t)hc->generic;
+    st.over_budget = (int64_t)hc->over_budget;
     for (int i = 0; i < 8; ++i) st.phase_cycles[i] = (int64_t)hc->phase[i];
     if (ctx->timed) {
       float ms = 0.f;

@@ -136,9 +136,10 @@ struct Counters {        // device counters of one call (zeroed by the host)
   unsigned long long thr;        // unit size of the call (paths)
   unsigned long long phase[8];   // unit kernel, thread 0's SM clocks per phase
   unsigned long long generic;    // outputs evaluated by the generic (layer-major) engine
+  unsigned long long over_budget;// outputs above the caller's path budget (NaN, not evaluated)
 };
 
-enum : uint8_t { kStatusOk = 0, kStatusZero = 1, kStatusBad = 2, kStatusUnsupported = 3 };
+enum : uint8_t { kStatusOk = 0, kStatusZero = 1, kStatusBad = 2, kStatusUnsupported = 3, kStatusOverBudget = 4 };
 
 struct CallParams {
   int M, D, N, B, nbs, ngate;
@@ -161,6 +162,7 @@ struct CallParams {
   const uint64_t *cone;      // generic engine: [D+1][M][2][2] past / future cone masks of (t, m)
   int seq_gl0;               // gates of layers 0..seq_gl0-1 apply before the first BS
   int force_generic;         // test hook (LOFP_FORCE_GENERIC): every output by the generic engine
+  unsigned long long path_budget;  // outputs with more paths are not evaluated (0 = no limit)
   const double *gate_ab;     // [ngate][2] (a, b)
   const int16_t *gate_mode;  // [ngate] mode, for M == 1 (no cut to fold into)
   const int16_t *gate_after; // [ngate] layer

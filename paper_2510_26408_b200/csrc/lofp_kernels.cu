@@ -1087,11 +1087,13 @@ __global__ void __launch_bounds__(kThreads) lofp_plan_kernel(const __grid_consta
       dp_counts(p, b, sh, 0, 0, true);
       if (b.cR[sh.cb[0]] == 0) st = kStatusZero;
     }
+    if (st == kStatusOk && p.path_budget && b.cR[sh.cb[0]] > p.path_budget) st = kStatusOverBudget;
     if (tid == 0) {
       p.pdone[q] = 0;
       p.status[q] = (uint8_t)st;
       p.pexp[q] = st == kStatusOk ? b.cR[sh.cb[0]] : 0ull;
       if (st == kStatusOk) atomicAdd(&p.ctr->feasible, 1ull);
+      if (st == kStatusOverBudget) atomicAdd(&p.ctr->over_budget, 1ull);
       if (st == kStatusBad) atomicAdd(&p.ctr->bad_rows, 1ull);
       if (st == kStatusUnsupported) atomicAdd(&p.ctr->unsupported, 1ull);
     }
@@ -1333,7 +1335,7 @@ __global__ void lofp_final_kernel(const __grid_constant__ CallParams p) {
         a.y += v.y;
       }
       if (p.pdone[q] != p.pexp[q]) atomicAdd(&p.ctr->table_error, 1ull);  // every path exactly once
-    } else if (st == kStatusBad || st == kStatusUnsupported) {
+    } else if (st == kStatusBad || st == kStatusUnsupported || st == kStatusOverBudget) {
       a = make_double2(__longlong_as_double(0x7ff8000000000000ll), __longlong_as_double(0x7ff8000000000000ll));
     }
     p.amps[q] = a;

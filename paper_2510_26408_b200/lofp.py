@@ -33,7 +33,7 @@ class lofp_run_stats(ctypes.Structure):
                 ("pairs", ctypes.c_int64), ("elements", ctypes.c_int64), ("unsupported", ctypes.c_int64),
                 ("bad_rows", ctypes.c_int64), ("check_errors", ctypes.c_int64), ("max_states", ctypes.c_int64),
                 ("max_list", ctypes.c_int64), ("table_entries", ctypes.c_int64), ("terms", ctypes.c_int64),
-                ("generic", ctypes.c_int64),
+                ("over_budget", ctypes.c_int64), ("generic", ctypes.c_int64),
                 ("phase_cycles", ctypes.c_int64 * 8),
                 ("grid_blocks", ctypes.c_int32), ("block_threads", ctypes.c_int32),
                 ("launches", ctypes.c_int32), ("mode", ctypes.c_int32),
@@ -41,7 +41,7 @@ class lofp_run_stats(ctypes.Structure):
 
 
 EXPORTS = ["lofp_create", "lofp_create_ex", "lofp_amplitudes", "lofp_amplitudes_counted", "lofp_amplitudes_contract",
-           "lofp_distribution", "lofp_amplitudes_host",
+           "lofp_distribution", "lofp_set_path_budget", "lofp_amplitudes_host",
            "lofp_destroy", "lofp_status_string", "lofp_last_error", "lofp_stats"]
 
 
@@ -66,6 +66,8 @@ def _load():
     lib.lofp_distribution.argtypes = [P, ctypes.POINTER(ctypes.c_int32), ctypes.c_int64, P, P,
                                       ctypes.POINTER(ctypes.c_int64), ctypes.c_int32, P]
     lib.lofp_distribution.restype = ctypes.c_int
+    lib.lofp_set_path_budget.argtypes = [P, ctypes.c_uint64]
+    lib.lofp_set_path_budget.restype = ctypes.c_int
     lib.lofp_amplitudes_host.argtypes = [P, ctypes.POINTER(ctypes.c_int32), ctypes.c_int64, P, P]
     lib.lofp_amplitudes_host.restype = ctypes.c_int
     lib.lofp_destroy.argtypes = [P]
@@ -224,6 +226,10 @@ class Circuit:
                                         0 if method == "contract" else 1, ctypes.c_void_p(strm))
         self._check(st)
         return T, torch.view_as_complex(out)
+
+    def set_path_budget(self, max_paths_per_output: int = 0):
+        """Skip (NaN) outputs with more valid paths than this in path-sum calls; 0 = no limit."""
+        self._check(_lib.lofp_set_path_budget(self._h, int(max_paths_per_output)))
 
     def amplitudes_host(self, S, T) -> np.ndarray:
         """End-to-end call with host buffers (numpy in, numpy out)."""

@@ -286,3 +286,24 @@ def test_context_reuse_new_input_and_two_streams(lofp):
     assert tol_ok(a1.cpu().numpy(), r1)[0]
     assert tol_ok(a2.cpu().numpy(), r2)[0]
     assert tol_ok(a3.cpu().numpy(), r1)[0]
+
+
+def test_path_budget(lofp):
+    """lofp_set_path_budget (SURVEY §5 failure guard): outputs above the budget are not
+    enumerated (NaN, counted); the others are unchanged."""
+    c, T, P = _cfg4_slice(96)
+    circ = lofp.Circuit(c.M, c.layers)
+    full, _, _ = run(lofp, c.M, c.layers, c.S, T)
+    budget = int(np.median(P))
+    circ.set_path_budget(budget)
+    cnt = torch.zeros(len(T), dtype=torch.int64, device="cuda")
+    a = circ.amplitudes(c.S, torch.from_numpy(T).cuda(), counts=cnt).cpu().numpy()
+    st = circ.stats()
+    over = P > budget
+    assert st["over_budget"] == int(over.sum()) > 0
+    assert np.isnan(a[over]).all()
+    assert tol_ok(a[~over], full[~over])[0]  # (another batch total: other unit sizes, other rounding)
+    assert np.array_equal(cnt.cpu().numpy()[~over].astype(np.uint64), P[~over])
+    circ.set_path_budget(0)
+    b = circ.amplitudes(c.S, torch.from_numpy(T).cuda()).cpu().numpy()
+    assert np.array_equal(b, full)
