@@ -1416,19 +1416,25 @@ __global__ void __launch_bounds__(kThreads) lofp_contract_kernel(const __grid_co
       double2 root = make_double2(1.0, 0.0);
       if (M == 1)
         for (int g = 0; g < p.ngate; ++g) root = cmul(root, p.gate_tab[g * (p.N + 1) + p.N]);
-      uint32_t *nz = b.tmp;  // states of column k with a nonzero entry in the current level
+      // nz[s] == k+1: state s of column k+1 has a nonzero entry in the level being built
+      // (generation stamps: no clearing; two arrays alternate between the columns)
+      uint32_t *nzc = b.tmp, *nzn = b.tmp2;
+      for (int s = tid; s < kMaxStates; s += kThreads) nzc[s] = 0u;
+      __syncthreads();
       for (int s1 = tid; s1 < sh.n[1]; s1 += kThreads) {
         const bool on = (!with_counts || b.cR[sh.cb[1] + s1] != 0) && compat(p, b, sh, 1, 0, s1);
         A[s1] = on ? root : make_double2(0.0, 0.0);
-        nz[s1] = on;
+        nzc[s1] = on ? 1u : 0u;
       }
+      for (int s = tid; s < kMaxStates; s += kThreads) nzn[s] = 0u;
       __syncthreads();
       for (int k = 1; k <= M - 1; ++k) {  // contract cut k: level (k-1, k) -> (k, k+1)
         const int nA = sh.n[k - 1], nB = sh.n[k], nC = sh.n[k + 1];
         for (int t = tid; t < nB * nC; t += kThreads) {
           const int sb = t / nC, sc = t - sb * nC;
           double2 sum = make_double2(0.0, 0.0);
-          if (nz[sb] && (!with_counts || b.cR[sh.cb[k + 1] + sc] != 0) && compat(p, b, sh, k + 1, sb, sc)) {
+          if (nzc[sb] == (uint32_t)k && (!with_counts || b.cR[sh.cb[k + 1] + sc] != 0) &&
+              compat(p, b, sh, k + 1, sb, sc)) {
             for (int sa = 0; sa < nA; ++sa) {
               const double2 a = A[sa * nB + sb];
               if (a.x == 0.0 && a.y == 0.0) continue;
@@ -1439,18 +1445,11 @@ __global__ void __launch_bounds__(kThreads) lofp_contract_kernel(const __grid_co
             }
           }
           Bn[t] = sum;
-        }
-        __syncthreads();
-        for (int sc = tid; sc < nC; sc += kThreads) {  // columns of the new level still carrying
-          uint32_t on = 0;
-          for (int sb = 0; sb < nB && !on; ++sb) {
-            const double2 v = Bn[sb * nC + sc];
-            on = (v.x != 0.0 || v.y != 0.0);
-          }
-          nz[sc] = on;
+          if (sum.x != 0.0 || sum.y != 0.0) nzn[sc] = (uint32_t)(k + 1);  // (same value from all writers)
         }
         __syncthreads();
         double2 *tt = A; A = Bn; Bn = tt;
+        uint32_t *tz = nzc; nzc = nzn; nzn = tz;
       }
       // the last level (c_{M-1}, c_M): its sum is the amplitude
       const int nL = sh.n[M - 1] * sh.n[M];
