@@ -218,6 +218,9 @@ typedef struct {
                              lists, 3 right lists, 4 pair list and scaling tables, 5 warp tiles
                              (path products), 6 waiting for the block's other warps after the
                              tiles, 7 unit fetch, output setup, stack pops and reduction */
+  int64_t tile_cycles[2]; /* unit kernel, warp clocks (lane 0, summed over warps) in the path-
+                             product tiles: [0] staging the tile's X and Y values, [1] the FMA
+                             loop */
   int32_t grid_blocks;    /* persistent grid of the unit kernel */
   int32_t block_threads;  /* threads per block */
   int32_t launches;       /* kernels launched by the call */

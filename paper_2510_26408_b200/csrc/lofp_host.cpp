@@ -1033,6 +1033,8 @@ lofp_status lofp_stats(lofp_ctx *ctx, lofp_run_stats *out) {
     st.terms = (int64_t)hc->contractions;
     st.generic = (int64_t)hc->generic;
     st.over_budget = (int64_t)hc->over_budget;
+    st.tile_cycles[0] = (int64_t)hc->tile_stage;
+    st.tile_cycles[1] = (int64_t)hc->tile_fma;
     for (int i = 0; i < 8; ++i) st.phase_cycles[i] = (int64_t)hc->phase[i];
     if (ctx->timed) {
       float ms = 0.f;

@@ -137,6 +137,8 @@ struct Counters {        // device counters of one call (zeroed by the host)
   unsigned long long phase[8];   // unit kernel, thread 0's SM clocks per phase
   unsigned long long generic;    // outputs evaluated by the generic (layer-major) engine
   unsigned long long over_budget;// outputs above the caller's path budget (NaN, not evaluated)
+  unsigned long long tile_stage; // warp clocks staging X / Y of the path-product tiles
+  unsigned long long tile_fma;   // warp clocks in the path-product FMA loop
 };
 
 enum : uint8_t { kStatusOk = 0, kStatusZero = 1, kStatusBad = 2, kStatusUnsupported = 3, kStatusOverBudget = 4 };

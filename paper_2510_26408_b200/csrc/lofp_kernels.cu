@@ -664,7 +664,7 @@ __device__ void expand_level(const CallParams &p, Block &b, Shared &sh, int k, i
 // cut factors of ks and ks+1 scale the two lists per pair.  Both lists are built level by
 // level (BFS with exact bucket offsets from the counts: deterministic, no atomics).
 __device__ void process_stack(const CallParams &p, Block &b, Shared &sh, double2 *sY, double2 (&acc)[kKX],
-                              ull &npaths, ull &cm, ull &nelem) {
+                              ull &npaths, ull &cm, ull &nelem, ull &tstage, ull &tfma) {
   const int M = p.M, tid = threadIdx.x;
   while (true) {
     if (tid == 0) {
@@ -889,6 +889,7 @@ __device__ void process_stack(const CallParams &p, Block &b, Shared &sh, double2
           const double2 *Yp = (pr.swap ? Lp[curL] : Rp[curR]) + pr.yoff;
           const uint16_t *Yc = (pr.swap ? Lc[curL] : Rc[curR]) + pr.yoff;
           const double2 *FY = pr.swap ? FLall + (long long)lo * nctxL : FRall + (long long)lo * nctxR;
+          const long long tc0 = clock64();
           const uint32_t y0 = yt * kYT, len = min((uint32_t)kYT, pr.nY - y0);
 #pragma unroll
           for (int r = 0; r < kYT / 32; ++r) {
@@ -915,9 +916,14 @@ __device__ void process_stack(const CallParams &p, Block &b, Shared &sh, double2
           }
           cm += nv;
           __syncwarp();
+          const long long tc1 = clock64();
           fma_block(x, sW, len, acc);
           npaths += (ull)nv * len;
           __syncwarp();
+          if (lane == 0) {
+            tstage += (ull)(tc1 - tc0);
+            tfma += (ull)(clock64() - tc1);
+          }
         }
         PHASE(sh, 5);
         __syncthreads();
@@ -1254,7 +1260,7 @@ __global__ void __launch_bounds__(kThreads, 2) lofp_units_kernel(const __grid_co
   Block b = make_block(p);
   load_cols(p, sh);
   const int tid = threadIdx.x;
-  ull cm = 0, nelem = 0;
+  ull cm = 0, nelem = 0, tstage = 0, tfma = 0;
   if (tid == 0) {
     for (int i = 0; i < 8; ++i) sh.ph[i] = 0;
     sh.tph = clock64();
@@ -1300,7 +1306,7 @@ __global__ void __launch_bounds__(kThreads, 2) lofp_units_kernel(const __grid_co
 #pragma unroll
     for (int r = 0; r < kKX; ++r) acc[r] = make_double2(0.0, 0.0);
     ull np = 0;
-    process_stack(p, b, sh, sY, acc, np, cm, nelem);
+    process_stack(p, b, sh, sY, acc, np, cm, nelem, tstage, tfma);
     ull np_tot = 0;
     reduce_block(sh, acc, &p.partial[u], np, &np_tot);
     if (tid == 0) {
@@ -1320,6 +1326,8 @@ __global__ void __launch_bounds__(kThreads, 2) lofp_units_kernel(const __grid_co
   if ((tid & 31) == 0) {
     atomicAdd(&p.ctr->cmuls, cm);
     atomicAdd(&p.ctr->elements, nelem);
+    atomicAdd(&p.ctr->tile_stage, tstage);
+    atomicAdd(&p.ctr->tile_fma, tfma);
   }
 }
 

@@ -34,7 +34,7 @@ class lofp_run_stats(ctypes.Structure):
                 ("bad_rows", ctypes.c_int64), ("check_errors", ctypes.c_int64), ("max_states", ctypes.c_int64),
                 ("max_list", ctypes.c_int64), ("table_entries", ctypes.c_int64), ("terms", ctypes.c_int64),
                 ("over_budget", ctypes.c_int64), ("generic", ctypes.c_int64),
-                ("phase_cycles", ctypes.c_int64 * 8),
+                ("phase_cycles", ctypes.c_int64 * 8), ("tile_cycles", ctypes.c_int64 * 2),
                 ("grid_blocks", ctypes.c_int32), ("block_threads", ctypes.c_int32),
                 ("launches", ctypes.c_int32), ("mode", ctypes.c_int32),
                 ("units_ms", ctypes.c_float), ("total_ms", ctypes.c_float)]
@@ -250,5 +250,6 @@ class Circuit:
             self._check(rc)
         d = {k: getattr(st, k) for k, _ in lofp_run_stats._fields_}
         d["phase_cycles"] = list(st.phase_cycles)
+        d["tile_cycles"] = list(st.tile_cycles)
         d["status"] = rc
         return d
