@@ -1561,7 +1561,7 @@ namespace {
 
 constexpr int kGenMaxBS = 1024;      // levels of the generic tree (BS count)
 constexpr int kGenFront = 8192;      // frontier entries of the prefix split
-constexpr ull kGenNodeBudget = 1ull << 26;  // tree nodes per thread before an output is given up
+constexpr ull kGenNodeBudget = 1ull << 22;  // tree nodes per thread before an output is given up (~5 s)
 
 struct GenEntry {
   double re, im;

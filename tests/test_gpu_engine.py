@@ -307,3 +307,29 @@ def test_path_budget(lofp):
     circ.set_path_budget(0)
     b = circ.amplitudes(c.S, torch.from_numpy(T).cuda()).cpu().numpy()
     assert np.array_equal(b, full)
+
+
+def test_limits_modes_layers(lofp):
+    """At the ABI limits: 128 modes (a 4-layer mesh, 10 photons) and 64 layers (a 4-mode
+    circuit whose BS sit in every 8th layer), values against the oracle and Ryser."""
+    rng = np.random.default_rng(128)
+    M = 128
+    layers = li.clements_mesh(M, 4, seed=128)
+    S = np.zeros(M, dtype=np.int32)
+    S[np.arange(0, 20, 2)] = 1
+    T = li.displaced_patterns(M, [i for i in range(M) if S[i]], 3, 200, rng)[0]
+    T = T[oracle.reachable(M, layers, S, T)][:40]
+    assert len(T) >= 10
+    got, cnt, st = run(lofp, M, layers, S, T)
+    ref, leaves = oracle.path_sum(M, layers, S, T, return_leaves=True)
+    assert tol_ok(got, ref)[0]
+    assert np.array_equal(cnt, leaves)
+    M, D = 4, 64  # 64 layers, every 8th carrying BS (a full 64-layer mesh has ~1e20 paths)
+    full = li.clements_mesh(M, 8, seed=64)
+    layers = [full[l // 8] if l % 8 == 0 else [] for l in range(D)]
+    S = np.array([1, 1, 0, 1], dtype=np.int32)
+    T = li.all_outputs(M, 3)
+    got, cnt, st = run(lofp, M, layers, S, T)
+    ref = oracle.amplitudes_permanent(M, layers, S, T)
+    assert tol_ok(got, ref)[0]
+    assert abs(np.sum(np.abs(got) ** 2) - 1) < 1e-12
