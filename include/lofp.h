@@ -228,6 +228,8 @@ typedef struct {
   float units_ms;         /* device time of the unit (enumeration) kernel, CUDA events;
                              contraction mode: of the contraction kernel */
   float total_ms;         /* device time from the first to the last kernel */
+  int64_t contract_deferred; /* contraction mode: outputs whose state space exceeded the
+                             warp-per-output kernel's limits and went to the block kernel */
 } lofp_run_stats;
 
 lofp_status lofp_stats(lofp_ctx *ctx, lofp_run_stats *out);

@@ -7,7 +7,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = [os.path.join(CSRC, f) for f in ("lofp_kernels.cu", "lofp_host.cpp")]
+SOURCES = [os.path.join(CSRC, f) for f in ("lofp_kernels.cu", "lofp_contract.cu", "lofp_host.cpp")]
 HEADERS = [os.path.join(CSRC, "lofp_internal.h"), os.path.join(ROOT, "include", "lofp.h")]
 LIB = os.path.join(HERE, "liblofp.so")
 PEAK_SRC = os.path.join(CSRC, "fp64_peak.cu")

@@ -1,0 +1,611 @@
+// lofp_contract.cu — the strip tensor contraction (NEXT-1) with one warp per
+// output, for nearest-neighbour circuits.
+//
+// The paper contracts the circuit block by block, keeping for every tuple of occupation
+// numbers that crosses from one block to the next its partial amplitude.  The
+// blocks here are the cuts: the state crossing cut k is the column pair
+// (c_{k-1}, c_k), and
+//     A_{k+1}(c_k, c_{k+1}) = sum_{c_{k-1}} A_k(c_{k-1}, c_k) f_k(c_{k-1}, c_k, c_{k+1})
+// with f_k the cut factor (the product of cut k's BS elements, eq. (1)).  The
+// amplitude is the sum of the last level.
+//
+// Why a warp per output: on the paper's workloads a column holds tens of states and a cut
+// a few hundred terms (configs[3]: <= 60 states, ~730 terms per cut), far too little for
+// a 256-thread block per output with a barrier per cut (lofp_contract_kernel, which stays
+// the fallback for larger state spaces and for non-local circuits).  Here 8 outputs share
+// a block, each warp walks its output's cuts with no block barrier, and a warp's lanes
+// split a level's entries evenly.
+//
+// Layout (no index arithmetic on a dense n x n square): for a nearest-neighbour mesh,
+// F_t(k-1) <= F_t(k) for every t is, for a fixed state of column k, an upper bound per
+// segment of column k-1 — the compatible states of column k-1 form a sub-box of its
+// mixed-radix state box, starting at the box's lower corner.  Level k stores, for every
+// state s of column k (a "row"), one entry per state of that sub-box in odometer order
+// (segment 0 fastest).  A row is walked by incrementing the packed segment values, so no
+// state is ever decoded inside the term loop.  Segment values are bytes packed in a u64
+// (<= 8 segments per column, i.e. <= 7 active layers per cut).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+
+#include "lofp_internal.h"
+
+using namespace lofp;
+
+namespace {
+
+typedef unsigned long long ull;
+
+#ifdef LOFP_DEBUG
+#define DCHECK_C(cond)                                                                         \
+  do {                                                                                         \
+    if (!(cond)) {                                                                             \
+      printf("LOFP_DEBUG contraction check failed at line %d block %d\n", __LINE__, blockIdx.x); \
+      __trap();                                                                                \
+    }                                                                                          \
+  } while (0)
+#else
+#define DCHECK_C(cond) \
+  do {                 \
+  } while (0)
+#endif
+
+constexpr int kCW = 8;             // warps (outputs in flight) per block
+constexpr int kCSeg = 8;           // segments per column: one byte each of a packed u64
+constexpr int kCMaxN = 4096;       // states per column (as the block kernel)
+constexpr int kCMaxStates = 16384; // states of all columns of one output
+constexpr int kCFac = 32;          // phase gates of one cut staged in shared memory
+
+constexpr int kCF = kCSeg - 1;     // BS of one cut (<= 7 active layers: 8 segments)
+constexpr int kCCmp = 2 * kCSeg;   // CmpPair checks between two columns
+
+struct GateW {           // one phase gate folded into the cut
+  int row;               // gate_tab row
+  uint8_t col_off;       // 0: it reads columns k-1 and k, 1: columns k and k+1
+  uint8_t seg_lo, seg_hi;
+  uint8_t slot;          // col_off 0: the byte of the entries' gather holding F(k-1)
+};
+
+struct CWarp {           // shared state of one warp's output
+  uint64_t lo[kMaxModes + 1];      // packed lower corner of each column's box
+  uint64_t hi[kMaxModes + 1];      // packed upper corner
+  uint32_t vbase[kMaxModes + 1];   // first packed state of each column in the scratch
+  uint16_t n[kMaxModes + 1];       // states per column
+  uint8_t nseg[kMaxModes + 1];
+  int16_t G[kMaxModes + 1];        // cum(T)
+  // cut k being contracted (staged once per cut)
+  int ftab[kCF];                   // Appendix-A block of each of its BS (offset in the table)
+  uint32_t fsh[kCF];               // segments it reads: i (column k) | sC << 8 (column k+1)
+  uint16_t cmpR[kCCmp];            // CmpPairs (sa | sb << 8) of column k+1
+  GateW gat[kCFac];
+  uint8_t gseg[kCSeg];             // cut k+1: the segments of column k its factors read
+  int ngs;                         // (the bytes each entry of level k+1 carries)
+};
+
+__device__ __forceinline__ int byte_at(uint64_t v, int j) { return (int)((v >> (8 * j)) & 0xffu); }
+
+__device__ __forceinline__ uint64_t set_byte(uint64_t v, int j, int b) {
+  const int s = 8 * j;
+  return (v & ~(0xffull << s)) | ((uint64_t)(uint32_t)b << s);
+}
+
+__device__ __forceinline__ ull sat_add_c(ull a, ull b) {
+  const ull c = a + b;
+  return c < a ? ~0ull : c;
+}
+
+// Upper corner of the sub-box of column k-1 compatible with state vr of column k:
+// F_t(k-1) <= F_t(k) on every time interval (CmpPair list of column k).
+__device__ __forceinline__ uint64_t sub_hi(const CallParams &p, const CWarp &w, int k, uint64_t vr) {
+  uint64_t h = w.hi[k - 1];
+  const ColInfo ck = p.col[k];
+  for (int c = 0; c < ck.ncmp; ++c) {
+    const CmpPair pr = p.cmp[ck.cmp_base + c];
+    const int v = byte_at(vr, pr.sb);
+    if (v < byte_at(h, pr.sa)) h = set_byte(h, pr.sa, v);
+  }
+  return h;
+}
+
+__device__ __forceinline__ uint32_t box_count(uint64_t lo, uint64_t hi, int ns) {
+  uint32_t c = 1;
+  for (int j = 0; j < ns; ++j) {
+    const int d = byte_at(hi, j) - byte_at(lo, j) + 1;
+    c = d > 0 ? c * (uint32_t)d : 0u;
+  }
+  return c;
+}
+
+// sub_hi with the column's CmpPairs staged in shared memory
+__device__ __forceinline__ uint64_t sub_hi_s(uint64_t h, const uint16_t *cmp, int ncmp, uint64_t vr) {
+  for (int c = 0; c < ncmp; ++c) {
+    const int sa = cmp[c] & 0xff, v = byte_at(vr, cmp[c] >> 8);
+    if (v < byte_at(h, sa)) h = set_byte(h, sa, v);
+  }
+  return h;
+}
+
+// The bytes of a column-(c-1) state that cut c's factor reads ("gather" slots): F_{l-1}(c-1)
+// for each BS of cut c in order, then the column-(c-1) end of each gate folded into cut c
+// with col_off 0.  Every level entry carries its row-side state's gather for the next cut,
+// so the term loop reads A = F_{l-1}(c-1) as byte f of one register.  (lane 0)
+__device__ void stage_gather(const CallParams &p, CWarp &w, int c) {
+  int n = 0;
+  if (c >= 1 && c <= p.M - 1) {
+    const ColInfo cc = p.col[c];
+    for (int f = 0; f < cc.nfac && n < kCSeg; ++f) w.gseg[n++] = p.fac[cc.fac_base + f].sA;
+    for (int g = 0; g < cc.ngate && n < kCSeg; ++g) {
+      const GateInfo gi = p.gat[cc.gate_base + g];
+      if (!gi.col_off) w.gseg[n++] = gi.seg_lo;
+    }
+  }
+  w.ngs = n;
+}
+
+__device__ __forceinline__ uint64_t gather(uint64_t v, const uint8_t *gseg, int ngs) {
+  uint64_t g = 0;
+  for (int j = 0; j < ngs; ++j) g |= (uint64_t)byte_at(v, gseg[j]) << (8 * j);
+  return g;
+}
+
+// Rows of the level whose rows are the states of column k (entries: the compatible
+// sub-box of column k-1): exclusive offsets into roff[0..n_k], returns the entry count.
+__device__ uint32_t level_rows(const CallParams &p, const CWarp &w, const uint64_t *vals, int k, uint32_t *roff,
+                               int lane) {
+  const int nk = w.n[k], ns = w.nseg[k - 1];
+  uint32_t run = 0;
+  for (int base = 0; base < nk; base += 32) {
+    const int s = base + lane;
+    uint32_t c = 0;
+    if (s < nk) c = box_count(w.lo[k - 1], sub_hi(p, w, k, vals[w.vbase[k] + s]), ns);
+    uint32_t incl = c;
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += v;
+    }
+    if (s < nk) roff[s] = run + incl - c;
+    run += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (lane == 0) roff[nk] = run;
+  __syncwarp();
+  return run;
+}
+
+// Per-output setup: G = cum(T), the light-cone box of every column (readings R5, R15),
+// the packed states.  Returns kStatusOk / Zero / Bad / Deferred (warp-uniform).
+__device__ int setup_warp(const CallParams &p, CWarp &w, uint64_t *vals, int q, int lane) {
+  const int M = p.M;
+  // G = cum(T); negative entries make the row bad, totals other than N an exact zero
+  int bad = 0, run = 0;
+  if (lane == 0) w.G[0] = 0;
+  for (int base = 0; base < M; base += 32) {
+    const int i = base + lane;
+    int t = 0;
+    if (i < M) {
+      t = p.T[(long long)q * M + i];
+      if (t < 0) bad = 1;
+      t = min(max(t, 0), 255);
+    }
+    int incl = t;
+    for (int d = 1; d < 32; d <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += v;
+    }
+    if (i < M) w.G[i + 1] = (int16_t)min(run + incl, 32767);
+    run += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  bad = __any_sync(0xffffffffu, bad);
+  if (bad) return kStatusBad;
+  if (run != p.N) return kStatusZero;  // photon number (reading R9)
+  __syncwarp();
+  // segment boxes: backward (T) and forward (S) light cones intersected
+  int zero = 0, defer = 0;
+  for (int k = lane; k <= M; k += 32) {
+    const ColInfo ci = p.col[k];
+    int slots = ci.nfac;
+    for (int g = 0; g < ci.ngate; ++g) slots += p.gat[ci.gate_base + g].col_off ? 0 : 1;
+    if (ci.nseg > kCSeg || ci.nfac > kCF || ci.ngate > kCFac || ci.ncmp > kCCmp || slots > kCSeg) {
+      defer = 1;
+      w.n[k] = 0;
+      continue;
+    }
+    uint64_t lo = 0, hi = 0;
+    uint32_t n = 1;
+    for (int i = 0; i < ci.nseg; ++i) {
+      const SegInfo si = p.seg[ci.seg_base + i];
+      const int l = max((int)w.G[si.rho], (int)p.cumS[si.rhop]);
+      const int h = min((int)w.G[si.sig], (int)p.cumS[si.sigp]);
+      if (h < l) {
+        n = 0;
+      } else {
+        lo = set_byte(lo, i, l);
+        hi = set_byte(hi, i, h);
+        n = min(n * (uint32_t)(h - l + 1), (uint32_t)kCMaxN + 1);
+      }
+    }
+    if (n == 0) zero = 1;
+    if (n > (uint32_t)kCMaxN) defer = 1;
+    w.lo[k] = lo;
+    w.hi[k] = hi;
+    w.n[k] = (uint16_t)min(n, (uint32_t)kCMaxN);
+    w.nseg[k] = ci.nseg;
+  }
+  zero = __any_sync(0xffffffffu, zero);
+  defer = __any_sync(0xffffffffu, defer);
+  if (zero) return kStatusZero;  // a column with no state: structurally unreachable (R5)
+  if (defer || p.tab_off[p.nbs] > 0x7fffffffll) return kStatusDeferred;  // (int32 table offsets)
+  __syncwarp();
+  // first packed state of each column
+  uint32_t tot = 0;
+  for (int base = 0; base <= M; base += 32) {
+    const int k = base + lane;
+    const uint32_t c = k <= M ? w.n[k] : 0u;
+    uint32_t incl = c;
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += v;
+    }
+    if (k <= M) w.vbase[k] = tot + incl - c;
+    tot += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (tot > (uint32_t)kCMaxStates) return kStatusDeferred;
+  __syncwarp();
+  if (lane == 0) atomicMax(&p.ctr->max_states, (ull)tot);
+  // packed segment values of every state (mixed radix, segment 0 fastest)
+  for (int k = 0; k <= M; ++k) {
+    const int nk = w.n[k], ns = w.nseg[k];
+    const uint64_t lo = w.lo[k], hi = w.hi[k];
+    for (int s = lane; s < nk; s += 32) {
+      uint64_t v = lo;
+      int r = s;
+      for (int i = 0; i < ns; ++i) {
+        const int rad = byte_at(hi, i) - byte_at(lo, i) + 1;
+        const int d = r % rad;
+        r /= rad;
+        v += (uint64_t)d << (8 * i);
+      }
+      vals[w.vbase[k] + s] = v;
+    }
+  }
+  __syncwarp();
+  return kStatusOk;
+}
+
+// Cut factor of one term (eq. (1)): for every BS f of the cut, the Appendix-A element
+// <y1, n-y1|BS|x1, n-x1> with x1 = Bm - A, y1 = Bp - A, n = C - A, where A = F_{l-1}(k-1)
+// is byte f of the entry's gather g and C, Bm, Bp are fixed by the entry (cb).  A vacuum
+// BS (n = 0) reads its block's first element, exactly 1 (reading R16).
+template <int NF, bool FULL>
+__device__ __forceinline__ double2 cut_fac(const double2 *__restrict__ table, const int *s_tri, const int (&tbo)[NF],
+                                           const uint32_t (&cb)[NF], int nfac, uint64_t g, double2 fac) {
+  // FULL (every cut of the circuit carries NF BS): no predicates, so the NF table loads are
+  // independent and issue back to back
+  double2 e[NF];
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    e[f] = make_double2(1.0, 0.0);
+    if (FULL || f < nfac) {
+      const int A = (int)((g >> (8 * f)) & 0xffu);
+      const int C = cb[f] & 0xff, Bm = (cb[f] >> 8) & 0xff, Bp = cb[f] >> 16;
+      const int n = C - A;
+      DCHECK_C(Bm >= A && C >= Bm && Bp >= A && Bp - A <= n);
+      e[f] = __ldg(table + (tbo[f] + s_tri[n] + (Bm - A) * (n + 1) + (Bp - A)));
+    }
+  }
+#pragma unroll
+  for (int f = 0; f < NF; ++f)
+    if (FULL || f < nfac) fac = make_double2(fac.x * e[f].x - fac.y * e[f].y, fac.x * e[f].y + fac.y * e[f].x);
+  return fac;
+}
+
+// phase gates of the cut on (column k-1, column k): n = F(k) - F(k-1) at their time
+__device__ __forceinline__ double2 gates_a(const CallParams &p, const CWarp &w, int ngate, uint64_t vb, uint64_t g,
+                                           double2 fac, ull &cm) {
+  for (int gi = 0; gi < ngate; ++gi) {
+    const GateW gw = w.gat[gi];
+    if (gw.col_off) continue;
+    const double2 ge = p.gate_tab[gw.row * (p.N + 1) + byte_at(vb, gw.seg_hi) - (int)((g >> (8 * gw.slot)) & 0xffu)];
+    fac = make_double2(fac.x * ge.x - fac.y * ge.y, fac.x * ge.y + fac.y * ge.x);
+    ++cm;
+  }
+  return fac;
+}
+
+// The sum over one row of level k (the states of column k-1 compatible with sb) of
+// A_k(c_{k-1}, sb) f_k(c_{k-1}, sb, sc): two entries per step, loads first.
+template <int NF, bool CNT, bool FULL>
+__device__ __forceinline__ void row_sum(const double2 *__restrict__ table, const int *s_tri, const int (&tbo)[NF],
+                                        const uint32_t (&cb)[NF], int nfac, double2 gfix, const CallParams &p,
+                                        const CWarp &w, int ngate, uint64_t vb, const double2 *__restrict__ Ac,
+                                        const uint64_t *__restrict__ Gc, const ull *__restrict__ Cc, uint32_t r0,
+                                        uint32_t r1, double &sx, double &sy, ull &csum, ull &cm, ull &terms) {
+  uint32_t r = r0;
+  for (; r + 2 <= r1; r += 2) {
+    const double2 a0 = Ac[r], a1 = Ac[r + 1];
+    const uint64_t g0 = Gc[r], g1 = Gc[r + 1];
+    if (CNT) csum = sat_add_c(csum, sat_add_c(Cc[r], Cc[r + 1]));
+    double2 f0 = cut_fac<NF, FULL>(table, s_tri, tbo, cb, nfac, g0, gfix);
+    double2 f1 = cut_fac<NF, FULL>(table, s_tri, tbo, cb, nfac, g1, gfix);
+    if (ngate) {
+      f0 = gates_a(p, w, ngate, vb, g0, f0, cm);
+      f1 = gates_a(p, w, ngate, vb, g1, f1, cm);
+    }
+    sx = fma(a0.x, f0.x, fma(-a0.y, f0.y, sx));
+    sy = fma(a0.x, f0.y, fma(a0.y, f0.x, sy));
+    sx = fma(a1.x, f1.x, fma(-a1.y, f1.y, sx));
+    sy = fma(a1.x, f1.y, fma(a1.y, f1.x, sy));
+    terms += (a0.x != 0.0 || a0.y != 0.0) + (a1.x != 0.0 || a1.y != 0.0);
+    cm += 2 * nfac;
+  }
+  if (r < r1) {
+    const double2 a0 = Ac[r];
+    const uint64_t g0 = Gc[r];
+    if (CNT) csum = sat_add_c(csum, Cc[r]);
+    double2 f0 = cut_fac<NF, FULL>(table, s_tri, tbo, cb, nfac, g0, gfix);
+    if (ngate) f0 = gates_a(p, w, ngate, vb, g0, f0, cm);
+    sx = fma(a0.x, f0.x, fma(-a0.y, f0.y, sx));
+    sy = fma(a0.x, f0.y, fma(a0.y, f0.x, sy));
+    terms += (a0.x != 0.0 || a0.y != 0.0);
+    cm += nfac;
+  }
+}
+
+}  // namespace
+
+// NF: the most BS any cut carries (<= 7; loops unrolled to it), CNT: exact path counts too
+template <int NF, bool CNT>
+__global__ void __launch_bounds__(32 * kCW, 2) lofp_contract_warp_kernel(const __grid_constant__ CallParams p) {
+  __shared__ CWarp sw[kCW];
+  __shared__ int s_tri[kMaxPhotons + 2];  // tri(n) = sum_{m<n} (m+1)^2: block offsets in a BS table
+  for (int n = threadIdx.x; n <= kMaxPhotons + 1; n += blockDim.x) s_tri[n] = n * (n + 1) * (2 * n + 1) / 6;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  CWarp &w = sw[wib];
+  const int M = p.M;
+  constexpr bool with_counts = CNT;
+  // warp scratch: packed states, two row-offset arrays, two levels (values, gathers [, counts])
+  char *ws = p.slab + ((long long)blockIdx.x * kCW + wib) * p.cw_bytes;
+  uint64_t *vals = (uint64_t *)ws;
+  uint32_t *const roff0 = (uint32_t *)(vals + kCMaxStates), *const roff1 = roff0 + (kCMaxN + 1);
+  char *lv0 = (char *)(roff1 + kCMaxN + 1);
+  lv0 = (char *)(((uintptr_t)lv0 + 15) & ~(uintptr_t)15);
+  const long long per = with_counts ? 32 : 24;
+  const long long capE = (p.cw_bytes - (lv0 - ws)) / (2 * per);
+  double2 *const lvA = (double2 *)lv0, *const lvB = lvA + capE;
+  uint64_t *const lgA = (uint64_t *)(lvB + capE), *const lgB = lgA + capE;
+  ull *const lcA = (ull *)(lgB + capE), *const lcB = lcA + capE;
+#define ROFF(i) ((i) ? roff1 : roff0)
+#define LV(i) ((i) ? lvB : lvA)
+#define LG(i) ((i) ? lgB : lgA)
+#define LC(i) ((i) ? lcB : lcA)
+  ull cm = 0, terms = 0;
+  while (true) {
+    int q = 0;
+    if (lane == 0) q = (int)atomicAdd(&p.ctr->cticket, 1ull);
+    q = __shfl_sync(0xffffffffu, q, 0);
+    if (q >= p.B) break;
+    int st = setup_warp(p, w, vals, q, lane);
+    double re = 0.0, im = 0.0;
+    ull count = 0;
+    int cur = 0;
+    if (st == kStatusOk) {
+      // level 1: rows = states of column 1, entries = the single state of column 0
+      double2 root = make_double2(1.0, 0.0);
+      if (M == 1)
+        for (int g = 0; g < p.ngate; ++g) {
+          const double2 e = p.gate_tab[g * (p.N + 1) + p.N];
+          root = make_double2(root.x * e.x - root.y * e.y, root.x * e.y + root.y * e.x);
+        }
+      if (lane == 0) stage_gather(p, w, 1);
+      const uint32_t tot = level_rows(p, w, vals, 1, roff0, lane);
+      if (tot > (uint64_t)capE) st = kStatusDeferred;
+      if (st == kStatusOk) {
+        const uint64_t g0 = gather(vals[w.vbase[0]], w.gseg, w.ngs);
+        for (uint32_t t = lane; t < tot; t += 32) {
+          lvA[t] = root;
+          lgA[t] = g0;
+          if (with_counts) lcA[t] = 1ull;
+        }
+        __syncwarp();
+      }
+    }
+    // cuts 1..M-1: level k (rows: column k, entries: column k-1) -> level k+1
+    for (int k = 1; k <= M - 1 && st == kStatusOk; ++k) {
+      const int nxt = cur ^ 1;
+      const uint32_t totn = level_rows(p, w, vals, k + 1, ROFF(nxt), lane);
+      if (totn > (uint64_t)capE) {
+        st = kStatusDeferred;
+        break;
+      }
+      const ColInfo ck = p.col[k], ck1 = p.col[k + 1];
+      const int nfac = ck.nfac, ngate = ck.ngate, ncR = ck1.ncmp;
+      if (lane < nfac) {
+        const FacInfo fi = p.fac[ck.fac_base + lane];
+        w.ftab[lane] = (int)p.tab_off[fi.bs];
+        w.fsh[lane] = (uint32_t)fi.i | (uint32_t)fi.sC << 8;
+      }
+      if (lane < ncR) {
+        const CmpPair pr = p.cmp[ck1.cmp_base + lane];
+        w.cmpR[lane] = (uint16_t)(pr.sa | pr.sb << 8);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        int slot = nfac;  // the gather order of stage_gather(k)
+        for (int g = 0; g < ngate; ++g) {
+          const GateInfo gi = p.gat[ck.gate_base + g];
+          GateW gw;
+          gw.row = gi.gate;
+          gw.col_off = gi.col_off;
+          gw.seg_lo = gi.seg_lo;
+          gw.seg_hi = gi.seg_hi;
+          gw.slot = gi.col_off ? 0 : (uint8_t)slot++;
+          w.gat[g] = gw;
+        }
+        stage_gather(p, w, k + 1);  // what the entries of level k+1 carry for cut k+1
+      }
+      __syncwarp();
+      const double2 *__restrict__ table = p.table;
+      int tbo[NF];
+#pragma unroll
+      for (int f = 0; f < NF; ++f) tbo[f] = f < nfac ? w.ftab[f] : 0;
+      const uint32_t *rn = ROFF(nxt), *rc = ROFF(cur);
+      const double2 *Ac = LV(cur);
+      const uint64_t *Gc = LG(cur);
+      const ull *Cc = LC(cur);
+      double2 *An = LV(nxt);
+      uint64_t *Gn = LG(nxt);
+      ull *Cn = LC(nxt);
+      const uint64_t loB = w.lo[k], hiB = w.hi[k];
+      const int nsB = w.nseg[k];
+      const uint32_t vbC = w.vbase[k + 1];
+      int sc = 0, sc_last = -1;
+      uint64_t vc = 0, hB = 0;
+      for (uint32_t t = lane; t < totn; t += 32) {
+        while (rn[sc + 1] <= t) ++sc;
+        if (sc != sc_last) {  // the row's state (column k+1) and its sub-box of column k
+          vc = vals[vbC + sc];
+          hB = sub_hi_s(hiB, w.cmpR, ncR, vc);
+          sc_last = sc;
+        }
+        // entry t = the pos-th state of the sub-box (odometer order, segment 0 fastest)
+        uint32_t pos = t - rn[sc];
+        uint64_t vb = loB;
+        uint32_t sb = 0, stride = 1;  // sb: the state's index in column k's full box
+        for (int j = 0; j < nsB; ++j) {
+          const int l = byte_at(loB, j), rad = byte_at(hB, j) - l + 1;
+          if (rad > 1) {
+            const uint32_t d = pos % (uint32_t)rad;
+            pos /= (uint32_t)rad;
+            vb += (uint64_t)d << (8 * j);
+            sb += d * stride;
+          }
+          stride *= (uint32_t)(byte_at(hiB, j) - l + 1);
+        }
+        // per BS f the photon numbers fixed by (sb, sc): C = F_{l-1}(k+1), Bm = F_{l-1}(k),
+        // Bp = F_l(k); only A = F_{l-1}(k-1) varies along the row
+        uint32_t cb[NF];
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+          const uint32_t sh = f < nfac ? w.fsh[f] : 0u;
+          const int i = sh & 0xff;
+          cb[f] = (uint32_t)byte_at(vc, sh >> 8) | (uint32_t)byte_at(vb, i) << 8 | (uint32_t)byte_at(vb, i + 1) << 16;
+        }
+        double2 gfix = make_double2(1.0, 0.0);  // gates on (column k, column k+1): fixed too
+        for (int g = 0; g < ngate; ++g) {
+          const GateW gw = w.gat[g];
+          if (!gw.col_off) continue;
+          const double2 ge = p.gate_tab[gw.row * (p.N + 1) + byte_at(vc, gw.seg_hi) - byte_at(vb, gw.seg_lo)];
+          gfix = make_double2(gfix.x * ge.x - gfix.y * ge.y, gfix.x * ge.y + gfix.y * ge.x);
+          ++cm;
+        }
+        // sum over row sb of level k: the states of column k-1 compatible with sb
+        const uint32_t r0 = rc[sb], r1 = rc[sb + 1];
+        // (two entries per step, loads first; an entry whose value is 0 contributes 0)
+        double sx = 0.0, sy = 0.0;
+        ull csum = 0;
+        if (nfac == NF)
+          row_sum<NF, CNT, true>(table, s_tri, tbo, cb, nfac, gfix, p, w, ngate, vb, Ac, Gc, Cc, r0, r1, sx, sy, csum, cm,
+                                 terms);
+        else
+          row_sum<NF, CNT, false>(table, s_tri, tbo, cb, nfac, gfix, p, w, ngate, vb, Ac, Gc, Cc, r0, r1, sx, sy, csum,
+                                  cm, terms);
+        An[t] = make_double2(sx, sy);
+        Gn[t] = gather(vb, w.gseg, w.ngs);
+        if (with_counts) Cn[t] = csum;
+      }
+      __syncwarp();
+      cur = nxt;
+    }
+    if (st == kStatusOk) {
+      // the last level: one row (column M has one state); its sum is the amplitude
+      const uint32_t e = ROFF(cur)[1];
+      const double2 *Al = LV(cur);
+      const ull *Cl = LC(cur);
+      for (uint32_t t = lane; t < e; t += 32) {
+        re += Al[t].x;
+        im += Al[t].y;
+        if (with_counts) count = sat_add_c(count, Cl[t]);
+      }
+    }
+    // fixed-order warp reduction (deterministic)
+    for (int d = 16; d > 0; d >>= 1) {
+      re += __shfl_down_sync(0xffffffffu, re, d);
+      im += __shfl_down_sync(0xffffffffu, im, d);
+      count = sat_add_c(count, __shfl_down_sync(0xffffffffu, count, d));
+    }
+    if (lane == 0) {
+      if (st == kStatusOk && with_counts && count == 0) st = kStatusZero;
+      if (st == kStatusDeferred) {
+        atomicAdd(&p.ctr->cdeferred, 1ull);
+      } else {
+        double2 a = make_double2(re, im);
+        if (st == kStatusBad) a = make_double2(__longlong_as_double(0x7ff8000000000000ll),
+                                               __longlong_as_double(0x7ff8000000000000ll));
+        if (st != kStatusOk) a = st == kStatusBad ? a : make_double2(0.0, 0.0);
+        p.amps[q] = a;
+        if (with_counts) p.counts[q] = st == kStatusOk ? count : 0ull;
+        if (st == kStatusOk) atomicAdd(&p.ctr->feasible, 1ull);
+        if (st == kStatusBad) atomicAdd(&p.ctr->bad_rows, 1ull);
+      }
+      p.status[q] = (uint8_t)st;
+    }
+    __syncwarp();
+  }
+  for (int d = 16; d > 0; d >>= 1) {
+    cm += __shfl_down_sync(0xffffffffu, cm, d);
+    terms += __shfl_down_sync(0xffffffffu, terms, d);
+  }
+  if (lane == 0) {
+    atomicAdd(&p.ctr->cmuls, cm);
+    atomicAdd(&p.ctr->contractions, terms);
+  }
+}
+
+template <int NF, bool CNT>
+static int launch_nf(const CallParams *p, int grid, cudaStream_t stream) {
+  static int per_sm[32] = {0};
+  static int nsm[32] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev &= 31;
+  if (!per_sm[dev]) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], lofp_contract_warp_kernel<NF, CNT>, 32 * kCW, 0);
+    cudaDeviceGetAttribute(&nsm[dev], cudaDevAttrMultiProcessorCount, dev);
+    if (per_sm[dev] < 1) per_sm[dev] = 1;
+  }
+  long long blocks = (long long)per_sm[dev] * nsm[dev];
+  const long long need = ((long long)p->B + kCW - 1) / kCW;
+  if (need < blocks) blocks = need;
+  if (blocks < 1) return 0;
+  CallParams q = *p;
+  const long long total = (long long)grid * p->slab_bytes;
+  q.cw_bytes = (total / (blocks * kCW)) & ~255ll;
+  const long long fixed = (long long)kCMaxStates * 8 + 2ll * (kCMaxN + 1) * 4 + 16;
+  if (q.cw_bytes < fixed + 64 * 1024) return (int)cudaErrorInvalidValue;  // (not with the default slab)
+  lofp_contract_warp_kernel<NF, CNT><<<(int)blocks, 32 * kCW, 0, stream>>>(q);
+  return (int)cudaGetLastError();
+}
+
+template <int NF>
+static int launch_cnt(const CallParams *p, int grid, cudaStream_t stream) {
+  return p->counts ? launch_nf<NF, true>(p, grid, stream) : launch_nf<NF, false>(p, grid, stream);
+}
+
+// Launch: blocks of kCW warps, as many as are resident at once (the warps pull outputs from
+// a ticket counter); each warp's scratch is carved from the slab of the block kernels
+// (grid x slab_bytes), which runs after it on the same stream.  Instantiated per the most
+// BS a cut carries (outputs of circuits with more than 7 per cut are deferred anyway).
+extern "C" int lofp_launch_contract_warp(const CallParams *p, int grid, void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (p->max_nfac) {
+    case 0:
+    case 1: return launch_cnt<1>(p, grid, st);
+    case 2: return launch_cnt<2>(p, grid, st);
+    case 3: return launch_cnt<3>(p, grid, st);
+    case 4: return launch_cnt<4>(p, grid, st);
+    case 5: return launch_cnt<5>(p, grid, st);
+    case 6: return launch_cnt<6>(p, grid, st);
+    default: return launch_cnt<7>(p, grid, st);
+  }
+}

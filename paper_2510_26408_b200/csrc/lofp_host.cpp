@@ -830,6 +830,9 @@ lofp_status prepare(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, cons
   P.slab_bytes = ctx->slab_bytes;
   P.units_per_block = (int)env_ll("LOFP_UNITS_PER_BLOCK", 2);
   P.force_generic = env_ll("LOFP_FORCE_GENERIC", 0) > 0 ? 1 : 0;
+  P.contract_block_only = env_ll("LOFP_CONTRACT_BLOCK", 0) > 0 ? 1 : 0;
+  P.max_nfac = 0;
+  for (const ColInfo &ci : ctx->col) P.max_nfac = std::max(P.max_nfac, (int)ci.nfac);
   P.path_budget = ctx->path_budget;
   CK(ctx->d_units.ensure_async((size_t)(B * budget) * sizeof(Unit), stream), "alloc units");
   CK(ctx->d_partial.ensure_async((size_t)(B * budget) * 16, stream), "alloc partials");
@@ -1033,6 +1036,7 @@ lofp_status lofp_stats(lofp_ctx *ctx, lofp_run_stats *out) {
     st.terms = (int64_t)hc->contractions;
     st.generic = (int64_t)hc->generic;
     st.over_budget = (int64_t)hc->over_budget;
+    st.contract_deferred = (int64_t)hc->cdeferred;
     st.tile_cycles[0] = (int64_t)hc->tile_stage;
     st.tile_cycles[1] = (int64_t)hc->tile_fma;
     for (int i = 0; i < 8; ++i) st.phase_cycles[i] = (int64_t)hc->phase[i];

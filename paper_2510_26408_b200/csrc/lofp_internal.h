@@ -139,9 +139,12 @@ struct Counters {        // device counters of one call (zeroed by the host)
   unsigned long long over_budget;// outputs above the caller's path budget (NaN, not evaluated)
   unsigned long long tile_stage; // warp clocks staging X / Y of the path-product tiles
   unsigned long long tile_fma;   // warp clocks in the path-product FMA loop
+  unsigned long long cticket;    // contraction: output queue of the warp kernel
+  unsigned long long cdeferred;  // contraction: outputs the warp kernel left to the block kernel
 };
 
-enum : uint8_t { kStatusOk = 0, kStatusZero = 1, kStatusBad = 2, kStatusUnsupported = 3, kStatusOverBudget = 4 };
+enum : uint8_t { kStatusOk = 0, kStatusZero = 1, kStatusBad = 2, kStatusUnsupported = 3, kStatusOverBudget = 4,
+                 kStatusDeferred = 5 /* contraction: left by the warp kernel to the block kernel */ };
 
 struct CallParams {
   int M, D, N, B, nbs, ngate;
@@ -150,6 +153,10 @@ struct CallParams {
   int units_per_block;   // unit size = max(thr, total paths / (units_per_block * grid))
   unsigned long long thr;  // smallest unit size (paths); the call's is in Counters::thr
   long long slab_bytes;  // per-block scratch in global memory
+  long long cw_bytes;    // contraction warp kernel: scratch per warp (carved from the slab)
+  int deferred_only;     // contraction block kernel: only outputs with kStatusDeferred
+  int max_nfac;          // most BS a cut carries (contraction warp kernel instantiation)
+  int contract_block_only;  // test hook (LOFP_CONTRACT_BLOCK): contraction by the block kernel only
   long long table_cap;   // entries allocated for the Appendix-A table
   const ColInfo *col;
   const SegInfo *seg;
@@ -200,6 +207,7 @@ extern "C" {
 int lofp_launch_tables(const lofp::CallParams *p, void *stream);
 int lofp_launch_paths(const lofp::CallParams *p, int grid, void *stream, void *ev_units0, void *ev_units1);
 int lofp_launch_contract(const lofp::CallParams *p, int grid, void *stream);
+int lofp_launch_contract_warp(const lofp::CallParams *p, int grid, void *stream);  // lofp_contract.cu
 int lofp_units_grid(int device);
 int lofp_launch_outputs(int M, int N, long long count, int32_t *T, void *stream);
 int lofp_launch_generic(const lofp::CallParams *p, int grid, void *stream);

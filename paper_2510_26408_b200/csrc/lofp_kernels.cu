@@ -1407,6 +1407,7 @@ __global__ void __launch_bounds__(kThreads) lofp_contract_kernel(const __grid_co
   const int M = p.M, tid = threadIdx.x;
   ull cm = 0, terms = 0;
   for (int q = blockIdx.x; q < p.B; q += gridDim.x) {
+    if (p.deferred_only && p.status[q] != kStatusDeferred) continue;  // done by the warp kernel (uniform)
     int st = setup_output(p, b, sh, q);
     const bool with_counts = p.counts != nullptr;
     if (st == kStatusOk && with_counts) {
@@ -1505,7 +1506,16 @@ __global__ void __launch_bounds__(kThreads) lofp_contract_kernel(const __grid_co
 
 extern "C" int lofp_launch_contract(const CallParams *p, int grid, void *stream) {
   const int g = p->B < grid ? p->B : grid;
-  lofp_contract_kernel<<<g, kThreads, 0, (cudaStream_t)stream>>>(*p);
+  CallParams q = *p;
+  // nearest-neighbour circuits: one warp per output first (lofp_contract.cu); this block
+  // kernel then takes only the outputs it deferred (state spaces over the warp limits)
+  q.deferred_only = 0;
+  if (!p->general && !p->force_generic && !p->contract_block_only) {
+    const int e = lofp_launch_contract_warp(p, grid, stream);
+    if (e != 0) return e;
+    q.deferred_only = 1;
+  }
+  lofp_contract_kernel<<<g, kThreads, 0, (cudaStream_t)stream>>>(q);
   lofp_generic_kernel<<<grid, kThreads, 0, (cudaStream_t)stream>>>(*p);  // outputs over the column limits
   return (int)cudaGetLastError();
 }

@@ -37,7 +37,8 @@ class lofp_run_stats(ctypes.Structure):
                 ("phase_cycles", ctypes.c_int64 * 8), ("tile_cycles", ctypes.c_int64 * 2),
                 ("grid_blocks", ctypes.c_int32), ("block_threads", ctypes.c_int32),
                 ("launches", ctypes.c_int32), ("mode", ctypes.c_int32),
-                ("units_ms", ctypes.c_float), ("total_ms", ctypes.c_float)]
+                ("units_ms", ctypes.c_float), ("total_ms", ctypes.c_float),
+                ("contract_deferred", ctypes.c_int64)]
 
 
 EXPORTS = ["lofp_create", "lofp_create_ex", "lofp_amplitudes", "lofp_amplitudes_counted", "lofp_amplitudes_contract",

@@ -1,6 +1,6 @@
 """Attribute an ncu --set full capture of lofp_units_kernel to source functions.
 
-usage: python scripts/ncu_regions.py <report.ncu-rep> [liblofp.so]
+usage: python scripts/ncu_regions.py <report.ncu-rep> [liblofp.so] [kernel] [source file in csrc/]
 Pairs the report's per-SASS-instruction counters (program order) with the
 nvdisasm -g line info of the same build, then sums executed instructions, FP64
 instructions and warp-stall samples per device function of lofp_kernels.cu.
@@ -16,7 +16,9 @@ import tempfile
 rep = sys.argv[1]
 so = sys.argv[2] if len(sys.argv) > 2 else os.path.join(os.path.dirname(__file__), "..", "paper_2510_26408_b200",
                                                          "liblofp.so")
-src_path = os.path.join(os.path.dirname(__file__), "..", "paper_2510_26408_b200", "csrc", "lofp_kernels.cu")
+src_path = os.path.join(os.path.dirname(__file__), "..", "paper_2510_26408_b200", "csrc",
+                        sys.argv[4] if len(sys.argv) > 4 else "lofp_kernels.cu")
+SRC = os.path.basename(src_path)
 KERNEL = sys.argv[3] if len(sys.argv) > 3 else "lofp_units_kernel"
 
 # function line ranges of lofp_kernels.cu
@@ -52,7 +54,7 @@ for l in L[st + 1:]:
         break
     m = re.search(r'## File ".*/(\w+\.\w+)", line (\d+)', l)
     if m:
-        cur = int(m.group(2)) if m.group(1) == "lofp_kernels.cu" else cur
+        cur = int(m.group(2)) if m.group(1) == SRC else cur
         continue
     if re.match(r"\s+/\*[0-9a-f]{4,}\*/\s+[A-Z@{]", l):
         seq.append(cur)
@@ -85,3 +87,9 @@ for f in sorted(ex, key=lambda k: -stl[k]):
 print("hottest lines (stall samples):")
 for (f, ln), v in byline.most_common(12):
     print(f"  {100 * v / ts:5.1f}%  line {ln:5d} {f:18s} {lines[ln - 1].strip()[:80] if ln else ''}")
+print("hottest lines (instructions executed):")
+exl = collections.Counter()
+for ln, x in zip(seq, rows):
+    exl[ln] += int(x[iE] or 0)
+for ln, v in exl.most_common(16):
+    print(f"  {100 * v / te:5.1f}%  line {ln:5d} {lines[ln - 1].strip()[:90] if ln else ''}")

@@ -186,3 +186,47 @@ def test_distribution_config1_unitarity(lofp):
     assert abs(np.sum(np.abs(a) ** 2) - 1.0) < 1e-11
     pick = np.random.default_rng(1).choice(len(T), 200, replace=False)
     assert tol_ok(a[pick], oracle.path_sum(c.M, c.layers, c.S, T[pick]))[0]
+
+
+def test_warp_kernel_matches_block_kernel(lofp, monkeypatch):
+    """The warp-per-output contraction (lofp_contract.cu) and the block-per-output kernel
+    (forced by LOFP_CONTRACT_BLOCK) compute the same amplitudes and path counts on configs[3]
+    as literally drawn; the warp kernel defers none of them."""
+    c = li.config(3)
+    d = load(3)
+    T = d["T_literal"][:512].astype(np.int32)
+    a_w, cnt_w, st_w = contract(lofp, c.M, c.layers, c.S, T)
+    assert st_w["contract_deferred"] == 0 and st_w["check_errors"] == 0
+    monkeypatch.setenv("LOFP_CONTRACT_BLOCK", "1")
+    a_b, cnt_b, st_b = contract(lofp, c.M, c.layers, c.S, T)
+    assert np.array_equal(cnt_w, cnt_b) and np.array_equal(cnt_w, d["P_literal"][:512])
+    ok, err = tol_ok(a_w, a_b)
+    assert ok, err
+
+
+def test_warp_kernel_deterministic(lofp):
+    """Each output is summed by one warp in a fixed order: repeated calls are bitwise equal."""
+    c = li.config(3)
+    T = load(3)["T_literal"][:256].astype(np.int32)
+    circ = lofp.Circuit(c.M, c.layers)
+    Td = torch.from_numpy(T).cuda()
+    a = circ.contract(c.S, Td).cpu().numpy()
+    for _ in range(3):
+        assert np.array_equal(circ.contract(c.S, Td).cpu().numpy(), a)
+
+
+@pytest.mark.parametrize("N", [1, 2])
+def test_deep_circuit_defers_to_block_kernel(lofp, N):
+    """16 layers put 9 segments in a column (more than the warp kernel's packed 8): those
+    outputs are deferred in the same call to the block kernel (N = 1) or, past its column
+    limits, to the generic engine (N = 2); parity with the oracle either way."""
+    M, D = 4, 16
+    layers = li.clements_mesh(M, D, seed=1616)
+    S = np.array([1, 1, 0, 0][:M], dtype=np.int32) if N == 2 else np.array([0, 1, 0, 0], dtype=np.int32)
+    T = li.all_outputs(M, N)
+    got, cnt, st = contract(lofp, M, layers, S, T)
+    assert st["contract_deferred"] > 0 and st["unsupported"] == 0
+    ref, leaves = oracle.path_sum(M, layers, S, T, return_leaves=True)
+    assert tol_ok(got, ref)[0]
+    assert np.array_equal(cnt, leaves)
+    assert abs(np.sum(np.abs(got) ** 2) - 1) < 1e-12
