@@ -275,6 +275,37 @@ def distribution_arm(args, rank, world, local):
         print(json.dumps(line), flush=True)
 
 
+def contract_roofline(terms, cmuls, kernel_ms):
+    """Roofline of the contraction: FP64 lane instructions of its terms (a
+    complex multiply-accumulate each, 4) and cut-factor products (4 per complex
+    multiplication) over the call's device time, against the measured DFMA issue rate.  The
+    kernel is issue/latency bound on the integer index work around those FP64 operations;
+    the ncu capture of the same command (profiles/) gives its issue-slot utilisation."""
+    from paper_2510_26408_b200 import _build
+    lib = ctypes.CDLL(_build.PEAK_LIB)
+    lib.lofp_probe_fp64_dfma_rate.restype = ctypes.c_double
+    lib.lofp_probe_fp64_dfma_rate.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+    nsm = ctypes.c_int(0)
+    peak = lib.lofp_probe_fp64_dfma_rate(5, ctypes.byref(nsm)) / 1e12
+    alg = 4.0 * terms + 4.0 * cmuls
+    achieved = alg / (kernel_ms * 1e-3) / 1e12
+    out = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFP64-inst/s",
+           "frac": achieved / peak if peak > 0 else None, "traffic": None,
+           "peak_source": f"measured DFMA issue rate (fp64_peak.cu, {nsm.value} SMs, burst)",
+           "work_per_launch": {"terms": terms, "cmuls": cmuls, "fp64_lane_inst": alg},
+           "kernel": "lofp_contract_warp_kernel", "kernel_ms": kernel_ms}
+    prof = os.path.join(ROOT, "profiles", "r2_ncu_contract_warp_cfg3.txt")
+    if os.path.exists(prof):
+        for line in open(prof):
+            if "smsp__issue_active.avg.pct_of_peak_sustained_active" in line:
+                out["issue_active_ncu"] = float(line.split()[1]) / 100
+            if line.startswith("  dram__bytes_read.sum") or line.startswith("  dram__bytes_write.sum"):
+                v, u = float(line.split()[1]), line.split()[2]
+                out["traffic"] = (out["traffic"] or 0) + v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
+        out["ncu_source"] = "profiles/r2_ncu_contract_warp_cfg3.txt"
+    return out
+
+
 def contract_arm(args, rank, world, local):
     """--contract: amplitudes/s of the strip tensor contraction on configs[3] as
     BASELINE.json draws it (2048 outputs, 2.5e18 paths: beyond any enumerator)."""
@@ -349,10 +380,7 @@ def contract_arm(args, rank, world, local):
                                    f"paths (not enumerated)", "global_batch": int(outs_all),
                        "l2": "flushed between steps (256 MiB write)"},
             "paths_equivalent_per_s": paths_all * args.steps / (t_max * 1e-3),
-            "roofline": {"bound": "alu", "note": "integer index arithmetic and Appendix-A table gathers "
-                                                 "(L1/L2 resident); FP64 work per step below",
-                         "terms": terms, "cmuls": int(st["cmuls"]),
-                         "fp64_lane_inst": 4 * terms + 4 * int(st["cmuls"]), "kernel_ms": float(np.mean(ms))},
+            "roofline": contract_roofline(terms, int(st["cmuls"]), float(np.mean(ms))),
             "e2e": e2e, "gpu_launches": int(st["launches"]) * args.steps, "clocks": clk,
         }
         print(json.dumps(line), flush=True)

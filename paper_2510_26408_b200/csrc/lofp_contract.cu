@@ -293,10 +293,14 @@ __device__ __forceinline__ double2 cut_fac(const double2 *__restrict__ table, co
       e[f] = __ldg(table + (tbo[f] + s_tri[n] + (Bm - A) * (n + 1) + (Bp - A)));
     }
   }
+  // product as a balanced tree (depth log2 NF instead of NF dependent multiplications);
+  // the unused slots hold exactly 1
 #pragma unroll
-  for (int f = 0; f < NF; ++f)
-    if (FULL || f < nfac) fac = make_double2(fac.x * e[f].x - fac.y * e[f].y, fac.x * e[f].y + fac.y * e[f].x);
-  return fac;
+  for (int st = 1; st < NF; st *= 2)
+#pragma unroll
+    for (int f = 0; f + st < NF; f += 2 * st)
+      e[f] = make_double2(e[f].x * e[f + st].x - e[f].y * e[f + st].y, e[f].x * e[f + st].y + e[f].y * e[f + st].x);
+  return make_double2(fac.x * e[0].x - fac.y * e[0].y, fac.x * e[0].y + fac.y * e[0].x);
 }
 
 // phase gates of the cut on (column k-1, column k): n = F(k) - F(k-1) at their time
