@@ -5,6 +5,7 @@ usage: python scripts/ncu_lanes.py <report.ncu-rep> <liblofp.so> <kernel (mangle
 """
 import csv, subprocess, sys, re, collections, os, tempfile
 rep, so, kern, src = sys.argv[1:5]
+so = os.path.abspath(so)
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", so], cwd=tmp, capture_output=True)
 cub = sorted(f for f in os.listdir(tmp) if f.endswith(".cubin"))[0]
