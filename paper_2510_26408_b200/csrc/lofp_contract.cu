@@ -79,8 +79,6 @@ struct CWarp {           // shared state of one warp's output
   uint32_t fsh[kCF];               // segments it reads: i (column k) | sC << 8 (column k+1)
   uint16_t cmpR[kCCmp];            // CmpPairs (sa | sb << 8) of column k+1
   GateW gat[kCFac];
-  uint8_t gseg[kCSeg];             // cut k+1: the segments of column k its factors read
-  int ngs;                         // (the bytes each entry of level k+1 carries)
 };
 
 __device__ __forceinline__ int byte_at(uint64_t v, int j) { return (int)((v >> (8 * j)) & 0xffu); }
@@ -129,18 +127,21 @@ __device__ __forceinline__ uint64_t sub_hi_s(uint64_t h, const uint16_t *cmp, in
 // The bytes of a column-(c-1) state that cut c's factor reads ("gather" slots): F_{l-1}(c-1)
 // for each BS of cut c in order, then the column-(c-1) end of each gate folded into cut c
 // with col_off 0.  Every level entry carries its row-side state's gather for the next cut,
-// so the term loop reads A = F_{l-1}(c-1) as byte f of one register.  (lane 0)
-__device__ void stage_gather(const CallParams &p, CWarp &w, int c) {
-  int n = 0;
-  if (c >= 1 && c <= p.M - 1) {
-    const ColInfo cc = p.col[c];
-    for (int f = 0; f < cc.nfac && n < kCSeg; ++f) w.gseg[n++] = p.fac[cc.fac_base + f].sA;
-    for (int g = 0; g < cc.ngate && n < kCSeg; ++g) {
-      const GateInfo gi = p.gat[cc.gate_base + g];
-      if (!gi.col_off) w.gseg[n++] = gi.seg_lo;
+// so the term loop reads A = F_{l-1}(c-1) as byte f of one register.  Built once per block
+// for every cut (the circuit's, not the output's).
+__device__ void gather_lists(const CallParams &p, uint8_t (*gseg)[kCSeg], uint8_t *ngs) {
+  for (int c = threadIdx.x; c <= p.M; c += blockDim.x) {
+    int n = 0;
+    if (c >= 1 && c <= p.M - 1) {
+      const ColInfo cc = p.col[c];
+      for (int f = 0; f < cc.nfac && n < kCSeg; ++f) gseg[c][n++] = p.fac[cc.fac_base + f].sA;
+      for (int g = 0; g < cc.ngate && n < kCSeg; ++g) {
+        const GateInfo gi = p.gat[cc.gate_base + g];
+        if (!gi.col_off) gseg[c][n++] = gi.seg_lo;
+      }
     }
+    ngs[c] = (uint8_t)n;
   }
-  w.ngs = n;
 }
 
 __device__ __forceinline__ uint64_t gather(uint64_t v, const uint8_t *gseg, int ngs) {
@@ -252,21 +253,25 @@ __device__ int setup_warp(const CallParams &p, CWarp &w, uint64_t *vals, int q, 
   if (tot > (uint32_t)kCMaxStates) return kStatusDeferred;
   __syncwarp();
   if (lane == 0) atomicMax(&p.ctr->max_states, (ull)tot);
-  // packed segment values of every state (mixed radix, segment 0 fastest)
-  for (int k = 0; k <= M; ++k) {
-    const int nk = w.n[k], ns = w.nseg[k];
-    const uint64_t lo = w.lo[k], hi = w.hi[k];
-    for (int s = lane; s < nk; s += 32) {
-      uint64_t v = lo;
-      int r = s;
-      for (int i = 0; i < ns; ++i) {
-        const int rad = byte_at(hi, i) - byte_at(lo, i) + 1;
-        const int d = r % rad;
-        r /= rad;
-        v += (uint64_t)d << (8 * i);
-      }
-      vals[w.vbase[k] + s] = v;
+  // packed segment values of every state (mixed radix, segment 0 fastest); lanes over the
+  // states of all columns (column by a search over vbase)
+  for (uint32_t x = lane; x < tot; x += 32) {
+    int lo_k = 0, hi_k = M;
+    while (lo_k < hi_k) {
+      const int mid = (lo_k + hi_k + 1) >> 1;
+      if (w.vbase[mid] <= x) lo_k = mid; else hi_k = mid - 1;
     }
+    const int k = lo_k, ns = w.nseg[k];
+    const uint64_t lo = w.lo[k], hi = w.hi[k];
+    uint64_t v = lo;
+    uint32_t r = x - w.vbase[k];
+    for (int i = 0; i < ns; ++i) {
+      const uint32_t rad = (uint32_t)(byte_at(hi, i) - byte_at(lo, i) + 1);
+      if (rad == 1) continue;
+      v += (uint64_t)(r % rad) << (8 * i);
+      r /= rad;
+    }
+    vals[x] = v;
   }
   __syncwarp();
   return kStatusOk;
@@ -362,7 +367,9 @@ template <int NF, bool CNT>
 __global__ void __launch_bounds__(32 * kCW, 2) lofp_contract_warp_kernel(const __grid_constant__ CallParams p) {
   __shared__ CWarp sw[kCW];
   __shared__ int s_tri[kMaxPhotons + 2];  // tri(n) = sum_{m<n} (m+1)^2: block offsets in a BS table
+  __shared__ uint8_t s_gseg[kMaxModes + 1][kCSeg], s_ngs[kMaxModes + 1];  // gather slots per cut
   for (int n = threadIdx.x; n <= kMaxPhotons + 1; n += blockDim.x) s_tri[n] = n * (n + 1) * (2 * n + 1) / 6;
+  gather_lists(p, s_gseg, s_ngs);
   __syncthreads();
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   CWarp &w = sw[wib];
@@ -401,11 +408,10 @@ __global__ void __launch_bounds__(32 * kCW, 2) lofp_contract_warp_kernel(const _
           const double2 e = p.gate_tab[g * (p.N + 1) + p.N];
           root = make_double2(root.x * e.x - root.y * e.y, root.x * e.y + root.y * e.x);
         }
-      if (lane == 0) stage_gather(p, w, 1);
       const uint32_t tot = level_rows(p, w, vals, 1, roff0, lane);
       if (tot > (uint64_t)capE) st = kStatusDeferred;
       if (st == kStatusOk) {
-        const uint64_t g0 = gather(vals[w.vbase[0]], w.gseg, w.ngs);
+        const uint64_t g0 = gather(vals[w.vbase[0]], s_gseg[1], s_ngs[1]);
         for (uint32_t t = lane; t < tot; t += 32) {
           lvA[t] = root;
           lgA[t] = g0;
@@ -446,7 +452,6 @@ __global__ void __launch_bounds__(32 * kCW, 2) lofp_contract_warp_kernel(const _
           gw.slot = gi.col_off ? 0 : (uint8_t)slot++;
           w.gat[g] = gw;
         }
-        stage_gather(p, w, k + 1);  // what the entries of level k+1 carry for cut k+1
       }
       __syncwarp();
       const double2 *__restrict__ table = p.table;
@@ -515,7 +520,7 @@ __global__ void __launch_bounds__(32 * kCW, 2) lofp_contract_warp_kernel(const _
           row_sum<NF, CNT, false>(table, s_tri, tbo, cb, nfac, gfix, p, w, ngate, vb, Ac, Gc, Cc, r0, r1, sx, sy, csum,
                                   cm, terms);
         An[t] = make_double2(sx, sy);
-        Gn[t] = gather(vb, w.gseg, w.ngs);
+        Gn[t] = gather(vb, s_gseg[k + 1], s_ngs[k + 1]);  // what cut k+1 reads of sb
         if (with_counts) Cn[t] = csum;
       }
       __syncwarp();

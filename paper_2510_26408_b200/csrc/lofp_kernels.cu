@@ -1402,6 +1402,7 @@ extern "C" int lofp_launch_paths(const CallParams *p, int grid, void *stream, vo
 __global__ void __launch_bounds__(kThreads) lofp_contract_kernel(const __grid_constant__ CallParams p) {
   __shared__ Shared sh;
   __shared__ double red_re[kThreads / 32], red_im[kThreads / 32];
+  if (p.deferred_only && p.ctr->cdeferred == 0) return;  // the warp kernel did every output
   Block b = make_block(p);
   load_cols(p, sh);
   const int M = p.M, tid = threadIdx.x;
@@ -1606,6 +1607,9 @@ __global__ void __launch_bounds__(kThreads) lofp_generic_kernel(const __grid_con
   __shared__ ull rnp[kThreads / 32];
   __shared__ int s_front, s_level, s_done;
   const int M = p.M, D = p.D, L = p.nbs, tid = threadIdx.x;
+  // no output over the column limits (an unsupported output keeps the counter above 0
+  // until this kernel evaluates it)
+  if (p.ctr->unsupported == 0) return;
   char *slab = p.slab + (long long)blockIdx.x * p.slab_bytes;
   GenEntry *fe[2] = {(GenEntry *)slab, (GenEntry *)slab + kGenFront};
   uint8_t *fo[2] = {(uint8_t *)((GenEntry *)slab + 2 * kGenFront),
