@@ -77,9 +77,33 @@ struct CWarp {           // shared state of one warp's output
   // cut k being contracted (staged once per cut)
   int ftab[kCF];                   // Appendix-A block of each of its BS (offset in the table)
   uint32_t fsh[kCF];               // segments it reads: i (column k) | sC << 8 (column k+1)
-  uint16_t cmpR[kCCmp];            // CmpPairs (sa | sb << 8) of column k+1
   GateW gat[kCFac];
 };
+
+struct CCirc {           // the circuit's column data, cached once per block
+  SegInfo seg[kMaxModes + 1][kCSeg];   // light-cone maps of each segment
+  uint16_t cmp[kMaxModes + 1][kCCmp];  // CmpPairs of column k: sa | sb << 8
+  uint8_t nseg[kMaxModes + 1], ncmp[kMaxModes + 1];
+  uint8_t ok[kMaxModes + 1];           // within the warp kernel's limits
+};
+
+__device__ void cache_circuit(const CallParams &p, CCirc &cc) {
+  for (int k = threadIdx.x; k <= p.M; k += blockDim.x) {
+    const ColInfo ci = p.col[k];
+    int slots = ci.nfac;
+    for (int g = 0; g < ci.ngate; ++g) slots += p.gat[ci.gate_base + g].col_off ? 0 : 1;
+    const bool ok = ci.nseg <= kCSeg && ci.nfac <= kCF && ci.ngate <= kCFac && ci.ncmp <= kCCmp && slots <= kCSeg;
+    cc.ok[k] = ok;
+    cc.nseg[k] = ci.nseg;
+    cc.ncmp[k] = ci.ncmp;
+    if (!ok) continue;
+    for (int i = 0; i < ci.nseg; ++i) cc.seg[k][i] = p.seg[ci.seg_base + i];
+    for (int c = 0; c < ci.ncmp; ++c) {
+      const CmpPair pr = p.cmp[ci.cmp_base + c];
+      cc.cmp[k][c] = (uint16_t)(pr.sa | pr.sb << 8);
+    }
+  }
+}
 
 __device__ __forceinline__ int byte_at(uint64_t v, int j) { return (int)((v >> (8 * j)) & 0xffu); }
 
@@ -95,13 +119,11 @@ __device__ __forceinline__ ull sat_add_c(ull a, ull b) {
 
 // Upper corner of the sub-box of column k-1 compatible with state vr of column k:
 // F_t(k-1) <= F_t(k) on every time interval (CmpPair list of column k).
-__device__ __forceinline__ uint64_t sub_hi(const CallParams &p, const CWarp &w, int k, uint64_t vr) {
+__device__ __forceinline__ uint64_t sub_hi(const CCirc &cc, const CWarp &w, int k, uint64_t vr) {
   uint64_t h = w.hi[k - 1];
-  const ColInfo ck = p.col[k];
-  for (int c = 0; c < ck.ncmp; ++c) {
-    const CmpPair pr = p.cmp[ck.cmp_base + c];
-    const int v = byte_at(vr, pr.sb);
-    if (v < byte_at(h, pr.sa)) h = set_byte(h, pr.sa, v);
+  for (int c = 0; c < cc.ncmp[k]; ++c) {
+    const int sa = cc.cmp[k][c] & 0xff, v = byte_at(vr, cc.cmp[k][c] >> 8);
+    if (v < byte_at(h, sa)) h = set_byte(h, sa, v);
   }
   return h;
 }
@@ -152,14 +174,14 @@ __device__ __forceinline__ uint64_t gather(uint64_t v, const uint8_t *gseg, int 
 
 // Rows of the level whose rows are the states of column k (entries: the compatible
 // sub-box of column k-1): exclusive offsets into roff[0..n_k], returns the entry count.
-__device__ uint32_t level_rows(const CallParams &p, const CWarp &w, const uint64_t *vals, int k, uint32_t *roff,
+__device__ uint32_t level_rows(const CCirc &cc, const CWarp &w, const uint64_t *vals, int k, uint32_t *roff,
                                int lane) {
   const int nk = w.n[k], ns = w.nseg[k - 1];
   uint32_t run = 0;
   for (int base = 0; base < nk; base += 32) {
     const int s = base + lane;
     uint32_t c = 0;
-    if (s < nk) c = box_count(w.lo[k - 1], sub_hi(p, w, k, vals[w.vbase[k] + s]), ns);
+    if (s < nk) c = box_count(w.lo[k - 1], sub_hi(cc, w, k, vals[w.vbase[k] + s]), ns);
     uint32_t incl = c;
     for (int d = 1; d < 32; d <<= 1) {
       const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
@@ -175,7 +197,7 @@ __device__ uint32_t level_rows(const CallParams &p, const CWarp &w, const uint64
 
 // Per-output setup: G = cum(T), the light-cone box of every column (readings R5, R15),
 // the packed states.  Returns kStatusOk / Zero / Bad / Deferred (warp-uniform).
-__device__ int setup_warp(const CallParams &p, CWarp &w, uint64_t *vals, int q, int lane) {
+__device__ int setup_warp(const CallParams &p, const CCirc &cc, CWarp &w, uint64_t *vals, int q, int lane) {
   const int M = p.M;
   // G = cum(T); negative entries make the row bad, totals other than N an exact zero
   int bad = 0, run = 0;
@@ -203,18 +225,16 @@ __device__ int setup_warp(const CallParams &p, CWarp &w, uint64_t *vals, int q, 
   // segment boxes: backward (T) and forward (S) light cones intersected
   int zero = 0, defer = 0;
   for (int k = lane; k <= M; k += 32) {
-    const ColInfo ci = p.col[k];
-    int slots = ci.nfac;
-    for (int g = 0; g < ci.ngate; ++g) slots += p.gat[ci.gate_base + g].col_off ? 0 : 1;
-    if (ci.nseg > kCSeg || ci.nfac > kCF || ci.ngate > kCFac || ci.ncmp > kCCmp || slots > kCSeg) {
+    if (!cc.ok[k]) {
       defer = 1;
       w.n[k] = 0;
       continue;
     }
+    const int nseg = cc.nseg[k];
     uint64_t lo = 0, hi = 0;
     uint32_t n = 1;
-    for (int i = 0; i < ci.nseg; ++i) {
-      const SegInfo si = p.seg[ci.seg_base + i];
+    for (int i = 0; i < nseg; ++i) {
+      const SegInfo si = cc.seg[k][i];
       const int l = max((int)w.G[si.rho], (int)p.cumS[si.rhop]);
       const int h = min((int)w.G[si.sig], (int)p.cumS[si.sigp]);
       if (h < l) {
@@ -230,7 +250,7 @@ __device__ int setup_warp(const CallParams &p, CWarp &w, uint64_t *vals, int q, 
     w.lo[k] = lo;
     w.hi[k] = hi;
     w.n[k] = (uint16_t)min(n, (uint32_t)kCMaxN);
-    w.nseg[k] = ci.nseg;
+    w.nseg[k] = (uint8_t)nseg;
   }
   zero = __any_sync(0xffffffffu, zero);
   defer = __any_sync(0xffffffffu, defer);
@@ -369,7 +389,9 @@ __global__ void __launch_bounds__(32 * kCW, 2) lofp_contract_warp_kernel(const _
   __shared__ int s_tri[kMaxPhotons + 2];  // tri(n) = sum_{m<n} (m+1)^2: block offsets in a BS table
   __shared__ uint8_t s_gseg[kMaxModes + 1][kCSeg], s_ngs[kMaxModes + 1];  // gather slots per cut
   for (int n = threadIdx.x; n <= kMaxPhotons + 1; n += blockDim.x) s_tri[n] = n * (n + 1) * (2 * n + 1) / 6;
+  __shared__ CCirc cc;
   gather_lists(p, s_gseg, s_ngs);
+  cache_circuit(p, cc);
   __syncthreads();
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   CWarp &w = sw[wib];
@@ -396,7 +418,7 @@ __global__ void __launch_bounds__(32 * kCW, 2) lofp_contract_warp_kernel(const _
     if (lane == 0) q = (int)atomicAdd(&p.ctr->cticket, 1ull);
     q = __shfl_sync(0xffffffffu, q, 0);
     if (q >= p.B) break;
-    int st = setup_warp(p, w, vals, q, lane);
+    int st = setup_warp(p, cc, w, vals, q, lane);
     double re = 0.0, im = 0.0;
     ull count = 0;
     int cur = 0;
@@ -408,7 +430,7 @@ __global__ void __launch_bounds__(32 * kCW, 2) lofp_contract_warp_kernel(const _
           const double2 e = p.gate_tab[g * (p.N + 1) + p.N];
           root = make_double2(root.x * e.x - root.y * e.y, root.x * e.y + root.y * e.x);
         }
-      const uint32_t tot = level_rows(p, w, vals, 1, roff0, lane);
+      const uint32_t tot = level_rows(cc, w, vals, 1, roff0, lane);
       if (tot > (uint64_t)capE) st = kStatusDeferred;
       if (st == kStatusOk) {
         const uint64_t g0 = gather(vals[w.vbase[0]], s_gseg[1], s_ngs[1]);
@@ -423,21 +445,17 @@ __global__ void __launch_bounds__(32 * kCW, 2) lofp_contract_warp_kernel(const _
     // cuts 1..M-1: level k (rows: column k, entries: column k-1) -> level k+1
     for (int k = 1; k <= M - 1 && st == kStatusOk; ++k) {
       const int nxt = cur ^ 1;
-      const uint32_t totn = level_rows(p, w, vals, k + 1, ROFF(nxt), lane);
+      const uint32_t totn = level_rows(cc, w, vals, k + 1, ROFF(nxt), lane);
       if (totn > (uint64_t)capE) {
         st = kStatusDeferred;
         break;
       }
-      const ColInfo ck = p.col[k], ck1 = p.col[k + 1];
-      const int nfac = ck.nfac, ngate = ck.ngate, ncR = ck1.ncmp;
+      const ColInfo ck = p.col[k];
+      const int nfac = ck.nfac, ngate = ck.ngate, ncR = cc.ncmp[k + 1];
       if (lane < nfac) {
         const FacInfo fi = p.fac[ck.fac_base + lane];
         w.ftab[lane] = (int)p.tab_off[fi.bs];
         w.fsh[lane] = (uint32_t)fi.i | (uint32_t)fi.sC << 8;
-      }
-      if (lane < ncR) {
-        const CmpPair pr = p.cmp[ck1.cmp_base + lane];
-        w.cmpR[lane] = (uint16_t)(pr.sa | pr.sb << 8);
       }
       __syncwarp();
       if (lane == 0) {
@@ -474,7 +492,7 @@ __global__ void __launch_bounds__(32 * kCW, 2) lofp_contract_warp_kernel(const _
         while (rn[sc + 1] <= t) ++sc;
         if (sc != sc_last) {  // the row's state (column k+1) and its sub-box of column k
           vc = vals[vbC + sc];
-          hB = sub_hi_s(hiB, w.cmpR, ncR, vc);
+          hB = sub_hi_s(hiB, cc.cmp[k + 1], ncR, vc);
           sc_last = sc;
         }
         // entry t = the pos-th state of the sub-box (odometer order, segment 0 fastest)
