@@ -21,7 +21,9 @@ for c in 4 2 3; do
 done
 P="python bench.py --contract --steps 1 --warmup 0 --no-e2e"
 timeout 300 $P > gpurun_out/prof_plain_contract.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:lofp_contract_kernel -s 1 -c 1 -o gpurun_out/${TAG}_contract_cfg3 $P > gpurun_out/ncu_full_contract.log 2>&1; echo "ncu contract rc=$?"
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:lofp_contract_warp -s 1 -c 1 -o gpurun_out/${TAG}_contract_warp_cfg3 $P > gpurun_out/ncu_full_contract.log 2>&1; echo "ncu contract rc=$?"
 timeout 300 python bench.py --nonlocal --outputs 256 --steps 3 --warmup 2 --no-cpu > gpurun_out/${TAG}_bench_nonlocal.log 2>&1; echo "nonlocal rc=$?"
 timeout 300 python bench.py --gates --steps 3 --warmup 3 --no-cpu > gpurun_out/${TAG}_bench_gates.log 2>&1; echo "gates rc=$?"
 timeout 300 python bench.py --distribution --steps 5 --warmup 3 > gpurun_out/${TAG}_bench_distribution.log 2>&1; echo "distribution rc=$?"
+timeout 600 python scripts/paper_scaling.py gpurun_out/${TAG}_paper_scaling.json > gpurun_out/${TAG}_paper_scaling.log 2>&1; echo "paper scaling rc=$?"
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1; echo "smoke rc=$?"
