@@ -609,7 +609,7 @@ static int launch_nf(const CallParams *p, int grid, cudaStream_t stream) {
   const long long total = (long long)grid * p->slab_bytes;
   q.cw_bytes = (total / (blocks * kCW)) & ~255ll;
   const long long fixed = (long long)kCMaxStates * 8 + 2ll * (kCMaxN + 1) * 4 + 16;
-  if (q.cw_bytes < fixed + 64 * 1024) return (int)cudaErrorInvalidValue;  // (not with the default slab)
+  if (q.cw_bytes < fixed + 64 * 1024) return -1;  // scratch too small (LOFP_SLAB_MB): not launched
   lofp_contract_warp_kernel<NF, CNT><<<(int)blocks, 32 * kCW, 0, stream>>>(q);
   return (int)cudaGetLastError();
 }
@@ -623,6 +623,8 @@ static int launch_cnt(const CallParams *p, int grid, cudaStream_t stream) {
 // a ticket counter); each warp's scratch is carved from the slab of the block kernels
 // (grid x slab_bytes), which runs after it on the same stream.  Instantiated per the most
 // BS a cut carries (outputs of circuits with more than 7 per cut are deferred anyway).
+// Returns 0 (launched), -1 (not launched: the caller runs the block kernel on every output)
+// or a CUDA error.
 extern "C" int lofp_launch_contract_warp(const CallParams *p, int grid, void *stream) {
   cudaStream_t st = (cudaStream_t)stream;
   switch (p->max_nfac) {

@@ -1513,8 +1513,8 @@ extern "C" int lofp_launch_contract(const CallParams *p, int grid, void *stream)
   q.deferred_only = 0;
   if (!p->general && !p->force_generic && !p->contract_block_only) {
     const int e = lofp_launch_contract_warp(p, grid, stream);
-    if (e != 0) return e;
-    q.deferred_only = 1;
+    if (e > 0) return e;
+    q.deferred_only = e == 0 ? 1 : 0;  // (-1: not launched, the block kernel takes every output)
   }
   lofp_contract_kernel<<<g, kThreads, 0, (cudaStream_t)stream>>>(q);
   lofp_generic_kernel<<<grid, kThreads, 0, (cudaStream_t)stream>>>(*p);  // outputs over the column limits

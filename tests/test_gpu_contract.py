@@ -230,3 +230,19 @@ def test_deep_circuit_defers_to_block_kernel(lofp, N):
     assert tol_ok(got, ref)[0]
     assert np.array_equal(cnt, leaves)
     assert abs(np.sum(np.abs(got) ** 2) - 1) < 1e-12
+
+
+
+def test_small_scratch(lofp, monkeypatch):
+    """The smallest per-block scratch the library accepts (LOFP_SLAB_MB below 4 is raised to
+    4): the warp kernel's slices shrink with it; every output is still evaluated."""
+    monkeypatch.setenv("LOFP_SLAB_MB", "1")
+    c = li.config(1)
+    d = load(1)
+    T = np.tile(d["T_literal"].astype(np.int32), (3, 1))
+    got, cnt, st = contract(lofp, c.M, c.layers, c.S, T)
+    assert st["unsupported"] == 0 and st["check_errors"] == 0
+    assert np.array_equal(cnt, np.tile(d["P_literal"], 3))
+    monkeypatch.delenv("LOFP_SLAB_MB")
+    ref, _, _ = contract(lofp, c.M, c.layers, c.S, T)
+    assert tol_ok(got, ref)[0]
