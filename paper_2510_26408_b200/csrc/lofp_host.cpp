@@ -747,8 +747,8 @@ lofp_status create_impl(int32_t modes, int32_t n_layers, const int32_t *bs_per_l
     ctx->grid = lofp_units_grid(ctx->device);
     if (ctx->grid <= 0) e = cudaErrorInvalidDevice;
   }
-  // per-block scratch: at least the fixed part of the column engine's layout (~1.4 MB)
-  ctx->slab_bytes = std::max(4ll, env_ll("LOFP_SLAB_MB", 16)) << 20;
+  // per-block scratch: at least the fixed part of the column engine's layout (1.36 MiB)
+  ctx->slab_bytes = std::max(2ll, env_ll("LOFP_SLAB_MB", 16)) << 20;
   if (e != cudaSuccess) {
     lofp_status s = e == cudaErrorMemoryAllocation ? LOFP_E_OOM : LOFP_E_CUDA;
     lofp_destroy(ctx);

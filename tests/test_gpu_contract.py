@@ -234,8 +234,8 @@ def test_deep_circuit_defers_to_block_kernel(lofp, N):
 
 
 def test_small_scratch(lofp, monkeypatch):
-    """The smallest per-block scratch the library accepts (LOFP_SLAB_MB below 4 is raised to
-    4): the warp kernel's slices shrink with it; every output is still evaluated."""
+    """The smallest per-block scratch the library accepts (LOFP_SLAB_MB below 2 is raised to
+    2): the warp kernel's slices shrink with it; every output is still evaluated."""
     monkeypatch.setenv("LOFP_SLAB_MB", "1")
     c = li.config(1)
     d = load(1)
