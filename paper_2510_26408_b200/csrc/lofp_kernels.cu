@@ -567,27 +567,30 @@ __device__ uint32_t bucket_offsets(Block &b, Shared &sh, int k, bool left, uint3
 // A warp holds kKX X values per lane (a tile of kXT = 32 kKX) in registers and streams a
 // tile of up to kYT Y values from its shared-memory slice (broadcast reads): per Y value
 // 1 LDS.128 and 4 kKX DFMA per lane.
-#define LOFP_CFMA(v)                                \
-  _Pragma("unroll") for (int r = 0; r < kKX; ++r) { \
+#define LOFP_CFMA(v, KX)                           \
+  _Pragma("unroll") for (int r = 0; r < KX; ++r) { \
     acc[r].x = fma(x[r].x, (v).x, acc[r].x);        \
     acc[r].y = fma(x[r].x, (v).y, acc[r].y);        \
     acc[r].x = fma(-x[r].y, (v).y, acc[r].x);       \
     acc[r].y = fma(x[r].y, (v).x, acc[r].y);        \
   }
 
+// KX <= kKX: only the first KX X slots of each lane hold values (a pair's last X tile with
+// at most 32 KX elements left): the other slots would multiply zeros
+template <int KX>
 __device__ __forceinline__ void fma_block(const double2 (&x)[kKX], const double2 *__restrict__ sW, uint32_t len,
                                           double2 (&acc)[kKX]) {
   uint32_t y = 0;
-  for (; y + 3 < len; y += 4) {  // four Y values loaded ahead of their 128 DFMA
+  for (; y + 3 < len; y += 4) {  // four Y values loaded ahead of their 16 KX DFMA
     const double2 v0 = sW[y], v1 = sW[y + 1], v2 = sW[y + 2], v3 = sW[y + 3];
-    LOFP_CFMA(v0)
-    LOFP_CFMA(v1)
-    LOFP_CFMA(v2)
-    LOFP_CFMA(v3)
+    LOFP_CFMA(v0, KX)
+    LOFP_CFMA(v1, KX)
+    LOFP_CFMA(v2, KX)
+    LOFP_CFMA(v3, KX)
   }
   for (; y < len; ++y) {
     const double2 v0 = sW[y];
-    LOFP_CFMA(v0)
+    LOFP_CFMA(v0, KX)
   }
 }
 
@@ -917,7 +920,12 @@ __device__ void process_stack(const CallParams &p, Block &b, Shared &sh, double2
           cm += nv;
           __syncwarp();
           const long long tc1 = clock64();
-          fma_block(x, sW, len, acc);
+          // X slots in use: the tile's X elements rounded up to 32 lanes, then to a power of 2
+          const uint32_t xs = (min((uint32_t)kXT, pr.nX - x0) + 31) / 32;
+          if (xs > kKX / 2) fma_block<kKX>(x, sW, len, acc);
+          else if (xs > kKX / 4) fma_block<kKX / 2>(x, sW, len, acc);
+          else if (xs > kKX / 8) fma_block<kKX / 4>(x, sW, len, acc);
+          else fma_block<kKX / 8>(x, sW, len, acc);
           npaths += (ull)nv * len;
           __syncwarp();
           if (lane == 0) {
