@@ -1207,6 +1207,16 @@ __global__ void __launch_bounds__(kThreads) lofp_split_kernel(const __grid_const
   }
 }
 
+// slot of unit u: output q = the last with ubase[q] <= u (ubase[B] = the unit count)
+__device__ __forceinline__ long long unit_slot(const CallParams &p, int u) {
+  int lo = 0, hi = p.B - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (p.ubase[mid] <= u) lo = mid; else hi = mid - 1;
+  }
+  return (long long)lo * p.budget + (u - p.ubase[lo]);
+}
+
 // exclusive scan of nunits -> ubase, total -> ctr->total_units; then the schedule: units
 // by decreasing size class (floor log2 of their path count), largest first (one block)
 __global__ void lofp_scan_kernel(const __grid_constant__ CallParams p) {
@@ -1238,12 +1248,12 @@ __global__ void lofp_scan_kernel(const __grid_constant__ CallParams p) {
   }
   __syncthreads();
   const int U = (int)p.ctr->total_units;
-  // size class of every unit (walk the outputs; unit u of output q is slot q*budget + i)
-  for (int q = tid; q < B; q += kThreads)
-    for (int i = 0; i < p.nunits[q]; ++i) {
-      const ull P = p.units[(long long)q * p.budget + i].paths;
-      atomicAdd(&hist[64 - (P ? 64 - __clzll(P) : 0)], 1u);
-    }
+  // size class of every unit (unit u of output q is slot q*budget + u - ubase[q]); threads
+  // over the units, so that one output split into thousands of units is not one thread's
+  for (int u = tid; u < U; u += kThreads) {
+    const ull P = p.units[unit_slot(p, u)].paths;
+    atomicAdd(&hist[64 - (P ? 64 - __clzll(P) : 0)], 1u);
+  }
   __syncthreads();
   if (tid == 0) {
     unsigned int r = 0;
@@ -1253,12 +1263,11 @@ __global__ void lofp_scan_kernel(const __grid_constant__ CallParams p) {
     }
   }
   __syncthreads();
-  for (int q = tid; q < B; q += kThreads)
-    for (int i = 0; i < p.nunits[q]; ++i) {
-      const ull P = p.units[(long long)q * p.budget + i].paths;
-      const unsigned int pos = atomicAdd(&base[64 - (P ? 64 - __clzll(P) : 0)], 1u);
-      if ((int)pos < U) p.sched[pos] = p.ubase[q] + i;
-    }
+  for (int u = tid; u < U; u += kThreads) {
+    const ull P = p.units[unit_slot(p, u)].paths;
+    const unsigned int pos = atomicAdd(&base[64 - (P ? 64 - __clzll(P) : 0)], 1u);
+    if ((int)pos < U) p.sched[pos] = u;
+  }
 }
 
 // ---- the hot path ----------------------------------------------------------------------
@@ -1339,23 +1348,35 @@ __global__ void __launch_bounds__(kThreads, 2) lofp_units_kernel(const __grid_co
   }
 }
 
-// per output: the sum of its units in unit order (deterministic), exact 0 / NaN otherwise
+// per output: the sum of its units (a warp per output: lane-strided partial sums in unit
+// order, then a fixed shuffle tree -- deterministic), exact 0 / NaN otherwise
 __global__ void lofp_final_kernel(const __grid_constant__ CallParams p) {
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < p.B; q += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int q = w0; q < p.B; q += nw) {
     const int st = p.status[q];
     double2 a = make_double2(0.0, 0.0);
-    if (st == kStatusOk) {
-      for (int u = p.ubase[q]; u < p.ubase[q + 1]; ++u) {
+    if (st == kStatusOk)
+      for (int u = p.ubase[q] + lane; u < p.ubase[q + 1]; u += 32) {
         const double2 v = p.partial[u];
         a.x += v.x;
         a.y += v.y;
       }
-      if (p.pdone[q] != p.pexp[q]) atomicAdd(&p.ctr->table_error, 1ull);  // every path exactly once
-    } else if (st == kStatusBad || st == kStatusUnsupported || st == kStatusOverBudget) {
-      a = make_double2(__longlong_as_double(0x7ff8000000000000ll), __longlong_as_double(0x7ff8000000000000ll));
+    for (int d = 16; d > 0; d >>= 1) {
+      a.x += __shfl_down_sync(0xffffffffu, a.x, d);
+      a.y += __shfl_down_sync(0xffffffffu, a.y, d);
     }
-    p.amps[q] = a;
-    if (p.counts) p.counts[q] = p.pdone[q];
+    if (lane == 0) {
+      if (st == kStatusOk) {
+        if (p.pdone[q] != p.pexp[q]) atomicAdd(&p.ctr->table_error, 1ull);  // every path exactly once
+      } else if (st == kStatusBad || st == kStatusUnsupported || st == kStatusOverBudget) {
+        a = make_double2(__longlong_as_double(0x7ff8000000000000ll), __longlong_as_double(0x7ff8000000000000ll));
+      } else {
+        a = make_double2(0.0, 0.0);
+      }
+      p.amps[q] = a;
+      if (p.counts) p.counts[q] = p.pdone[q];
+    }
   }
 }
 
@@ -1393,7 +1414,7 @@ extern "C" int lofp_launch_paths(const CallParams *p, int grid, void *stream, vo
   if (ev0) cudaEventRecord((cudaEvent_t)ev0, st);
   lofp_units_kernel<<<grid, kThreads, smem, st>>>(*p);
   if (ev1) cudaEventRecord((cudaEvent_t)ev1, st);
-  lofp_final_kernel<<<(p->B + 255) / 256 < 1024 ? (p->B + 255) / 256 : 1024, 256, 0, st>>>(*p);
+  lofp_final_kernel<<<(p->B + 7) / 8 < 1184 ? (p->B + 7) / 8 : 1184, 256, 0, st>>>(*p);  // a warp per output
   lofp_generic_kernel<<<grid, kThreads, 0, st>>>(*p);  // outputs over the column limits
   return (int)cudaGetLastError();
 }
