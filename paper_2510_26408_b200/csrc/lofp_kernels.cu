@@ -21,6 +21,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 
 #include "lofp_internal.h"
 
@@ -71,6 +73,12 @@ struct StackEnt {
   uint16_t sjm1, sj;
   double re, im;
   ull pad;
+};
+
+struct SplitEnt {         // a node of the split kernel's frontier: columns 0..j fixed
+  uint16_t sjm1, sj;
+  uint32_t pad;
+  double re, im;           // product of the cut factors of cuts 1..j-1
 };
 
 constexpr long long kOffSegs = 0;
@@ -263,6 +271,14 @@ __device__ uint32_t block_scan(Shared &sh, const uint32_t *in, uint32_t *out, in
   const uint32_t total = sh.total;
   __syncthreads();
   return total;
+}
+
+// The same scan as a call: inlined into the level-synchronous split kernel, nvcc 12.9
+// emitted code that raised "illegal instruction" on sm_100a (warp 0's shuffles after a
+// barrier); as a call it is correct (the unit kernel keeps the inlined form: measured
+// 2.5 % faster on configs[4]).
+__device__ __noinline__ uint32_t block_scan_call(Shared &sh, const uint32_t *in, uint32_t *out, int n) {
+  return block_scan(sh, in, out, n);
 }
 
 __device__ __forceinline__ ull warp_sum_sat(ull v) {
@@ -1160,48 +1176,116 @@ __global__ void __launch_bounds__(kThreads) lofp_split_kernel(const __grid_const
     }
     setup_output(p, b, sh, q);
     dp_counts(p, b, sh, 0, 0, true);
-    if (tid == 0) {
-      int count = 0;
-      while (true) {
-        count = 0;
-        int sp = 0;
-        StackEnt e;
-        e.j = 0; e.sjm1 = 0; e.sj = 0; e.re = root.x; e.im = root.y; e.pad = 0;
-        b.stack[sp++] = e;
-        while (sp > 0) {
-          const StackEnt t = b.stack[--sp];
-          const ull below = b.cR[sh.cb[t.j] + t.sj];
-          bool leaf = below <= thr || t.j >= M - 1;
-          if (!leaf) {
-            const int n1 = sh.n[t.j + 1];
-            int pushed = 0;
-            for (int s = n1 - 1; s >= 0; --s) {
-              if (!live(b, sh, t.j + 1, s) || !compat(p, b, sh, t.j + 1, t.sj, s)) continue;
-              if (sp >= kStackMax) { leaf = true; break; }
-              ull cm = 0;
-              const double2 f = cut_factor(p, b, sh, t.j, t.sjm1, t.sj, s, cm);
-              const double2 np = cmul(make_double2(t.re, t.im), f);
-              StackEnt c;
-              c.j = t.j + 1; c.sjm1 = t.sj; c.sj = (uint16_t)s; c.re = np.x; c.im = np.y; c.pad = 0;
-              b.stack[sp++] = c;
-              ++pushed;
-            }
-            if (leaf) sp -= pushed;  // stack full: keep this node whole
+    // Level-synchronous expansion of the prefix tree (all threads): a node (columns 0..j
+    // fixed) whose subtree holds at most thr paths -- or that reached column M-1 -- becomes
+    // a unit; every other node is replaced by its live, compatible children at column j+1.
+    // Units are numbered level by level, in frontier order (deterministic).  If the units
+    // exceed the output's slots, the unit size grows 4x and the expansion restarts; if a
+    // frontier outgrows the scratch, its nodes become (larger) units.
+    SplitEnt *fr[2];
+    uint32_t *cnt, *off, *flag;
+    long long cap;
+    {
+      char *q0 = (char *)(((uintptr_t)b.lists + 15) & ~(uintptr_t)15);
+      cap = (b.list_bytes - 64) / (2 * (long long)sizeof(SplitEnt) + 12);
+      fr[0] = (SplitEnt *)q0;
+      fr[1] = fr[0] + cap;
+      cnt = (uint32_t *)(fr[1] + cap);
+      off = cnt + cap;
+      flag = off + cap;
+    }
+    while (true) {
+      if (tid == 0) {
+        SplitEnt e;
+        e.sjm1 = 0; e.sj = 0; e.re = root.x; e.im = root.y;
+        fr[0][0] = e;
+      }
+      __syncthreads();
+      uint32_t nf = 1, units = 0;
+      int cur = 0;
+      for (int j = 0; nf > 0; ++j) {
+        const bool last = j >= M - 1;
+        // children per node (0 for a unit); a unit is marked with bit 31
+        for (uint32_t i = tid; i < nf; i += kThreads) {
+          const SplitEnt t = fr[cur][i];
+          DCHECK(j <= M && t.sj < sh.n[j] && (j == 0 || t.sjm1 < sh.n[j - 1]), "split node");
+          const ull below = b.cR[sh.cb[j] + t.sj];
+          uint32_t c = 0;
+          if (!(below <= thr || last)) {
+            const int n1 = sh.n[j + 1];
+            for (int s1 = 0; s1 < n1; ++s1)
+              if (live(b, sh, j + 1, s1) && compat(p, b, sh, j + 1, t.sj, s1)) ++c;
           }
-          if (leaf) {
-            if (count < p.budget) {
-              Unit u;
-              u.q = q; u.j = (int16_t)t.j; u.sjm1 = t.sjm1; u.sj = t.sj; u.pad = 0;
-              u.re = t.re; u.im = t.im; u.paths = below;
-              U[count] = u;
-            }
-            ++count;
+          cnt[i] = c ? c : 0x80000000u;
+        }
+        __syncthreads();
+        // units of this level: nodes with bit 31; children: the rest (scan of the low bits)
+        for (uint32_t i = tid; i < nf; i += kThreads) flag[i] = cnt[i] >> 31;
+        __syncthreads();
+        const uint32_t nunit = block_scan_call(sh, flag, off, (int)nf);
+        for (uint32_t i = tid; i < nf; i += kThreads) {
+          if (!(cnt[i] >> 31)) continue;
+          const uint32_t k = units + off[i];
+          if (k < (uint32_t)p.budget) {
+            const SplitEnt t = fr[cur][i];
+            Unit u;
+            u.q = q; u.j = (int16_t)j; u.sjm1 = t.sjm1; u.sj = t.sj; u.pad = 0;
+            u.re = t.re; u.im = t.im; u.paths = b.cR[sh.cb[j] + t.sj];
+            U[k] = u;
           }
         }
-        if (count <= p.budget) break;
-        thr = thr > (~0ull >> 2) ? ~0ull : thr * 4;  // too many units for the slots: coarser
+        units += nunit;
+        __syncthreads();
+        for (uint32_t i = tid; i < nf; i += kThreads) flag[i] = (cnt[i] >> 31) ? 0u : cnt[i];
+        __syncthreads();
+        const uint32_t nchild = block_scan_call(sh, flag, off, (int)nf);
+        if ((long long)nchild > cap) {
+          // the next frontier does not fit: the remaining nodes become units as they are
+          for (uint32_t i = tid; i < nf; i += kThreads) flag[i] = (cnt[i] >> 31) ? 0u : 1u;
+          __syncthreads();
+          const uint32_t nrest = block_scan_call(sh, flag, off, (int)nf);
+          for (uint32_t i = tid; i < nf; i += kThreads) {
+            if (cnt[i] >> 31) continue;
+            const uint32_t k = units + off[i];
+            if (k < (uint32_t)p.budget) {
+              const SplitEnt t = fr[cur][i];
+              Unit u;
+              u.q = q; u.j = (int16_t)j; u.sjm1 = t.sjm1; u.sj = t.sj; u.pad = 0;
+              u.re = t.re; u.im = t.im; u.paths = b.cR[sh.cb[j] + t.sj];
+              U[k] = u;
+            }
+          }
+          units += nrest;
+          __syncthreads();
+          break;
+        }
+        // children in node order, states of column j+1 in increasing order
+        for (uint32_t i = tid; i < nf; i += kThreads) {
+          if (cnt[i] >> 31) continue;
+          const SplitEnt t = fr[cur][i];
+          const double2 pr = make_double2(t.re, t.im);
+          uint32_t o = off[i];
+          const int n1 = sh.n[j + 1];
+          for (int s1 = 0; s1 < n1; ++s1) {
+            if (!live(b, sh, j + 1, s1) || !compat(p, b, sh, j + 1, t.sj, s1)) continue;
+            ull c2 = 0;
+            const double2 np = cmul(pr, cut_factor(p, b, sh, j, t.sjm1, t.sj, s1, c2));
+            SplitEnt e;
+            e.sjm1 = t.sj; e.sj = (uint16_t)s1; e.re = np.x; e.im = np.y;
+            DCHECK(o < nchild && (long long)o < cap, "split child");
+            fr[cur ^ 1][o++] = e;
+          }
+        }
+        __syncthreads();
+        nf = nchild;
+        cur ^= 1;
       }
-      p.nunits[q] = count;
+      if (units <= (uint32_t)p.budget) {
+        if (tid == 0) p.nunits[q] = (int)units;
+        break;
+      }
+      thr = thr > (~0ull >> 2) ? ~0ull : thr * 4;  // too many units for the slots: coarser
+      __syncthreads();
     }
     __syncthreads();
   }
@@ -1407,14 +1491,27 @@ extern "C" int lofp_launch_paths(const CallParams *p, int grid, void *stream, vo
     attr_device_mask |= 1 << (dev & 31);
   }
   const int pgrid = p->B < grid ? p->B : grid;
+#define LOFP_CHECK_STEP(name)                                                                  \
+  if (getenv("LOFP_SYNC_EACH")) {                                                              \
+    const cudaError_t e_ = cudaStreamSynchronize(st);                                          \
+    if (e_ != cudaSuccess) {                                                                   \
+      fprintf(stderr, "liblofp: %s failed: %s\n", name, cudaGetErrorString(e_));               \
+      return (int)e_;                                                                          \
+    }                                                                                          \
+  }
   lofp_plan_kernel<<<pgrid, kThreads, 0, st>>>(*p);
+  LOFP_CHECK_STEP("plan")
   lofp_thr_kernel<<<1, kThreads, 0, st>>>(*p, grid);
   lofp_split_kernel<<<pgrid, kThreads, 0, st>>>(*p);
+  LOFP_CHECK_STEP("split")
   lofp_scan_kernel<<<1, kThreads, 0, st>>>(*p);
+  LOFP_CHECK_STEP("scan")
   if (ev0) cudaEventRecord((cudaEvent_t)ev0, st);
   lofp_units_kernel<<<grid, kThreads, smem, st>>>(*p);
   if (ev1) cudaEventRecord((cudaEvent_t)ev1, st);
+  LOFP_CHECK_STEP("units")
   lofp_final_kernel<<<(p->B + 7) / 8 < 1184 ? (p->B + 7) / 8 : 1184, 256, 0, st>>>(*p);  // a warp per output
+  LOFP_CHECK_STEP("final")
   lofp_generic_kernel<<<grid, kThreads, 0, st>>>(*p);  // outputs over the column limits
   return (int)cudaGetLastError();
 }
