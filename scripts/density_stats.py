@@ -1,3 +1,5 @@
+"""P:318 density workload (10 modes, depth 4, S = T = (k,...,k)) single outputs: path-sum
+statistics per unit-size setting (units, pairs, list elements, phase split, tile staging share)."""
 import os, sys, numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import lofp_inputs as li
