@@ -512,6 +512,7 @@ def main():
                 "peak_source": f"measured DFMA issue rate (fp64_peak.cu, {nsm.value} SMs, burst); "
                                f"MEASURED_PEAKS.json has no FP64 entry",
                 "nominal_peak": 148 * 64 * 1965e6 / 1e12,
+                "frac_of_nominal": achieved / (148 * 64 * 1965e6 / 1e12),
                 "work_per_launch": {"paths": paths, "cmuls": cmuls, "fp64_lane_inst": alg},
                 "kernel": "lofp_units_kernel", "kernel_ms": umean,
                 "kernel_share_of_step": umean / (t_local / args.steps)}
