@@ -67,13 +67,14 @@ struct GateW {           // one phase gate folded into the cut
   uint8_t slot;          // col_off 0: the byte of the entries' gather holding F(k-1)
 };
 
-struct CWarp {           // shared state of one warp's output
-  uint64_t lo[kMaxModes + 1];      // packed lower corner of each column's box
-  uint64_t hi[kMaxModes + 1];      // packed upper corner
-  uint32_t vbase[kMaxModes + 1];   // first packed state of each column in the scratch
-  uint16_t n[kMaxModes + 1];       // states per column
-  uint8_t nseg[kMaxModes + 1];
-  int16_t G[kMaxModes + 1];        // cum(T)
+template <int MM>          // MM: the most modes of a circuit this instantiation takes
+struct CWarpT {          // shared state of one lane group's output
+  uint64_t lo[MM + 1];             // packed lower corner of each column's box
+  uint64_t hi[MM + 1];             // packed upper corner
+  uint32_t vbase[MM + 1];          // first packed state of each column in the scratch
+  uint16_t n[MM + 1];              // states per column
+  uint8_t nseg[MM + 1];
+  int16_t G[MM + 1];               // cum(T)
   // cut k being contracted (staged once per cut)
   int ftab[kCF];                   // Appendix-A block of each of its BS (offset in the table)
   uint32_t fsh[kCF];               // segments it reads: i (column k) | sC << 8 (column k+1)
@@ -117,9 +118,49 @@ __device__ __forceinline__ ull sat_add_c(ull a, ull b) {
   return c < a ? ~0ull : c;
 }
 
+// A group of G consecutive lanes of a warp that evaluates one output (G = 32: the whole
+// warp; G = 8: four small outputs per warp).  Groups of one warp run different outputs, so
+// every collective names the group's lanes only.
+template <int G>
+struct Grp {
+  int lane;       // lane within the group
+  unsigned mask;  // the group's lanes
+  __device__ __forceinline__ Grp() {
+    const int l = threadIdx.x & 31;
+    lane = l % G;
+    mask = G == 32 ? 0xffffffffu : (((1u << (G & 31)) - 1u) << (l - lane));
+  }
+  template <class T>
+  __device__ __forceinline__ T scan(T v) const {  // inclusive prefix sum over the group
+#pragma unroll
+    for (int d = 1; d < G; d <<= 1) {
+      const T u = __shfl_up_sync(mask, v, d, G);
+      if (lane >= d) v += u;
+    }
+    return v;
+  }
+  template <class T>
+  __device__ __forceinline__ T last(T v) const { return __shfl_sync(mask, v, G - 1, G); }
+  template <class T>
+  __device__ __forceinline__ T first(T v) const { return __shfl_sync(mask, v, 0, G); }
+  __device__ __forceinline__ bool any(bool b) const { return (__ballot_sync(mask, b) & mask) != 0u; }
+  __device__ __forceinline__ void sync() const { __syncwarp(mask); }
+  __device__ __forceinline__ double sum(double v) const {  // fixed-order tree (deterministic)
+#pragma unroll
+    for (int d = G / 2; d > 0; d >>= 1) v += __shfl_down_sync(mask, v, d, G);
+    return v;
+  }
+  __device__ __forceinline__ ull sum_sat(ull v) const {
+#pragma unroll
+    for (int d = G / 2; d > 0; d >>= 1) v = sat_add_c(v, __shfl_down_sync(mask, v, d, G));
+    return v;
+  }
+};
+
 // Upper corner of the sub-box of column k-1 compatible with state vr of column k:
 // F_t(k-1) <= F_t(k) on every time interval (CmpPair list of column k).
-__device__ __forceinline__ uint64_t sub_hi(const CCirc &cc, const CWarp &w, int k, uint64_t vr) {
+template <class W>
+__device__ __forceinline__ uint64_t sub_hi(const CCirc &cc, const W &w, int k, uint64_t vr) {
   uint64_t h = w.hi[k - 1];
   for (int c = 0; c < cc.ncmp[k]; ++c) {
     const int sa = cc.cmp[k][c] & 0xff, v = byte_at(vr, cc.cmp[k][c] >> 8);
@@ -174,57 +215,50 @@ __device__ __forceinline__ uint64_t gather(uint64_t v, const uint8_t *gseg, int 
 
 // Rows of the level whose rows are the states of column k (entries: the compatible
 // sub-box of column k-1): exclusive offsets into roff[0..n_k], returns the entry count.
-__device__ uint32_t level_rows(const CCirc &cc, const CWarp &w, const uint64_t *vals, int k, uint32_t *roff,
-                               int lane) {
+template <int G, class W>
+__device__ uint32_t level_rows(const CCirc &cc, const W &w, const uint64_t *vals, int k, uint32_t *roff,
+                               const Grp<G> &g) {
   const int nk = w.n[k], ns = w.nseg[k - 1];
   uint32_t run = 0;
-  for (int base = 0; base < nk; base += 32) {
-    const int s = base + lane;
+  for (int base = 0; base < nk; base += G) {
+    const int s = base + g.lane;
     uint32_t c = 0;
     if (s < nk) c = box_count(w.lo[k - 1], sub_hi(cc, w, k, vals[w.vbase[k] + s]), ns);
-    uint32_t incl = c;
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= d) incl += v;
-    }
+    const uint32_t incl = g.scan(c);
     if (s < nk) roff[s] = run + incl - c;
-    run += __shfl_sync(0xffffffffu, incl, 31);
+    run += g.last(incl);
   }
-  if (lane == 0) roff[nk] = run;
-  __syncwarp();
+  if (g.lane == 0) roff[nk] = run;
+  g.sync();
   return run;
 }
 
 // Per-output setup: G = cum(T), the light-cone box of every column (readings R5, R15),
 // the packed states.  Returns kStatusOk / Zero / Bad / Deferred (warp-uniform).
-__device__ int setup_warp(const CallParams &p, const CCirc &cc, CWarp &w, uint64_t *vals, int q, int lane) {
+template <int G, class W>
+__device__ int setup_warp(const CallParams &p, const CCirc &cc, W &w, uint64_t *vals, int q, const Grp<G> &g) {
   const int M = p.M;
   // G = cum(T); negative entries make the row bad, totals other than N an exact zero
   int bad = 0, run = 0;
-  if (lane == 0) w.G[0] = 0;
-  for (int base = 0; base < M; base += 32) {
-    const int i = base + lane;
+  if (g.lane == 0) w.G[0] = 0;
+  for (int base = 0; base < M; base += G) {
+    const int i = base + g.lane;
     int t = 0;
     if (i < M) {
       t = p.T[(long long)q * M + i];
       if (t < 0) bad = 1;
       t = min(max(t, 0), 255);
     }
-    int incl = t;
-    for (int d = 1; d < 32; d <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= d) incl += v;
-    }
+    const int incl = g.scan(t);
     if (i < M) w.G[i + 1] = (int16_t)min(run + incl, 32767);
-    run += __shfl_sync(0xffffffffu, incl, 31);
+    run += g.last(incl);
   }
-  bad = __any_sync(0xffffffffu, bad);
-  if (bad) return kStatusBad;
+  if (g.any(bad)) return kStatusBad;
   if (run != p.N) return kStatusZero;  // photon number (reading R9)
-  __syncwarp();
+  g.sync();
   // segment boxes: backward (T) and forward (S) light cones intersected
   int zero = 0, defer = 0;
-  for (int k = lane; k <= M; k += 32) {
+  for (int k = g.lane; k <= M; k += G) {
     if (!cc.ok[k]) {
       defer = 1;
       w.n[k] = 0;
@@ -252,30 +286,25 @@ __device__ int setup_warp(const CallParams &p, const CCirc &cc, CWarp &w, uint64
     w.n[k] = (uint16_t)min(n, (uint32_t)kCMaxN);
     w.nseg[k] = (uint8_t)nseg;
   }
-  zero = __any_sync(0xffffffffu, zero);
-  defer = __any_sync(0xffffffffu, defer);
-  if (zero) return kStatusZero;  // a column with no state: structurally unreachable (R5)
-  if (defer || p.tab_off[p.nbs] > 0x7fffffffll) return kStatusDeferred;  // (int32 table offsets)
-  __syncwarp();
+  const bool any_zero = g.any(zero), any_defer = g.any(defer);
+  if (any_zero) return kStatusZero;  // a column with no state: structurally unreachable (R5)
+  if (any_defer || p.tab_off[p.nbs] > 0x7fffffffll) return kStatusDeferred;  // (int32 table offsets)
+  g.sync();
   // first packed state of each column
   uint32_t tot = 0;
-  for (int base = 0; base <= M; base += 32) {
-    const int k = base + lane;
+  for (int base = 0; base <= M; base += G) {
+    const int k = base + g.lane;
     const uint32_t c = k <= M ? w.n[k] : 0u;
-    uint32_t incl = c;
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= d) incl += v;
-    }
+    const uint32_t incl = g.scan(c);
     if (k <= M) w.vbase[k] = tot + incl - c;
-    tot += __shfl_sync(0xffffffffu, incl, 31);
+    tot += g.last(incl);
   }
   if (tot > (uint32_t)kCMaxStates) return kStatusDeferred;
-  __syncwarp();
-  if (lane == 0) atomicMax(&p.ctr->max_states, (ull)tot);
+  g.sync();
+  if (g.lane == 0) atomicMax(&p.ctr->max_states, (ull)tot);
   // packed segment values of every state (mixed radix, segment 0 fastest); lanes over the
   // states of all columns (column by a search over vbase)
-  for (uint32_t x = lane; x < tot; x += 32) {
+  for (uint32_t x = g.lane; x < tot; x += G) {
     int lo_k = 0, hi_k = M;
     while (lo_k < hi_k) {
       const int mid = (lo_k + hi_k + 1) >> 1;
@@ -293,7 +322,7 @@ __device__ int setup_warp(const CallParams &p, const CCirc &cc, CWarp &w, uint64
     }
     vals[x] = v;
   }
-  __syncwarp();
+  g.sync();
   return kStatusOk;
 }
 
@@ -329,7 +358,8 @@ __device__ __forceinline__ double2 cut_fac(const double2 *__restrict__ table, co
 }
 
 // phase gates of the cut on (column k-1, column k): n = F(k) - F(k-1) at their time
-__device__ __forceinline__ double2 gates_a(const CallParams &p, const CWarp &w, int ngate, uint64_t vb, uint64_t g,
+template <class W>
+__device__ __forceinline__ double2 gates_a(const CallParams &p, const W &w, int ngate, uint64_t vb, uint64_t g,
                                            double2 fac, ull &cm) {
   for (int gi = 0; gi < ngate; ++gi) {
     const GateW gw = w.gat[gi];
@@ -343,10 +373,10 @@ __device__ __forceinline__ double2 gates_a(const CallParams &p, const CWarp &w, 
 
 // The sum over one row of level k (the states of column k-1 compatible with sb) of
 // A_k(c_{k-1}, sb) f_k(c_{k-1}, sb, sc): two entries per step, loads first.
-template <int NF, bool CNT, bool FULL>
+template <int NF, bool CNT, bool FULL, class W>
 __device__ __forceinline__ void row_sum(const double2 *__restrict__ table, const int *s_tri, const int (&tbo)[NF],
                                         const uint32_t (&cb)[NF], int nfac, double2 gfix, const CallParams &p,
-                                        const CWarp &w, int ngate, uint64_t vb, const double2 *__restrict__ Ac,
+                                        const W &w, int ngate, uint64_t vb, const double2 *__restrict__ Ac,
                                         const uint64_t *__restrict__ Gc, const ull *__restrict__ Cc, uint32_t r0,
                                         uint32_t r1, double &sx, double &sy, ull &csum, ull &cm, ull &terms) {
   uint32_t r = r0;
@@ -382,10 +412,12 @@ __device__ __forceinline__ void row_sum(const double2 *__restrict__ table, const
 
 }  // namespace
 
-// NF: the most BS any cut carries (<= 7; loops unrolled to it), CNT: exact path counts too
-template <int NF, bool CNT>
+// NF: the most BS any cut carries (<= 7; loops unrolled to it), CNT: exact path counts too,
+// G: lanes per output (32, or 8 for small circuits in large batches), MM: most modes
+template <int NF, bool CNT, int G, int MM>
 __global__ void __launch_bounds__(32 * kCW, 2) lofp_contract_warp_kernel(const __grid_constant__ CallParams p) {
-  __shared__ CWarp sw[kCW];
+  constexpr int kGroups = kCW * (32 / G);  // outputs in flight per block
+  __shared__ CWarpT<MM> sw[kGroups];
   __shared__ int s_tri[kMaxPhotons + 2];  // tri(n) = sum_{m<n} (m+1)^2: block offsets in a BS table
   __shared__ uint8_t s_gseg[kMaxModes + 1][kCSeg], s_ngs[kMaxModes + 1];  // gather slots per cut
   for (int n = threadIdx.x; n <= kMaxPhotons + 1; n += blockDim.x) s_tri[n] = n * (n + 1) * (2 * n + 1) / 6;
@@ -393,12 +425,13 @@ __global__ void __launch_bounds__(32 * kCW, 2) lofp_contract_warp_kernel(const _
   gather_lists(p, s_gseg, s_ngs);
   cache_circuit(p, cc);
   __syncthreads();
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  CWarp &w = sw[wib];
+  const Grp<G> g;
+  const int gib = threadIdx.x / G;  // group in the block
+  CWarpT<MM> &w = sw[gib];
   const int M = p.M;
   constexpr bool with_counts = CNT;
-  // warp scratch: packed states, two row-offset arrays, two levels (values, gathers [, counts])
-  char *ws = p.slab + ((long long)blockIdx.x * kCW + wib) * p.cw_bytes;
+  // group scratch: packed states, two row-offset arrays, two levels (values, gathers [, counts])
+  char *ws = p.slab + ((long long)blockIdx.x * kGroups + gib) * p.cw_bytes;
   uint64_t *vals = (uint64_t *)ws;
   uint32_t *const roff0 = (uint32_t *)(vals + kCMaxStates), *const roff1 = roff0 + (kCMaxN + 1);
   char *lv0 = (char *)(roff1 + kCMaxN + 1);
@@ -415,10 +448,10 @@ __global__ void __launch_bounds__(32 * kCW, 2) lofp_contract_warp_kernel(const _
   ull cm = 0, terms = 0;
   while (true) {
     int q = 0;
-    if (lane == 0) q = (int)atomicAdd(&p.ctr->cticket, 1ull);
-    q = __shfl_sync(0xffffffffu, q, 0);
+    if (g.lane == 0) q = (int)atomicAdd(&p.ctr->cticket, 1ull);
+    q = g.first(q);
     if (q >= p.B) break;
-    int st = setup_warp(p, cc, w, vals, q, lane);
+    int st = setup_warp(p, cc, w, vals, q, g);
     double re = 0.0, im = 0.0;
     ull count = 0;
     int cur = 0;
@@ -430,48 +463,48 @@ __global__ void __launch_bounds__(32 * kCW, 2) lofp_contract_warp_kernel(const _
           const double2 e = p.gate_tab[g * (p.N + 1) + p.N];
           root = make_double2(root.x * e.x - root.y * e.y, root.x * e.y + root.y * e.x);
         }
-      const uint32_t tot = level_rows(cc, w, vals, 1, roff0, lane);
+      const uint32_t tot = level_rows(cc, w, vals, 1, roff0, g);
       if (tot > (uint64_t)capE) st = kStatusDeferred;
       if (st == kStatusOk) {
         const uint64_t g0 = gather(vals[w.vbase[0]], s_gseg[1], s_ngs[1]);
-        for (uint32_t t = lane; t < tot; t += 32) {
+        for (uint32_t t = g.lane; t < tot; t += G) {
           lvA[t] = root;
           lgA[t] = g0;
           if (with_counts) lcA[t] = 1ull;
         }
-        __syncwarp();
+        g.sync();
       }
     }
     // cuts 1..M-1: level k (rows: column k, entries: column k-1) -> level k+1
     for (int k = 1; k <= M - 1 && st == kStatusOk; ++k) {
       const int nxt = cur ^ 1;
-      const uint32_t totn = level_rows(cc, w, vals, k + 1, ROFF(nxt), lane);
+      const uint32_t totn = level_rows(cc, w, vals, k + 1, ROFF(nxt), g);
       if (totn > (uint64_t)capE) {
         st = kStatusDeferred;
         break;
       }
       const ColInfo ck = p.col[k];
       const int nfac = ck.nfac, ngate = ck.ngate, ncR = cc.ncmp[k + 1];
-      if (lane < nfac) {
-        const FacInfo fi = p.fac[ck.fac_base + lane];
-        w.ftab[lane] = (int)p.tab_off[fi.bs];
-        w.fsh[lane] = (uint32_t)fi.i | (uint32_t)fi.sC << 8;
+      for (int f = g.lane; f < nfac; f += G) {
+        const FacInfo fi = p.fac[ck.fac_base + f];
+        w.ftab[f] = (int)p.tab_off[fi.bs];
+        w.fsh[f] = (uint32_t)fi.i | (uint32_t)fi.sC << 8;
       }
-      __syncwarp();
-      if (lane == 0) {
-        int slot = nfac;  // the gather order of stage_gather(k)
-        for (int g = 0; g < ngate; ++g) {
-          const GateInfo gi = p.gat[ck.gate_base + g];
+      g.sync();
+      if (g.lane == 0) {
+        int slot = nfac;  // the gather order of gather_lists
+        for (int gt = 0; gt < ngate; ++gt) {
+          const GateInfo gi = p.gat[ck.gate_base + gt];
           GateW gw;
           gw.row = gi.gate;
           gw.col_off = gi.col_off;
           gw.seg_lo = gi.seg_lo;
           gw.seg_hi = gi.seg_hi;
           gw.slot = gi.col_off ? 0 : (uint8_t)slot++;
-          w.gat[g] = gw;
+          w.gat[gt] = gw;
         }
       }
-      __syncwarp();
+      g.sync();
       const double2 *__restrict__ table = p.table;
       int tbo[NF];
 #pragma unroll
@@ -488,7 +521,7 @@ __global__ void __launch_bounds__(32 * kCW, 2) lofp_contract_warp_kernel(const _
       const uint32_t vbC = w.vbase[k + 1];
       int sc = 0, sc_last = -1;
       uint64_t vc = 0, hB = 0;
-      for (uint32_t t = lane; t < totn; t += 32) {
+      for (uint32_t t = g.lane; t < totn; t += G) {
         while (rn[sc + 1] <= t) ++sc;
         if (sc != sc_last) {  // the row's state (column k+1) and its sub-box of column k
           vc = vals[vbC + sc];
@@ -519,8 +552,8 @@ __global__ void __launch_bounds__(32 * kCW, 2) lofp_contract_warp_kernel(const _
           cb[f] = (uint32_t)byte_at(vc, sh >> 8) | (uint32_t)byte_at(vb, i) << 8 | (uint32_t)byte_at(vb, i + 1) << 16;
         }
         double2 gfix = make_double2(1.0, 0.0);  // gates on (column k, column k+1): fixed too
-        for (int g = 0; g < ngate; ++g) {
-          const GateW gw = w.gat[g];
+        for (int gt = 0; gt < ngate; ++gt) {
+          const GateW gw = w.gat[gt];
           if (!gw.col_off) continue;
           const double2 ge = p.gate_tab[gw.row * (p.N + 1) + byte_at(vc, gw.seg_hi) - byte_at(vb, gw.seg_lo)];
           gfix = make_double2(gfix.x * ge.x - gfix.y * ge.y, gfix.x * ge.y + gfix.y * ge.x);
@@ -541,7 +574,7 @@ __global__ void __launch_bounds__(32 * kCW, 2) lofp_contract_warp_kernel(const _
         Gn[t] = gather(vb, s_gseg[k + 1], s_ngs[k + 1]);  // what cut k+1 reads of sb
         if (with_counts) Cn[t] = csum;
       }
-      __syncwarp();
+      g.sync();
       cur = nxt;
     }
     if (st == kStatusOk) {
@@ -549,19 +582,17 @@ __global__ void __launch_bounds__(32 * kCW, 2) lofp_contract_warp_kernel(const _
       const uint32_t e = ROFF(cur)[1];
       const double2 *Al = LV(cur);
       const ull *Cl = LC(cur);
-      for (uint32_t t = lane; t < e; t += 32) {
+      for (uint32_t t = g.lane; t < e; t += G) {
         re += Al[t].x;
         im += Al[t].y;
         if (with_counts) count = sat_add_c(count, Cl[t]);
       }
     }
-    // fixed-order warp reduction (deterministic)
-    for (int d = 16; d > 0; d >>= 1) {
-      re += __shfl_down_sync(0xffffffffu, re, d);
-      im += __shfl_down_sync(0xffffffffu, im, d);
-      count = sat_add_c(count, __shfl_down_sync(0xffffffffu, count, d));
-    }
-    if (lane == 0) {
+    // fixed-order group reduction (deterministic)
+    re = g.sum(re);
+    im = g.sum(im);
+    count = g.sum_sat(count);
+    if (g.lane == 0) {
       if (st == kStatusOk && with_counts && count == 0) st = kStatusZero;
       if (st == kStatusDeferred) {
         atomicAdd(&p.ctr->cdeferred, 1ull);
@@ -577,8 +608,10 @@ __global__ void __launch_bounds__(32 * kCW, 2) lofp_contract_warp_kernel(const _
       }
       p.status[q] = (uint8_t)st;
     }
-    __syncwarp();
+    g.sync();
   }
+  __syncwarp();
+  const int lane = threadIdx.x & 31;
   for (int d = 16; d > 0; d >>= 1) {
     cm += __shfl_down_sync(0xffffffffu, cm, d);
     terms += __shfl_down_sync(0xffffffffu, terms, d);
@@ -589,34 +622,49 @@ __global__ void __launch_bounds__(32 * kCW, 2) lofp_contract_warp_kernel(const _
   }
 }
 
-template <int NF, bool CNT>
+template <int NF, bool CNT, int G, int MM>
 static int launch_nf(const CallParams *p, int grid, cudaStream_t stream) {
   static int per_sm[32] = {0};
   static int nsm[32] = {0};
+  constexpr int kGroups = kCW * (32 / G);
   int dev = 0;
   cudaGetDevice(&dev);
   dev &= 31;
   if (!per_sm[dev]) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], lofp_contract_warp_kernel<NF, CNT>, 32 * kCW, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], lofp_contract_warp_kernel<NF, CNT, G, MM>, 32 * kCW, 0);
     cudaDeviceGetAttribute(&nsm[dev], cudaDevAttrMultiProcessorCount, dev);
     if (per_sm[dev] < 1) per_sm[dev] = 1;
   }
   long long blocks = (long long)per_sm[dev] * nsm[dev];
-  const long long need = ((long long)p->B + kCW - 1) / kCW;
+  const long long need = ((long long)p->B + kGroups - 1) / kGroups;
   if (need < blocks) blocks = need;
   if (blocks < 1) return 0;
   CallParams q = *p;
   const long long total = (long long)grid * p->slab_bytes;
-  q.cw_bytes = (total / (blocks * kCW)) & ~255ll;
+  q.cw_bytes = (total / (blocks * kGroups)) & ~255ll;
   const long long fixed = (long long)kCMaxStates * 8 + 2ll * (kCMaxN + 1) * 4 + 16;
   if (q.cw_bytes < fixed + 64 * 1024) return -1;  // scratch too small (LOFP_SLAB_MB): not launched
-  lofp_contract_warp_kernel<NF, CNT><<<(int)blocks, 32 * kCW, 0, stream>>>(q);
+  lofp_contract_warp_kernel<NF, CNT, G, MM><<<(int)blocks, 32 * kCW, 0, stream>>>(q);
   return (int)cudaGetLastError();
 }
 
+// Small circuits (<= 32 modes, <= 4 BS per cut) in batches that fill the GPU four times over
+// run with 8 lanes per output (four outputs per warp): their levels hold a few entries per
+// lane of a full warp (configs[1]-sized outputs: lanes mostly idle).
+constexpr int kSmallM = 32;
+
 template <int NF>
 static int launch_cnt(const CallParams *p, int grid, cudaStream_t stream) {
-  return p->counts ? launch_nf<NF, true>(p, grid, stream) : launch_nf<NF, false>(p, grid, stream);
+  if constexpr (NF <= 4) {
+    const bool small = p->M <= kSmallM && (long long)p->B >= 4ll * 32 * grid;
+    if (p->contract_group == 8 || (p->contract_group == 0 && small && p->M <= kSmallM)) {
+      if (p->M <= kSmallM)
+        return p->counts ? launch_nf<NF, true, 8, kSmallM>(p, grid, stream)
+                         : launch_nf<NF, false, 8, kSmallM>(p, grid, stream);
+    }
+  }
+  return p->counts ? launch_nf<NF, true, 32, kMaxModes>(p, grid, stream)
+                   : launch_nf<NF, false, 32, kMaxModes>(p, grid, stream);
 }
 
 // Launch: blocks of kCW warps, as many as are resident at once (the warps pull outputs from

@@ -157,6 +157,7 @@ struct CallParams {
   int deferred_only;     // contraction block kernel: only outputs with kStatusDeferred
   int max_nfac;          // most BS a cut carries (contraction warp kernel instantiation)
   int contract_block_only;  // test hook (LOFP_CONTRACT_BLOCK): contraction by the block kernel only
+  int contract_group;    // test hook (LOFP_CONTRACT_GROUP = 8 or 32): lanes per output of the warp kernel
   long long table_cap;   // entries allocated for the Appendix-A table
   const ColInfo *col;
   const SegInfo *seg;

@@ -246,3 +246,43 @@ def test_small_scratch(lofp, monkeypatch):
     monkeypatch.delenv("LOFP_SLAB_MB")
     ref, _, _ = contract(lofp, c.M, c.layers, c.S, T)
     assert tol_ok(got, ref)[0]
+
+
+@pytest.mark.parametrize("counts", [False, True])
+def test_eight_lane_groups_match_full_warps(lofp, monkeypatch, counts):
+    """Small circuits in large batches run with 8 lanes per output (four outputs per warp);
+    forced on and off (LOFP_CONTRACT_GROUP) on configs[1]'s literal batch tiled to 40960
+    outputs, and on random small circuits with gates: same amplitudes and path counts."""
+    c = li.config(1)
+    d = load(1)
+    T = np.tile(d["T_literal"].astype(np.int32), (40, 1))
+    res = {}
+    for grp in ("8", "32"):
+        monkeypatch.setenv("LOFP_CONTRACT_GROUP", grp)
+        circ = lofp.Circuit(c.M, c.layers)
+        Td = torch.from_numpy(T).cuda()
+        cnt = torch.zeros(len(T), dtype=torch.int64, device="cuda") if counts else None
+        a = circ.contract(c.S, Td, counts=cnt).cpu().numpy()
+        res[grp] = (a, None if cnt is None else cnt.cpu().numpy().astype(np.uint64))
+    assert tol_ok(res["8"][0], res["32"][0])[0]
+    assert tol_ok(res["8"][0][:1024], oracle.path_sum(c.M, c.layers, c.S, T[:1024]))[0]
+    if counts:
+        assert np.array_equal(res["8"][1], res["32"][1])
+        assert np.array_equal(res["8"][1][:1024], d["P_literal"])
+    rng = np.random.default_rng(808)
+    for _ in range(6):
+        M = int(rng.integers(2, 12))
+        D = int(rng.integers(1, 7))
+        N = int(rng.integers(1, 5))
+        layers = li.random_nn_circuit(M, D, rng, fill=0.8, reverse_prob=0.3)
+        S = np.zeros(M, dtype=np.int32)
+        for m in rng.integers(0, M, size=N):
+            S[m] += 1
+        gates = [(int(rng.integers(0, M)), int(rng.integers(0, D + 1)), float(rng.uniform(-3, 3)),
+                  float(rng.uniform(-1, 1))) for _ in range(int(rng.integers(0, 3)))]
+        Tr = li.all_outputs(M, N)
+        monkeypatch.setenv("LOFP_CONTRACT_GROUP", "8")
+        got, cnt, _ = contract(lofp, M, layers, S, Tr, gates)
+        ref, leaves = oracle.path_sum(M, layers, S, Tr, return_leaves=True, gates=gates)
+        assert tol_ok(got, ref)[0]
+        assert np.array_equal(cnt, leaves)
