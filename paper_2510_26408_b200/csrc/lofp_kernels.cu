@@ -890,6 +890,8 @@ __device__ void process_stack(const CallParams &p, Block &b, Shared &sh, double2
         // every warp takes every (kThreads/32)-th tile: a static, deterministic assignment
         const int warp = tid >> 5, lane = tid & 31;
         double2 *sW = sY + warp * kYT;
+        int last_lo = -1;
+        uint32_t last_yt = 0;
         for (uint32_t t = warp; t < ntiles; t += kThreads / 32) {
           int lo = 0, hi = ne - 1;
           while (lo < hi) {
@@ -910,15 +912,21 @@ __device__ void process_stack(const CallParams &p, Block &b, Shared &sh, double2
           const double2 *FY = pr.swap ? FLall + (long long)lo * nctxL : FRall + (long long)lo * nctxR;
           const long long tc0 = clock64();
           const uint32_t y0 = yt * kYT, len = min((uint32_t)kYT, pr.nY - y0);
+          // the warp's previous tile had the same pair and Y slice (the tiles of a pair go
+          // X-tile fastest, so a warp's consecutive tiles often share it): already staged
+          if (lo != last_lo || yt != last_yt) {
 #pragma unroll
-          for (int r = 0; r < kYT / 32; ++r) {
-            const uint32_t jj = lane + 32 * r;
-            if (jj < len) {
-              DCHECK(Yc[y0 + jj] < (pr.swap ? nctxL : nctxR), "Y ctx");
-              sW[jj] = cmul(Yp[y0 + jj], FY[Yc[y0 + jj]]);
+            for (int r = 0; r < kYT / 32; ++r) {
+              const uint32_t jj = lane + 32 * r;
+              if (jj < len) {
+                DCHECK(Yc[y0 + jj] < (pr.swap ? nctxL : nctxR), "Y ctx");
+                sW[jj] = cmul(Yp[y0 + jj], FY[Yc[y0 + jj]]);
+              }
             }
+            cm += (len + 31 - lane) / 32;
+            last_lo = lo;
+            last_yt = yt;
           }
-          cm += (len + 31 - lane) / 32;
           const uint32_t x0 = xt * kXT;
           double2 x[kKX];
           int nv = 0;
