@@ -51,6 +51,12 @@ typedef unsigned long long ull;
   } while (0)
 #endif
 
+#ifdef LOFP_CPROF  // phase clocks and level statistics of the warp kernel (A/B experiments only)
+#define CPROF(x) x
+#else
+#define CPROF(x)
+#endif
+
 constexpr int kCW = 8;             // warps (outputs in flight) per block
 constexpr int kCSeg = 8;           // segments per column: one byte each of a packed u64
 constexpr int kCMaxN = 4096;       // states per column (as the block kernel)
@@ -76,7 +82,8 @@ struct CWarpT {          // shared state of one lane group's output
   uint8_t nseg[MM + 1];
   int16_t G[MM + 1];               // cum(T)
   // cut k being contracted (staged once per cut)
-  int ftab[kCF];                   // Appendix-A block of each of its BS (offset in the table)
+  int ftab[kCF];                   // Appendix-A block of each of its BS (offset in the x1-linear table)
+  uint8_t fcap[kCF];               // its photon cap (the block's extent)
   uint32_t fsh[kCF];               // segments it reads: i (column k) | sC << 8 (column k+1)
   GateW gat[kCFac];
 };
@@ -288,7 +295,7 @@ __device__ int setup_warp(const CallParams &p, const CCirc &cc, W &w, uint64_t *
   }
   const bool any_zero = g.any(zero), any_defer = g.any(defer);
   if (any_zero) return kStatusZero;  // a column with no state: structurally unreachable (R5)
-  if (any_defer || p.tab_off[p.nbs] > 0x7fffffffll) return kStatusDeferred;  // (int32 table offsets)
+  if (any_defer || p.tabA_off[p.nbs] > 0x7fffffffll) return kStatusDeferred;  // (int32 table offsets)
   g.sync();
   // first packed state of each column
   uint32_t tot = 0;
@@ -328,10 +335,12 @@ __device__ int setup_warp(const CallParams &p, const CCirc &cc, W &w, uint64_t *
 
 // Cut factor of one term (eq. (1)): for every BS f of the cut, the Appendix-A element
 // <y1, n-y1|BS|x1, n-x1> with x1 = Bm - A, y1 = Bp - A, n = C - A, where A = F_{l-1}(k-1)
-// is byte f of the entry's gather g and C, Bm, Bp are fixed by the entry (cb).  A vacuum
-// BS (n = 0) reads its block's first element, exactly 1 (reading R16).
+// is byte f of the entry's gather g and C, Bm, Bp are fixed by the entry (cb).  In the
+// x1-linear table (lofp_tableA_kernel) x2 = C - Bm and y2 = C - Bp are fixed by the entry too,
+// so the element sits at pidx[f] - A with pidx[f] = block (x2, y2) + Bm, set once per entry.
+// A vacuum BS (n = 0) reads its block's element (0, 0, 0), exactly 1 (reading R16).
 template <int NF, bool FULL>
-__device__ __forceinline__ double2 cut_fac(const double2 *__restrict__ table, const int *s_tri, const int (&tbo)[NF],
+__device__ __forceinline__ double2 cut_fac(const double2 *__restrict__ tableA, const int (&pidx)[NF],
                                            const uint32_t (&cb)[NF], int nfac, uint64_t g, double2 fac) {
   // FULL (every cut of the circuit carries NF BS): no predicates, so the NF table loads are
   // independent and issue back to back
@@ -341,12 +350,12 @@ __device__ __forceinline__ double2 cut_fac(const double2 *__restrict__ table, co
     e[f] = make_double2(1.0, 0.0);
     if (FULL || f < nfac) {
       const int A = (int)((g >> (8 * f)) & 0xffu);
-      const int C = cb[f] & 0xff, Bm = (cb[f] >> 8) & 0xff, Bp = cb[f] >> 16;
-      const int n = C - A;
-      DCHECK_C(Bm >= A && C >= Bm && Bp >= A && Bp - A <= n);
-      e[f] = __ldg(table + (tbo[f] + s_tri[n] + (Bm - A) * (n + 1) + (Bp - A)));
+      DCHECK_C(((cb[f] >> 8) & 0xff) >= (uint32_t)A && (cb[f] & 0xff) >= ((cb[f] >> 8) & 0xff) &&
+               (cb[f] >> 16) >= (uint32_t)A && (cb[f] >> 16) <= (cb[f] & 0xff));
+      e[f] = __ldg(tableA + (pidx[f] - A));
     }
   }
+  (void)cb;
   // product as a balanced tree (depth log2 NF instead of NF dependent multiplications);
   // the unused slots hold exactly 1
 #pragma unroll
@@ -372,36 +381,48 @@ __device__ __forceinline__ double2 gates_a(const CallParams &p, const W &w, int 
 }
 
 // The sum over one row of level k (the states of column k-1 compatible with sb) of
-// A_k(c_{k-1}, sb) f_k(c_{k-1}, sb, sc): two entries per step, loads first.
+// A_k(c_{k-1}, sb) f_k(c_{k-1}, sb, sc): kRowU entries per step, their loads first.
+#ifndef LOFP_ROW_UNROLL
+#define LOFP_ROW_UNROLL 2
+#endif
+constexpr int kRowU = LOFP_ROW_UNROLL;
+
 template <int NF, bool CNT, bool FULL, class W>
-__device__ __forceinline__ void row_sum(const double2 *__restrict__ table, const int *s_tri, const int (&tbo)[NF],
+__device__ __forceinline__ void row_sum(const double2 *__restrict__ table, const int (&pidx)[NF],
                                         const uint32_t (&cb)[NF], int nfac, double2 gfix, const CallParams &p,
                                         const W &w, int ngate, uint64_t vb, const double2 *__restrict__ Ac,
                                         const uint64_t *__restrict__ Gc, const ull *__restrict__ Cc, uint32_t r0,
                                         uint32_t r1, double &sx, double &sy, ull &csum, ull &cm, ull &terms) {
   uint32_t r = r0;
-  for (; r + 2 <= r1; r += 2) {
-    const double2 a0 = Ac[r], a1 = Ac[r + 1];
-    const uint64_t g0 = Gc[r], g1 = Gc[r + 1];
-    if (CNT) csum = sat_add_c(csum, sat_add_c(Cc[r], Cc[r + 1]));
-    double2 f0 = cut_fac<NF, FULL>(table, s_tri, tbo, cb, nfac, g0, gfix);
-    double2 f1 = cut_fac<NF, FULL>(table, s_tri, tbo, cb, nfac, g1, gfix);
-    if (ngate) {
-      f0 = gates_a(p, w, ngate, vb, g0, f0, cm);
-      f1 = gates_a(p, w, ngate, vb, g1, f1, cm);
+  for (; r + kRowU <= r1; r += kRowU) {
+    double2 a[kRowU], f[kRowU];
+    uint64_t gg[kRowU];
+#pragma unroll
+    for (int u = 0; u < kRowU; ++u) {
+      a[u] = Ac[r + u];
+      gg[u] = Gc[r + u];
     }
-    sx = fma(a0.x, f0.x, fma(-a0.y, f0.y, sx));
-    sy = fma(a0.x, f0.y, fma(a0.y, f0.x, sy));
-    sx = fma(a1.x, f1.x, fma(-a1.y, f1.y, sx));
-    sy = fma(a1.x, f1.y, fma(a1.y, f1.x, sy));
-    terms += (a0.x != 0.0 || a0.y != 0.0) + (a1.x != 0.0 || a1.y != 0.0);
-    cm += 2 * nfac;
+    if (CNT)
+#pragma unroll
+      for (int u = 0; u < kRowU; ++u) csum = sat_add_c(csum, Cc[r + u]);
+#pragma unroll
+    for (int u = 0; u < kRowU; ++u) f[u] = cut_fac<NF, FULL>(table, pidx, cb, nfac, gg[u], gfix);
+    if (ngate)
+#pragma unroll
+      for (int u = 0; u < kRowU; ++u) f[u] = gates_a(p, w, ngate, vb, gg[u], f[u], cm);
+#pragma unroll
+    for (int u = 0; u < kRowU; ++u) {
+      sx = fma(a[u].x, f[u].x, fma(-a[u].y, f[u].y, sx));
+      sy = fma(a[u].x, f[u].y, fma(a[u].y, f[u].x, sy));
+      terms += (a[u].x != 0.0 || a[u].y != 0.0);
+    }
+    cm += kRowU * nfac;
   }
-  if (r < r1) {
+  for (; r < r1; ++r) {
     const double2 a0 = Ac[r];
     const uint64_t g0 = Gc[r];
     if (CNT) csum = sat_add_c(csum, Cc[r]);
-    double2 f0 = cut_fac<NF, FULL>(table, s_tri, tbo, cb, nfac, g0, gfix);
+    double2 f0 = cut_fac<NF, FULL>(table, pidx, cb, nfac, g0, gfix);
     if (ngate) f0 = gates_a(p, w, ngate, vb, g0, f0, cm);
     sx = fma(a0.x, f0.x, fma(-a0.y, f0.y, sx));
     sy = fma(a0.x, f0.y, fma(a0.y, f0.x, sy));
@@ -418,9 +439,7 @@ template <int NF, bool CNT, int G, int MM>
 __global__ void __launch_bounds__(32 * kCW, 2) lofp_contract_warp_kernel(const __grid_constant__ CallParams p) {
   constexpr int kGroups = kCW * (32 / G);  // outputs in flight per block
   __shared__ CWarpT<MM> sw[kGroups];
-  __shared__ int s_tri[kMaxPhotons + 2];  // tri(n) = sum_{m<n} (m+1)^2: block offsets in a BS table
   __shared__ uint8_t s_gseg[kMaxModes + 1][kCSeg], s_ngs[kMaxModes + 1];  // gather slots per cut
-  for (int n = threadIdx.x; n <= kMaxPhotons + 1; n += blockDim.x) s_tri[n] = n * (n + 1) * (2 * n + 1) / 6;
   __shared__ CCirc cc;
   gather_lists(p, s_gseg, s_ngs);
   cache_circuit(p, cc);
@@ -451,7 +470,9 @@ __global__ void __launch_bounds__(32 * kCW, 2) lofp_contract_warp_kernel(const _
     if (g.lane == 0) q = (int)atomicAdd(&p.ctr->cticket, 1ull);
     q = g.first(q);
     if (q >= p.B) break;
+    CPROF(long long c0 = clock64();)
     int st = setup_warp(p, cc, w, vals, q, g);
+    CPROF(if (g.lane == 0) atomicAdd(&p.ctr->phase[0], (ull)(clock64() - c0));)
     double re = 0.0, im = 0.0;
     ull count = 0;
     int cur = 0;
@@ -478,6 +499,7 @@ __global__ void __launch_bounds__(32 * kCW, 2) lofp_contract_warp_kernel(const _
     // cuts 1..M-1: level k (rows: column k, entries: column k-1) -> level k+1
     for (int k = 1; k <= M - 1 && st == kStatusOk; ++k) {
       const int nxt = cur ^ 1;
+      CPROF(long long c1 = clock64();)
       const uint32_t totn = level_rows(cc, w, vals, k + 1, ROFF(nxt), g);
       if (totn > (uint64_t)capE) {
         st = kStatusDeferred;
@@ -487,7 +509,9 @@ __global__ void __launch_bounds__(32 * kCW, 2) lofp_contract_warp_kernel(const _
       const int nfac = ck.nfac, ngate = ck.ngate, ncR = cc.ncmp[k + 1];
       for (int f = g.lane; f < nfac; f += G) {
         const FacInfo fi = p.fac[ck.fac_base + f];
-        w.ftab[f] = (int)p.tab_off[fi.bs];
+        const BSInfo bi = p.bsi[fi.bs];
+        w.ftab[f] = (int)p.tabA_off[fi.bs];
+        w.fcap[f] = (uint8_t)min(p.N, (int)p.cumS[bi.cap_hi] - (int)p.cumS[bi.cap_lo]);  // (bs_cap)
         w.fsh[f] = (uint32_t)fi.i | (uint32_t)fi.sC << 8;
       }
       g.sync();
@@ -505,10 +529,13 @@ __global__ void __launch_bounds__(32 * kCW, 2) lofp_contract_warp_kernel(const _
         }
       }
       g.sync();
-      const double2 *__restrict__ table = p.table;
-      int tbo[NF];
+      const double2 *__restrict__ table = p.tableA;
+      int tbo[NF], tc1[NF];
 #pragma unroll
-      for (int f = 0; f < NF; ++f) tbo[f] = f < nfac ? w.ftab[f] : 0;
+      for (int f = 0; f < NF; ++f) {
+        tbo[f] = f < nfac ? w.ftab[f] : 0;
+        tc1[f] = f < nfac ? (int)w.fcap[f] + 1 : 1;
+      }
       const uint32_t *rn = ROFF(nxt), *rc = ROFF(cur);
       const double2 *Ac = LV(cur);
       const uint64_t *Gc = LG(cur);
@@ -521,6 +548,9 @@ __global__ void __launch_bounds__(32 * kCW, 2) lofp_contract_warp_kernel(const _
       const uint32_t vbC = w.vbase[k + 1];
       int sc = 0, sc_last = -1;
       uint64_t vc = 0, hB = 0;
+      CPROF(long long c2 = clock64(); if (g.lane == 0) { atomicAdd(&p.ctr->phase[1], (ull)(c2 - c1));
+                                                         atomicAdd(&p.ctr->phase[4], (ull)totn);
+                                                         atomicAdd(&p.ctr->phase[7], 1ull); })
       for (uint32_t t = g.lane; t < totn; t += G) {
         while (rn[sc + 1] <= t) ++sc;
         if (sc != sc_last) {  // the row's state (column k+1) and its sub-box of column k
@@ -551,6 +581,14 @@ __global__ void __launch_bounds__(32 * kCW, 2) lofp_contract_warp_kernel(const _
           const int i = sh & 0xff;
           cb[f] = (uint32_t)byte_at(vc, sh >> 8) | (uint32_t)byte_at(vb, i) << 8 | (uint32_t)byte_at(vb, i + 1) << 16;
         }
+        int pidx[NF];  // x1-linear block (x2, y2) of each BS, offset by Bm: element at pidx - A
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+          const int C = cb[f] & 0xff, Bm = (cb[f] >> 8) & 0xff, Bp = cb[f] >> 16;
+          const int x2 = C - Bm, y2 = C - Bp, c1 = tc1[f];
+          pidx[f] = f < nfac ? tbo[f] + c1 * (x2 * c1 - ((x2 * (x2 - 1)) >> 1)) + y2 * (c1 - x2) + Bm : 0;
+          DCHECK_C(f >= nfac || (x2 >= 0 && y2 >= 0 && x2 < c1 && y2 < c1));
+        }
         double2 gfix = make_double2(1.0, 0.0);  // gates on (column k, column k+1): fixed too
         for (int gt = 0; gt < ngate; ++gt) {
           const GateW gw = w.gat[gt];
@@ -561,20 +599,27 @@ __global__ void __launch_bounds__(32 * kCW, 2) lofp_contract_warp_kernel(const _
         }
         // sum over row sb of level k: the states of column k-1 compatible with sb
         const uint32_t r0 = rc[sb], r1 = rc[sb + 1];
+        CPROF({
+          const unsigned am = __activemask();
+          const uint32_t mx = __reduce_max_sync(am, r1 - r0);
+          if ((threadIdx.x & 31) == __ffs(am) - 1) atomicAdd(&p.ctr->phase[5], (ull)mx);
+          atomicAdd(&p.ctr->phase[6], (ull)(r1 - r0));
+        })
         // (two entries per step, loads first; an entry whose value is 0 contributes 0)
         double sx = 0.0, sy = 0.0;
         ull csum = 0;
         if (nfac == NF)
-          row_sum<NF, CNT, true>(table, s_tri, tbo, cb, nfac, gfix, p, w, ngate, vb, Ac, Gc, Cc, r0, r1, sx, sy, csum, cm,
+          row_sum<NF, CNT, true>(table, pidx, cb, nfac, gfix, p, w, ngate, vb, Ac, Gc, Cc, r0, r1, sx, sy, csum, cm,
                                  terms);
         else
-          row_sum<NF, CNT, false>(table, s_tri, tbo, cb, nfac, gfix, p, w, ngate, vb, Ac, Gc, Cc, r0, r1, sx, sy, csum,
+          row_sum<NF, CNT, false>(table, pidx, cb, nfac, gfix, p, w, ngate, vb, Ac, Gc, Cc, r0, r1, sx, sy, csum,
                                   cm, terms);
         An[t] = make_double2(sx, sy);
         Gn[t] = gather(vb, s_gseg[k + 1], s_ngs[k + 1]);  // what cut k+1 reads of sb
         if (with_counts) Cn[t] = csum;
       }
       g.sync();
+      CPROF(if (g.lane == 0) atomicAdd(&p.ctr->phase[2], (ull)(clock64() - c2));)
       cur = nxt;
     }
     if (st == kStatusOk) {
@@ -662,6 +707,9 @@ static int launch_cnt(const CallParams *p, int grid, cudaStream_t stream) {
         return p->counts ? launch_nf<NF, true, 8, kSmallM>(p, grid, stream)
                          : launch_nf<NF, false, 8, kSmallM>(p, grid, stream);
     }
+    if (p->contract_group == 16 && p->M <= kSmallM)
+      return p->counts ? launch_nf<NF, true, 16, kSmallM>(p, grid, stream)
+                       : launch_nf<NF, false, 16, kSmallM>(p, grid, stream);
   }
   return p->counts ? launch_nf<NF, true, 32, kMaxModes>(p, grid, stream)
                    : launch_nf<NF, false, 32, kMaxModes>(p, grid, stream);

@@ -121,10 +121,11 @@ struct lofp_ctx {
   size_t off_col = 0, off_seg = 0, off_cmp = 0, off_fac = 0, off_gat = 0, off_bsi = 0, off_gab = 0, off_gm = 0,
          off_gl = 0, off_eqc = 0, off_bnd = 0, off_seq = 0, off_cone = 0;
   // per-call device buffers
+  DevBuf d_tableA, d_tabAoff;  // contraction: the x1-linear copy of the tables (lofp_tableA_kernel)
   DevBuf d_table, d_taboff, d_gatetab, d_units, d_sched, d_nunits, d_ubase, d_status, d_pexp, d_pdone, d_partial, d_slab,
       d_ctr, d_hostT, d_hostA;
   HostPinned h_ctr;
-  long long table_entries = 0;
+  long long table_entries = 0, tableA_entries = 0;
   int grid = 0;
   long long slab_bytes = 0;
   unsigned long long path_budget = 0;  // lofp_set_path_budget
@@ -802,7 +803,7 @@ lofp_status prepare(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, cons
   P.cone = (const uint64_t *)(topo + ctx->off_cone);
   P.seq_gl0 = ctx->seq_gl0;
   // Appendix-A table: per BS all (x1, x2, y1) with x1 + x2 <= its past-cone photon bound
-  long long entries = 0;
+  long long entries = 0, entriesA = 0;
   for (int i = 0; i < ctx->nbs; ++i) {
     const BSInfo &bi = ctx->bsi[i];
     int c = 0;
@@ -813,8 +814,10 @@ lofp_status prepare(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, cons
         if ((bi.capmask[m >> 6] >> (m & 63)) & 1ull) c += input_occ[m];
     }
     entries += tri_entries(std::min(N, c));
+    entriesA += lin_entries(std::min(N, c));
   }
   ctx->table_entries = entries;
+  ctx->tableA_entries = entriesA;
   CK(ctx->d_table.ensure_async((size_t)std::max(entries, 1ll) * 16, stream), "alloc table");
   CK(ctx->d_taboff.ensure_async((size_t)(ctx->nbs + 1) * 8, stream), "alloc table offsets");
   CK(ctx->d_gatetab.ensure_async((size_t)std::max(ctx->ngate, 1) * (N + 1) * 16, stream), "alloc gate table");
@@ -881,6 +884,13 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
   if (batch == 0) return LOFP_OK;
   P.counts = counts;
   P.mode = mode;
+  if (mode == 1) {  // the contraction's x1-linear copy of the tables
+    CK(ctx->d_tableA.ensure_async((size_t)std::max(ctx->tableA_entries, 1ll) * 16, stream), "alloc table (x1-linear)");
+    CK(ctx->d_tabAoff.ensure_async((size_t)(ctx->nbs + 1) * 8, stream), "alloc table offsets (x1-linear)");
+    P.tableA = (double2 *)ctx->d_tableA.p;
+    P.tabA_off = (long long *)ctx->d_tabAoff.p;
+    P.tableA_cap = (long long)(ctx->d_tableA.n / 16);
+  }
   ctx->timed = !capturing;
   if (ctx->timed) CK(cudaEventRecord(ctx->ev_start, stream), "cudaEventRecord");
   CK(cudaMemsetAsync(P.ctr, 0, sizeof(Counters), stream), "clear counters");
@@ -896,7 +906,7 @@ lofp_status run(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, const in
     launches += 7;
   } else {
     CK((cudaError_t)lofp_launch_contract(&P, ctx->grid, stream), "contraction kernels");
-    launches += 2;
+    launches += ctx->general ? 2 : 4;  // (x1-linear tables, warp kernel,) block kernel, generic kernel
   }
   if (!capturing) {  // statistics of calls replayed from a graph are not read back
     CK(cudaMemcpyAsync(ctx->h_ctr.p, P.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, stream), "read counters");
@@ -1058,7 +1068,7 @@ void lofp_destroy(lofp_ctx *ctx) {
   if (!ctx) return;
   DeviceGuard guard(ctx->device);
   if (ctx->have_call && ctx->ev_end) cudaEventSynchronize(ctx->ev_end);
-  for (DevBuf *b : {&ctx->d_topo, &ctx->d_table, &ctx->d_taboff, &ctx->d_gatetab, &ctx->d_units, &ctx->d_sched, &ctx->d_nunits,
+  for (DevBuf *b : {&ctx->d_topo, &ctx->d_tableA, &ctx->d_tabAoff, &ctx->d_table, &ctx->d_taboff, &ctx->d_gatetab, &ctx->d_units, &ctx->d_sched, &ctx->d_nunits,
                     &ctx->d_ubase, &ctx->d_status, &ctx->d_pexp, &ctx->d_pdone, &ctx->d_partial, &ctx->d_slab,
                     &ctx->d_ctr, &ctx->d_hostT, &ctx->d_hostA})
     b->release();

@@ -178,6 +178,9 @@ struct CallParams {
   const int16_t *gate_after; // [ngate] layer
   double2 *table;            // Appendix-A elements, per BS: tri(n) + x1 (n+1) + y1
   long long *tab_off;        // [nbs + 1]
+  double2 *tableA;           // contraction only: the same elements, per BS [x2][y2][x1] (x1 <= cap - x2),
+  long long *tabA_off;       //   so that for fixed (x2, y2) the index is linear in x1; [nbs + 1]
+  long long tableA_cap;      //   entries allocated (0: not built)
   double2 *gate_tab;         // [ngate][N+1] exp(i (a n + b n^2))
   const int32_t *T;          // [B][M] device
   double2 *amps;             // [B]
@@ -199,6 +202,12 @@ struct CallParams {
 inline long long tri_entries(int cap) {  // sum_{n=0}^{cap} (n+1)^2
   long long n = cap + 1;
   return n * (n + 1) * (2 * n + 1) / 6;
+}
+
+// host-side size of the contraction's x1-linear block ([x2][y2][x1], x1 + x2 <= cap)
+inline long long lin_entries(int cap) {  // (cap+1) * sum_{x2=0}^{cap} (cap+1-x2)
+  const long long c = cap + 1;
+  return c * c * (c + 1) / 2;
 }
 
 }  // namespace lofp

@@ -58,6 +58,11 @@ __device__ __forceinline__ ull sat_add(ull a, ull b) {
   return c < a ? ~0ull : c;
 }
 
+__device__ __forceinline__ long long lin_dev(int cap) {  // lin_entries (lofp_internal.h)
+  const long long c = cap + 1;
+  return c * c * (c + 1) / 2;
+}
+
 __device__ __forceinline__ long long tri_dev(int n) {  // sum_{m<n} (m+1)^2
   return (long long)n * (n + 1) * (2 * n + 1) / 6;
 }
@@ -1055,6 +1060,29 @@ __global__ void lofp_table_off_kernel(const __grid_constant__ CallParams p) {
     p.tab_off[i] = run;
     run += tri_dev(bs_cap(p, i) + 1);
   }
+  if (p.tableA) {  // the contraction's x1-linear layout: offsets by the same two-pass scan
+    __syncthreads();
+    s = 0;
+    for (int i = a; i < e; ++i) s += lin_dev(bs_cap(p, i));
+    part[tid] = s;
+    __syncthreads();
+    if (tid == 0) {
+      long long r = 0;
+      for (int i = 0; i < kThreads; ++i) {
+        const long long v = part[i];
+        part[i] = r;
+        r += v;
+      }
+      p.tabA_off[nb] = r;
+      if (r > p.tableA_cap) atomicAdd(&p.ctr->table_error, 1ull);
+    }
+    __syncthreads();
+    long long r = part[tid];
+    for (int i = a; i < e; ++i) {
+      p.tabA_off[i] = r;
+      r += lin_dev(bs_cap(p, i));
+    }
+  }
   // phase gates exp(i (a n + b n^2)) for n = 0..N (reading R19)
   for (int t = tid; t < p.ngate * (p.N + 1); t += kThreads) {
     const int g = t / (p.N + 1), n = t % (p.N + 1);
@@ -1110,6 +1138,31 @@ __global__ void __launch_bounds__(kThreads) lofp_table_kernel(const __grid_const
       const double d = curr[idx].x;
       curr[idx] = make_double2(d * cs, d * sn);
     }
+  }
+}
+
+// The contraction's copy of each BS block in the x1-linear layout: element (x2, y2, x1), i.e.
+// <y1, y2|BS|x1, x2> with y1 = x1 + x2 - y2, at (cap+1) R(x2) + y2 (cap+1-x2) + x1 where
+// R(x2) = sum_{x' < x2} (cap+1-x') (lin_base).  A term of the contraction fixes x2 and y2 per
+// entry and varies x1 with one byte of its row (lofp_contract.cu), so its index is one
+// subtraction.  Elements with y1 < 0 do not exist (0; never read).
+__global__ void __launch_bounds__(kThreads) lofp_tableA_kernel(const __grid_constant__ CallParams p) {
+  const int bs = blockIdx.x;
+  if (p.tab_off[p.nbs] > p.table_cap || p.tabA_off[p.nbs] > p.tableA_cap) return;
+  const int cap = bs_cap(p, bs), c1 = cap + 1;
+  const double2 *src = p.table + p.tab_off[bs];
+  double2 *dst = p.tableA + p.tabA_off[bs];
+  const long long tot = lin_dev(cap);
+  for (long long idx = threadIdx.x; idx < tot; idx += kThreads) {
+    int x2 = 0;  // the run of x2 spans c1 * (c1 - x2) entries
+    long long off = idx;
+    while (off >= (long long)c1 * (c1 - x2)) {
+      off -= (long long)c1 * (c1 - x2);
+      ++x2;
+    }
+    const int w = c1 - x2, y2 = (int)(off / w), x1 = (int)(off % w);
+    const int n = x1 + x2, y1 = n - y2;
+    dst[idx] = y1 >= 0 ? src[tri_dev(n) + (long long)x1 * (n + 1) + y1] : make_double2(0.0, 0.0);
   }
 }
 
@@ -1645,7 +1698,8 @@ extern "C" int lofp_launch_contract(const CallParams *p, int grid, void *stream)
   // nearest-neighbour circuits: one warp per output first (lofp_contract.cu); this block
   // kernel then takes only the outputs it deferred (state spaces over the warp limits)
   q.deferred_only = 0;
-  if (!p->general && !p->force_generic && !p->contract_block_only) {
+  if (!p->general && !p->force_generic && !p->contract_block_only && p->tableA) {
+    if (p->nbs > 0) lofp_tableA_kernel<<<p->nbs, kThreads, 0, (cudaStream_t)stream>>>(*p);
     const int e = lofp_launch_contract_warp(p, grid, stream);
     if (e > 0) return e;
     q.deferred_only = e == 0 ? 1 : 0;  // (-1: not launched, the block kernel takes every output)
