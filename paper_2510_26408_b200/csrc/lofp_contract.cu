@@ -66,6 +66,7 @@ constexpr int kCMaxN = 4096;       // states per column (as the block kernel)
 constexpr int kCMaxStates = 16384; // states of all columns of one output
 constexpr int kCFac = 32;          // phase gates of one cut staged in shared memory
 
+constexpr int kLB = 32;            // row-length classes of the entry schedule
 constexpr int kCF = kCSeg - 1;     // BS of one cut (<= 7 active layers: 8 segments)
 constexpr int kCCmp = 2 * kCSeg;   // CmpPair checks between two columns
 
@@ -444,6 +445,7 @@ __global__ void __launch_bounds__(32 * kCW, 16 / kCW) lofp_contract_warp_kernel(
   __shared__ CWarpT<MM> sw[kGroups];
   __shared__ uint8_t s_gseg[kMaxModes + 1][kCSeg], s_ngs[kMaxModes + 1];  // gather slots per cut
   __shared__ CCirc cc;
+  __shared__ uint32_t s_hist[kGroups][kLB];  // entries per row-length class (the cut's schedule)
   gather_lists(p, s_gseg, s_ngs);
   cache_circuit(p, cc);
   __syncthreads();
@@ -459,10 +461,12 @@ __global__ void __launch_bounds__(32 * kCW, 16 / kCW) lofp_contract_warp_kernel(
   char *lv0 = (char *)(roff1 + kCMaxN + 1);
   lv0 = (char *)(((uintptr_t)lv0 + 15) & ~(uintptr_t)15);
   const long long per = with_counts ? 32 : 24;
-  const long long capE = (p.cw_bytes - (lv0 - ws)) / (2 * per);
+  const long long capE = (p.cw_bytes - (lv0 - ws)) / (2 * per + 16);
   double2 *const lvA = (double2 *)lv0, *const lvB = lvA + capE;
   uint64_t *const lgA = (uint64_t *)(lvB + capE), *const lgB = lgA + capE;
-  ull *const lcA = (ull *)(lgB + capE), *const lcB = lcA + capE;
+  uint64_t *const rec_t = lgB + capE, *const rec_s = rec_t + capE;  // the cut's entry records
+  ull *const lcA = (ull *)(rec_s + capE), *const lcB = lcA + capE;
+  uint32_t *const hist = s_hist[gib];
 #define ROFF(i) ((i) ? roff1 : roff0)
 #define LV(i) ((i) ? lvB : lvA)
 #define LG(i) ((i) ? lgB : lgA)
@@ -549,32 +553,77 @@ __global__ void __launch_bounds__(32 * kCW, 16 / kCW) lofp_contract_warp_kernel(
       const uint64_t loB = w.lo[k], hiB = w.hi[k];
       const int nsB = w.nseg[k];
       const uint32_t vbC = w.vbase[k + 1];
-      int sc = 0, sc_last = -1;
-      uint64_t vc = 0, hB = 0;
+      // Pass 1 — the cut's entry records: entry t of the next level is (row sc = a state of
+      // column k+1, the pos-th state sb of its sub-box of column k); its sum runs over row sb
+      // of the current level.  Rows differ in length (the sub-box of column k-1 under sb), and
+      // lanes that take entries in storage order wait for the longest row of their round
+      // (configs[3]: 30 % of the lane-steps of the row loop did work).  So levels of more than
+      // two rounds are scheduled by row length, longest first (a counting sort over kLB length
+      // classes): the entries of a round have rows of about one length.  Each entry's value
+      // is formed exactly as before and stored at its own t, so the results do not depend on
+      // the schedule (bitwise the same).
+      const bool sorted = totn > 2u * G && !p.contract_nosort;
+      if (sorted) {
+        for (int b = g.lane; b < kLB; b += G) hist[b] = 0u;
+        g.sync();
+      }
+      {
+        int sc = 0, sc_last = -1;
+        uint64_t hB = 0;
+        for (uint32_t t = g.lane; t < totn; t += G) {
+          while (rn[sc + 1] <= t) ++sc;
+          if (sc != sc_last) {  // the row's state (column k+1) bounds its sub-box of column k
+            hB = sub_hi_s(hiB, cc.cmp[k + 1], ncR, vals[vbC + sc]);
+            sc_last = sc;
+          }
+          // entry t = the pos-th state of the sub-box (odometer order, segment 0 fastest)
+          uint32_t pos = t - rn[sc];
+          uint32_t sb = 0, stride = 1;  // sb: the state's index in column k's full box
+          for (int j = 0; j < nsB; ++j) {
+            const int l = byte_at(loB, j), rad = byte_at(hB, j) - l + 1;
+            if (rad > 1) {
+              const uint32_t d = pos % (uint32_t)rad;
+              pos /= (uint32_t)rad;
+              sb += d * stride;
+            }
+            stride *= (uint32_t)(byte_at(hiB, j) - l + 1);
+          }
+          DCHECK_C(sb < (uint32_t)w.n[k] && sc < (int)w.n[k + 1]);
+          const uint32_t len = rc[sb + 1] - rc[sb];
+          const uint32_t cls = len < 24u ? len : min(24u + ((len - 24u) >> 3), (uint32_t)kLB - 1u);
+          rec_t[t] = (uint64_t)t | (uint64_t)sc << 32 | (uint64_t)sb << 44 | (uint64_t)cls << 56;
+          if (sorted) atomicAdd(&hist[cls], 1u);
+        }
+      }
+      g.sync();
+      const uint64_t *recs = rec_t;
+      if (sorted) {
+        if (g.lane == 0) {  // first slot of each class, longest rows first
+          uint32_t run = 0;
+          for (int b = kLB - 1; b >= 0; --b) {
+            const uint32_t c = hist[b];
+            hist[b] = run;
+            run += c;
+          }
+        }
+        g.sync();
+        for (uint32_t t = g.lane; t < totn; t += G) {
+          const uint64_t rec = rec_t[t];
+          const uint32_t slot = atomicAdd(&hist[rec >> 56], 1u);
+          DCHECK_C(slot < totn);
+          rec_s[slot] = rec;
+        }
+        g.sync();
+        recs = rec_s;
+      }
+      const uint64_t *const valsB = vals + w.vbase[k];
       CPROF(long long c2 = clock64(); if (g.lane == 0) { atomicAdd(&p.ctr->phase[1], (ull)(c2 - c1));
                                                          atomicAdd(&p.ctr->phase[4], (ull)totn);
                                                          atomicAdd(&p.ctr->phase[7], 1ull); })
-      for (uint32_t t = g.lane; t < totn; t += G) {
-        while (rn[sc + 1] <= t) ++sc;
-        if (sc != sc_last) {  // the row's state (column k+1) and its sub-box of column k
-          vc = vals[vbC + sc];
-          hB = sub_hi_s(hiB, cc.cmp[k + 1], ncR, vc);
-          sc_last = sc;
-        }
-        // entry t = the pos-th state of the sub-box (odometer order, segment 0 fastest)
-        uint32_t pos = t - rn[sc];
-        uint64_t vb = loB;
-        uint32_t sb = 0, stride = 1;  // sb: the state's index in column k's full box
-        for (int j = 0; j < nsB; ++j) {
-          const int l = byte_at(loB, j), rad = byte_at(hB, j) - l + 1;
-          if (rad > 1) {
-            const uint32_t d = pos % (uint32_t)rad;
-            pos /= (uint32_t)rad;
-            vb += (uint64_t)d << (8 * j);
-            sb += d * stride;
-          }
-          stride *= (uint32_t)(byte_at(hiB, j) - l + 1);
-        }
+      for (uint32_t it = g.lane; it < totn; it += G) {
+        const uint64_t rec = recs[it];
+        const uint32_t t = (uint32_t)rec, sb = (uint32_t)(rec >> 44) & 0xfffu;
+        const uint64_t vc = vals[vbC + ((uint32_t)(rec >> 32) & 0xfffu)], vb = valsB[sb];
         // per BS f the photon numbers fixed by (sb, sc): C = F_{l-1}(k+1), Bm = F_{l-1}(k),
         // Bp = F_l(k); only A = F_{l-1}(k-1) varies along the row
         uint32_t cb[NF];

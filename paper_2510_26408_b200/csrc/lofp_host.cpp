@@ -836,6 +836,7 @@ lofp_status prepare(lofp_ctx *ctx, const int32_t *input_occ, int64_t batch, cons
   P.force_generic = env_ll("LOFP_FORCE_GENERIC", 0) > 0 ? 1 : 0;
   P.contract_block_only = env_ll("LOFP_CONTRACT_BLOCK", 0) > 0 ? 1 : 0;
   P.contract_group = (int)env_ll("LOFP_CONTRACT_GROUP", 0);
+  P.contract_nosort = env_ll("LOFP_CONTRACT_NOSORT", 0) > 0 ? 1 : 0;
   P.max_nfac = 0;
   for (const ColInfo &ci : ctx->col) P.max_nfac = std::max(P.max_nfac, (int)ci.nfac);
   P.path_budget = ctx->path_budget;

@@ -158,6 +158,7 @@ struct CallParams {
   int max_nfac;          // most BS a cut carries (contraction warp kernel instantiation)
   int contract_block_only;  // test hook (LOFP_CONTRACT_BLOCK): contraction by the block kernel only
   int contract_group;    // test hook (LOFP_CONTRACT_GROUP = 8 or 32): lanes per output of the warp kernel
+  int contract_nosort;   // test hook (LOFP_CONTRACT_NOSORT): entries taken in storage order, not by row length
   long long table_cap;   // entries allocated for the Appendix-A table
   const ColInfo *col;
   const SegInfo *seg;

@@ -286,3 +286,30 @@ def test_eight_lane_groups_match_full_warps(lofp, monkeypatch, counts):
         ref, leaves = oracle.path_sum(M, layers, S, Tr, return_leaves=True, gates=gates)
         assert tol_ok(got, ref)[0]
         assert np.array_equal(cnt, leaves)
+
+
+@pytest.mark.parametrize("counts", [False, True])
+def test_entry_schedule_does_not_change_results(lofp, monkeypatch, counts):
+    """The warp kernel takes a cut's entries longest row first (a counting sort by row length);
+    with LOFP_CONTRACT_NOSORT it takes them in storage order.  Every entry's sum is formed in
+    the same order either way: bitwise equal amplitudes and equal path counts on configs[3] as
+    literally drawn (levels of several rounds) and on a high-density output (k = 6)."""
+    c = li.config(3)
+    d = load(3)
+    T = d["T_literal"][:384].astype(np.int32)
+    layers318 = li.clements_mesh(10, 4, 318 + 4)
+    S318 = np.full(10, 6, dtype=np.int32)
+    res = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("LOFP_CONTRACT_NOSORT", flag)
+        circ = lofp.Circuit(c.M, c.layers)
+        Td = torch.from_numpy(T).cuda()
+        cnt = torch.zeros(len(T), dtype=torch.int64, device="cuda") if counts else None
+        a = circ.contract(c.S, Td, counts=cnt).cpu().numpy()
+        circ2 = lofp.Circuit(10, layers318)
+        b = circ2.contract(S318, torch.from_numpy(S318[None, :].copy()).cuda()).cpu().numpy()
+        res[flag] = (a, None if cnt is None else cnt.cpu().numpy().astype(np.uint64), b)
+    assert np.array_equal(res["0"][0], res["1"][0]) and np.array_equal(res["0"][2], res["1"][2])
+    if counts:
+        assert np.array_equal(res["0"][1], res["1"][1])
+        assert np.array_equal(res["0"][1], d["P_literal"][:384])
