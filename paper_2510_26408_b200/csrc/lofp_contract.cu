@@ -345,7 +345,7 @@ __device__ int setup_warp(const CallParams &p, const CCirc &cc, W &w, uint64_t *
 // A vacuum BS (n = 0) reads its block's element (0, 0, 0), exactly 1 (reading R16).
 template <int NF, bool FULL>
 __device__ __forceinline__ double2 cut_fac(const double2 *__restrict__ tableA, const int (&pidx)[NF],
-                                           const uint32_t (&cb)[NF], int nfac, uint64_t g, double2 fac) {
+                                           const uint32_t (&cb)[NF], int nfac, uint64_t g) {
   // FULL (every cut of the circuit carries NF BS): no predicates, so the NF table loads are
   // independent and issue back to back
   double2 e[NF];
@@ -367,7 +367,7 @@ __device__ __forceinline__ double2 cut_fac(const double2 *__restrict__ tableA, c
 #pragma unroll
     for (int f = 0; f + st < NF; f += 2 * st)
       e[f] = make_double2(e[f].x * e[f + st].x - e[f].y * e[f + st].y, e[f].x * e[f + st].y + e[f].y * e[f + st].x);
-  return make_double2(fac.x * e[0].x - fac.y * e[0].y, fac.x * e[0].y + fac.y * e[0].x);
+  return e[0];
 }
 
 // phase gates of the cut on (column k-1, column k): n = F(k) - F(k-1) at their time
@@ -387,7 +387,7 @@ __device__ __forceinline__ double2 gates_a(const CallParams &p, const W &w, int 
 // The sum over one row of level k (the states of column k-1 compatible with sb) of
 // A_k(c_{k-1}, sb) f_k(c_{k-1}, sb, sc): kRowU entries per step, their loads first.
 #ifndef LOFP_ROW_UNROLL
-#define LOFP_ROW_UNROLL 2
+#define LOFP_ROW_UNROLL 3
 #endif
 constexpr int kRowU = LOFP_ROW_UNROLL;
 
@@ -410,7 +410,7 @@ __device__ __forceinline__ void row_sum(const double2 *__restrict__ table, const
 #pragma unroll
       for (int u = 0; u < kRowU; ++u) csum = sat_add_c(csum, Cc[r + u]);
 #pragma unroll
-    for (int u = 0; u < kRowU; ++u) f[u] = cut_fac<NF, FULL>(table, pidx, cb, nfac, gg[u], gfix);
+    for (int u = 0; u < kRowU; ++u) f[u] = cut_fac<NF, FULL>(table, pidx, cb, nfac, gg[u]);
     if (ngate)
 #pragma unroll
       for (int u = 0; u < kRowU; ++u) f[u] = gates_a(p, w, ngate, vb, gg[u], f[u], cm);
@@ -418,20 +418,26 @@ __device__ __forceinline__ void row_sum(const double2 *__restrict__ table, const
     for (int u = 0; u < kRowU; ++u) {
       sx = fma(a[u].x, f[u].x, fma(-a[u].y, f[u].y, sx));
       sy = fma(a[u].x, f[u].y, fma(a[u].y, f[u].x, sy));
-      terms += (a[u].x != 0.0 || a[u].y != 0.0);
     }
-    cm += kRowU * nfac;
   }
   for (; r < r1; ++r) {
     const double2 a0 = Ac[r];
     const uint64_t g0 = Gc[r];
     if (CNT) csum = sat_add_c(csum, Cc[r]);
-    double2 f0 = cut_fac<NF, FULL>(table, pidx, cb, nfac, g0, gfix);
+    double2 f0 = cut_fac<NF, FULL>(table, pidx, cb, nfac, g0);
     if (ngate) f0 = gates_a(p, w, ngate, vb, g0, f0, cm);
     sx = fma(a0.x, f0.x, fma(-a0.y, f0.y, sx));
     sy = fma(a0.x, f0.y, fma(a0.y, f0.x, sy));
-    terms += (a0.x != 0.0 || a0.y != 0.0);
-    cm += nfac;
+  }
+  // every term of the row is a live (c_{k-1}, c_k, c_{k+1}) triple: nfac - 1 multiplications
+  // of Appendix-A elements and one multiply-accumulate each
+  terms += r1 - r0;
+  cm += (ull)(r1 - r0) * (ull)(nfac > 1 ? nfac - 1 : 0);
+  if (ngate) {  // the gates on (column k, column k+1) are fixed along the row: applied to its sum
+    ++cm;
+    const double tx = sx * gfix.x - sy * gfix.y;
+    sy = sx * gfix.y + sy * gfix.x;
+    sx = tx;
   }
 }
 
