@@ -60,6 +60,9 @@ def parse():
                         "layer instead of the nearest-neighbour pairs they displace; outputs = the conditioned batch")
     p.add_argument("--distribution", action="store_true",
                    help="NEXT-2: all C(N+M-1, M-1) outputs of configs[1]'s input in one call; metric amplitudes/s")
+    p.add_argument("--tile", type=int, default=1,
+                   help="--contract: the batch repeated this many times in one call (the 2048 outputs of "
+                        "configs[3] are under one output per resident warp; copies fill the GPU)")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-paths", type=float, default=3e7, help="paths in the cpu_baseline sample")
@@ -323,6 +326,8 @@ def contract_arm(args, rank, world, local):
     T, P = d["T_literal"].astype(np.int32), d["P_literal"].astype(np.uint64)
     if args.outputs:
         T, P = T[:args.outputs], P[:args.outputs]
+    if args.tile > 1:
+        T, P = np.tile(T, (args.tile, 1)), np.tile(P, args.tile)
     B = len(T)
     circ = Circuit(c.M, c.layers)
     Td = torch.from_numpy(np.ascontiguousarray(T)).to(dev)
@@ -376,7 +381,9 @@ def contract_arm(args, rank, world, local):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": f"configs[{idx}] literal batch by the strip tensor contraction (NEXT-1): "
-                                   f"M={c.M} N={c.N} D={c.D}, {B} outputs, {float(P.astype(np.float64).sum()):.3e} "
+                                   f"M={c.M} N={c.N} D={c.D}, {B} outputs"
+                                   + (f" (the batch x {args.tile})" if args.tile > 1 else "")
+                                   + f", {float(P.astype(np.float64).sum()):.3e} "
                                    f"paths (not enumerated)", "global_batch": int(outs_all),
                        "l2": "flushed between steps (256 MiB write)"},
             "paths_equivalent_per_s": paths_all * args.steps / (t_max * 1e-3),

@@ -44,9 +44,15 @@ def func_of(line):
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(so)], cwd=tmp, capture_output=True)
 cubins = sorted(f for f in os.listdir(tmp) if f.endswith(".cubin") and "host" not in f)
-dis = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cubins[0])], capture_output=True, text=True).stdout
-L = dis.split("\n")
-st = next(i for i, l in enumerate(L) if ".text." in l and KERNEL in l and l.lstrip().startswith(".section"))
+# the library holds one cubin per .cu file: take the one with the kernel's .text section
+for cb in cubins:
+    dis = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cb)], capture_output=True, text=True).stdout
+    L = dis.split("\n")
+    st = next((i for i, l in enumerate(L) if ".text." in l and KERNEL in l and l.lstrip().startswith(".section")), None)
+    if st is not None:
+        break
+else:
+    sys.exit(f"no .text section of {KERNEL} in {so}")
 seq = []
 cur = 0
 for l in L[st + 1:]:
