@@ -1127,16 +1127,24 @@ __global__ void __launch_bounds__(kThreads) lofp_table_kernel(const __grid_const
     }
     __syncthreads();
   }
-  // phases: <y1,y2|BS(theta,phi)|x1,x2> = e^{i phi (x1 - y1)} d
+  // phases: <y1,y2|BS(theta,phi)|x1,x2> = e^{i phi (x1 - y1)} d; the 2 cap + 1
+  // distinct phases are tabulated once (a sincos per element was most of this kernel at
+  // 100 photons)
+  __shared__ double2 ph[2 * kMaxPhotons + 1];
+  for (int d = tid; d <= 2 * cap; d += kThreads) {
+    double sn, cs;
+    sincos(bi.phi * (double)(d - cap), &sn, &cs);
+    ph[d] = make_double2(cs, sn);
+  }
+  __syncthreads();
   for (int n = 1; n <= cap; ++n) {
     double2 *curr = tb + tri_dev(n);
     for (int idx = tid; idx < (n + 1) * (n + 1); idx += kThreads) {
       const int x1 = idx / (n + 1), y1 = idx - x1 * (n + 1);
       if (x1 == y1) continue;
-      double sn, cs;
-      sincos(bi.phi * (double)(x1 - y1), &sn, &cs);
+      const double2 e = ph[x1 - y1 + cap];
       const double d = curr[idx].x;
-      curr[idx] = make_double2(d * cs, d * sn);
+      curr[idx] = make_double2(d * e.x, d * e.y);
     }
   }
 }
@@ -1147,22 +1155,20 @@ __global__ void __launch_bounds__(kThreads) lofp_table_kernel(const __grid_const
 // entry and varies x1 with one byte of its row (lofp_contract.cu), so its index is one
 // subtraction.  Elements with y1 < 0 do not exist (0; never read).
 __global__ void __launch_bounds__(kThreads) lofp_tableA_kernel(const __grid_constant__ CallParams p) {
-  const int bs = blockIdx.x;
+  // block (bs, x2): the run of x2, c1 (c1 - x2) entries starting at c1 R(x2) (one block per
+  // BS walked to its x2 entry by entry: 1.2 ms of a 2.6 ms call at 100 photons)
+  const int bs = blockIdx.x, x2 = blockIdx.y;
   if (p.tab_off[p.nbs] > p.table_cap || p.tabA_off[p.nbs] > p.tableA_cap) return;
   const int cap = bs_cap(p, bs), c1 = cap + 1;
+  if (x2 > cap) return;
   const double2 *src = p.table + p.tab_off[bs];
-  double2 *dst = p.tableA + p.tabA_off[bs];
-  const long long tot = lin_dev(cap);
-  for (long long idx = threadIdx.x; idx < tot; idx += kThreads) {
-    int x2 = 0;  // the run of x2 spans c1 * (c1 - x2) entries
-    long long off = idx;
-    while (off >= (long long)c1 * (c1 - x2)) {
-      off -= (long long)c1 * (c1 - x2);
-      ++x2;
-    }
-    const int w = c1 - x2, y2 = (int)(off / w), x1 = (int)(off % w);
+  const int w = c1 - x2;
+  double2 *dst = p.tableA + p.tabA_off[bs] + (long long)c1 * ((long long)x2 * c1 - ((long long)x2 * (x2 - 1)) / 2);
+  const int tot = c1 * w;
+  for (int off = threadIdx.x; off < tot; off += kThreads) {
+    const int y2 = off / w, x1 = off - y2 * w;
     const int n = x1 + x2, y1 = n - y2;
-    dst[idx] = y1 >= 0 ? src[tri_dev(n) + (long long)x1 * (n + 1) + y1] : make_double2(0.0, 0.0);
+    dst[off] = y1 >= 0 ? src[tri_dev(n) + (long long)x1 * (n + 1) + y1] : make_double2(0.0, 0.0);
   }
 }
 
@@ -1699,7 +1705,7 @@ extern "C" int lofp_launch_contract(const CallParams *p, int grid, void *stream)
   // kernel then takes only the outputs it deferred (state spaces over the warp limits)
   q.deferred_only = 0;
   if (!p->general && !p->force_generic && !p->contract_block_only && p->tableA) {
-    if (p->nbs > 0) lofp_tableA_kernel<<<p->nbs, kThreads, 0, (cudaStream_t)stream>>>(*p);
+    if (p->nbs > 0) lofp_tableA_kernel<<<dim3(p->nbs, p->N + 1), kThreads, 0, (cudaStream_t)stream>>>(*p);
     const int e = lofp_launch_contract_warp(p, grid, stream);
     if (e > 0) return e;
     q.deferred_only = e == 0 ? 1 : 0;  // (-1: not launched, the block kernel takes every output)

@@ -1,6 +1,6 @@
 """Summarise an ncu launch list (``--metrics gpu__time_duration.sum --csv``) into the
 per-kernel table kept under profiles/: launches, total time, share, and the share of the
-enumeration kernel within one bench step (the last launch of each hot-path kernel).
+unit kernel within one bench step (the last launch of each hot-path kernel).
 
 usage: python scripts/summarize_launches.py launches.csv "<command that produced it>" [note]
 """
@@ -9,7 +9,9 @@ import re
 import sys
 from collections import OrderedDict
 
-HOT = ("lofp_prep_kernel", "lofp_table_kernel", "lofp_plan_kernel", "lofp_enum_kernel")
+HOT = ("lofp_table_off_kernel", "lofp_table_kernel", "lofp_tableA_kernel", "lofp_plan_kernel", "lofp_thr_kernel",
+       "lofp_split_kernel", "lofp_scan_kernel", "lofp_units_kernel", "lofp_final_kernel", "lofp_generic_kernel",
+       "lofp_contract_warp_kernel", "lofp_contract_kernel", "lofp_outputs_kernel")
 
 
 def short(name: str) -> str:
@@ -45,10 +47,10 @@ def main() -> None:
         print(f"{k:60s} {n:9d} {t:12.3f} {100 * t / tot:7.2f}%")
     last = OrderedDict()
     for k, ms in rows:
-        if any(h in k for h in HOT) and not k.startswith("lofp_enum_kernel<1"):
+        if any(k.split("<")[0] == h for h in HOT):
             last[k.split("<")[0]] = (k, ms)
     step = sum(ms for _, ms in last.values())
-    print("\none step (last launch of each hot-path kernel, uncounted enumeration):")
+    print("\none step (last launch of each hot-path kernel: the timed, uncounted call):")
     for k, ms in last.values():
         print(f"  {k:50s} {ms:12.3f} ms {100 * ms / step:9.4f}% of the step")
 

@@ -30,9 +30,10 @@ for k in ["gpu__time_duration.sum", "sm__cycles_elapsed.avg.per_second",
         print(f"  {k:78s} {d[k]} {units.get(k, '')}")
 import re
 for k in sorted(d):  # the memory pipes: which unit is closest to its peak
-    if re.match(r"(l1tex__throughput|lts__throughput|sm__throughput|l1tex__data_pipe_lsu_wavefronts\.sum|"
-                r"l1tex__t_(requests|sectors)_pipe_lsu_mem_global_op_ld\.sum$|l1tex__lsu_writeback_active|"
-                r"sm__memory_throughput)", k):
+    if re.match(r"((l1tex__throughput|lts__throughput|sm__throughput|l1tex__lsu_writeback_active|"
+                r"sm__memory_throughput)\.avg\.pct_of_peak_sustained_elapsed$|"
+                r"l1tex__data_pipe_lsu_wavefronts\.sum\.pct_of_peak_sustained_elapsed$|"
+                r"l1tex__t_(requests|sectors)_pipe_lsu_mem_global_op_ld\.sum$)", k):
         print(f"  {k:78s} {d[k]} {units.get(k, '')}")
 dfma = d.get("smsp__sass_thread_inst_executed_op_dfma_pred_on.sum.per_cycle_elapsed")
 cyc = d.get("sm__cycles_elapsed.avg")
