@@ -117,7 +117,30 @@ __device__ void cache_circuit(const CallParams &p, CCirc &cc) {
   }
 }
 
-__device__ __forceinline__ int byte_at(uint64_t v, int j) { return (int)((v >> (8 * j)) & 0xffu); }
+// byte j (0..7) of a packed state: one PRMT (selector nibble j picks the byte of the two
+// words) and a mask, instead of a 64-bit funnel shift (16 % of the warp kernel's instructions)
+__device__ __forceinline__ int byte_at(uint64_t v, int j) {
+#ifdef LOFP_DEBUG
+  if ((unsigned)j >= 8u) __trap();
+#endif
+#ifdef LOFP_BYTE_SHIFT
+  return (int)((v >> (8 * j)) & 0xffu);
+#else
+  return (int)(__byte_perm((uint32_t)v, (uint32_t)(v >> 32), (uint32_t)j) & 0xffu);
+#endif
+}
+
+// floor(x / d) for the mixed-radix decodes (d <= 121 photons + 1, x d < 2^32): one multiply
+// by ceil(2^32 / d) from a shared table (exact in that range) instead of a division
+__device__ __forceinline__ uint32_t div_small(const uint32_t *inv, uint32_t x, uint32_t d) {
+#ifdef LOFP_DIV_PLAIN
+  (void)inv;
+  return x / d;
+#else
+  DCHECK_C(d >= 2u && d < 128u && (unsigned long long)x * d < (1ull << 32));
+  return __umulhi(x, inv[d]);
+#endif
+}
 
 __device__ __forceinline__ uint64_t set_byte(uint64_t v, int j, int b) {
   const int s = 8 * j;
@@ -226,15 +249,20 @@ __device__ __forceinline__ uint64_t gather(uint64_t v, const uint8_t *gseg, int 
 
 // Rows of the level whose rows are the states of column k (entries: the compatible
 // sub-box of column k-1): exclusive offsets into roff[0..n_k], returns the entry count.
+// hrow[s] keeps the sub-box's upper corner of row s (the entry pass reads it per row).
 template <int G, class W>
 __device__ uint32_t level_rows(const CCirc &cc, const W &w, const uint64_t *vals, int k, uint32_t *roff,
-                               const Grp<G> &g) {
+                               uint64_t *hrow, const Grp<G> &g) {
   const int nk = w.n[k], ns = w.nseg[k - 1];
   uint32_t run = 0;
   for (int base = 0; base < nk; base += G) {
     const int s = base + g.lane;
     uint32_t c = 0;
-    if (s < nk) c = box_count(w.lo[k - 1], sub_hi(cc, w, k, vals[w.vbase[k] + s]), ns);
+    if (s < nk) {
+      const uint64_t h = sub_hi(cc, w, k, vals[w.vbase[k] + s]);
+      hrow[s] = h;
+      c = box_count(w.lo[k - 1], h, ns);
+    }
     const uint32_t incl = g.scan(c);
     if (s < nk) roff[s] = run + incl - c;
     run += g.last(incl);
@@ -247,7 +275,8 @@ __device__ uint32_t level_rows(const CCirc &cc, const W &w, const uint64_t *vals
 // Per-output setup: G = cum(T), the light-cone box of every column (readings R5, R15),
 // the packed states.  Returns kStatusOk / Zero / Bad / Deferred (warp-uniform).
 template <int G, class W>
-__device__ int setup_warp(const CallParams &p, const CCirc &cc, W &w, uint64_t *vals, int q, const Grp<G> &g) {
+__device__ int setup_warp(const CallParams &p, const CCirc &cc, W &w, uint64_t *vals, const uint32_t *inv, int q,
+                          const Grp<G> &g) {
   const int M = p.M;
   // G = cum(T); negative entries make the row bad, totals other than N an exact zero
   int bad = 0, run = 0;
@@ -328,8 +357,9 @@ __device__ int setup_warp(const CallParams &p, const CCirc &cc, W &w, uint64_t *
     for (int i = 0; i < ns; ++i) {
       const uint32_t rad = (uint32_t)(byte_at(hi, i) - byte_at(lo, i) + 1);
       if (rad == 1) continue;
-      v += (uint64_t)(r % rad) << (8 * i);
-      r /= rad;
+      const uint32_t qd = div_small(inv, r, rad);
+      v += (uint64_t)(r - qd * rad) << (8 * i);
+      r = qd;
     }
     vals[x] = v;
   }
@@ -452,6 +482,8 @@ __global__ void __launch_bounds__(32 * kCW, 16 / kCW) lofp_contract_warp_kernel(
   __shared__ uint8_t s_gseg[kMaxModes + 1][kCSeg], s_ngs[kMaxModes + 1];  // gather slots per cut
   __shared__ CCirc cc;
   __shared__ uint32_t s_hist[kGroups][kLB];  // entries per row-length class (the cut's schedule)
+  __shared__ uint32_t s_inv[128];  // ceil(2^32 / d) (div_small)
+  for (int d = threadIdx.x; d < 128; d += blockDim.x) s_inv[d] = d >= 2 ? 0xffffffffu / (uint32_t)d + 1u : 0u;
   gather_lists(p, s_gseg, s_ngs);
   cache_circuit(p, cc);
   __syncthreads();
@@ -460,10 +492,11 @@ __global__ void __launch_bounds__(32 * kCW, 16 / kCW) lofp_contract_warp_kernel(
   CWarpT<MM> &w = sw[gib];
   const int M = p.M;
   constexpr bool with_counts = CNT;
-  // group scratch: packed states, two row-offset arrays, two levels (values, gathers [, counts])
+  // group scratch: packed states, row corners, two row-offset arrays, two levels (values, gathers [, counts])
   char *ws = p.slab + ((long long)blockIdx.x * kGroups + gib) * p.cw_bytes;
   uint64_t *vals = (uint64_t *)ws;
-  uint32_t *const roff0 = (uint32_t *)(vals + kCMaxStates), *const roff1 = roff0 + (kCMaxN + 1);
+  uint64_t *const hrow = vals + kCMaxStates;  // sub-box corner per row of the level being built
+  uint32_t *const roff0 = (uint32_t *)(hrow + kCMaxN), *const roff1 = roff0 + (kCMaxN + 1);
   char *lv0 = (char *)(roff1 + kCMaxN + 1);
   lv0 = (char *)(((uintptr_t)lv0 + 15) & ~(uintptr_t)15);
   const long long per = with_counts ? 32 : 24;
@@ -484,7 +517,7 @@ __global__ void __launch_bounds__(32 * kCW, 16 / kCW) lofp_contract_warp_kernel(
     q = g.first(q);
     if (q >= p.B) break;
     CPROF(long long c0 = clock64();)
-    int st = setup_warp(p, cc, w, vals, q, g);
+    int st = setup_warp(p, cc, w, vals, s_inv, q, g);
     CPROF(if (g.lane == 0) atomicAdd(&p.ctr->phase[0], (ull)(clock64() - c0));)
     double re = 0.0, im = 0.0;
     ull count = 0;
@@ -497,7 +530,7 @@ __global__ void __launch_bounds__(32 * kCW, 16 / kCW) lofp_contract_warp_kernel(
           const double2 e = p.gate_tab[g * (p.N + 1) + p.N];
           root = make_double2(root.x * e.x - root.y * e.y, root.x * e.y + root.y * e.x);
         }
-      const uint32_t tot = level_rows(cc, w, vals, 1, roff0, g);
+      const uint32_t tot = level_rows(cc, w, vals, 1, roff0, hrow, g);
       if (tot > (uint64_t)capE) st = kStatusDeferred;
       if (st == kStatusOk) {
         const uint64_t g0 = gather(vals[w.vbase[0]], s_gseg[1], s_ngs[1]);
@@ -513,13 +546,14 @@ __global__ void __launch_bounds__(32 * kCW, 16 / kCW) lofp_contract_warp_kernel(
     for (int k = 1; k <= M - 1 && st == kStatusOk; ++k) {
       const int nxt = cur ^ 1;
       CPROF(long long c1 = clock64();)
-      const uint32_t totn = level_rows(cc, w, vals, k + 1, ROFF(nxt), g);
+      const uint32_t totn = level_rows(cc, w, vals, k + 1, ROFF(nxt), hrow, g);
       if (totn > (uint64_t)capE) {
         st = kStatusDeferred;
         break;
       }
       const ColInfo ck = p.col[k];
       const int nfac = ck.nfac, ngate = ck.ngate, ncR = cc.ncmp[k + 1];
+      (void)ncR;
       for (int f = g.lane; f < nfac; f += G) {
         const FacInfo fi = p.fac[ck.fac_base + f];
         const BSInfo bi = p.bsi[fi.bs];
@@ -579,7 +613,8 @@ __global__ void __launch_bounds__(32 * kCW, 16 / kCW) lofp_contract_warp_kernel(
         for (uint32_t t = g.lane; t < totn; t += G) {
           while (rn[sc + 1] <= t) ++sc;
           if (sc != sc_last) {  // the row's state (column k+1) bounds its sub-box of column k
-            hB = sub_hi_s(hiB, cc.cmp[k + 1], ncR, vals[vbC + sc]);
+            hB = hrow[sc];
+            DCHECK_C(hB == sub_hi_s(hiB, cc.cmp[k + 1], ncR, vals[vbC + sc]));
             sc_last = sc;
           }
           // entry t = the pos-th state of the sub-box (odometer order, segment 0 fastest)
@@ -588,9 +623,9 @@ __global__ void __launch_bounds__(32 * kCW, 16 / kCW) lofp_contract_warp_kernel(
           for (int j = 0; j < nsB; ++j) {
             const int l = byte_at(loB, j), rad = byte_at(hB, j) - l + 1;
             if (rad > 1) {
-              const uint32_t d = pos % (uint32_t)rad;
-              pos /= (uint32_t)rad;
-              sb += d * stride;
+              const uint32_t qd = div_small(s_inv, pos, (uint32_t)rad);
+              sb += (pos - qd * (uint32_t)rad) * stride;
+              pos = qd;
             }
             stride *= (uint32_t)(byte_at(hiB, j) - l + 1);
           }
@@ -745,7 +780,7 @@ static int launch_nf(const CallParams *p, int grid, cudaStream_t stream) {
   CallParams q = *p;
   const long long total = (long long)grid * p->slab_bytes;
   q.cw_bytes = (total / (blocks * kGroups)) & ~255ll;
-  const long long fixed = (long long)kCMaxStates * 8 + 2ll * (kCMaxN + 1) * 4 + 16;
+  const long long fixed = (long long)kCMaxStates * 8 + (long long)kCMaxN * 8 + 2ll * (kCMaxN + 1) * 4 + 16;
   if (q.cw_bytes < fixed + 64 * 1024) return -1;  // scratch too small (LOFP_SLAB_MB): not launched
   lofp_contract_warp_kernel<NF, CNT, G, MM><<<(int)blocks, 32 * kCW, 0, stream>>>(q);
   return (int)cudaGetLastError();
