@@ -69,7 +69,7 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-so
 r = list(csv.reader(out))
 hdr = r[1]
 rows = r[2:]
-iS, iE, iSt = hdr.index("Source"), hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)")
+iS, iE, iSt = hdr.index("Source"), hdr.index("Instructions Executed"), hdr.index(os.environ.get("STALL_COL", "Warp Stall Sampling (All Samples)"))
 if len(seq) != len(rows):
     print(f"warning: {len(seq)} SASS lines in the build vs {len(rows)} in the report", file=sys.stderr)
 ex = collections.Counter()
