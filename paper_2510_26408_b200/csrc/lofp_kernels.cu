@@ -1438,6 +1438,9 @@ __global__ void __launch_bounds__(kThreads, 2) lofp_units_kernel(const __grid_co
     __syncthreads();
     const int k_ = sh.unit;
     if ((ull)k_ >= p.ctr->total_units) break;
+#ifdef LOFP_UNIT_CLOCKS
+    const long long uc0 = clock64();
+#endif
     const int u = p.sched[k_];
     DCHECK(u >= 0 && u < (int)p.ctr->total_units, "sched");
     // unit u -> output q (binary search over ubase) -> slot
@@ -1477,6 +1480,16 @@ __global__ void __launch_bounds__(kThreads, 2) lofp_units_kernel(const __grid_co
     process_stack(p, b, sh, sY, acc, np, cm, nelem, tstage, tfma);
     ull np_tot = 0;
     reduce_block(sh, acc, &p.partial[u], np, &np_tot);
+#ifdef LOFP_UNIT_CLOCKS  // experiment (scripts/unit_clocks.py): the unit's partial replaced by
+                         // (its SM clocks + block / 1024, its end time in ns)
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long gt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+      p.partial[u] = make_double2((double)(clock64() - uc0) + blockIdx.x / 1024.0, (double)gt);
+    }
+    __syncthreads();
+#endif
     if (tid == 0) {
       atomicAdd(&p.pdone[q], np_tot);
       atomicAdd(&p.ctr->paths, np_tot);

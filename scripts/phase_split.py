@@ -21,6 +21,8 @@ for idx in [int(x) for x in (sys.argv[1:] or ["4", "2", "3"])]:
     print(f"cfg{idx}: units_ms {st['units_ms']:.1f} paths/s {st['paths'] / st['units_ms'] * 1e3:.3e} units {st['units']} "
           f"pairs {st['pairs']} elements {st['elements']}")
     print("   " + "  ".join(f"{n} {100 * v / tot:.1f}%" for n, v in zip(NAMES, ph)))
+    # block time accounted by the phases over grid x kernel time (the rest: blocks that ran out of units)
+    print(f"   blocks busy {tot / (st['grid_blocks'] * st['units_ms'] * 1e-3 * 1.965e9):.3f} of grid x kernel time")
     tc = st["tile_cycles"]
     print(f"   tiles: staging {100 * tc[0] / max(1, tc[0] + tc[1]):.1f}% of warp tile time")
 if os.environ.get("HERO"):
