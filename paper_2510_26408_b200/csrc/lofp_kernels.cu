@@ -1731,14 +1731,6 @@ extern "C" int lofp_launch_contract(const CallParams *p, int grid, void *stream)
 // ---- NEXT-2: every output pattern of N photons in M modes ----------------------
 // Pattern r (0 <= r < C(N+M-1, M-1)) in the order of decreasing T_0, then decreasing T_1,
 // ...: unranked independently per thread from the binomial counts of the suffixes.
-__device__ __forceinline__ ull binom_dev(int n, int k) {  // C(n, k), n < 256 (caller bounds it)
-  if (k < 0 || k > n) return 0;
-  if (k > n - k) k = n - k;
-  ull r = 1;
-  for (int i = 1; i <= k; ++i) r = r * (ull)(n - k + i) / (ull)i;
-  return r;
-}
-
 __global__ void lofp_outputs_kernel(int M, int N, long long count, int32_t *T) {
   for (long long r0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; r0 < count;
        r0 += (long long)gridDim.x * blockDim.x) {
@@ -1746,11 +1738,17 @@ __global__ void lofp_outputs_kernel(int M, int N, long long count, int32_t *T) {
     int rem = N;
     int32_t *row = T + r0 * M;
     for (int i = 0; i < M - 1; ++i) {
-      int v = rem;
-      for (; v > 0; --v) {  // patterns of the remaining modes holding rem - v photons
-        const ull c = binom_dev(rem - v + (M - i - 2), M - i - 2);
+      // patterns of the remaining m + 1 modes holding rem - v photons: c = C(rem - v + m, m),
+      // stepped with v by C(n + 1, m) = C(n, m) (n + 1) / (n + 1 - m) (exact; one division per
+      // step instead of m: the kernel was 10 % of the distribution call)
+      const int m = M - i - 2;
+      int v = rem, n = m;
+      ull c = 1;
+      for (; v > 0; --v) {
         if (r < c) break;
         r -= c;
+        c = c * (ull)(n + 1) / (ull)(n + 1 - m);
+        ++n;
       }
       row[i] = v;
       rem -= v;
