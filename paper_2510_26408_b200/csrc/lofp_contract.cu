@@ -61,6 +61,9 @@ typedef unsigned long long ull;
 #define LOFP_CW 4
 #endif
 constexpr int kCW = LOFP_CW;       // warps (outputs in flight) per block
+#ifndef LOFP_CWPS
+#define LOFP_CWPS 16               // resident warps per SM the register cap is set for (128 registers)
+#endif
 constexpr int kCSeg = 8;           // segments per column: one byte each of a packed u64
 constexpr int kCMaxN = 4096;       // states per column (as the block kernel)
 constexpr int kCMaxStates = 16384; // states of all columns of one output
@@ -476,7 +479,7 @@ __device__ __forceinline__ void row_sum(const double2 *__restrict__ table, const
 // NF: the most BS any cut carries (<= 7; loops unrolled to it), CNT: exact path counts too,
 // G: lanes per output (32, or 8 for small circuits in large batches), MM: most modes
 template <int NF, bool CNT, int G, int MM>
-__global__ void __launch_bounds__(32 * kCW, 16 / kCW) lofp_contract_warp_kernel(const __grid_constant__ CallParams p) {
+__global__ void __launch_bounds__(32 * kCW, LOFP_CWPS / kCW) lofp_contract_warp_kernel(const __grid_constant__ CallParams p) {
   constexpr int kGroups = kCW * (32 / G);  // outputs in flight per block
   __shared__ CWarpT<MM> sw[kGroups];
   __shared__ uint8_t s_gseg[kMaxModes + 1][kCSeg], s_ngs[kMaxModes + 1];  // gather slots per cut
