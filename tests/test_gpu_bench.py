@@ -29,3 +29,18 @@ def test_bench_json_line():
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] == 512 * 16
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["gpu_launches"] >= 2 * 8
+
+
+def test_bench_contract_line_tiled():
+    """bench.py --contract (NEXT-1) with the batch repeated: the counted call's
+    path counts must equal the oracle's for every copy (bench.py exits non-zero otherwise),
+    and the line carries the contraction's roofline and e2e keys."""
+    r = subprocess.run([sys.executable, "bench.py", "--contract", "--outputs", "256", "--tile", "3", "--steps", "2",
+                        "--warmup", "1", "--no-cpu"], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert d["metric"] == "amplitudes/s" and d["value"] > 1e4 and d["dtype"] == "f64"
+    assert d["config"]["global_batch"] == 768 and "x 3" in d["config"]["workload"]
+    ro = d["roofline"]
+    assert ro["kernel"] == "lofp_contract_warp_kernel" and ro["work_per_launch"]["terms"] > 0
+    assert d["e2e"]["d2h_bytes_per_step"] == 768 * 16 and d["gpu_launches"] >= 2
